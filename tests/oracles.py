@@ -38,7 +38,7 @@ def _u64(seq):
 
 def _ext(t, mode):
     """Extent of a 1-based mode, 1 when out of range (the library reports it)."""
-    return _ext(t, mode) if 1 <= mode <= t.ndim else 1
+    return t.shape[mode - 1] if 1 <= mode <= t.ndim else 1
 
 
 def fortran(a) -> np.ndarray:
