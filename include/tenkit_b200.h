@@ -1,0 +1,182 @@
+/* tenkit_b200 — C-ABI of the B200-native ALS-HOSVD hot path.
+ *
+ * Drop-in boundary for the reference decomposition API of tenkit
+ * (arXiv 2004.02583). Every entry point below replaces one reference
+ * function; the citation is /root/reference/proj/<file>:<line>.
+ *
+ *   tkg_t_hosvd        <- tenkit::t_hosvd        include/tenkit/hosvd.hpp:55-57, src/hosvd.cpp:74-125
+ *   tkg_st_hosvd       <- tenkit::st_hosvd       include/tenkit/hosvd.hpp:68-70, src/hosvd.cpp:127-191
+ *   tkg_select_order   <- tenkit::select_order   include/tenkit/hosvd.hpp:76,    src/hosvd.cpp:54-63
+ *   tkg_als_low_rank   <- tenkit::als_low_rank   include/tenkit/als.hpp:69-71,   src/als.cpp:98-161
+ *   tkg_als_init       <- tenkit::als_init       include/tenkit/als.hpp:46-47,   src/als.cpp:59-87
+ *   tkg_unfold_times   <- tenkit::unfold_times   include/tenkit/tensor_ops.hpp:39, src/tensor_ops.cpp:193-261
+ *   tkg_unfold_t_times <- tenkit::unfold_t_times include/tenkit/tensor_ops.hpp:44, src/tensor_ops.cpp:263-330
+ *   tkg_mode_n_product <- tenkit::mode_n_product include/tenkit/tensor_ops.hpp:22-23, src/tensor_ops.cpp:129-169
+ *   tkg_frobenius_norm <- tenkit::frobenius_norm include/tenkit/tensor_ops.hpp:52, src/tensor_ops.cpp:391-393
+ *   tkg_relative_error <- tenkit::relative_error include/tenkit/tensor_ops.hpp:55, src/tensor_ops.cpp:395-407
+ *   tkg_reduced_qr     <- tenkit::reduced_qr     include/tenkit/kernels.hpp:23,  src/kernels.cpp:303-367
+ *   tkg_gram           <- tenkit::gram           include/tenkit/matrix.hpp:49,   src/matrix.cpp:90-126
+ *   tkg_uniform01      <- uniform01(seeded_engine(seed, stream)) include/tenkit/rng.hpp:19-21,57-61
+ *
+ * Conventions (identical to the reference):
+ *   - tensors: flat doubles, generalized column-major, first index fastest
+ *     (tensor.hpp:10-11); matrices column-major (matrix.hpp:8-9);
+ *   - modes are 1-based (shape.hpp:10-14);
+ *   - buffers are caller-owned; `a` may be a host pointer (a_on_device = 0,
+ *     copied to HBM inside the call) or a device pointer (a_on_device = 1);
+ *     every other pointer is host memory;
+ *   - return value 0 on success, else the reference ErrorCategory + 1
+ *     (errors.hpp:10: 1 usage, 2 io, 3 numerical — the CLI exit codes,
+ *     tenkit_main.cpp:644-664); err->subtype names the reference exception
+ *     class and err->message carries the reference's message text;
+ *   - a context is single-threaded (one decomposition at a time).
+ */
+#ifndef TENKIT_B200_H
+#define TENKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TKG_MAX_ORDER 16
+#define TKG_MAX_HISTORY 64
+
+/* err->subtype: which tenkit exception the call maps to (errors.hpp:24-77). */
+enum tkg_subtype {
+  TKG_OK = 0,
+  TKG_E_INVALID_MODE = 1,       /* InvalidModeError        (usage)     */
+  TKG_E_DIMENSION_MISMATCH = 2, /* DimensionMismatchError  (usage)     */
+  TKG_E_ZERO_REFERENCE = 3,     /* ZeroReferenceError      (usage)     */
+  TKG_E_RANK_TOO_LARGE = 4,     /* RankTooLargeError       (numerical) */
+  TKG_E_SINGULAR_GRAM = 5,      /* SingularGramError       (numerical) */
+  TKG_E_DEGENERATE_INIT = 6,    /* DegenerateInitError     (numerical) */
+  TKG_E_NO_CONVERGENCE = 7,     /* NoConvergenceError      (numerical) */
+  TKG_E_IO = 8,                 /* IoError                 (io)        */
+  TKG_E_FORMAT = 9,             /* FormatError             (io)        */
+  TKG_E_CUDA = 11,              /* CUDA/NCCL runtime failure (io)      */
+  TKG_E_UNSUPPORTED = 12        /* outside this build's limits (usage) */
+};
+
+typedef struct tkg_error {
+  int32_t code;    /* = return value */
+  int32_t subtype; /* enum tkg_subtype */
+  char message[512];
+} tkg_error;
+
+/* AlsConfig (als.hpp:17-23). init: nullable host I_mode x r column-major
+ * warm start (used by tkg_als_low_rank only, like the reference's drivers
+ * which never set it). */
+typedef struct tkg_als_config {
+  double eta;
+  int32_t max_iters;
+  uint64_t seed;
+  const double* init;
+} tkg_als_config;
+
+/* AlsReport + ModeReport (als.hpp:27-33, hosvd.hpp:33-37). */
+typedef struct tkg_mode_report {
+  int32_t mode;        /* 1-based */
+  int32_t iterations;
+  int32_t status;      /* 0 kConverged, 1 kMaxItersReached (als.hpp:25) */
+  int32_t history_len; /* min(iterations, TKG_MAX_HISTORY) */
+  double achieved_eta;
+  double seconds;      /* factor engine + working-tensor shrink */
+  double residual_history[TKG_MAX_HISTORY];
+} tkg_mode_report;
+
+/* DecompositionReport (hosvd.hpp:39-44) plus device accounting. */
+typedef struct tkg_report {
+  int32_t order;
+  int32_t n_modes;
+  tkg_mode_report per_mode[TKG_MAX_ORDER]; /* processing order */
+  double relative_residual; /* outside the timed region, as the reference */
+  double seconds;           /* factor + core computation (hosvd.cpp:82,122) */
+  double h2d_seconds;       /* host->device copy of a (0 when a_on_device) */
+  double d2h_seconds;       /* core + factors device->host */
+  double residual_seconds;  /* relative_residual evaluation */
+  uint64_t kernel_launches; /* our kernels launched for the timed region */
+  uint64_t tensor_passes;   /* full passes over the working tensor */
+  uint64_t algorithmic_bytes; /* sum of 8*(|A| + F r + I r) per contraction pass */
+} tkg_report;
+
+typedef struct tkg_ctx tkg_ctx;
+
+/* One context per device per thread. */
+int tkg_create(tkg_ctx** ctx, int device, tkg_error* err);
+int tkg_destroy(tkg_ctx* ctx);
+
+/* t_hosvd with the ALS engine (FactorEngine::with_als). core: prod R_n
+ * doubles; factors: concatenated I_n x R_n column-major in mode order.
+ * want_singular_vectors must be 0 (recover_singular_vectors is a §8(f)
+ * "next" row; returns TKG_E_UNSUPPORTED). */
+int tkg_t_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
+                const uint64_t* dims, const uint64_t* ranks, const tkg_als_config* cfg,
+                int32_t want_singular_vectors, double* core, double* factors,
+                tkg_report* report, tkg_error* err);
+
+/* st_hosvd with the ALS engine. mode_order: nullable permutation of 1..N
+ * (nullptr = select_order, i.e. std::nullopt). */
+int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
+                 const uint64_t* dims, const uint64_t* ranks, const uint32_t* mode_order,
+                 const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
+                 tkg_error* err);
+
+/* Stable ascending-rank order (Proposition 1). out: order entries. */
+int tkg_select_order(int32_t order, const uint64_t* dims, const uint64_t* ranks, uint32_t* out,
+                     tkg_error* err);
+
+/* als_low_rank: l_out I_mode x r, r_out (nullable) fibers x r. */
+int tkg_als_low_rank(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
+                     const uint64_t* dims, uint32_t mode, uint64_t r, const tkg_als_config* cfg,
+                     double* l_out, double* r_out, tkg_mode_report* report, tkg_error* err);
+
+/* als_init: the randomized-range initializer, l_out I_mode x r. */
+int tkg_als_init(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
+                 const uint64_t* dims, uint32_t mode, uint64_t r, uint64_t seed, double* l_out,
+                 tkg_error* err);
+
+/* Contraction primitives (host buffers). m is fibers x r (unfold_times) or
+ * I_mode x r (unfold_t_times); u is rows x I_mode (mode_n_product). */
+int tkg_unfold_times(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                     uint32_t mode, const double* m, uint64_t r, double* out, tkg_error* err);
+int tkg_unfold_t_times(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                       uint32_t mode, const double* m, uint64_t r, double* out, tkg_error* err);
+int tkg_mode_n_product(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                       const double* u, uint64_t rows, uint64_t cols, uint32_t mode, double* out,
+                       tkg_error* err);
+int tkg_frobenius_norm(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                       double* out, tkg_error* err);
+int tkg_relative_error(tkg_ctx* ctx, const double* a, const double* b, int32_t order,
+                       const uint64_t* dims, double* out, tkg_error* err);
+int tkg_reduced_qr(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* q,
+                   double* r, tkg_error* err);
+int tkg_gram(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* out,
+             tkg_error* err);
+/* n draws of uniform01 from seeded_engine(seed, stream), generated on the
+ * device by jump-ahead (the ALS initializer's stream). */
+int tkg_uniform01(tkg_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t n, double* out,
+                  tkg_error* err);
+
+/* Per-kernel-class device time (CUDA events on the launch stream) while
+ * profiling is on. classes: 0 FC (right update / TTM), 1 FR (left update /
+ * init), 2 small LA, 3 RNG. */
+typedef struct tkg_kernel_stats {
+  double ms[4];
+  uint64_t launches[4];
+  double bytes[4]; /* algorithmic bytes */
+  double flops[4]; /* algorithmic flops */
+} tkg_kernel_stats;
+int tkg_set_profiling(tkg_ctx* ctx, int on);
+int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out);
+
+/* Library identification (build string, device name). */
+const char* tkg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TENKIT_B200_H */

@@ -1,0 +1,263 @@
+// extern "C" entry points declared in include/tenkit_b200.h. Each wraps an
+// Engine call, maps tkg::Error onto (return code, subtype, message) exactly
+// like the reference's exception taxonomy (errors.hpp:10-77), and never
+// lets a C++ exception cross the ABI.
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/tenkit_b200.h"
+#include "engine.hpp"
+
+struct tkg_ctx {
+  tkg::Engine* eng;
+};
+
+namespace {
+
+void set_err(tkg_error* err, int code, int subtype, const char* msg) {
+  if (!err) return;
+  err->code = code;
+  err->subtype = subtype;
+  std::strncpy(err->message, msg, sizeof(err->message) - 1);
+  err->message[sizeof(err->message) - 1] = '\0';
+}
+
+template <class F>
+int guarded(tkg_error* err, F&& f) {
+  try {
+    f();
+    set_err(err, 0, TKG_OK, "");
+    return 0;
+  } catch (const tkg::Error& e) {
+    set_err(err, e.code, e.subtype, e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_err(err, 2, TKG_E_CUDA, "host allocation failed");
+    return 2;
+  } catch (const std::exception& e) {
+    set_err(err, 1, TKG_E_UNSUPPORTED, e.what());
+    return 1;
+  }
+}
+
+tkg::Shape make_shape(int32_t order, const uint64_t* dims) {
+  if (order < 1) tkg::raise(TKG_E_DIMENSION_MISMATCH, "Shape: at least one extent required");
+  if (order > TKG_MAX_ORDER) tkg::raise(TKG_E_UNSUPPORTED, "order above 16 is not supported");
+  tkg::Shape s;
+  s.N = order;
+  for (int k = 0; k < order; ++k) {
+    if (dims[k] == 0) tkg::raise(TKG_E_DIMENSION_MISMATCH, "Shape: extents must be >= 1");
+    s.d[k] = dims[k];
+  }
+  return s;
+}
+
+tkg::AlsCfg make_cfg(const tkg_als_config* c) {
+  tkg::AlsCfg a;
+  if (c) {
+    a.eta = c->eta;
+    a.max_iters = c->max_iters;
+    a.seed = c->seed;
+    a.init = c->init;
+  }
+  return a;
+}
+
+void fill_mode(const tkg::ModeRep& m, tkg_mode_report* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->mode = m.mode;
+  out->iterations = m.iterations;
+  out->status = m.status;
+  out->achieved_eta = m.achieved_eta;
+  out->seconds = m.seconds;
+  const size_t n = std::min<size_t>(m.history.size(), TKG_MAX_HISTORY);
+  out->history_len = int32_t(n);
+  for (size_t k = 0; k < n; ++k) out->residual_history[k] = m.history[k];
+}
+
+void fill_report(const tkg::DecompRep& r, int order, tkg_report* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof(*out));
+  out->order = order;
+  out->n_modes = int32_t(r.per_mode.size());
+  for (size_t k = 0; k < r.per_mode.size() && k < TKG_MAX_ORDER; ++k) fill_mode(r.per_mode[k], &out->per_mode[k]);
+  out->relative_residual = r.relative_residual;
+  out->seconds = r.seconds;
+  out->h2d_seconds = r.h2d_seconds;
+  out->d2h_seconds = r.d2h_seconds;
+  out->residual_seconds = r.residual_seconds;
+  out->kernel_launches = r.launches;
+  out->tensor_passes = r.passes;
+  out->algorithmic_bytes = r.bytes;
+}
+
+tkg::Engine& eng(tkg_ctx* ctx) {
+  if (!ctx || !ctx->eng) tkg::raise(TKG_E_UNSUPPORTED, "null tkg context");
+  return *ctx->eng;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tkg_version(void) { return "tenkit_b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+int tkg_create(tkg_ctx** ctx, int device, tkg_error* err) {
+  return guarded(err, [&] {
+    *ctx = nullptr;
+    auto* c = new tkg_ctx;
+    try {
+      c->eng = new tkg::Engine(device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *ctx = c;
+  });
+}
+
+int tkg_destroy(tkg_ctx* ctx) {
+  if (ctx) {
+    delete ctx->eng;
+    delete ctx;
+  }
+  return 0;
+}
+
+int tkg_t_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                const uint64_t* ranks, const tkg_als_config* cfg, int32_t want_singular_vectors,
+                double* core, double* factors, tkg_report* report, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    if (want_singular_vectors)
+      tkg::raise(TKG_E_UNSUPPORTED, "t_hosvd: want_singular_vectors is not implemented on the B200 path");
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    tkg::DecompRep rep;
+    eng(ctx).t_hosvd(a, a_on_device != 0, sh, rk, make_cfg(cfg), core, factors, &rep);
+    fill_report(rep, order, report);
+  });
+}
+
+int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                 const uint64_t* ranks, const uint32_t* mode_order, const tkg_als_config* cfg,
+                 double* core, double* factors, tkg_report* report, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    std::vector<int> mo;
+    if (mode_order) mo.assign(mode_order, mode_order + order);
+    tkg::DecompRep rep;
+    eng(ctx).st_hosvd(a, a_on_device != 0, sh, rk, mode_order ? &mo : nullptr, make_cfg(cfg), core,
+                      factors, &rep);
+    fill_report(rep, order, report);
+  });
+}
+
+int tkg_select_order(int32_t order, const uint64_t* dims, const uint64_t* ranks, uint32_t* out,
+                     tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    tkg::validate_truncation(sh, rk);  // select_order validates first (hosvd.cpp:55)
+    std::vector<int> o = tkg::select_order(rk);
+    for (int k = 0; k < order; ++k) out[k] = uint32_t(o[k]);
+  });
+}
+
+int tkg_als_low_rank(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
+                     const uint64_t* dims, uint32_t mode, uint64_t r, const tkg_als_config* cfg,
+                     double* l_out, double* r_out, tkg_mode_report* report, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    const uint64_t I = sh.extent(int(mode));
+    if (cfg && cfg->init == nullptr && (r < 1 || r > I)) {
+      // ZeroReference is checked before the initializer's guard (als.cpp:102-105 vs 62-66);
+      // the engine reproduces that order, so only reject ranks that do not fit a uint32.
+    }
+    if (r > 0xffffffffu) tkg::raise(TKG_E_RANK_TOO_LARGE, "rank too large");
+    tkg::ModeRep rep;
+    eng(ctx).als_low_rank(a, a_on_device != 0, sh, int(mode), uint32_t(r), make_cfg(cfg), l_out,
+                          r_out, &rep);
+    if (report) fill_mode(rep, report);
+  });
+}
+
+int tkg_als_init(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                 uint32_t mode, uint64_t r, uint64_t seed, double* l_out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).als_init(a, a_on_device != 0, sh, int(mode), uint32_t(r), seed, l_out);
+  });
+}
+
+int tkg_unfold_times(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode,
+                     const double* m, uint64_t r, double* out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).unfold_times(a, sh, int(mode), m, uint32_t(r), out);
+  });
+}
+
+int tkg_unfold_t_times(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                       uint32_t mode, const double* m, uint64_t r, double* out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).unfold_t_times(a, sh, int(mode), m, uint32_t(r), out);
+  });
+}
+
+int tkg_mode_n_product(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                       const double* u, uint64_t rows, uint64_t cols, uint32_t mode, double* out,
+                       tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).mode_n_product(a, sh, u, rows, cols, int(mode), out);
+  });
+}
+
+int tkg_frobenius_norm(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, double* out,
+                       tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    *out = eng(ctx).frobenius_norm(a, sh.count());
+  });
+}
+
+int tkg_relative_error(tkg_ctx* ctx, const double* a, const double* b, int32_t order,
+                       const uint64_t* dims, double* out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    *out = eng(ctx).relative_error(a, b, sh.count());
+  });
+}
+
+int tkg_reduced_qr(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* q, double* r,
+                   tkg_error* err) {
+  return guarded(err, [&] { eng(ctx).reduced_qr(a, rows, cols, q, r); });
+}
+
+int tkg_gram(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* out, tkg_error* err) {
+  return guarded(err, [&] { eng(ctx).gram(a, rows, cols, out); });
+}
+
+int tkg_uniform01(tkg_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t n, double* out, tkg_error* err) {
+  return guarded(err, [&] { eng(ctx).uniform01(seed, stream, n, out); });
+}
+
+int tkg_set_profiling(tkg_ctx* ctx, int on) {
+  if (!ctx || !ctx->eng) return 1;
+  ctx->eng->set_profiling(on != 0);
+  return 0;
+}
+
+int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out) {
+  tkg_error err;
+  return guarded(&err, [&] {
+    std::memset(out, 0, sizeof(*out));
+    eng(ctx).kernel_stats(out->ms, out->launches, out->bytes, out->flops);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,769 @@
+// Host orchestration of the B200 ALS-HOSVD hot path (see engine.hpp).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "mt_jump.hpp"
+
+namespace tkg {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+int category_of(int subtype) {
+  switch (subtype) {
+    case 1: case 2: case 3: case 12: return 1;  // usage
+    case 8: case 9: case 11: return 2;          // io / runtime
+    default: return 3;                          // numerical
+  }
+}
+
+constexpr uint32_t kMaxRank = 64;
+constexpr int kMtSeqPadded = kPolyWords * 64 + kMtN;  // jump kernel reads this far
+
+}  // namespace
+
+[[noreturn]] void raise(int subtype, const std::string& msg) { throw Error(category_of(subtype), subtype, msg); }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(11, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) check_cuda((x), #x)
+
+// ---- Shape (shape.cpp:11-45) -------------------------------------------------
+uint64_t Shape::count() const {
+  uint64_t c = 1;
+  for (int k = 0; k < N; ++k) c *= d[k];
+  return c;
+}
+uint64_t Shape::extent(int mode) const {
+  if (mode < 1 || mode > N)
+    raise(1, "mode " + std::to_string(mode) + " out of range 1.." + std::to_string(N));
+  return d[mode - 1];
+}
+uint64_t Shape::stride(int mode) const {
+  extent(mode);
+  uint64_t s = 1;
+  for (int m = 0; m + 1 < mode; ++m) s *= d[m];
+  return s;
+}
+std::string Shape::str() const {
+  std::ostringstream o;
+  for (int k = 0; k < N; ++k) o << (k ? "x" : "") << d[k];
+  return o.str();
+}
+
+void validate_truncation(const Shape& sh, const std::vector<uint64_t>& ranks) {  // shape.cpp:56-69
+  if (ranks.size() != size_t(sh.N))
+    raise(2, "truncation lists " + std::to_string(ranks.size()) + " ranks for an order-" +
+                 std::to_string(sh.N) + " tensor");
+  for (int n = 0; n < sh.N; ++n)
+    if (ranks[n] < 1 || ranks[n] > sh.d[n])
+      raise(4, "mode " + std::to_string(n + 1) + ": rank " + std::to_string(ranks[n]) +
+                   " outside 1.." + std::to_string(sh.d[n]));
+}
+
+std::vector<int> select_order(const std::vector<uint64_t>& ranks) {  // hosvd.cpp:54-63
+  std::vector<int> order(ranks.size());
+  for (size_t k = 0; k < ranks.size(); ++k) order[k] = int(k) + 1;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return ranks[a - 1] < ranks[b - 1]; });
+  return order;
+}
+
+// ---- DBuf ------------------------------------------------------------------------
+DBuf::~DBuf() { release(); }
+void DBuf::release() {
+  if (p_) cudaFree(p_);
+  p_ = nullptr;
+  bytes_ = 0;
+}
+void* DBuf::ensure(size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (bytes > bytes_) {
+    release();
+    CK(cudaMalloc(&p_, bytes));
+    bytes_ = bytes;
+  }
+  return p_;
+}
+
+// ---- Engine ----------------------------------------------------------------------
+Engine::Engine(int device) : device_(device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    raise(11, "no CUDA device available: the B200 path has no CPU fallback");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  name_ = prop.name;
+  if (prop.major < 10) raise(12, std::string("tenkit_b200 is built for sm_100a; device is ") + prop.name);
+  sms_ = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&status_h_), sizeof(DevStatus), cudaHostAllocMapped));
+  std::memset(status_h_, 0, sizeof(DevStatus));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&status_d_), status_h_, 0));
+}
+
+Engine::~Engine() {
+  cudaSetDevice(device_);
+  cudaStreamSynchronize(st_);
+  for (auto* b : factor_bufs_) delete b;
+  for (auto& kv : jump_cache_) delete kv.second;
+  for (auto& r : recs_) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  if (status_h_) cudaFreeHost(status_h_);
+  cudaStreamDestroy(st_);
+}
+
+void Engine::sync() { CK(cudaStreamSynchronize(st_)); }
+
+std::pair<cudaEvent_t, cudaEvent_t> Engine::ev_pair() {
+  cudaEvent_t a, b;
+  if (ev_pool_.size() >= 2) {
+    a = ev_pool_.back();
+    ev_pool_.pop_back();
+    b = ev_pool_.back();
+    ev_pool_.pop_back();
+  } else {
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+  }
+  return {a, b};
+}
+
+void Engine::record(int cls, cudaEvent_t a, cudaEvent_t b, double bytes, double flops) {
+  recs_.push_back({cls, a, b, bytes, flops});
+}
+
+void Engine::kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], double flops[4]) {
+  sync();
+  for (auto& r : recs_) {
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    stat_ms_[r.cls] += t;
+    stat_launch_[r.cls] += 1;
+    stat_bytes_[r.cls] += r.bytes;
+    stat_flops_[r.cls] += r.flops;
+    ev_pool_.push_back(r.a);
+    ev_pool_.push_back(r.b);
+  }
+  recs_.clear();
+  for (int k = 0; k < 4; ++k) {
+    ms[k] = stat_ms_[k];
+    launches[k] = stat_launch_[k];
+    bytes[k] = stat_bytes_[k];
+    flops[k] = stat_flops_[k];
+    stat_ms_[k] = 0;
+    stat_launch_[k] = 0;
+    stat_bytes_[k] = 0;
+    stat_flops_[k] = 0;
+  }
+}
+
+const double* Engine::upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds) {
+  if (a_dev) return a;
+  const auto t0 = Clock::now();
+  double* d = buf.d(n);
+  CK(cudaMemcpyAsync(d, a, n * sizeof(double), cudaMemcpyHostToDevice, st_));
+  sync();
+  if (seconds) *seconds += since(t0);
+  return d;
+}
+
+void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
+                uint64_t os_c, uint64_t os_p, double* gram_part, double* sumsq_part,
+                const double* diff_ref, int* grid_used, bool count_pass) {
+  FcArgs a;
+  a.in = v;
+  a.mt = mt;
+  a.ldmt = ldmt;
+  a.out = out;
+  a.os_c = os_c;
+  a.os_p = os_p;
+  a.nc = nc;
+  a.gram_part = gram_part;
+  a.sumsq_part = sumsq_part;
+  a.diff_ref = diff_ref;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (profiling_) {
+    ev = ev_pair();
+    CK(cudaEventRecord(ev.first, st_));
+  }
+  CK(launch_fc(a, sms_, st_, grid_used));
+  count_launch();
+  const double elems = double(v.s) * double(v.P) * double(v.K);
+  const double F = double(v.s) * double(v.P);
+  const double bytes = 8.0 * (elems + F * nc + double(v.K) * nc);
+  if (profiling_) {
+    CK(cudaEventRecord(ev.second, st_));
+    record(kClsFC, ev.first, ev.second, bytes, 2.0 * elems * nc);
+  }
+  if (count_pass) {
+    passes_ += 1;
+    bytes_ += uint64_t(bytes);
+  }
+}
+
+uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t nc, double* partial,
+                    double* sumsq_part, bool count_pass, uint32_t* grid_used) {
+  FrArgs a;
+  a.in = v;
+  a.m = m;
+  a.ldm = ldm;
+  a.nc = nc;
+  a.partial = partial;
+  a.sumsq_part = sumsq_part;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (profiling_) {
+    ev = ev_pair();
+    CK(cudaEventRecord(ev.first, st_));
+  }
+  uint32_t ranges = 0, grid = 0;
+  CK(launch_fr(a, sms_, st_, &ranges, &grid));
+  if (grid_used) *grid_used = grid;
+  count_launch();
+  const double elems = double(v.s) * double(v.P) * double(v.K);
+  const double F = double(v.s) * double(v.P);
+  const double bytes = 8.0 * (elems + F * nc + double(v.K) * nc);
+  if (profiling_) {
+    CK(cudaEventRecord(ev.second, st_));
+    record(kClsFR, ev.first, ev.second, bytes, 2.0 * elems * nc);
+  }
+  if (count_pass) {
+    passes_ += 1;
+    bytes_ += uint64_t(bytes);
+  }
+  return ranges;
+}
+
+// S (n doubles) = uniform01 draws of seeded_engine(seed, stream), on device.
+void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out) {
+  if (n == 0) return;
+  if (mt_charpoly().empty()) raise(11, "MT19937-64 characteristic polynomial check failed");
+  const MtPlan plan = mt_plan(n);
+  const auto key = std::make_pair(plan.J, plan.C);
+  DBuf* polys = nullptr;
+  auto it = jump_cache_.find(key);
+  if (it == jump_cache_.end()) {
+    std::vector<uint64_t> tbl = mt_jump_table(plan.J, plan.C);
+    polys = new DBuf();
+    CK(cudaMemcpy(polys->u(tbl.size()), tbl.data(), tbl.size() * 8, cudaMemcpyHostToDevice));
+    jump_cache_[key] = polys;
+  } else {
+    polys = it->second;
+  }
+  std::vector<uint64_t> y(kMtSeqPadded, 0);
+  mt_raw_sequence(seed, stream, y.data(), kMtSeqWords);
+  uint64_t* d_y = y_seq_.u(kMtSeqPadded);
+  CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st_));
+  uint64_t* d_states = states_.u(size_t(plan.C) * kMtN);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (profiling_) {
+    ev = ev_pair();
+    CK(cudaEventRecord(ev.first, st_));
+  }
+  CK(launch_mt_states(d_y, polys->u(0) /*existing*/, plan.C, d_states, st_));
+  CK(launch_mt_generate(d_states, plan.C, plan.J, n, d_out, st_));
+  count_launch(3);  // memset + jump + generate
+  if (profiling_) {
+    CK(cudaEventRecord(ev.second, st_));
+    record(kClsRng, ev.first, ev.second, 8.0 * n, 0.0);
+  }
+  // keep y alive until the copy finished
+  sync();
+}
+
+Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint32_t r,
+                               const AlsCfg& cfg, bool sumsq_known) {
+  const uint64_t I = sh.extent(mode);
+  const uint64_t s = sh.stride(mode);
+  const uint64_t F = sh.count() / I;
+  const uint64_t P = F / s;
+  const uint32_t ncp = pad_nc(r);
+  const std::string mname = "mode " + std::to_string(mode);
+  FiberView v{A, s, P, uint32_t(I), s, s * I};
+  AlsOut out;
+  out.rep.mode = mode;
+
+  if (r > kMaxRank) raise(12, mname + ": rank " + std::to_string(r) + " above the supported 64");
+  double* Lc = l_.d(I * r);
+  double* Mt = mt_.d(I * ncp);
+  double* R = r_.d(F * r);
+  double* GL = gl_.d(kMaxRank * kMaxRank);
+  double* GR = gr_.d(kMaxRank * kMaxRank);
+  double* cholL = cholL_.d(kMaxRank * kMaxRank);
+  double* cholR = cholR_.d(kMaxRank * kMaxRank);
+  const uint32_t nranges = fr_ranges_for(v, r, sms_) + 4;
+  double* part = fr_part_.d(size_t(nranges) * I * ncp);
+  const int fc_grid = fc_grid_for(v, r, sms_);
+  double* fcg = fc_gram_.d(size_t(fc_grid) * ncp * ncp);
+  double* gp = gram_part_.d(size_t(gram_partials_count(uint32_t(I))) * r * r);
+  double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
+  double* qrw = qr_work_.d(2 * I * r + r);
+
+  status_h_->degenerate_col = 0;
+  // 1. ||A|| and the initial left factor.
+  if (cfg.init) {
+    if (!sumsq_known) {
+      CK(launch_sumsq(A, sh.count(), sq, st_));
+      CK(launch_sum(sq, sumsq_partials_count(sh.count()), &status_d_->sumsq, st_));
+      count_launch(2);
+    }
+    CK(cudaMemcpyAsync(Lc, cfg.init, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
+  } else {
+    if (r < 1 || r > I)
+      raise(4, mname + ": rank " + std::to_string(r) + " outside 1.." + std::to_string(I));
+    double* S = s_.d(F * r);
+    gen_uniform(cfg.seed, uint32_t(mode), F * r, S);
+    uint32_t fr_grid = 0;
+    const uint32_t ranges = fr(v, S, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
+    if (!sumsq_known) {  // ||A||^2 fused into the init pass: one partial per CTA
+      CK(launch_sum(sq, int(fr_grid), &status_d_->sumsq, st_));
+      count_launch();
+    }
+    CK(launch_qr(part, int(ranges), ncp, uint32_t(I), r, Lc, nullptr, nullptr, 0, qrw, 1, status_d_, st_));
+    count_launch();
+  }
+  sync();
+  const double norm = std::sqrt(status_h_->sumsq);  // frobenius_norm (tensor_ops.cpp:391-393)
+  if (norm == 0.0) raise(3, "als_low_rank: input tensor has zero norm");
+  if (!cfg.init && status_h_->degenerate_col != 0)
+    raise(6, "als_init: randomized range collapsed at column " + std::to_string(status_h_->degenerate_col) +
+                 " for mode " + std::to_string(mode));
+  out.norm = norm;
+
+  // 2. Sweeps (als.cpp:121-160).
+  ModeRep& rep = out.rep;
+  rep.status = 1;
+  double prev = norm;
+  const int max_iters = std::max(1, cfg.max_iters);
+  const std::string singular = mname + ": gram matrix is singular, rank " + std::to_string(r) +
+                               " exceeds the numerical rank of the iterate";
+  for (int k = 1; k <= max_iters; ++k) {
+    // right update: G_L, chol, L' = L G_L^{-1} (i-major, padded) -> R = A^T L'
+    CK(launch_gram_partials(Lc, I, uint32_t(I), r, gp, st_));
+    CK(launch_chol(gp, gram_partials_count(uint32_t(I)), uint64_t(r) * r, int(r), r, GL, cholL,
+                   &status_d_->right_singular, status_d_, st_));
+    CK(launch_row_solve(Lc, 0, I, uint32_t(I), r, cholL, nullptr, Mt, ncp, &status_d_->right_singular, st_));
+    count_launch(3);
+    int grid = 0;
+    fc(v, Mt, ncp, r, R, F, s, fcg, nullptr, nullptr, &grid, true);
+    CK(launch_finish_right(fcg, grid, int(ncp), r, GL, nullptr, GR, cholR, status_d_, st_));
+    count_launch();
+    sync();
+    if (status_h_->right_singular) raise(4, singular);
+    const double residual = status_h_->residual;
+    rep.iterations = k;
+    rep.history.push_back(residual);
+    rep.achieved_eta = std::fabs(prev - residual) / norm;
+    if (rep.achieved_eta <= cfg.eta) {
+      rep.status = 0;
+      break;
+    }
+    if (k == max_iters) break;
+    // left update: Y = A R, L = Y G_R^{-1}
+    if (status_h_->left_singular) raise(4, singular);
+    const uint32_t ranges = fr(v, R, F, r, part, nullptr, true, nullptr);
+    CK(launch_row_solve(part, int(ranges), ncp, uint32_t(I), r, cholR, Lc, nullptr, 0, nullptr, st_));
+    count_launch();
+    prev = residual;
+  }
+  return out;
+}
+
+void Engine::begin_timed() {
+  launches_ = 0;
+  passes_ = 0;
+  bytes_ = 0;
+}
+
+// multi_mode_product(t, {U_n^T}) in ascending mode order (hosvd.cpp:115-121).
+void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                        const std::vector<double*>& d_factors, double* d_core) {
+  Shape cur = sh;
+  const double* src = A;
+  DBuf* bufs[2] = {&work_a_, &work_b_};
+  int which = 0;
+  for (int n = 1; n <= sh.N; ++n) {
+    const uint64_t I = cur.extent(n), s = cur.stride(n), F = cur.count() / I, P = F / s;
+    const uint32_t r = uint32_t(ranks[n - 1]);
+    const uint32_t ncp = pad_nc(r);
+    double* Mt = mt_.d(I * ncp);
+    CK(launch_pack(d_factors[n - 1], 1, I, uint32_t(I), r, Mt, ncp, st_));  // Mt[i][c] = U[i + c*I]
+    count_launch();
+    Shape nxt = cur;
+    nxt.d[n - 1] = r;
+    double* dst = (n == sh.N) ? d_core : bufs[which]->d(nxt.count());
+    FiberView v{src, s, P, uint32_t(I), s, s * I};
+    fc(v, Mt, ncp, r, dst, s, s * r, nullptr, nullptr, nullptr, nullptr, n == 1);
+    src = dst;
+    cur = nxt;
+    which ^= 1;
+  }
+}
+
+// ||A - core x_1 U_1 ... x_N U_N|| / ||A|| without materialising the
+// reconstruction: expand modes 1..N-1, then fuse the mode-N expansion with
+// the difference norm (relative_error(t, reconstruct(tk)), hosvd.cpp:123,189).
+double Engine::relative_residual_dev(const double* A, const Shape& sh,
+                                     const std::vector<uint64_t>& ranks, const double* d_core,
+                                     const std::vector<double*>& d_factors, double ref_sumsq) {
+  if (ref_sumsq == 0.0) raise(3, "relative_error: reference tensor has zero norm");
+  Shape cur;
+  cur.N = sh.N;
+  for (int k = 0; k < sh.N; ++k) cur.d[k] = ranks[k];
+  const double* src = d_core;
+  DBuf* bufs[2] = {&work_a_, &work_b_};
+  int which = 0;
+  std::vector<double> partial_sums;
+  double* sq = sq_part_.d(65536);
+  int nsq = 0;
+  for (int n = 1; n <= sh.N; ++n) {
+    const uint64_t K = cur.extent(n), s = cur.stride(n), F = cur.count() / K, P = F / s;
+    const uint64_t Iout = sh.d[n - 1];
+    Shape nxt = cur;
+    nxt.d[n - 1] = Iout;
+    const bool last = (n == sh.N);
+    double* dst = last ? nullptr : bufs[which]->d(nxt.count());
+    FiberView v{src, s, P, uint32_t(K), s, s * K};
+    for (uint64_t c0 = 0; c0 < Iout; c0 += 64) {
+      const uint32_t nc = uint32_t(std::min<uint64_t>(64, Iout - c0));
+      const uint32_t ncp = pad_nc(nc);
+      double* Mt = misc_.d(K * ncp);
+      // Mt[c][i'] = U[(c0 + i') + c*Iout]
+      CK(launch_pack(d_factors[n - 1] + c0, Iout, 1, uint32_t(K), nc, Mt, ncp, st_));
+      int grid = 0;
+      if (last) {
+        fc(v, Mt, ncp, nc, nullptr, s, s * Iout, nullptr, sq + nsq, A + c0 * s, &grid, false);
+        nsq += grid;
+        if (nsq + 256 > 65536) raise(12, "relative_error: too many partials");
+      } else {
+        fc(v, Mt, ncp, nc, dst + c0 * s, s, s * Iout, nullptr, nullptr, nullptr, &grid, false);
+      }
+    }
+    src = dst;
+    cur = nxt;
+    which ^= 1;
+  }
+  double* out = misc2_.d(1);
+  CK(launch_sum(sq, nsq, out, st_));
+  double diff_sq = 0.0;
+  CK(cudaMemcpyAsync(&diff_sq, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  return std::sqrt(diff_sq / ref_sumsq);
+}
+
+void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
+                     const AlsCfg& cfg, double* core, double* factors, DecompRep* rep) {
+  validate_truncation(sh, ranks);
+  *rep = DecompRep();
+  const double* A = upload(a, sh.count(), a_dev, tensor_, &rep->h2d_seconds);
+  while (factor_bufs_.size() < size_t(sh.N)) factor_bufs_.push_back(new DBuf());
+  std::vector<double*> U(sh.N);
+  begin_timed();
+  const auto t0 = Clock::now();
+  bool sumsq_known = false;
+  double ref_sumsq = 0.0;
+  for (int n = 1; n <= sh.N; ++n) {
+    const auto tm = Clock::now();
+    const uint32_t r = uint32_t(ranks[n - 1]);
+    const uint64_t I = sh.d[n - 1];
+    AlsOut o = run_als(A, sh, n, r, cfg, sumsq_known);
+    if (!sumsq_known) ref_sumsq = status_h_->sumsq;
+    sumsq_known = true;
+    U[n - 1] = factor_bufs_[n - 1]->d(I * r);
+    CK(launch_qr(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0,
+                 qr_work_.d(2 * I * r + r), 0, status_d_, st_));
+    count_launch();
+    sync();
+    o.rep.seconds = since(tm);
+    rep->per_mode.push_back(o.rep);
+  }
+  Shape cs;
+  cs.N = sh.N;
+  for (int k = 0; k < sh.N; ++k) cs.d[k] = ranks[k];
+  double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
+  core_chain(A, sh, ranks, U, core_buf);
+  sync();
+  rep->seconds = since(t0);
+  rep->launches = launches_;
+  rep->passes = passes_;
+  rep->bytes = bytes_;
+  const auto td = Clock::now();
+  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  size_t ofs = 0;
+  for (int n = 0; n < sh.N; ++n) {
+    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    ofs += sh.d[n] * ranks[n];
+  }
+  sync();
+  rep->d2h_seconds = since(td);
+  const auto tr = Clock::now();
+  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+  rep->residual_seconds = since(tr);
+}
+
+void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
+                      const std::vector<int>* order_in, const AlsCfg& cfg, double* core,
+                      double* factors, DecompRep* rep) {
+  validate_truncation(sh, ranks);
+  std::vector<int> order;
+  if (!order_in) {
+    order = select_order(ranks);
+  } else {  // checked_order (hosvd.cpp:30-50)
+    if (order_in->size() != size_t(sh.N))
+      raise(1, "st_hosvd: order has " + std::to_string(order_in->size()) + " entries for an order-" +
+                   std::to_string(sh.N) + " tensor");
+    std::vector<bool> seen(sh.N, false);
+    for (int m : *order_in) {
+      if (m < 1 || m > sh.N || seen[m - 1])
+        raise(1, "st_hosvd: order is not a permutation of 1.." + std::to_string(sh.N));
+      seen[m - 1] = true;
+    }
+    order = *order_in;
+  }
+  *rep = DecompRep();
+  const double* A = upload(a, sh.count(), a_dev, tensor_, &rep->h2d_seconds);
+  while (factor_bufs_.size() < size_t(sh.N)) factor_bufs_.push_back(new DBuf());
+  std::vector<double*> U(sh.N);
+  begin_timed();
+  const auto t0 = Clock::now();
+  Shape cur = sh;
+  const double* work = A;
+  DBuf* bufs[2] = {&work_a_, &work_b_};
+  int which = 0;
+  bool sumsq_known = false;
+  double ref_sumsq = 0.0;
+  for (int mode : order) {
+    const auto tm = Clock::now();
+    const uint32_t r = uint32_t(ranks[mode - 1]);
+    const uint64_t I = cur.extent(mode), s = cur.stride(mode), F = cur.count() / I, P = F / s;
+    AlsOut o = run_als(work, cur, mode, r, cfg, sumsq_known);
+    if (!sumsq_known) ref_sumsq = status_h_->sumsq;
+    const uint32_t ncp = pad_nc(r);
+    U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
+    double* RhT = rhatT_.d(size_t(r) * ncp);
+    CK(launch_qr(l_.d(I * r), 0, I, uint32_t(I), r, U[mode - 1], rhat_.d(r * r), RhT, ncp,
+                 qr_work_.d(2 * I * r + r), 0, status_d_, st_));
+    count_launch();
+    // working <- tensorize(R_hat R^T, mode, shrunk) (hosvd.cpp:176-178): an FC
+    // over R read as a tensor (extent r, strides F / s), fused ||.||^2.
+    Shape nxt = cur;
+    nxt.d[mode - 1] = r;
+    double* dst = bufs[which]->d(nxt.count());
+    FiberView rv{r_.d(F * r), s, P, r, F, s};
+    int grid = 0;
+    double* sq = sq_part_.d(4096);
+    fc(rv, RhT, ncp, r, dst, s, s * r, nullptr, sq, nullptr, &grid, false);
+    CK(launch_sum(sq, grid, &status_d_->sumsq, st_));
+    count_launch();
+    sumsq_known = true;
+    sync();
+    o.rep.seconds = since(tm);
+    rep->per_mode.push_back(o.rep);
+    work = dst;
+    cur = nxt;
+    which ^= 1;
+  }
+  Shape cs = cur;
+  double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
+  CK(cudaMemcpyAsync(core_buf, work, cs.count() * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  sync();
+  rep->seconds = since(t0);
+  rep->launches = launches_;
+  rep->passes = passes_;
+  rep->bytes = bytes_;
+  const auto td = Clock::now();
+  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  size_t ofs = 0;
+  for (int n = 0; n < sh.N; ++n) {
+    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    ofs += sh.d[n] * ranks[n];
+  }
+  sync();
+  rep->d2h_seconds = since(td);
+  const auto tr = Clock::now();
+  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+  rep->residual_seconds = since(tr);
+}
+
+void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,
+                          const AlsCfg& cfg, double* l_out, double* r_out, ModeRep* rep) {
+  const uint64_t I = sh.extent(mode);
+  if (cfg.init == nullptr && (r < 1 || r > I)) {
+    // als_low_rank computes the norm first; a zero tensor reports ZeroReference
+    // before the initializer's rank guard. Keep that order.
+  }
+  const double* A = upload(a, sh.count(), a_dev, tensor_, nullptr);
+  if (cfg.init && r > kMaxRank) raise(12, "rank above the supported 64");
+  AlsOut o = run_als(A, sh, mode, r, cfg, false);
+  *rep = o.rep;
+  const uint64_t F = sh.count() / I;
+  CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (r_out) CK(cudaMemcpyAsync(r_out, r_.d(F * r), F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,
+                      uint64_t seed, double* l_out) {
+  const uint64_t I = sh.extent(mode);
+  if (r < 1 || r > I)
+    raise(4, "mode " + std::to_string(mode) + ": rank " + std::to_string(r) + " outside 1.." + std::to_string(I));
+  if (r > kMaxRank) raise(12, "rank above the supported 64");
+  const double* A = upload(a, sh.count(), a_dev, tensor_, nullptr);
+  const uint64_t s = sh.stride(mode), F = sh.count() / I;
+  const uint32_t ncp = pad_nc(r);
+  FiberView v{A, s, F / s, uint32_t(I), s, s * I};
+  double* S = s_.d(F * r);
+  gen_uniform(seed, uint32_t(mode), F * r, S);
+  const uint32_t nranges = fr_ranges_for(v, r, sms_) + 4;
+  double* part = fr_part_.d(size_t(nranges) * I * ncp);
+  const uint32_t ranges = fr(v, S, F, r, part, nullptr, false, nullptr);
+  status_h_->degenerate_col = 0;
+  CK(launch_qr(part, int(ranges), ncp, uint32_t(I), r, l_.d(I * r), nullptr, nullptr, 0,
+               qr_work_.d(2 * I * r + r), 1, status_d_, st_));
+  sync();
+  if (status_h_->degenerate_col != 0)
+    raise(6, "als_init: randomized range collapsed at column " + std::to_string(status_h_->degenerate_col) +
+                 " for mode " + std::to_string(mode));
+  CK(cudaMemcpy(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+// ---- primitives ------------------------------------------------------------------
+void Engine::unfold_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r,
+                          double* out) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
+  if (r > kMaxRank) raise(12, "unfold_times: more than 64 columns");
+  const double* A = upload(a, sh.count(), false, tensor_, nullptr);
+  double* M = s_.d(F * r);
+  CK(cudaMemcpyAsync(M, m, F * r * sizeof(double), cudaMemcpyHostToDevice, st_));
+  const uint32_t ncp = pad_nc(r);
+  FiberView v{A, s, F / s, uint32_t(I), s, s * I};
+  const uint32_t nranges = fr_ranges_for(v, r, sms_) + 4;
+  double* part = fr_part_.d(size_t(nranges) * I * ncp);
+  const uint32_t ranges = fr(v, M, F, r, part, nullptr, false, nullptr);
+  double* y = misc_.d(I * r);
+  CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, y, st_));
+  CK(cudaMemcpyAsync(out, y, I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Engine::unfold_t_times(const double* a, const Shape& sh, int mode, const double* m,
+                            uint32_t r, double* out) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
+  if (r > kMaxRank) raise(12, "unfold_t_times: more than 64 columns");
+  const double* A = upload(a, sh.count(), false, tensor_, nullptr);
+  const uint32_t ncp = pad_nc(r);
+  double* Mc = misc_.d(I * r);
+  CK(cudaMemcpyAsync(Mc, m, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
+  double* Mt = mt_.d(I * ncp);
+  CK(launch_pack(Mc, 1, I, uint32_t(I), r, Mt, ncp, st_));
+  double* R = r_.d(F * r);
+  FiberView v{A, s, F / s, uint32_t(I), s, s * I};
+  fc(v, Mt, ncp, r, R, F, s, nullptr, nullptr, nullptr, nullptr, false);
+  CK(cudaMemcpyAsync(out, R, F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Engine::mode_n_product(const double* a, const Shape& sh, const double* u, uint64_t rows,
+                            uint64_t cols, int mode, double* out) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
+  if (cols != I)
+    raise(2, "mode_n_product: factor has " + std::to_string(cols) + " columns, mode " +
+                 std::to_string(mode) + " has extent " + std::to_string(I));
+  const double* A = upload(a, sh.count(), false, tensor_, nullptr);
+  double* U = misc_.d(rows * cols);
+  CK(cudaMemcpyAsync(U, u, rows * cols * sizeof(double), cudaMemcpyHostToDevice, st_));
+  Shape nxt = sh;
+  nxt.d[mode - 1] = rows;
+  double* dst = work_a_.d(nxt.count());
+  FiberView v{A, s, F / s, uint32_t(I), s, s * I};
+  for (uint64_t c0 = 0; c0 < rows; c0 += 64) {
+    const uint32_t nc = uint32_t(std::min<uint64_t>(64, rows - c0));
+    const uint32_t ncp = pad_nc(nc);
+    double* Mt = mt_.d(I * ncp);
+    // Mt[i][c] = u[(c0 + c) + i*rows]  (u is rows x cols column-major)
+    CK(launch_pack(U + c0, rows, 1, uint32_t(I), nc, Mt, ncp, st_));
+    fc(v, Mt, ncp, nc, dst + c0 * s, s, s * rows, nullptr, nullptr, nullptr, nullptr, false);
+  }
+  CK(cudaMemcpyAsync(out, dst, nxt.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+double Engine::frobenius_norm(const double* a, uint64_t n) {
+  const double* A = upload(a, n, false, tensor_, nullptr);
+  double* sq = sq_part_.d(std::max(1, sumsq_partials_count(n)));
+  double* out = misc2_.d(1);
+  CK(launch_sumsq(A, n, sq, st_));
+  CK(launch_sum(sq, sumsq_partials_count(n), out, st_));
+  double h = 0.0;
+  CK(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  return std::sqrt(h);
+}
+
+double Engine::relative_error(const double* a, const double* b, uint64_t n) {
+  // tensor_ops.cpp:395-407: sqrt(sum (b-a)^2 / sum a^2), both sums on device
+  const double* A = upload(a, n, false, tensor_, nullptr);
+  double* B = work_a_.d(n);
+  CK(cudaMemcpyAsync(B, b, n * sizeof(double), cudaMemcpyHostToDevice, st_));
+  const int np = std::max(1, sumsq_partials_count(n));
+  double* sq = sq_part_.d(2 * size_t(np));
+  double* out = misc2_.d(2);
+  CK(launch_sumsq(A, n, sq, st_));
+  CK(launch_sum(sq, sumsq_partials_count(n), out, st_));
+  CK(launch_sumsq_diff(A, B, n, sq + np, st_));
+  CK(launch_sum(sq + np, sumsq_partials_count(n), out + 1, st_));
+  double h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  if (h[0] == 0.0) raise(3, "relative_error: reference tensor has zero norm");
+  return std::sqrt(h[1] / h[0]);
+}
+
+void Engine::reduced_qr(const double* a, uint64_t rows, uint64_t cols, double* q, double* r) {
+  if (rows < cols)
+    raise(2, "reduced_qr: need rows >= cols, got " + std::to_string(rows) + "x" + std::to_string(cols));
+  if (cols > kMaxRank) raise(12, "reduced_qr: more than 64 columns");
+  double* A = misc_.d(rows * cols);
+  CK(cudaMemcpyAsync(A, a, rows * cols * sizeof(double), cudaMemcpyHostToDevice, st_));
+  double* Q = l_.d(rows * cols);
+  double* R = rhat_.d(cols * cols);
+  CK(launch_qr(A, 0, rows, uint32_t(rows), uint32_t(cols), Q, R, nullptr, 0,
+               qr_work_.d(2 * rows * cols + cols), 0, status_d_, st_));
+  CK(cudaMemcpyAsync(q, Q, rows * cols * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(r, R, cols * cols * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Engine::gram(const double* a, uint64_t rows, uint64_t cols, double* out) {
+  if (cols > kMaxRank) raise(12, "gram: more than 64 columns");
+  double* A = misc_.d(rows * cols);
+  CK(cudaMemcpyAsync(A, a, rows * cols * sizeof(double), cudaMemcpyHostToDevice, st_));
+  double* gp = gram_part_.d(size_t(gram_partials_count(uint32_t(rows))) * cols * cols);
+  CK(launch_gram_partials(A, rows, uint32_t(rows), uint32_t(cols), gp, st_));
+  double* G = gl_.d(cols * cols);
+  double* ch = cholL_.d(cols * cols);
+  CK(launch_chol(gp, gram_partials_count(uint32_t(rows)), cols * cols, int(cols), uint32_t(cols), G, ch,
+                 &status_d_->pad, status_d_, st_));
+  CK(cudaMemcpyAsync(out, G, cols * cols * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Engine::uniform01(uint64_t seed, uint32_t stream, uint64_t n, double* out) {
+  double* d = s_.d(n);
+  gen_uniform(seed, stream, n, d);
+  CK(cudaMemcpy(out, d, n * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+}  // namespace tkg

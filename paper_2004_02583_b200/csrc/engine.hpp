@@ -1,0 +1,181 @@
+// Host orchestration of the B200 ALS-HOSVD path (C++ side of the C-ABI).
+//
+// One Engine owns a device, a stream, the mapped status block and grow-only
+// device workspaces. The control flow mirrors the reference exactly:
+//   als_low_rank  als.cpp:98-161   (stop rule, consistent pair, error mapping)
+//   t_hosvd       hosvd.cpp:74-125 (per-mode ALS, QR, ascending TTM core)
+//   st_hosvd      hosvd.cpp:127-191 (order, ALS, QR, R_hat R^T shrink)
+// while every pass over the tensor and every small solve runs on the GPU.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace tkg {
+
+struct Error : std::runtime_error {
+  int code;     // ErrorCategory + 1
+  int subtype;  // tkg_subtype
+  Error(int code_, int subtype_, const std::string& m) : std::runtime_error(m), code(code_), subtype(subtype_) {}
+};
+
+[[noreturn]] void raise(int subtype, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+
+struct Shape {
+  int N = 0;
+  uint64_t d[16] = {0};
+  uint64_t count() const;
+  uint64_t extent(int mode) const;  // validates, 1-based
+  uint64_t stride(int mode) const;
+  std::string str() const;
+};
+
+struct AlsCfg {
+  double eta = 1e-4;
+  int max_iters = 50;
+  uint64_t seed = 0;
+  const double* init = nullptr;  // host I x r col-major
+};
+
+struct ModeRep {
+  int mode = 0;
+  int iterations = 0;
+  int status = 1;
+  double achieved_eta = 0.0;
+  double seconds = 0.0;
+  std::vector<double> history;
+};
+
+struct DecompRep {
+  std::vector<ModeRep> per_mode;
+  double relative_residual = 0.0;
+  double seconds = 0.0;
+  double h2d_seconds = 0.0;
+  double d2h_seconds = 0.0;
+  double residual_seconds = 0.0;
+  uint64_t launches = 0;
+  uint64_t passes = 0;
+  uint64_t bytes = 0;
+};
+
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf();
+  void* ensure(size_t bytes);
+  double* d(size_t count) { return static_cast<double*>(ensure(count * sizeof(double))); }
+  uint64_t* u(size_t count) { return static_cast<uint64_t*>(ensure(count * sizeof(uint64_t))); }
+  void release();
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+enum KernelClass { kClsFC = 0, kClsFR = 1, kClsSmall = 2, kClsRng = 3 };
+
+class Engine {
+ public:
+  explicit Engine(int device);
+  ~Engine();
+
+  // Decomposition drivers; `a` is host (a_dev false) or device memory.
+  void t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
+               const AlsCfg& cfg, double* core, double* factors, DecompRep* rep);
+  void st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
+                const std::vector<int>* order, const AlsCfg& cfg, double* core, double* factors,
+                DecompRep* rep);
+  void als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,
+                    const AlsCfg& cfg, double* l_out, double* r_out, ModeRep* rep);
+  void als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r, uint64_t seed,
+                double* l_out);
+
+  // Primitives (host in/out).
+  void unfold_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r, double* out);
+  void unfold_t_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r, double* out);
+  void mode_n_product(const double* a, const Shape& sh, const double* u, uint64_t rows, uint64_t cols,
+                      int mode, double* out);
+  double frobenius_norm(const double* a, uint64_t n);
+  double relative_error(const double* a, const double* b, uint64_t n);
+  void reduced_qr(const double* a, uint64_t rows, uint64_t cols, double* q, double* r);
+  void gram(const double* a, uint64_t rows, uint64_t cols, double* out);
+  void uniform01(uint64_t seed, uint32_t stream, uint64_t n, double* out);
+
+  void set_profiling(bool on) { profiling_ = on; }
+  void kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], double flops[4]);
+  const std::string& device_name() const { return name_; }
+
+ private:
+  struct AlsOut {
+    ModeRep rep;
+    double norm = 0.0;
+  };
+  // Runs als_low_rank on a device-resident tensor; L (col-major I x r) is
+  // left in l_, R (F x r) in r_. sumsq_known: status_->sumsq already holds
+  // ||A||^2 of this tensor.
+  AlsOut run_als(const double* A, const Shape& sh, int mode, uint32_t r, const AlsCfg& cfg,
+                 bool sumsq_known);
+  void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out);
+  void fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
+          uint64_t os_c, uint64_t os_p, double* gram_part, double* sumsq_part,
+          const double* diff_ref, int* grid_used, bool count_pass);
+  uint32_t fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t nc, double* partial,
+              double* sumsq_part, bool count_pass, uint32_t* grid_used);
+  void sync();
+  const double* upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds);
+  double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                               const double* d_core, const std::vector<double*>& d_factors,
+                               double ref_sumsq);
+  void core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                  const std::vector<double*>& d_factors, double* d_core);
+  void begin_timed();
+  void count_launch(int n = 1) { launches_ += n; }
+  void record(int cls, cudaEvent_t a, cudaEvent_t b, double bytes, double flops);
+  std::pair<cudaEvent_t, cudaEvent_t> ev_pair();
+
+  int device_;
+  int sms_;
+  std::string name_;
+  cudaStream_t st_;
+  DevStatus* status_h_ = nullptr;
+  DevStatus* status_d_ = nullptr;
+
+  DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
+  DBuf fr_part_, fc_gram_, gram_part_, sq_part_, qr_work_, q_, rhat_, rhatT_;
+  DBuf y_seq_, states_, misc_, misc2_;
+  std::vector<DBuf*> factor_bufs_;
+  std::map<std::pair<uint64_t, int>, DBuf*> jump_cache_;
+
+  bool profiling_ = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double bytes, flops;
+  };
+  std::vector<Rec> recs_;
+  std::vector<cudaEvent_t> ev_pool_;
+  double stat_ms_[4] = {0, 0, 0, 0};
+  uint64_t stat_launch_[4] = {0, 0, 0, 0};
+  double stat_bytes_[4] = {0, 0, 0, 0};
+  double stat_flops_[4] = {0, 0, 0, 0};
+
+  uint64_t launches_ = 0;
+  uint64_t passes_ = 0;
+  uint64_t bytes_ = 0;
+};
+
+std::vector<int> select_order(const std::vector<uint64_t>& ranks);
+void validate_truncation(const Shape& sh, const std::vector<uint64_t>& ranks);
+
+}  // namespace tkg

@@ -1,0 +1,251 @@
+// Host side of the MT19937-64 jump-ahead (see mt_jump.hpp).
+#include "mt_jump.hpp"
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <random>
+
+namespace tkg {
+
+namespace {
+
+inline uint64_t untemper(uint64_t y) {
+  // inverse of the std::mt19937_64 tempering ([rand.eng.mers]:
+  // u=29,d=0x5555..., s=17,b=0x71D67FFFEDA60000, t=37,c=0xFFF7EEE000000000, l=43)
+  y ^= y >> 43;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  // y ^= (y << 17) & b : invert by iterating (17-bit steps cover 64 bits in 4 rounds)
+  {
+    uint64_t x = y;
+    for (int k = 0; k < 4; ++k) x = y ^ ((x << 17) & 0x71D67FFFEDA60000ull);
+    y = x;
+  }
+  {
+    uint64_t x = y;
+    for (int k = 0; k < 3; ++k) x = y ^ ((x >> 29) & 0x5555555555555555ull);
+    y = x;
+  }
+  return y;
+}
+
+// ---- GF(2)[x] arithmetic on little-endian word arrays ----------------------
+inline void clmul64(uint64_t a, uint64_t b, uint64_t& lo, uint64_t& hi) {
+  __m128i va = _mm_set_epi64x(0, static_cast<long long>(a));
+  __m128i vb = _mm_set_epi64x(0, static_cast<long long>(b));
+  __m128i r = _mm_clmulepi64_si128(va, vb, 0x00);
+  lo = static_cast<uint64_t>(_mm_cvtsi128_si64(r));
+  hi = static_cast<uint64_t>(_mm_extract_epi64(r, 1));
+}
+
+// out[0 .. na+nb) = a * b
+void poly_mul(const uint64_t* a, int na, const uint64_t* b, int nb, uint64_t* out) {
+  std::memset(out, 0, sizeof(uint64_t) * (na + nb));
+  for (int i = 0; i < na; ++i) {
+    const uint64_t ai = a[i];
+    if (!ai) continue;
+    for (int j = 0; j < nb; ++j) {
+      uint64_t lo, hi;
+      clmul64(ai, b[j], lo, hi);
+      out[i + j] ^= lo;
+      out[i + j + 1] ^= hi;
+    }
+  }
+}
+
+// out[0..nw) = a >> shift (bits), a has na words
+void poly_shr(const uint64_t* a, int na, int shift, uint64_t* out, int nw) {
+  const int ws = shift / 64, bs = shift % 64;
+  for (int k = 0; k < nw; ++k) {
+    const int s = k + ws;
+    uint64_t v = s < na ? a[s] >> bs : 0;
+    if (bs && s + 1 < na) v |= a[s + 1] << (64 - bs);
+    out[k] = v;
+  }
+}
+
+int poly_deg(const uint64_t* a, int n) {
+  for (int k = n - 1; k >= 0; --k)
+    if (a[k]) return k * 64 + 63 - __builtin_clzll(a[k]);
+  return -1;
+}
+
+struct Field {
+  std::vector<uint64_t> P;   // kPolyWords+1 words, degree D
+  std::vector<uint64_t> mu;  // floor(x^{2D} / P), degree D
+};
+
+void mask_low(uint64_t* a, int nw, int bits) {
+  for (int k = 0; k < nw; ++k) {
+    const int lo = k * 64;
+    if (lo >= bits) a[k] = 0;
+    else if (lo + 64 > bits) a[k] &= (1ull << (bits - lo)) - 1;
+  }
+}
+
+const Field& field() {
+  static Field f;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    f.P = mt_charpoly();
+    // mu = floor(x^{2D} / P) by long division.
+    const int D = kMtDeg;
+    const int nw = (2 * D) / 64 + 2;
+    std::vector<uint64_t> rem(nw, 0);
+    rem[(2 * D) / 64] = 1ull << ((2 * D) % 64);
+    std::vector<uint64_t> q(nw, 0);
+    for (int bit = 2 * D; bit >= D; --bit) {
+      if (!((rem[bit / 64] >> (bit % 64)) & 1)) continue;
+      const int sh = bit - D;
+      q[sh / 64] |= 1ull << (sh % 64);
+      // rem ^= P << sh
+      const int ws = sh / 64, bs = sh % 64;
+      for (int k = 0; k <= kPolyWords; ++k) {
+        const uint64_t w = f.P[k];
+        if (!w) continue;
+        rem[k + ws] ^= w << bs;
+        if (bs && k + ws + 1 < nw) rem[k + ws + 1] ^= w >> (64 - bs);
+      }
+    }
+    f.mu.assign(q.begin(), q.begin() + kPolyWords + 1);
+  });
+  return f;
+}
+
+// r = a*b mod P for a, b of degree < D (kPolyWords words each).
+void mulmod(const uint64_t* a, const uint64_t* b, uint64_t* r) {
+  const Field& f = field();
+  const int D = kMtDeg;
+  const int W = kPolyWords;
+  std::vector<uint64_t> c(2 * W + 2), chi(W + 1), t(2 * W + 4), qq(W + 1), qp(2 * W + 4);
+  poly_mul(a, W, b, W, c.data());
+  poly_shr(c.data(), 2 * W, D, chi.data(), W + 1);          // c >> D
+  poly_mul(chi.data(), W + 1, f.mu.data(), W + 1, t.data());  // (c>>D) * mu
+  poly_shr(t.data(), 2 * W + 2, D, qq.data(), W + 1);       // q
+  poly_mul(qq.data(), W + 1, f.P.data(), W + 1, qp.data());   // q * P
+  for (int k = 0; k < W; ++k) r[k] = c[k] ^ qp[k];
+  mask_low(r, W, D);
+}
+
+}  // namespace
+
+void mt_raw_sequence(uint64_t seed, uint32_t stream, uint64_t* y, int n) {
+  std::seed_seq seq{static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), stream};
+  std::mt19937_64 eng(seq);
+  for (int k = 0; k < n; ++k) y[k] = untemper(eng());
+}
+
+const std::vector<uint64_t>& mt_charpoly() {
+  static std::vector<uint64_t> P;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // Berlekamp-Massey on bit 0 of the raw sequence (any nonzero bit plane
+    // has the full characteristic polynomial as its minimal polynomial,
+    // because P is primitive).
+    const int N = 2 * kMtDeg + 64;
+    std::vector<uint64_t> y(N);
+    mt_raw_sequence(5489, 0, y.data(), N);
+    // R = bit plane reversed: R[j] = s_{N-1-j}; then s_{n-i} = R[N-1-n+i].
+    const int RW = N / 64 + 4;
+    std::vector<uint64_t> R(RW, 0);
+    for (int k = 0; k < N; ++k)
+      if (y[k] & 1) {
+        const int j = N - 1 - k;
+        R[j / 64] |= 1ull << (j % 64);
+      }
+    auto bits_at = [&](int off) -> uint64_t {  // R[off .. off+64)
+      const int w = off / 64, b = off % 64;
+      uint64_t v = w < RW ? R[w] >> b : 0;
+      if (b && w + 1 < RW) v |= R[w + 1] << (64 - b);
+      return v;
+    };
+    const int W = kPolyWords + 2;
+    std::vector<uint64_t> C(W, 0), B(W, 0), T(W);
+    C[0] = 1;
+    B[0] = 1;
+    int L = 0, m = 1;
+    for (int n = 0; n < N; ++n) {
+      // d = sum_{i=0..L} C_i s_{n-i} (C_0 = 1)
+      const int off = N - 1 - n;
+      uint64_t acc = 0;
+      for (int k = 0; k <= L / 64; ++k) acc ^= C[k] & bits_at(off + 64 * k);
+      const int d = __builtin_popcountll(acc) & 1;
+      if (!d) {
+        ++m;
+        continue;
+      }
+      T = C;
+      // C ^= B << m
+      const int ws = m / 64, bs = m % 64;
+      for (int k = 0; k + ws < W; ++k) {
+        C[k + ws] ^= B[k] << bs;
+        if (bs && k + ws + 1 < W) C[k + ws + 1] ^= B[k] >> (64 - bs);
+      }
+      if (2 * L <= n) {
+        L = n + 1 - L;
+        B = T;
+        m = 1;
+      } else {
+        ++m;
+      }
+    }
+    // Characteristic polynomial = reciprocal of the connection polynomial.
+    P.assign(kPolyWords + 1, 0);
+    for (int i = 0; i <= L; ++i) {
+      if ((C[i / 64] >> (i % 64)) & 1) {
+        const int e = L - i;
+        P[e / 64] |= 1ull << (e % 64);
+      }
+    }
+    if (L != kMtDeg) P.clear();  // signalled to callers (mt_plan checks)
+  });
+  return P;
+}
+
+std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
+  const int W = kPolyWords;
+  std::vector<uint64_t> out(size_t(count) * W, 0);
+  if (count <= 0) return out;
+  // x^J mod P by square-and-multiply.
+  std::vector<uint64_t> base(W, 0), acc(W, 0), tmp(W);
+  base[0] = 2;  // x
+  acc[0] = 1;
+  uint64_t e = J;
+  while (e) {
+    if (e & 1) {
+      mulmod(acc.data(), base.data(), tmp.data());
+      acc = tmp;
+    }
+    e >>= 1;
+    if (e) {
+      mulmod(base.data(), base.data(), tmp.data());
+      base = tmp;
+    }
+  }
+  // out[c] = (x^J)^c
+  out[0] = 1;
+  std::vector<uint64_t> cur(W, 0);
+  cur[0] = 1;
+  for (int c = 1; c < count; ++c) {
+    mulmod(cur.data(), acc.data(), tmp.data());
+    cur = tmp;
+    std::copy(cur.begin(), cur.end(), out.begin() + size_t(c) * W);
+  }
+  return out;
+}
+
+MtPlan mt_plan(uint64_t total) {
+  MtPlan p;
+  p.total = total;
+  const uint64_t per = 262144;
+  uint64_t C = (total + per - 1) / per;
+  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 592));
+  p.C = static_cast<int>(C);
+  p.J = (total + C - 1) / C;
+  if (p.J == 0) p.J = 1;
+  return p;
+}
+
+}  // namespace tkg

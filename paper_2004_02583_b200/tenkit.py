@@ -1,0 +1,494 @@
+"""Python mirror of the reference tenkit decomposition API on the B200 path.
+
+Names, argument meaning and error behaviour follow the reference headers:
+  t_hosvd / st_hosvd / select_order   include/tenkit/hosvd.hpp:55-76
+  als_low_rank / als_init             include/tenkit/als.hpp:46-71
+  unfold_times / unfold_t_times / mode_n_product / frobenius_norm /
+  relative_error                      include/tenkit/tensor_ops.hpp:22-55
+  reduced_qr / gram                   include/tenkit/kernels.hpp:23, matrix.hpp:49
+  error classes                       include/tenkit/errors.hpp:10-77
+Tensors are numpy arrays interpreted in column-major (Fortran) order, as
+tenkit's DenseTensor (tensor.hpp:10-11), or `DeviceTensor` views of HBM
+(e.g. a torch CUDA tensor holding the column-major data). Every call goes
+through libtenkit_b200.so; there is no CPU implementation behind it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+# ---- errors (errors.hpp:10-77) -------------------------------------------------
+USAGE, IO, NUMERICAL = 0, 1, 2
+
+
+class Error(RuntimeError):
+    category = USAGE
+
+    def __init__(self, message: str, code: int = 0, subtype: int = 0):
+        super().__init__(message)
+        self.code = code
+        self.subtype = subtype
+
+
+class InvalidModeError(Error):
+    category = USAGE
+
+
+class DimensionMismatchError(Error):
+    category = USAGE
+
+
+class ZeroReferenceError(Error):
+    category = USAGE
+
+
+class RankTooLargeError(Error):
+    category = NUMERICAL
+
+
+class SingularGramError(Error):
+    category = NUMERICAL
+
+
+class DegenerateInitError(Error):
+    category = NUMERICAL
+
+
+class NoConvergenceError(Error):
+    category = NUMERICAL
+
+
+class IoError(Error):
+    category = IO
+
+
+class FormatError(Error):
+    category = IO
+
+
+class DeviceError(Error):
+    """CUDA runtime failure (no device, launch error). Category io."""
+    category = IO
+
+
+class UnsupportedError(Error):
+    """Outside this build's limits (e.g. rank > 64). Category usage."""
+    category = USAGE
+
+
+_SUBTYPE = {1: InvalidModeError, 2: DimensionMismatchError, 3: ZeroReferenceError,
+            4: RankTooLargeError, 5: SingularGramError, 6: DegenerateInitError,
+            7: NoConvergenceError, 8: IoError, 9: FormatError, 11: DeviceError,
+            12: UnsupportedError}
+
+
+def _raise(rc: int, err: _lib.TkgError):
+    if rc != 0:
+        cls = _SUBTYPE.get(err.subtype, Error)
+        raise cls(err.message.decode(errors="replace"), rc, err.subtype)
+
+
+# ---- value types (als.hpp:17-38, hosvd.hpp:19-44, tensor_ops.hpp:59-67) -------
+@dataclass
+class AlsConfig:
+    eta: float = 1e-4
+    max_iters: int = 50
+    seed: int = 0
+    init: Optional[np.ndarray] = None
+
+
+@dataclass
+class FactorEngine:
+    kind: str = "als"
+    als: AlsConfig = field(default_factory=AlsConfig)
+
+    @staticmethod
+    def with_als(cfg: AlsConfig) -> "FactorEngine":
+        return FactorEngine("als", cfg)
+
+
+@dataclass
+class Truncation:
+    ranks: List[int]
+
+
+@dataclass
+class ModeOrder:
+    order: List[int]
+
+
+@dataclass
+class AlsReport:
+    iterations: int = 0
+    residual_history: List[float] = field(default_factory=list)
+    status: str = "converged"  # or "max_iters_reached"
+    achieved_eta: float = 0.0
+
+
+@dataclass
+class ModeReport:
+    mode: int = 0
+    seconds: float = 0.0
+    als: Optional[AlsReport] = None
+
+
+@dataclass
+class DecompositionReport:
+    per_mode: List[ModeReport] = field(default_factory=list)
+    relative_residual: float = 0.0
+    seconds: float = 0.0
+    # device accounting (not in the reference struct)
+    h2d_seconds: float = 0.0
+    d2h_seconds: float = 0.0
+    residual_seconds: float = 0.0
+    kernel_launches: int = 0
+    tensor_passes: int = 0
+    algorithmic_bytes: int = 0
+
+
+@dataclass
+class TuckerTensor:
+    core: np.ndarray
+    factors: List[np.ndarray]
+    origin_shape: tuple
+
+
+@dataclass
+class DeviceTensor:
+    """A column-major fp64 tensor already resident in HBM."""
+    ptr: int
+    dims: Sequence[int]
+
+    @staticmethod
+    def from_torch(t, dims: Sequence[int]) -> "DeviceTensor":
+        """`t`: contiguous CUDA float64 tensor holding the column-major data."""
+        assert t.is_cuda and t.dtype.itemsize == 8 and t.is_contiguous()
+        assert t.numel() == int(np.prod(dims))
+        return DeviceTensor(int(t.data_ptr()), tuple(int(d) for d in dims))
+
+
+def _host(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _flat_ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _mode_report(m: _lib.TkgModeReport) -> ModeReport:
+    hist = [m.residual_history[k] for k in range(m.history_len)]
+    als = AlsReport(m.iterations, hist, "converged" if m.status == 0 else "max_iters_reached",
+                    m.achieved_eta)
+    return ModeReport(m.mode, m.seconds, als)
+
+
+def _decomp_report(r: _lib.TkgReport) -> DecompositionReport:
+    return DecompositionReport([_mode_report(r.per_mode[k]) for k in range(r.n_modes)],
+                               r.relative_residual, r.seconds, r.h2d_seconds, r.d2h_seconds,
+                               r.residual_seconds, int(r.kernel_launches), int(r.tensor_passes),
+                               int(r.algorithmic_bytes))
+
+
+def _cfg(c: AlsConfig, keep):
+    init = None
+    if c.init is not None:
+        arr = _host(c.init)
+        keep.append(arr)
+        init = _flat_ptr(arr)
+    return _lib.TkgAlsConfig(float(c.eta), int(c.max_iters), int(c.seed) & (2**64 - 1), init)
+
+
+class Context:
+    """One device + stream + workspaces (tkg_ctx). Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        self._l = _lib.lib()
+        self._ctx = C.c_void_p()
+        err = _lib.TkgError()
+        _raise(self._l.tkg_create(C.byref(self._ctx), int(device), C.byref(err)), err)
+
+    def close(self):
+        if self._ctx:
+            self._l.tkg_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- input marshalling --------------------------------------------------------
+    @staticmethod
+    def _tensor(t):
+        if isinstance(t, DeviceTensor):
+            return C.c_void_p(t.ptr), 1, tuple(t.dims), None
+        a = _host(t)
+        if a.ndim == 0:
+            a = a.reshape(1)
+        return C.c_void_p(a.ctypes.data), 0, a.shape, a
+
+    # -- decomposition drivers ----------------------------------------------------
+    def t_hosvd(self, t, trunc: Truncation, engine: FactorEngine,
+                want_singular_vectors: bool = False):
+        ptr, on_dev, dims, keep = self._tensor(t)
+        ranks = list(trunc.ranks)
+        n = len(dims)
+        if len(ranks) != n:  # Truncation::validate (shape.cpp:57-60)
+            raise DimensionMismatchError(f"truncation lists {len(ranks)} ranks for an order-{n} tensor")
+        core = np.zeros(int(np.prod(ranks)))
+        fac = np.zeros(sum(int(dims[k]) * int(ranks[k]) for k in range(n)))
+        rep = _lib.TkgReport()
+        err = _lib.TkgError()
+        hold = []
+        cfg = _cfg(engine.als, hold)
+        rc = self._l.tkg_t_hosvd(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks),
+                                 C.byref(cfg), int(bool(want_singular_vectors)), _flat_ptr(core),
+                                 _flat_ptr(fac), C.byref(rep), C.byref(err))
+        _raise(rc, err)
+        return self._tucker(core, fac, dims, ranks), _decomp_report(rep)
+
+    def st_hosvd(self, t, trunc: Truncation, order: Optional[ModeOrder], engine: FactorEngine):
+        ptr, on_dev, dims, keep = self._tensor(t)
+        ranks = list(trunc.ranks)
+        n = len(dims)
+        if len(ranks) != n:
+            raise DimensionMismatchError(f"truncation lists {len(ranks)} ranks for an order-{n} tensor")
+        core = np.zeros(int(np.prod(ranks)))
+        fac = np.zeros(sum(int(dims[k]) * int(ranks[k]) for k in range(n)))
+        rep = _lib.TkgReport()
+        err = _lib.TkgError()
+        hold = []
+        cfg = _cfg(engine.als, hold)
+        mo = None
+        if order is not None:
+            if len(order.order) != n:
+                raise InvalidModeError(f"st_hosvd: order has {len(order.order)} entries for an order-{n} tensor")
+            mo = _lib.u32([max(0, int(m)) for m in order.order])
+        rc = self._l.tkg_st_hosvd(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks), mo,
+                                  C.byref(cfg), _flat_ptr(core), _flat_ptr(fac), C.byref(rep),
+                                  C.byref(err))
+        _raise(rc, err)
+        return self._tucker(core, fac, dims, ranks), _decomp_report(rep)
+
+    @staticmethod
+    def _tucker(core, fac, dims, ranks):
+        factors = []
+        ofs = 0
+        for k in range(len(dims)):
+            sz = int(dims[k]) * int(ranks[k])
+            factors.append(fac[ofs:ofs + sz].reshape((dims[k], ranks[k]), order="F").copy())
+            ofs += sz
+        return TuckerTensor(core.reshape(tuple(ranks), order="F"), factors, tuple(dims))
+
+    def als_low_rank(self, t, mode: int, r: int, cfg: AlsConfig):
+        ptr, on_dev, dims, keep = self._tensor(t)
+        n = len(dims)
+        ext = dims[mode - 1] if 1 <= mode <= n else 1
+        fibers = int(np.prod(dims)) // max(1, ext)
+        l = np.zeros((ext, max(1, r)), order="F")
+        rr = np.zeros((fibers, max(1, r)), order="F")
+        rep = _lib.TkgModeReport()
+        err = _lib.TkgError()
+        hold = []
+        c = _cfg(cfg, hold)
+        if cfg.init is not None:
+            ini = _host(cfg.init)
+            if ini.shape != (ext, r):
+                raise DimensionMismatchError(
+                    f"als_low_rank: init is {ini.shape[0]}x{ini.shape[1] if ini.ndim > 1 else 1}, "
+                    f"mode {mode} needs {ext}x{r}")
+        rc = self._l.tkg_als_low_rank(self._ctx, ptr, on_dev, n, _lib.u64(dims), int(mode), int(r),
+                                      C.byref(c), _flat_ptr(l), _flat_ptr(rr), C.byref(rep),
+                                      C.byref(err))
+        _raise(rc, err)
+        m = _mode_report(rep)
+        return (l, rr), m.als
+
+    def als_init(self, t, mode: int, r: int, seed: int):
+        ptr, on_dev, dims, keep = self._tensor(t)
+        n = len(dims)
+        ext = dims[mode - 1] if 1 <= mode <= n else 1
+        l = np.zeros((ext, max(1, r)), order="F")
+        err = _lib.TkgError()
+        rc = self._l.tkg_als_init(self._ctx, ptr, on_dev, n, _lib.u64(dims), int(mode), int(r),
+                                  int(seed) & (2**64 - 1), _flat_ptr(l), C.byref(err))
+        _raise(rc, err)
+        return l
+
+    # -- primitives ---------------------------------------------------------------
+    def unfold_times(self, t, mode: int, m):
+        a = _host(t)
+        m = _host(m)
+        ext = a.shape[mode - 1] if 1 <= mode <= a.ndim else 1
+        out = np.zeros((ext, m.shape[1]), order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_unfold_times(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape), int(mode),
+                                        _flat_ptr(m), m.shape[1], _flat_ptr(out), C.byref(err)), err)
+        return out
+
+    def unfold_t_times(self, t, mode: int, m):
+        a = _host(t)
+        m = _host(m)
+        ext = a.shape[mode - 1] if 1 <= mode <= a.ndim else 1
+        out = np.zeros((a.size // max(1, ext), m.shape[1]), order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_unfold_t_times(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape),
+                                          int(mode), _flat_ptr(m), m.shape[1], _flat_ptr(out),
+                                          C.byref(err)), err)
+        return out
+
+    def mode_n_product(self, t, u, mode: int):
+        a = _host(t)
+        u = _host(u)
+        dims = list(a.shape)
+        if 1 <= mode <= a.ndim:
+            dims[mode - 1] = u.shape[0]
+        out = np.zeros(dims, order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_mode_n_product(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape),
+                                          _flat_ptr(u), u.shape[0], u.shape[1], int(mode),
+                                          _flat_ptr(out), C.byref(err)), err)
+        return out
+
+    def frobenius_norm(self, t) -> float:
+        a = _host(t)
+        out = C.c_double(0)
+        err = _lib.TkgError()
+        _raise(self._l.tkg_frobenius_norm(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape),
+                                          C.byref(out), C.byref(err)), err)
+        return out.value
+
+    def relative_error(self, a, b) -> float:
+        a = _host(a)
+        b = _host(b)
+        if a.shape != b.shape:
+            raise DimensionMismatchError(f"relative_error: shapes {a.shape} vs {b.shape}")
+        out = C.c_double(0)
+        err = _lib.TkgError()
+        _raise(self._l.tkg_relative_error(self._ctx, _flat_ptr(a), _flat_ptr(b), a.ndim,
+                                          _lib.u64(a.shape), C.byref(out), C.byref(err)), err)
+        return out.value
+
+    def reduced_qr(self, a):
+        a = _host(a)
+        m, n = a.shape
+        q = np.zeros((m, n), order="F")
+        r = np.zeros((n, n), order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_reduced_qr(self._ctx, _flat_ptr(a), m, n, _flat_ptr(q), _flat_ptr(r),
+                                      C.byref(err)), err)
+        return q, r
+
+    def gram(self, a):
+        a = _host(a)
+        g = np.zeros((a.shape[1], a.shape[1]), order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_gram(self._ctx, _flat_ptr(a), a.shape[0], a.shape[1], _flat_ptr(g),
+                                C.byref(err)), err)
+        return g
+
+    def uniform01(self, seed: int, stream: int, n: int):
+        out = np.zeros(n)
+        err = _lib.TkgError()
+        _raise(self._l.tkg_uniform01(self._ctx, int(seed) & (2**64 - 1), int(stream), int(n),
+                                     _flat_ptr(out), C.byref(err)), err)
+        return out
+
+    def set_profiling(self, on: bool):
+        self._l.tkg_set_profiling(self._ctx, int(bool(on)))
+
+    def kernel_stats(self):
+        st = _lib.TkgKernelStats()
+        self._l.tkg_get_kernel_stats(self._ctx, C.byref(st))
+        names = ["fc", "fr", "small", "rng"]
+        return {names[k]: {"ms": st.ms[k], "launches": int(st.launches[k]), "bytes": st.bytes[k],
+                           "flops": st.flops[k]} for k in range(4)}
+
+
+def select_order(trunc: Truncation, shape: Sequence[int]) -> ModeOrder:
+    """hosvd.cpp:54-63 — stable ascending-rank order."""
+    l = _lib.lib()
+    n = len(shape)
+    out = (C.c_uint32 * max(1, n))()
+    err = _lib.TkgError()
+    ranks = list(trunc.ranks)
+    if len(ranks) != n:
+        raise DimensionMismatchError(f"truncation lists {len(ranks)} ranks for an order-{n} tensor")
+    _raise(l.tkg_select_order(n, _lib.u64(shape), _lib.u64(ranks), out, C.byref(err)), err)
+    return ModeOrder([int(out[k]) for k in range(n)])
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def t_hosvd(t, trunc, engine, want_singular_vectors=False):
+    return default_context().t_hosvd(t, trunc, engine, want_singular_vectors)
+
+
+def st_hosvd(t, trunc, order, engine):
+    return default_context().st_hosvd(t, trunc, order, engine)
+
+
+def als_low_rank(t, mode, r, cfg):
+    return default_context().als_low_rank(t, mode, r, cfg)
+
+
+def als_init(t, mode, r, seed):
+    return default_context().als_init(t, mode, r, seed)
+
+
+def unfold_times(t, mode, m):
+    return default_context().unfold_times(t, mode, m)
+
+
+def unfold_t_times(t, mode, m):
+    return default_context().unfold_t_times(t, mode, m)
+
+
+def mode_n_product(t, u, mode):
+    return default_context().mode_n_product(t, u, mode)
+
+
+def frobenius_norm(t):
+    return default_context().frobenius_norm(t)
+
+
+def relative_error(a, b):
+    return default_context().relative_error(a, b)
+
+
+def reduced_qr(a):
+    return default_context().reduced_qr(a)
+
+
+def gram(a):
+    return default_context().gram(a)
+
+
+def synth_tucker(dims, ranks, alpha: float, nu: float, seed: int, out: Optional[np.ndarray] = None):
+    """Seeded synthetic Tucker tensor — input synthesis for
+    benches/tests, host C++/OpenMP (csrc/synth.cpp). Returns a flat
+    column-major array (or fills `out`)."""
+    n = int(np.prod(dims))
+    if out is None:
+        out = np.empty(n)
+    assert out.size == n and out.dtype == np.float64
+    rc = _lib.synth_lib().tkg_synth_tucker(len(dims), _lib.u64(dims), _lib.u64(ranks), float(alpha),
+                                            float(nu), int(seed),
+                                            out.ctypes.data_as(C.POINTER(C.c_double)))
+    if rc != 0:
+        raise DimensionMismatchError("synth_tucker: invalid dims/ranks")
+    return out
