@@ -172,6 +172,13 @@ typedef struct tkg_kernel_stats {
 int tkg_set_profiling(tkg_ctx* ctx, int on);
 int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out);
 
+/* Device-side timing on the context's stream (CUDA events): start, then
+ * stop returns the elapsed milliseconds (synchronizes). */
+int tkg_timer_start(tkg_ctx* ctx);
+int tkg_timer_stop(tkg_ctx* ctx, double* ms);
+/* Overwrite a buffer larger than L2 on the context's stream (bench hygiene). */
+int tkg_flush_l2(tkg_ctx* ctx);
+
 /* Library identification (build string, device name). */
 const char* tkg_version(void);
 

@@ -85,6 +85,9 @@ SIGNATURES = [
                                 C.POINTER(TkgError)]),
     ("tkg_set_profiling", C.c_int, [_ctxp, C.c_int]),
     ("tkg_get_kernel_stats", C.c_int, [_ctxp, C.POINTER(TkgKernelStats)]),
+    ("tkg_timer_start", C.c_int, [_ctxp]),
+    ("tkg_timer_stop", C.c_int, [_ctxp, _dp]),
+    ("tkg_flush_l2", C.c_int, [_ctxp]),
 ]
 
 _lock = threading.Lock()

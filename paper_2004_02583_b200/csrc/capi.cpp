@@ -260,4 +260,19 @@ int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out) {
   });
 }
 
+int tkg_timer_start(tkg_ctx* ctx) {
+  tkg_error err;
+  return guarded(&err, [&] { eng(ctx).timer_start(); });
+}
+
+int tkg_timer_stop(tkg_ctx* ctx, double* ms) {
+  tkg_error err;
+  return guarded(&err, [&] { *ms = eng(ctx).timer_stop(); });
+}
+
+int tkg_flush_l2(tkg_ctx* ctx) {
+  tkg_error err;
+  return guarded(&err, [&] { eng(ctx).flush_l2(); });
+}
+
 }  // extern "C"

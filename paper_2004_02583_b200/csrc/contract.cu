@@ -481,7 +481,10 @@ cudaError_t fc_launch_t(const FcArgs& a, int grid, cudaStream_t st) {
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Cfg::kSmem));
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
     attr_set = true;
   }
   k<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a);
@@ -520,7 +523,10 @@ cudaError_t fr_launch_t(const FrArgs& a, int wgi, int wgj, cudaStream_t st) {
   const size_t red = sizeof(double) * size_t(wgj) * rows_cta * NC;
   const size_t smem = std::max(ring, red);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
   const int grid = int(a.ranges * a.igroups);
   k<<<grid, 32 * wgi * wgj, smem, st>>>(a, wgi, wgj);
   return cudaGetLastError();
@@ -542,9 +548,12 @@ void fr_shape(uint32_t K, uint32_t ncp, int* wi_out, int* wgi, int* wgj) {
   const int tiles = int((K + wi - 1) / wi);
   const int igroups = (tiles + 7) / 8;
   const int g = (tiles + igroups - 1) / igroups;
+  // keep the M ring (kStages x 16*wgj rows x ld doubles) within 128 KB
+  const size_t per_wgj = sizeof(double) * kStages * kSub * size_t(smem_ld(int(ncp)));
+  const int cap = int(std::max<size_t>(1, (128u << 10) / per_wgj));
   *wi_out = wi;
   *wgi = g;
-  *wgj = std::max(1, 8 / g);
+  *wgj = std::max(1, std::min(8 / g, cap));
 }
 
 }  // namespace

@@ -121,11 +121,34 @@ Engine::~Engine() {
     cudaEventDestroy(r.b);
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
+  if (t0_) cudaEventDestroy(t0_);
+  if (t1_) cudaEventDestroy(t1_);
   if (status_h_) cudaFreeHost(status_h_);
   cudaStreamDestroy(st_);
 }
 
 void Engine::sync() { CK(cudaStreamSynchronize(st_)); }
+
+void Engine::timer_start() {
+  if (!t0_) {
+    CK(cudaEventCreate(&t0_));
+    CK(cudaEventCreate(&t1_));
+  }
+  CK(cudaEventRecord(t0_, st_));
+}
+
+double Engine::timer_stop() {
+  CK(cudaEventRecord(t1_, st_));
+  CK(cudaEventSynchronize(t1_));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, t0_, t1_));
+  return ms;
+}
+
+void Engine::flush_l2() {
+  const size_t bytes = size_t(512) << 20;  // 4x the 126 MB L2
+  CK(cudaMemsetAsync(flush_.ensure(bytes), 0, bytes, st_));
+}
 
 std::pair<cudaEvent_t, cudaEvent_t> Engine::ev_pair() {
   cudaEvent_t a, b;

@@ -113,6 +113,9 @@ class Engine {
   void uniform01(uint64_t seed, uint32_t stream, uint64_t n, double* out);
 
   void set_profiling(bool on) { profiling_ = on; }
+  void timer_start();
+  double timer_stop();
+  void flush_l2();
   void kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], double flops[4]);
   const std::string& device_name() const { return name_; }
 
@@ -153,7 +156,8 @@ class Engine {
 
   DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
   DBuf fr_part_, fc_gram_, gram_part_, sq_part_, qr_work_, q_, rhat_, rhatT_;
-  DBuf y_seq_, states_, misc_, misc2_;
+  DBuf y_seq_, states_, misc_, misc2_, flush_;
+  cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   std::vector<DBuf*> factor_bufs_;
   std::map<std::pair<uint64_t, int>, DBuf*> jump_cache_;
 

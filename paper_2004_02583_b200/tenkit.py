@@ -400,6 +400,17 @@ class Context:
                                      _flat_ptr(out), C.byref(err)), err)
         return out
 
+    def timer_start(self):
+        self._l.tkg_timer_start(self._ctx)
+
+    def timer_stop(self) -> float:
+        ms = C.c_double(0)
+        self._l.tkg_timer_stop(self._ctx, C.byref(ms))
+        return ms.value
+
+    def flush_l2(self):
+        self._l.tkg_flush_l2(self._ctx)
+
     def set_profiling(self, on: bool):
         self._l.tkg_set_profiling(self._ctx, int(bool(on)))
 
