@@ -88,6 +88,8 @@ SIGNATURES = [
     ("tkg_timer_start", C.c_int, [_ctxp]),
     ("tkg_timer_stop", C.c_int, [_ctxp, _dp]),
     ("tkg_flush_l2", C.c_int, [_ctxp]),
+    ("tkg_bench_contractions", C.c_int, [_ctxp, C.c_void_p, C.c_int32, _u64p, C.c_uint32,
+                                         C.c_uint32, C.c_int32, _dp, C.POINTER(TkgError)]),
 ]
 
 _lock = threading.Lock()

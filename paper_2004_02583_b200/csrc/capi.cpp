@@ -260,6 +260,14 @@ int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out) {
   });
 }
 
+int tkg_bench_contractions(tkg_ctx* ctx, const double* d_a, int32_t order, const uint64_t* dims,
+                           uint32_t mode, uint32_t r, int32_t reps, double* out_ms, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).bench_contractions(d_a, sh, int(mode), r, reps < 1 ? 1 : reps, out_ms);
+  });
+}
+
 int tkg_timer_start(tkg_ctx* ctx) {
   tkg_error err;
   return guarded(&err, [&] { eng(ctx).timer_start(); });

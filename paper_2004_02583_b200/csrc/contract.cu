@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256, 1) fc_kernel(FcArgs a) {
       if (!mok[m]) j = 0;
       const uint64_t p = j / v.s;
       const uint64_t jl = j - p * v.s;
-      ob[m] = int64_t(jl + p * a.os_p);
+      ob[m] = int64_t(jl * a.os_j + p * a.os_p);
       const int g = MODE == kPair ? (m >> 1) : m;
       if (MODE != kPair || (m & 1) == 0) {
         ib[g] = int64_t(jl + p * v.is_p);
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256) fr_kernel(FrArgs a, int wgi, int wgj) {
       const uint64_t j = jb + jl;
       double* d = dst + srow * Cfg::kLd + c;
       if (j < f1 && c < int(a.nc)) {
-        cp_async8(d, a.m + j + uint64_t(c) * a.ldm);
+        cp_async8(d, a.m + j * a.mj + uint64_t(c) * a.mc);
       } else {
         *d = 0.0;
       }

@@ -25,7 +25,8 @@ struct FcArgs {
   const double* mt;       // [K][ldmt] i-major contraction matrix, zero beyond nc
   uint32_t ldmt;          // >= NC
   double* out;            // output (nullable when only epilogue reductions are wanted)
-  uint64_t os_c, os_p;    // out(jl, c, p) = out[jl + c*os_c + p*os_p]
+  uint64_t os_j = 1;      // out(jl, c, p) = out[jl*os_j + c*os_c + p*os_p]
+  uint64_t os_c, os_p;
   uint32_t nc;            // true output columns
   double* gram_part;      // [grid][NC*NC] (nullable)
   double* sumsq_part;     // [grid] (nullable)
@@ -34,8 +35,8 @@ struct FcArgs {
 
 struct FrArgs {
   FiberView in;           // X(jl, i, p), i < K = I_n
-  const double* m;        // Mr(j, c) = m[j + c*ldm], j = p*s + jl
-  uint64_t ldm;
+  const double* m;        // Mr(j, c) = m[j*mj + c*mc], j = p*s + jl
+  uint64_t mj, mc;
   uint32_t nc;
   uint64_t fibers_per_range;  // multiple of the kernel's chunk
   uint32_t ranges;

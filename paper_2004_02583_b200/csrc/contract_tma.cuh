@@ -1,0 +1,47 @@
+// TMA-fed FC / FR kernels (contract_tma.cu). The FC output / FR operand
+// conventions match contract.cuh except that FR's small operand M is
+// row-major [F][ldm] (R and S are kept row-major on the device).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace tkg {
+
+enum TmaMode { kFibI = 0, kFibJ = 1 };
+
+struct FcTmaArgs {
+  uint64_t s = 0, P = 0;
+  uint32_t K = 0;
+  uint32_t nc = 0;
+  double* out = nullptr;                       // out[jl*os_j + c*os_c + p*os_p]
+  uint64_t os_j = 1, os_c = 0, os_p = 0;
+  double* sumsq_part = nullptr;                // [grid]
+  const double* diff_ref = nullptr;            // diff-norm epilogue instead of a store
+};
+
+struct FrTmaArgs {
+  uint64_t s = 0, P = 0;
+  uint32_t K = 0;
+  uint32_t nc = 0;
+  uint64_t fibers_per_range = 0;
+  uint32_t ranges = 0, igroups = 0;
+  double* partial = nullptr;                   // [ranges][K][ncp]
+  uint32_t ncp = 0;
+  double* sumsq_part = nullptr;                // [ranges*igroups]
+};
+
+// -1 when the layout is not covered (the caller uses contract.cu's kernels).
+int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt);
+int fr_tma_mode(const FiberView& v, const double* m, uint64_t ldm);
+int fc_tma_grid(const FiberView& v, int num_sms);
+uint32_t fr_tma_ranges(const FiberView& v, int num_sms);
+
+cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, FcTmaArgs a, int mode,
+                          int num_sms, cudaStream_t st, int* grid_used);
+cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t ldm, FrTmaArgs a, int mode,
+                          int num_sms, cudaStream_t st, uint32_t* ranges_used, uint32_t* grid_used);
+
+}  // namespace tkg

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <sstream>
 
+#include "contract_tma.cuh"
 #include "mt_jump.hpp"
 
 namespace tkg {
@@ -106,6 +107,12 @@ Engine::Engine(int device) : device_(device) {
   if (prop.major < 10) raise(12, std::string("tenkit_b200 is built for sm_100a; device is ") + prop.name);
   sms_ = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&st2_, cudaStreamNonBlocking, lo));  // lowest priority
+    CK(cudaEventCreateWithFlags(&pre_gate_, cudaEventDisableTiming));
+  }
   CK(cudaHostAlloc(reinterpret_cast<void**>(&status_h_), sizeof(DevStatus), cudaHostAllocMapped));
   std::memset(status_h_, 0, sizeof(DevStatus));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&status_d_), status_h_, 0));
@@ -123,7 +130,14 @@ Engine::~Engine() {
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
+  cudaStreamSynchronize(st2_);
+  for (auto* b : pre_bufs_) delete b;
+  for (auto* b : pre_y_) delete b;
+  for (auto* b : pre_st_) delete b;
+  for (auto ev : pre_ev_) cudaEventDestroy(ev);
+  cudaEventDestroy(pre_gate_);
   if (status_h_) cudaFreeHost(status_h_);
+  cudaStreamDestroy(st2_);
   cudaStreamDestroy(st_);
 }
 
@@ -204,25 +218,39 @@ const double* Engine::upload(const double* a, uint64_t n, bool a_dev, DBuf& buf,
 }
 
 void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
-                uint64_t os_c, uint64_t os_p, double* gram_part, double* sumsq_part,
+                uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
                 const double* diff_ref, int* grid_used, bool count_pass) {
-  FcArgs a;
-  a.in = v;
-  a.mt = mt;
-  a.ldmt = ldmt;
-  a.out = out;
-  a.os_c = os_c;
-  a.os_p = os_p;
-  a.nc = nc;
-  a.gram_part = gram_part;
-  a.sumsq_part = sumsq_part;
-  a.diff_ref = diff_ref;
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (profiling_) {
     ev = ev_pair();
     CK(cudaEventRecord(ev.first, st_));
   }
-  CK(launch_fc(a, sms_, st_, grid_used));
+  const int mode = force_v1_ ? -1 : fc_tma_mode(v, mt, ldmt);
+  if (mode >= 0) {
+    FcTmaArgs a;
+    a.nc = nc;
+    a.out = out;
+    a.os_j = os_j;
+    a.os_c = os_c;
+    a.os_p = os_p;
+    a.sumsq_part = sumsq_part;
+    a.diff_ref = diff_ref;
+    CK(launch_fc_tma(v, mt, ldmt, a, mode, sms_, st_, grid_used));
+  } else {
+    FcArgs a;
+    a.in = v;
+    a.mt = mt;
+    a.ldmt = ldmt;
+    a.out = out;
+    a.os_j = os_j;
+    a.os_c = os_c;
+    a.os_p = os_p;
+    a.nc = nc;
+    a.gram_part = nullptr;
+    a.sumsq_part = sumsq_part;
+    a.diff_ref = diff_ref;
+    CK(launch_fc(a, sms_, st_, grid_used));
+  }
   count_launch();
   const double elems = double(v.s) * double(v.P) * double(v.K);
   const double F = double(v.s) * double(v.P);
@@ -237,22 +265,42 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
   }
 }
 
+int Engine::fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc) {
+  const int mode = force_v1_ ? -1 : fc_tma_mode(v, mt, ldmt);
+  return mode >= 0 ? fc_tma_grid(v, sms_) : fc_grid_for(v, nc, sms_);
+}
+
+uint32_t Engine::fr_ranges(const FiberView& v, uint32_t nc) {
+  return std::max(fr_ranges_for(v, nc, sms_), fr_tma_ranges(v, sms_)) + 4;
+}
+
 uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t nc, double* partial,
                     double* sumsq_part, bool count_pass, uint32_t* grid_used) {
-  FrArgs a;
-  a.in = v;
-  a.m = m;
-  a.ldm = ldm;
-  a.nc = nc;
-  a.partial = partial;
-  a.sumsq_part = sumsq_part;
+  // m is row-major [F][ldm]
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (profiling_) {
     ev = ev_pair();
     CK(cudaEventRecord(ev.first, st_));
   }
   uint32_t ranges = 0, grid = 0;
-  CK(launch_fr(a, sms_, st_, &ranges, &grid));
+  const int mode = force_v1_ ? -1 : fr_tma_mode(v, m, ldm);
+  if (mode >= 0) {
+    FrTmaArgs a;
+    a.nc = nc;
+    a.partial = partial;
+    a.sumsq_part = sumsq_part;
+    CK(launch_fr_tma(v, m, ldm, a, mode, sms_, st_, &ranges, &grid));
+  } else {
+    FrArgs a;
+    a.in = v;
+    a.m = m;
+    a.mj = ldm;
+    a.mc = 1;
+    a.nc = nc;
+    a.partial = partial;
+    a.sumsq_part = sumsq_part;
+    CK(launch_fr(a, sms_, st_, &ranges, &grid));
+  }
   if (grid_used) *grid_used = grid;
   count_launch();
   const double elems = double(v.s) * double(v.P) * double(v.K);
@@ -269,8 +317,10 @@ uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t 
   return ranges;
 }
 
-// S (n doubles) = uniform01 draws of seeded_engine(seed, stream), on device.
-void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out) {
+// S (n doubles) = uniform01 draws of seeded_engine(seed, stream), on device,
+// enqueued on `st` with its own sequence/state buffers.
+void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F,
+                            uint64_t ld, cudaStream_t st, DBuf& ybuf, DBuf& sbuf) {
   if (n == 0) return;
   if (mt_charpoly().empty()) raise(11, "MT19937-64 characteristic polynomial check failed");
   const MtPlan plan = mt_plan(n);
@@ -280,30 +330,98 @@ void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_o
   if (it == jump_cache_.end()) {
     std::vector<uint64_t> tbl = mt_jump_table(plan.J, plan.C);
     polys = new DBuf();
-    CK(cudaMemcpy(polys->u(tbl.size()), tbl.data(), tbl.size() * 8, cudaMemcpyHostToDevice));
+    uint64_t* d = polys->u(tbl.size());
+    CK(cudaMemcpyAsync(d, tbl.data(), tbl.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
     jump_cache_[key] = polys;
   } else {
     polys = it->second;
   }
   std::vector<uint64_t> y(kMtSeqPadded, 0);
   mt_raw_sequence(seed, stream, y.data(), kMtSeqWords);
-  uint64_t* d_y = y_seq_.u(kMtSeqPadded);
-  CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st_));
-  uint64_t* d_states = states_.u(size_t(plan.C) * kMtN);
+  uint64_t* d_y = ybuf.u(kMtSeqPadded);
+  // pageable source: the copy is staged before cudaMemcpyAsync returns
+  CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st));
+  uint64_t* d_states = sbuf.u(size_t(plan.C) * kMtN);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
-  if (profiling_) {
+  const bool prof = profiling_ && st == st_;
+  if (prof) {
     ev = ev_pair();
-    CK(cudaEventRecord(ev.first, st_));
+    CK(cudaEventRecord(ev.first, st));
   }
-  CK(launch_mt_states(d_y, polys->u(0) /*existing*/, plan.C, d_states, st_));
-  CK(launch_mt_generate(d_states, plan.C, plan.J, n, d_out, st_));
+  CK(launch_mt_states(d_y, polys->u(0) /*existing*/, plan.C, d_states, st));
+  CK(launch_mt_generate(d_states, plan.C, plan.J, n, d_out, F, ld, st));
   count_launch(3);  // memset + jump + generate
-  if (profiling_) {
-    CK(cudaEventRecord(ev.second, st_));
+  if (prof) {
+    CK(cudaEventRecord(ev.second, st));
     record(kClsRng, ev.first, ev.second, 8.0 * n, 0.0);
   }
-  // keep y alive until the copy finished
-  sync();
+}
+
+void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F,
+                         uint64_t ld) {
+  gen_uniform_on(seed, stream, n, d_out, F, ld, st_, y_seq_, states_);
+}
+
+// The initializer streams depend only on (seed, mode, fibers, rank), not on
+// the data: generate those of every mode after the first on a second stream
+// while the first modes' sweeps run (the RNG kernels fit beside the
+// contraction kernels' shared-memory footprint).
+void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
+  pre_.clear();
+  while (pre_bufs_.size() < items.size()) {
+    pre_bufs_.push_back(new DBuf());
+    pre_y_.push_back(new DBuf());
+    pre_st_.push_back(new DBuf());
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    pre_ev_.push_back(ev);
+  }
+  CK(cudaEventRecord(pre_gate_, st_));  // buffers of a previous call are free
+  CK(cudaStreamWaitEvent(st2_, pre_gate_, 0));
+  for (size_t k = 0; k < items.size(); ++k) {
+    const PreGen& g = items[k];
+    const uint32_t ncp = pad_nc(g.r);
+    double* d = pre_bufs_[k]->d(g.F * ncp + 8);
+    gen_uniform_on(seed, uint32_t(g.mode), g.F * g.r, d, g.F, ncp, st2_, *pre_y_[k], *pre_st_[k]);
+    CK(cudaEventRecord(pre_ev_[k], st2_));
+    pre_[g.mode] = {d, pre_ev_[k], g.F, g.r};
+  }
+}
+
+// Thin QR with a nonnegative R diagonal (reduced_qr, kernels.cpp:303-367) by
+// CholQR2 on the device: Y = Q1 R1, Q1 = Q R2, R = R2 R1 — multi-CTA Gram
+// partials, a one-CTA Cholesky and row-parallel triangular solves. The thin
+// QR with positive diagonal is unique, so Q matches Householder's to rounding
+// for the well-conditioned factors ALS produces.
+void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
+                    double* rmat, double* rt, uint32_t ldrt, bool check) {
+  const double* Yc = Y;
+  if (nparts > 0) {
+    double* y = qy_.d(uint64_t(I) * r);
+    CK(launch_reduce_partials(Y, nparts, I, uint32_t(ld), r, y, st_));
+    count_launch();
+    Yc = y;
+  } else if (ld != I) {
+    double* y = qy_.d(uint64_t(I) * r);
+    CK(launch_pack(Y, 1, ld, r, I, y, I, st_));  // y[c*I + i] = Y[i + c*ld]
+    count_launch();
+    Yc = y;
+  }
+  const int ng = gram_partials_count(I);
+  double* gp = gram_part_.d(size_t(ng) * r * r);
+  double* L1 = qrl1_.d(size_t(r) * r);
+  double* L2 = qrl2_.d(size_t(r) * r);
+  double* Q1 = qrq1_.d(uint64_t(I) * r);
+  CK(launch_gram_partials(Yc, I, I, r, gp, st_));
+  CK(launch_chol(gp, ng, uint64_t(r) * r, int(r), r, nullptr, L1, &status_d_->qr_fail1, status_d_, st_, 0.0));
+  CK(launch_row_solve(Yc, 0, I, I, r, L1, Q1, nullptr, 0, &status_d_->qr_fail1, st_, 1));
+  CK(launch_gram_partials(Q1, I, I, r, gp, st_));
+  CK(launch_chol(gp, ng, uint64_t(r) * r, int(r), r, nullptr, L2, &status_d_->qr_fail2, status_d_, st_, 0.0));
+  CK(launch_row_solve(Q1, 0, I, I, r, L2, Q, nullptr, 0, &status_d_->qr_fail2, st_, 1));
+  CK(launch_cholqr_finish(L1, L2, r, &status_d_->qr_fail1, &status_d_->qr_fail2, rmat, rt, ldrt,
+                          check ? 1 : 0, status_d_, st_));
+  count_launch(7);
 }
 
 Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint32_t r,
@@ -321,18 +439,17 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   if (r > kMaxRank) raise(12, mname + ": rank " + std::to_string(r) + " above the supported 64");
   double* Lc = l_.d(I * r);
   double* Mt = mt_.d(I * ncp);
-  double* R = r_.d(F * r);
+  double* R = r_.d(F * ncp + 8);  // row-major [F][ncp]
   double* GL = gl_.d(kMaxRank * kMaxRank);
   double* GR = gr_.d(kMaxRank * kMaxRank);
   double* cholL = cholL_.d(kMaxRank * kMaxRank);
   double* cholR = cholR_.d(kMaxRank * kMaxRank);
-  const uint32_t nranges = fr_ranges_for(v, r, sms_) + 4;
+  const uint32_t nranges = fr_ranges(v, r);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const int fc_grid = fc_grid_for(v, r, sms_);
-  double* fcg = fc_gram_.d(size_t(fc_grid) * ncp * ncp);
+  const int ngr = gram_rm_count(F, sms_);
+  double* grp = fc_gram_.d(size_t(ngr) * ncp * ncp);
   double* gp = gram_part_.d(size_t(gram_partials_count(uint32_t(I))) * r * r);
   double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
-  double* qrw = qr_work_.d(2 * I * r + r);
 
   status_h_->degenerate_col = 0;
   // 1. ||A|| and the initial left factor.
@@ -346,16 +463,24 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   } else {
     if (r < 1 || r > I)
       raise(4, mname + ": rank " + std::to_string(r) + " outside 1.." + std::to_string(I));
-    double* S = s_.d(F * r);
-    gen_uniform(cfg.seed, uint32_t(mode), F * r, S);
+    const double* S = nullptr;
+    auto pit = pre_.find(mode);
+    if (pit != pre_.end() && pit->second.F == F && pit->second.r == r) {
+      CK(cudaStreamWaitEvent(st_, pit->second.ready, 0));
+      S = pit->second.ptr;
+      pre_.erase(pit);
+    } else {
+      double* Sg = s_.d(F * ncp + 8);  // row-major [F][ncp]
+      gen_uniform(cfg.seed, uint32_t(mode), F * r, Sg, F, ncp);
+      S = Sg;
+    }
     uint32_t fr_grid = 0;
-    const uint32_t ranges = fr(v, S, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
+    const uint32_t ranges = fr(v, S, ncp, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
     if (!sumsq_known) {  // ||A||^2 fused into the init pass: one partial per CTA
       CK(launch_sum(sq, int(fr_grid), &status_d_->sumsq, st_));
       count_launch();
     }
-    CK(launch_qr(part, int(ranges), ncp, uint32_t(I), r, Lc, nullptr, nullptr, 0, qrw, 1, status_d_, st_));
-    count_launch();
+    qr_dev(part, int(ranges), ncp, uint32_t(I), r, Lc, nullptr, nullptr, 0, true);
   }
   sync();
   const double norm = std::sqrt(status_h_->sumsq);  // frobenius_norm (tensor_ops.cpp:391-393)
@@ -379,10 +504,10 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
                    &status_d_->right_singular, status_d_, st_));
     CK(launch_row_solve(Lc, 0, I, uint32_t(I), r, cholL, nullptr, Mt, ncp, &status_d_->right_singular, st_));
     count_launch(3);
-    int grid = 0;
-    fc(v, Mt, ncp, r, R, F, s, fcg, nullptr, nullptr, &grid, true);
-    CK(launch_finish_right(fcg, grid, int(ncp), r, GL, nullptr, GR, cholR, status_d_, st_));
-    count_launch();
+    fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, true);
+    CK(launch_gram_rm(R, F, r, ncp, grp, sms_, st_));
+    CK(launch_finish_right(grp, ngr, int(ncp), r, GL, nullptr, GR, cholR, status_d_, st_));
+    count_launch(2);
     sync();
     if (status_h_->right_singular) raise(4, singular);
     const double residual = status_h_->residual;
@@ -396,9 +521,11 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     if (k == max_iters) break;
     // left update: Y = A R, L = Y G_R^{-1}
     if (status_h_->left_singular) raise(4, singular);
-    const uint32_t ranges = fr(v, R, F, r, part, nullptr, true, nullptr);
-    CK(launch_row_solve(part, int(ranges), ncp, uint32_t(I), r, cholR, Lc, nullptr, 0, nullptr, st_));
-    count_launch();
+    const uint32_t ranges = fr(v, R, ncp, r, part, nullptr, true, nullptr);
+    double* Y = qy_.d(I * r);
+    CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, Y, st_));
+    CK(launch_row_solve(Y, 0, I, uint32_t(I), r, cholR, Lc, nullptr, 0, nullptr, st_));
+    count_launch(2);
     prev = residual;
   }
   return out;
@@ -428,7 +555,7 @@ void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint
     nxt.d[n - 1] = r;
     double* dst = (n == sh.N) ? d_core : bufs[which]->d(nxt.count());
     FiberView v{src, s, P, uint32_t(I), s, s * I};
-    fc(v, Mt, ncp, r, dst, s, s * r, nullptr, nullptr, nullptr, nullptr, n == 1);
+    fc(v, Mt, ncp, r, dst, 1, s, s * r, nullptr, nullptr, nullptr, n == 1);
     src = dst;
     cur = nxt;
     which ^= 1;
@@ -448,33 +575,32 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
   const double* src = d_core;
   DBuf* bufs[2] = {&work_a_, &work_b_};
   int which = 0;
-  std::vector<double> partial_sums;
-  double* sq = sq_part_.d(65536);
   int nsq = 0;
+  double* sq = nullptr;
   for (int n = 1; n <= sh.N; ++n) {
     const uint64_t K = cur.extent(n), s = cur.stride(n), F = cur.count() / K, P = F / s;
     const uint64_t Iout = sh.d[n - 1];
     Shape nxt = cur;
     nxt.d[n - 1] = Iout;
     const bool last = (n == sh.N);
-    double* dst = last ? nullptr : bufs[which]->d(nxt.count());
-    FiberView v{src, s, P, uint32_t(K), s, s * K};
-    for (uint64_t c0 = 0; c0 < Iout; c0 += 64) {
-      const uint32_t nc = uint32_t(std::min<uint64_t>(64, Iout - c0));
-      const uint32_t ncp = pad_nc(nc);
-      double* Mt = misc_.d(K * ncp);
-      // Mt[c][i'] = U[(c0 + i') + c*Iout]
-      CK(launch_pack(d_factors[n - 1] + c0, Iout, 1, uint32_t(K), nc, Mt, ncp, st_));
-      int grid = 0;
-      if (last) {
-        fc(v, Mt, ncp, nc, nullptr, s, s * Iout, nullptr, sq + nsq, A + c0 * s, &grid, false);
-        nsq += grid;
-        if (nsq + 256 > 65536) raise(12, "relative_error: too many partials");
-      } else {
-        fc(v, Mt, ncp, nc, dst + c0 * s, s, s * Iout, nullptr, nullptr, nullptr, &grid, false);
-      }
+    ExpandArgs ea;
+    ea.in = src;
+    ea.s = s;
+    ea.P = P;
+    ea.K = uint32_t(K);
+    ea.U = d_factors[n - 1];
+    ea.Iout = uint32_t(Iout);
+    if (last) {
+      nsq = expand_grid(F, sms_);
+      sq = sq_part_.d(size_t(std::max(4096, nsq)));
+      ea.ref = A;
+      ea.sumsq_part = sq;
+    } else {
+      ea.out = bufs[which]->d(nxt.count());
     }
-    src = dst;
+    CK(launch_expand(ea, sms_, st_, nullptr));
+    count_launch();
+    src = ea.out;
     cur = nxt;
     which ^= 1;
   }
@@ -495,6 +621,11 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   std::vector<double*> U(sh.N);
   begin_timed();
   const auto t0 = Clock::now();
+  {
+    std::vector<PreGen> items;
+    for (int n = 2; n <= sh.N; ++n) items.push_back({n, sh.count() / sh.d[n - 1], uint32_t(ranks[n - 1])});
+    pregenerate(items, cfg.seed);
+  }
   bool sumsq_known = false;
   double ref_sumsq = 0.0;
   for (int n = 1; n <= sh.N; ++n) {
@@ -505,9 +636,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     if (!sumsq_known) ref_sumsq = status_h_->sumsq;
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
-    CK(launch_qr(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0,
-                 qr_work_.d(2 * I * r + r), 0, status_d_, st_));
-    count_launch();
+    qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
     sync();
     o.rep.seconds = since(tm);
     rep->per_mode.push_back(o.rep);
@@ -567,6 +696,16 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
   int which = 0;
   bool sumsq_known = false;
   double ref_sumsq = 0.0;
+  {
+    std::vector<PreGen> items;
+    Shape w = sh;
+    for (size_t k = 0; k < order.size(); ++k) {
+      const int m = order[k];
+      if (k > 0) items.push_back({m, w.count() / w.d[m - 1], uint32_t(ranks[m - 1])});
+      w.d[m - 1] = ranks[m - 1];
+    }
+    pregenerate(items, cfg.seed);
+  }
   for (int mode : order) {
     const auto tm = Clock::now();
     const uint32_t r = uint32_t(ranks[mode - 1]);
@@ -576,20 +715,18 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     const uint32_t ncp = pad_nc(r);
     U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
     double* RhT = rhatT_.d(size_t(r) * ncp);
-    CK(launch_qr(l_.d(I * r), 0, I, uint32_t(I), r, U[mode - 1], rhat_.d(r * r), RhT, ncp,
-                 qr_work_.d(2 * I * r + r), 0, status_d_, st_));
-    count_launch();
+    qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[mode - 1], rhat_.d(r * r), RhT, ncp, false);
     // working <- tensorize(R_hat R^T, mode, shrunk) (hosvd.cpp:176-178): an FC
     // over R read as a tensor (extent r, strides F / s), fused ||.||^2.
     Shape nxt = cur;
     nxt.d[mode - 1] = r;
     double* dst = bufs[which]->d(nxt.count());
-    FiberView rv{r_.d(F * r), s, P, r, F, s};
-    int grid = 0;
-    double* sq = sq_part_.d(4096);
-    fc(rv, RhT, ncp, r, dst, s, s * r, nullptr, sq, nullptr, &grid, false);
-    CK(launch_sum(sq, grid, &status_d_->sumsq, st_));
-    count_launch();
+    const int nsh = shrink_count(F);
+    double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
+    CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_));
+    CK(launch_sum(sq, nsh, &status_d_->sumsq, st_));
+    count_launch(2);
+    (void)RhT;
     sumsq_known = true;
     sync();
     o.rep.seconds = since(tm);
@@ -633,7 +770,12 @@ void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode
   *rep = o.rep;
   const uint64_t F = sh.count() / I;
   CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  if (r_out) CK(cudaMemcpyAsync(r_out, r_.d(F * r), F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (r_out) {  // R is row-major [F][ncp] on the device; the API returns column-major F x r
+    const uint32_t ncp = pad_nc(r);
+    double* rc = work_b_.d(F * r);
+    CK(launch_pack(r_.d(F * ncp + 8), 1, ncp, r, uint32_t(F), rc, uint32_t(F), st_));
+    CK(cudaMemcpyAsync(r_out, rc, F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  }
   sync();
 }
 
@@ -647,19 +789,19 @@ void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, ui
   const uint64_t s = sh.stride(mode), F = sh.count() / I;
   const uint32_t ncp = pad_nc(r);
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  double* S = s_.d(F * r);
-  gen_uniform(seed, uint32_t(mode), F * r, S);
-  const uint32_t nranges = fr_ranges_for(v, r, sms_) + 4;
+  double* S = s_.d(F * ncp + 8);
+  gen_uniform(seed, uint32_t(mode), F * r, S, F, ncp);
+  const uint32_t nranges = fr_ranges(v, r);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const uint32_t ranges = fr(v, S, F, r, part, nullptr, false, nullptr);
+  const uint32_t ranges = fr(v, S, ncp, r, part, nullptr, false, nullptr);
   status_h_->degenerate_col = 0;
-  CK(launch_qr(part, int(ranges), ncp, uint32_t(I), r, l_.d(I * r), nullptr, nullptr, 0,
-               qr_work_.d(2 * I * r + r), 1, status_d_, st_));
+  qr_dev(part, int(ranges), ncp, uint32_t(I), r, l_.d(I * r), nullptr, nullptr, 0, true);
   sync();
   if (status_h_->degenerate_col != 0)
     raise(6, "als_init: randomized range collapsed at column " + std::to_string(status_h_->degenerate_col) +
                  " for mode " + std::to_string(mode));
-  CK(cudaMemcpy(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
 }
 
 // ---- primitives ------------------------------------------------------------------
@@ -668,13 +810,15 @@ void Engine::unfold_times(const double* a, const Shape& sh, int mode, const doub
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
   if (r > kMaxRank) raise(12, "unfold_times: more than 64 columns");
   const double* A = upload(a, sh.count(), false, tensor_, nullptr);
-  double* M = s_.d(F * r);
-  CK(cudaMemcpyAsync(M, m, F * r * sizeof(double), cudaMemcpyHostToDevice, st_));
+  double* Mc = work_b_.d(F * r);
+  CK(cudaMemcpyAsync(Mc, m, F * r * sizeof(double), cudaMemcpyHostToDevice, st_));
   const uint32_t ncp = pad_nc(r);
+  double* M = s_.d(F * ncp + 8);  // row-major FR operand
+  CK(launch_pack(Mc, 1, F, uint32_t(F), r, M, ncp, st_));
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  const uint32_t nranges = fr_ranges_for(v, r, sms_) + 4;
+  const uint32_t nranges = fr_ranges(v, r);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const uint32_t ranges = fr(v, M, F, r, part, nullptr, false, nullptr);
+  const uint32_t ranges = fr(v, M, ncp, r, part, nullptr, false, nullptr);
   double* y = misc_.d(I * r);
   CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, y, st_));
   CK(cudaMemcpyAsync(out, y, I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -693,7 +837,7 @@ void Engine::unfold_t_times(const double* a, const Shape& sh, int mode, const do
   CK(launch_pack(Mc, 1, I, uint32_t(I), r, Mt, ncp, st_));
   double* R = r_.d(F * r);
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  fc(v, Mt, ncp, r, R, F, s, nullptr, nullptr, nullptr, nullptr, false);
+  fc(v, Mt, ncp, r, R, 1, F, s, nullptr, nullptr, nullptr, false);  // column-major F x r
   CK(cudaMemcpyAsync(out, R, F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
 }
@@ -717,7 +861,7 @@ void Engine::mode_n_product(const double* a, const Shape& sh, const double* u, u
     double* Mt = mt_.d(I * ncp);
     // Mt[i][c] = u[(c0 + c) + i*rows]  (u is rows x cols column-major)
     CK(launch_pack(U + c0, rows, 1, uint32_t(I), nc, Mt, ncp, st_));
-    fc(v, Mt, ncp, nc, dst + c0 * s, s, s * rows, nullptr, nullptr, nullptr, nullptr, false);
+    fc(v, Mt, ncp, nc, dst + c0 * s, 1, s, s * rows, nullptr, nullptr, nullptr, false);
   }
   CK(cudaMemcpyAsync(out, dst, nxt.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
@@ -783,10 +927,45 @@ void Engine::gram(const double* a, uint64_t rows, uint64_t cols, double* out) {
   sync();
 }
 
+void Engine::bench_contractions(const double* A, const Shape& sh, int mode, uint32_t r, int reps,
+                                double* out_ms) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
+  if (r < 1 || r > kMaxRank) raise(12, "bench_contractions: r must be in 1..64");
+  const uint32_t ncp = pad_nc(r);
+  FiberView v{A, s, F / s, uint32_t(I), s, s * I};
+  double* Mt = mt_.d(I * ncp);
+  double* R = r_.d(F * ncp + 8);
+  CK(cudaMemsetAsync(Mt, 0, I * ncp * sizeof(double), st_));
+  CK(cudaMemsetAsync(R, 0, F * ncp * sizeof(double), st_));
+  const uint32_t nranges = fr_ranges(v, r);
+  double* part = fr_part_.d(size_t(nranges) * I * ncp);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, false);  // warm-up
+  fr(v, R, ncp, r, part, nullptr, false, nullptr);
+  CK(cudaEventRecord(e0, st_));
+  for (int k = 0; k < reps; ++k) fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, false);
+  CK(cudaEventRecord(e1, st_));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  out_ms[0] = ms / reps;
+  CK(cudaEventRecord(e0, st_));
+  for (int k = 0; k < reps; ++k) fr(v, R, ncp, r, part, nullptr, false, nullptr);
+  CK(cudaEventRecord(e1, st_));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  out_ms[1] = ms / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 void Engine::uniform01(uint64_t seed, uint32_t stream, uint64_t n, double* out) {
   double* d = s_.d(n);
   gen_uniform(seed, stream, n, d);
-  CK(cudaMemcpy(out, d, n * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(out, d, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
 }
 
 }  // namespace tkg

@@ -112,7 +112,10 @@ class Engine {
   void gram(const double* a, uint64_t rows, uint64_t cols, double* out);
   void uniform01(uint64_t seed, uint32_t stream, uint64_t n, double* out);
 
+  void bench_contractions(const double* dA, const Shape& sh, int mode, uint32_t r, int reps,
+                          double* out_ms);
   void set_profiling(bool on) { profiling_ = on; }
+  void force_v1(bool on) { force_v1_ = on; }
   void timer_start();
   double timer_stop();
   void flush_l2();
@@ -129,13 +132,27 @@ class Engine {
   // ||A||^2 of this tensor.
   AlsOut run_als(const double* A, const Shape& sh, int mode, uint32_t r, const AlsCfg& cfg,
                  bool sumsq_known);
-  void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out);
+  // ld == 0: storage order; else S (F x r col-major draw order) written row-major [F][ld]
+  void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F = 0,
+                   uint64_t ld = 0);
+  void gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F,
+                      uint64_t ld, cudaStream_t st, DBuf& ybuf, DBuf& sbuf);
+  struct PreGen {
+    int mode;
+    uint64_t F;
+    uint32_t r;
+  };
+  void pregenerate(const std::vector<PreGen>& items, uint64_t seed);
   void fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
-          uint64_t os_c, uint64_t os_p, double* gram_part, double* sumsq_part,
+          uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
           const double* diff_ref, int* grid_used, bool count_pass);
+  int fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc);
+  uint32_t fr_ranges(const FiberView& v, uint32_t nc);
   uint32_t fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t nc, double* partial,
               double* sumsq_part, bool count_pass, uint32_t* grid_used);
   void sync();
+  void qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
+              double* rmat, double* rt, uint32_t ldrt, bool check);
   const double* upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds);
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                                const double* d_core, const std::vector<double*>& d_factors,
@@ -151,17 +168,29 @@ class Engine {
   int sms_;
   std::string name_;
   cudaStream_t st_;
+  cudaStream_t st2_;  // low-priority side stream for the initializer streams
+  cudaEvent_t pre_gate_;
+  struct PreS {
+    double* ptr;
+    cudaEvent_t ready;
+    uint64_t F;
+    uint32_t r;
+  };
+  std::map<int, PreS> pre_;
+  std::vector<DBuf*> pre_bufs_, pre_y_, pre_st_;
+  std::vector<cudaEvent_t> pre_ev_;
   DevStatus* status_h_ = nullptr;
   DevStatus* status_d_ = nullptr;
 
   DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
   DBuf fr_part_, fc_gram_, gram_part_, sq_part_, qr_work_, q_, rhat_, rhatT_;
-  DBuf y_seq_, states_, misc_, misc2_, flush_;
+  DBuf y_seq_, states_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_;
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   std::vector<DBuf*> factor_bufs_;
   std::map<std::pair<uint64_t, int>, DBuf*> jump_cache_;
 
   bool profiling_ = false;
+  bool force_v1_ = false;
   struct Rec {
     int cls;
     cudaEvent_t a, b;

@@ -21,13 +21,17 @@ struct DevStatus {
   int32_t left_singular;   // chol(R^T R) hit the pivot floor
   int32_t degenerate_col;  // als_init collapse column (1-based), 0 if none
   int32_t pad;
+  int32_t qr_fail1;        // CholQR2 first / second factorisation failed
+  int32_t qr_fail2;
 };
 
 // ---- MT19937-64 (mtrng.cu) -------------------------------------------------
 cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C,
                              uint64_t* d_states, cudaStream_t st);
+// ld == 0: out[idx] (storage order); ld > 0: out[(idx % F)*ld + idx / F],
+// i.e. the column-major F x r matrix S written row-major (the FR operand layout).
 cudaError_t launch_mt_generate(const uint64_t* d_states, int C, uint64_t J, uint64_t total,
-                               double* d_out, cudaStream_t st);
+                               double* d_out, uint64_t F, uint64_t ld, cudaStream_t st);
 
 // ---- small dense LA (smallla.cu) -------------------------------------------
 // part[b] = upper triangle of X_b^T X_b over row blocks of X (rows x r, col-major, ld).
@@ -41,18 +45,27 @@ cudaError_t launch_gram_partials(const double* X, uint64_t ld, uint32_t rows, ui
 // (kernels.cpp:378-393). On failure sets *flag = 1 and status->pivot.
 // part_ld: stride between consecutive partials (>= r*r), part_rowstride:
 // row stride inside a partial (r for gram_partials, NC for FC Gram partials).
+// floor_rel: pivot floor relative to max diag (1e-13 = spd_solve; 0 = only
+// non-positive pivots fail, used by the CholQR2 factorisation).
 cudaError_t launch_chol(const double* part, int nparts, uint64_t part_ld, int part_rowstride,
                         uint32_t r, double* G, double* chol, int32_t* flag, DevStatus* status,
-                        cudaStream_t st);
+                        cudaStream_t st, double floor_rel = 1e-13);
 
 // Row-wise SPD solve X(i,:) = B(i,:) G^{-1} via the Cholesky factor, with
 // forward/back substitution in the order of spd_solve (kernels.cpp:398-415).
 // B is either the sum of `nparts` partials part[k][i][ldp] (FR output) or a
 // column-major matrix (nparts == 0: B[i + c*ldb]).
 // Output: column-major X (x_cm, ld = rows) and/or i-major padded Xt (xt, ldxt).
+// forward_only: X(i,:)^T = L^{-1} B(i,:)^T (the CholQR step Q = Y R^{-1}, R = L^T).
 cudaError_t launch_row_solve(const double* B, int nparts, uint64_t ldb_or_ldp, uint32_t rows,
                              uint32_t r, const double* chol, double* x_cm, double* xt,
-                             uint32_t ldxt, const int32_t* skip_flag, cudaStream_t st);
+                             uint32_t ldxt, const int32_t* skip_flag, cudaStream_t st,
+                             int forward_only = 0);
+
+// CholQR2 epilogue: R = L2^T L1^T, degeneracy test, optional R / R^T outputs.
+cudaError_t launch_cholqr_finish(const double* L1, const double* L2, uint32_t r, const int32_t* fail1,
+                                 const int32_t* fail2, double* rmat, double* rt, uint32_t ldrt,
+                                 int check, DevStatus* status, cudaStream_t st);
 
 // Householder thin QR (kernels.cpp:303-367, R_ii >= 0) of Y (rows x r), where
 // Y = sum of `nparts` FR partials [k][i][ldp] (or a column-major matrix when
@@ -85,6 +98,35 @@ cudaError_t launch_sumsq(const double* x, uint64_t n, double* part, cudaStream_t
 // part[b] = sum of (b[k] - a[k])^2 over block b (same blocking as launch_sumsq).
 cudaError_t launch_sumsq_diff(const double* a, const double* b, uint64_t n, double* part,
                               cudaStream_t st);
+
+// Upper-triangle Gram partials of a row-major [rows][ld] matrix with r
+// columns (gram(R), matrix.cpp:90-126), one partial per CTA, DMMA tiles.
+// Partial layout: [cta][ncp][ncp] with entry (c1, c2), c1 <= c2 at c1*ncp + c2.
+int gram_rm_count(uint64_t rows, int num_sms);
+cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t ld, double* part,
+                           int num_sms, cudaStream_t st);
+
+// st-HOSVD shrink B_(n) <- R_hat R^T written in tensor layout (hosvd.cpp:176-178):
+// out[jl + c*s + p*s*r] = sum_c' rhat[c + c'*r] * R[(p*s + jl)*ld + c'], plus
+// per-CTA partial sums of squares of the output (the next mode's ||B||^2).
+int shrink_count(uint64_t F);
+cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
+                          const double* rhat, double* out, double* sumsq_part, cudaStream_t st);
+
+// Mode expansion out(jl, i, p) = sum_c in(jl, c, p) U[i + c*Iout] (recon.cu);
+// with ref set, accumulates sum (ref - out)^2 per CTA instead of storing.
+struct ExpandArgs {
+  const double* in = nullptr;   // in[jl + c*s + p*s*K]
+  uint64_t s = 1, P = 1;
+  uint32_t K = 0;
+  const double* U = nullptr;    // Iout x K column-major
+  uint32_t Iout = 0;
+  double* out = nullptr;        // out[jl + i*s + p*s*Iout]
+  const double* ref = nullptr;
+  double* sumsq_part = nullptr; // [grid]
+};
+int expand_grid(uint64_t F, int num_sms);
+cudaError_t launch_expand(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used);
 
 // Y = sum of FR partials, written column-major (rows x r).
 cudaError_t launch_reduce_partials(const double* part, int nparts, uint32_t rows, uint32_t ldp,

@@ -239,8 +239,11 @@ std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
 MtPlan mt_plan(uint64_t total) {
   MtPlan p;
   p.total = total;
-  const uint64_t per = 262144;
-  uint64_t C = (total + per - 1) / per;
+  // Enough chunks to fill the GPU for small totals (>= 8192 draws each),
+  // ~64K draws per chunk for large ones, at most 592 (jump cost ~ C).
+  const uint64_t big = (total + 65535) / 65536;
+  const uint64_t small = std::min<uint64_t>(148, (total + 8191) / 8192);
+  uint64_t C = std::max(big, small);
   C = std::max<uint64_t>(1, std::min<uint64_t>(C, 592));
   p.C = static_cast<int>(C);
   p.J = (total + C - 1) / C;

@@ -2,7 +2,8 @@
 // by GF(2) XOR-sums over the raw sequence, then one CTA per chunk generates
 // its J draws with the standard twist (in-place semantics of
 // std::mersenne_twister_engine) and writes uniform01 values
-// ((y >> 11) * 2^-53, rng.hpp:19-21) straight into S in storage order.
+// ((y >> 11) * 2^-53, rng.hpp:19-21) straight into S (storage order, or
+// transposed into the row-major FR operand layout).
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -49,11 +50,13 @@ __global__ void mt_jump_kernel(const uint64_t* __restrict__ y, const uint64_t* _
   if (t >= kMtN) return;
   uint64_t acc = 0;
   for (int w = 0; w < w1 - w0; ++w) {
-    const uint64_t bits = pw[w];
-    if (!bits) continue;
+    uint64_t bits = pw[w];  // same word for the whole CTA: uniform control flow
     const uint64_t* row = ys + w * 64 + t;
-#pragma unroll 16
-    for (int b = 0; b < 64; ++b) acc ^= row[b] & (0ull - ((bits >> b) & 1ull));
+    while (bits) {
+      const int b = __ffsll(static_cast<long long>(bits)) - 1;
+      acc ^= row[b];
+      bits &= bits - 1;
+    }
   }
   atomicXor(reinterpret_cast<unsigned long long*>(states + size_t(c) * kMtN + t),
             static_cast<unsigned long long>(acc));
@@ -61,7 +64,8 @@ __global__ void mt_jump_kernel(const uint64_t* __restrict__ y, const uint64_t* _
 
 // One CTA (160 threads) per chunk.
 __global__ void __launch_bounds__(160) mt_gen_kernel(const uint64_t* __restrict__ states, uint64_t J,
-                                                     uint64_t total, double* __restrict__ out) {
+                                                     uint64_t total, double* __restrict__ out,
+                                                     uint64_t F, uint64_t ld) {
   __shared__ uint64_t mt[kMtN];
   const int c = blockIdx.x;
   const int tid = threadIdx.x;
@@ -71,8 +75,23 @@ __global__ void __launch_bounds__(160) mt_gen_kernel(const uint64_t* __restrict_
   __syncthreads();
   uint64_t pos = start;
   while (true) {
-    for (int k = tid; k < kMtN; k += blockDim.x)
-      if (pos + k < end) out[pos + k] = to_uniform01(mt[k]);
+    if (ld == 0) {
+      for (int k = tid; k < kMtN; k += blockDim.x)
+        if (pos + k < end) out[pos + k] = to_uniform01(mt[k]);
+    } else {
+      // S(j, c) with idx = j + c*F, stored at j*ld + c
+      const uint64_t c0 = pos / F;
+      const uint64_t j0 = pos - c0 * F;
+      for (int k = tid; k < kMtN; k += blockDim.x) {
+        if (pos + k >= end) continue;
+        uint64_t j = j0 + k, col = c0;
+        if (j >= F) {
+          col += j / F;
+          j %= F;
+        }
+        out[j * ld + col] = to_uniform01(mt[k]);
+      }
+    }
     pos += kMtN;
     if (pos >= end) break;
     // In-place twist, i = 0..155 (reads old i, i+1, i+156).
@@ -114,8 +133,8 @@ cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C
 }
 
 cudaError_t launch_mt_generate(const uint64_t* d_states, int C, uint64_t J, uint64_t total,
-                               double* d_out, cudaStream_t st) {
-  mt_gen_kernel<<<C, 160, 0, st>>>(d_states, J, total, d_out);
+                               double* d_out, uint64_t F, uint64_t ld, cudaStream_t st) {
+  mt_gen_kernel<<<C, 160, 0, st>>>(d_states, J, total, d_out, F, ld);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 // solves, Householder QR with the reference's sign convention, and the
 // closed-form residual. They run on-device so a sweep never round-trips
 // through the host except for the one status read that decides the stop.
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -36,7 +37,8 @@ __global__ void gram_partials_kernel(const double* __restrict__ X, uint64_t ld, 
 
 // ---- Cholesky (spd_solve's factorisation, kernels.cpp:369-393) -------------
 // Single CTA. G(i,j) for i <= j = sum_k part[k][i*rowstride + j].
-__device__ void block_chol(double* G, double* L, uint32_t r, int32_t* flag, DevStatus* status) {
+__device__ void block_chol(double* G, double* L, uint32_t r, int32_t* flag, DevStatus* status,
+                           double floor_rel = 1e-13) {
   __shared__ double piv_s;
   __shared__ int fail_s;
   // max diagonal (kernels.cpp:378-379) and floor
@@ -44,7 +46,7 @@ __device__ void block_chol(double* G, double* L, uint32_t r, int32_t* flag, DevS
   if (threadIdx.x == 0) {
     double md = 0.0;
     for (uint32_t i = 0; i < r; ++i) md = fmax(md, G[i + i * r]);
-    floor_s = 1e-13 * md;
+    floor_s = floor_rel * md;
     fail_s = 0;
   }
   for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) L[e] = 0.0;
@@ -82,20 +84,22 @@ __device__ void reduce_upper(const double* part, int nparts, uint64_t part_ld, i
     const uint32_t i = e % r, j = e / r;  // column-major entry (i, j)
     const uint32_t a = min(i, j), b = max(i, j);
     double s = 0.0;
-    for (int k = 0; k < nparts; ++k) s += part[size_t(k) * part_ld + size_t(a) * rowstride + b];
+    const double* p = part + size_t(a) * rowstride + b;
+#pragma unroll 8
+    for (int k = 0; k < nparts; ++k) s += p[size_t(k) * part_ld];
     G[e] = s;
   }
 }
 
 __global__ void chol_kernel(const double* __restrict__ part, int nparts, uint64_t part_ld,
                             int rowstride, uint32_t r, double* G, double* chol, int32_t* flag,
-                            DevStatus* status) {
+                            DevStatus* status, double floor_rel) {
   extern __shared__ double sm[];
   double* Gs = sm;
   double* Ls = sm + r * r;
   reduce_upper(part, nparts, part_ld, rowstride, r, Gs);
   __syncthreads();
-  block_chol(Gs, Ls, r, flag, status);
+  block_chol(Gs, Ls, r, flag, status, floor_rel);
   __syncthreads();
   for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
     if (G) G[e] = Gs[e];
@@ -106,7 +110,8 @@ __global__ void chol_kernel(const double* __restrict__ part, int nparts, uint64_
 // ---- row-wise SPD solve ------------------------------------------------------
 __global__ void row_solve_kernel(const double* __restrict__ B, int nparts, uint64_t ldb,
                                  uint32_t rows, uint32_t r, const double* __restrict__ chol,
-                                 double* x_cm, double* xt, uint32_t ldxt, const int32_t* skip) {
+                                 double* x_cm, double* xt, uint32_t ldxt, const int32_t* skip,
+                                 int forward_only) {
   if (skip && *skip) return;
   extern __shared__ double sm[];
   double* Ls = sm;                 // r*r
@@ -132,10 +137,12 @@ __global__ void row_solve_kernel(const double* __restrict__ B, int nparts, uint6
     for (uint32_t p = 0; p < a; ++p) acc -= Ls[a + p * r] * xs[p * T + t];
     xs[a * T + t] = acc / Ls[a + a * r];
   }
-  for (uint32_t a = r; a-- > 0;) {
-    double acc = xs[a * T + t];
-    for (uint32_t p = a + 1; p < r; ++p) acc -= Ls[p + a * r] * xs[p * T + t];
-    xs[a * T + t] = acc / Ls[a + a * r];
+  if (!forward_only) {
+    for (uint32_t a = r; a-- > 0;) {
+      double acc = xs[a * T + t];
+      for (uint32_t p = a + 1; p < r; ++p) acc -= Ls[p + a * r] * xs[p * T + t];
+      xs[a * T + t] = acc / Ls[a + a * r];
+    }
   }
   for (uint32_t c = 0; c < r; ++c) {
     const double v = xs[c * T + t];
@@ -379,7 +386,199 @@ __global__ void sumsq_diff_kernel(const double* __restrict__ a, const double* __
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// ---- Gram of a row-major matrix on the tensor pipe ----------------------------
+// Each CTA owns a contiguous row range, streams 128-row blocks through a
+// double-buffered cp.async ring (row pitch NC+4 = 4 mod 16 doubles) and
+// accumulates its upper-triangle 8x8 tiles with DMMA in registers.
+template <int NC>
+__global__ void __launch_bounds__(256) gram_rm_kernel(const double* __restrict__ X, uint64_t rows,
+                                                      uint32_t r, uint64_t ld, double* part) {
+  constexpr int kRows = 128, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2;
+  constexpr int kPer = (kTri + 7) / 8;
+  extern __shared__ __align__(16) double tile[];  // [2][kRows][kLd]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
+  double acc[kPer][2];
+  int tm[kPer], tn[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    acc[k][0] = acc[k][1] = 0.0;
+    int tt = warp + 8 * k, mt = 0;
+    if (tt < kTri) {
+      int rem = tt;
+      while (rem >= kNT - mt) { rem -= kNT - mt; ++mt; }
+      tm[k] = mt;
+      tn[k] = mt + rem;
+    } else {
+      tm[k] = tn[k] = -1;
+    }
+  }
+  const uint64_t nblk = (rows + kRows - 1) / kRows;
+  const uint64_t per = (nblk + gridDim.x - 1) / gridDim.x;
+  const uint64_t b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
+  const bool vec = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (NC % 2 == 0);
+  auto load = [&](uint64_t b, int buf) {
+    double* t = tile + buf * kRows * kLd;
+    const uint64_t r0 = b * kRows;
+    if (vec) {
+      for (int e = threadIdx.x; e < kRows * (NC / 2); e += blockDim.x) {
+        const int row = e / (NC / 2), c = (e % (NC / 2)) * 2;
+        const uint64_t gr = r0 + row;
+        if (gr < rows) cp_async16(t + row * kLd + c, X + gr * ld + c);
+        else { t[row * kLd + c] = 0.0; t[row * kLd + c + 1] = 0.0; }
+      }
+    } else {
+      for (int e = threadIdx.x; e < kRows * NC; e += blockDim.x) {
+        const int row = e / NC, c = e % NC;
+        const uint64_t gr = r0 + row;
+        t[row * kLd + c] = gr < rows ? X[gr * ld + c] : 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+  if (b0 < b1) load(b0, 0);
+  for (uint64_t b = b0; b < b1; ++b) {
+    const int buf = int((b - b0) & 1);
+    if (b + 1 < b1) {
+      load(b + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* t = tile + buf * kRows * kLd;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      if (tm[k] < 0) continue;
+#pragma unroll 8
+      for (int k0 = 0; k0 < kRows; k0 += 4) {
+        const double* rp = t + (k0 + q) * kLd;
+        dmma(acc[k][0], acc[k][1], rp[tm[k] * 8 + r8], rp[tn[k] * 8 + r8]);
+      }
+    }
+    __syncthreads();
+  }
+  // columns >= r hold whatever the padding held; the consumer reads c < r only
+  double* out = part + size_t(blockIdx.x) * NC * NC;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if (tm[k] < 0) continue;
+    const int c1 = tm[k] * 8 + r8, c2 = tn[k] * 8 + 2 * q;
+    out[c1 * NC + c2] = acc[k][0];
+    out[c1 * NC + c2 + 1] = acc[k][1];
+  }
+}
+
+// ---- st-HOSVD shrink ---------------------------------------------------------
+constexpr int kShrinkThreads = 256;
+constexpr int kShrinkFibers = 4096;  // fibers per CTA
+
+__global__ void __launch_bounds__(kShrinkThreads) shrink_kernel(
+    const double* __restrict__ R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
+    const double* __restrict__ rhat, double* __restrict__ out, double* sumsq_part) {
+  extern __shared__ double rh[];  // r x r column-major
+  __shared__ double red[32];
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) rh[e] = rhat[e];
+  __syncthreads();
+  const uint64_t F = s * P;
+  const uint64_t f0 = uint64_t(blockIdx.x) * kShrinkFibers;
+  const uint64_t f1 = min(F, f0 + kShrinkFibers);
+  double sq = 0.0;
+  for (uint64_t j = f0 + threadIdx.x; j < f1; j += blockDim.x) {
+    const uint64_t p = j / s, jl = j - p * s;
+    const double* row = R + j * ld;
+    double* o = out + jl + p * s * r;
+    for (uint32_t c = 0; c < r; ++c) {
+      double acc = 0.0;
+      for (uint32_t k = 0; k < r; ++k) acc = fma(rh[c + k * r], row[k], acc);
+      o[uint64_t(c) * s] = acc;
+      sq = fma(acc, acc, sq);
+    }
+  }
+  sq = block_sum(sq, red);
+  if (threadIdx.x == 0) sumsq_part[blockIdx.x] = sq;
+}
+
+// R = R2 R1 with R_k = L_k^T (CholQR2), the reference's degeneracy test on
+// diag(R) (als.cpp:74-86), and optional outputs R (col-major) / R^T padded.
+__global__ void cholqr_finish_kernel(const double* __restrict__ L1, const double* __restrict__ L2,
+                                     uint32_t r, const int32_t* fail1, const int32_t* fail2,
+                                     double* rmat, double* rt, uint32_t ldrt, int check,
+                                     DevStatus* status) {
+  extern __shared__ double Rs[];
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const uint32_t i = e % r, j = e / r;
+    double acc = 0.0;
+    if (i <= j)
+      for (uint32_t k = i; k <= j; ++k) acc += L2[k + i * r] * L1[j + k * r];  // R2[i][k] R1[k][j]
+    Rs[e] = acc;
+    if (rmat) rmat[e] = acc;
+  }
+  __syncthreads();
+  if (rt)
+    for (uint32_t e = threadIdx.x; e < r * ldrt; e += blockDim.x) {
+      const uint32_t row = e / ldrt, c = e % ldrt;  // rt[c'][c] = R[c][c']
+      rt[e] = c < r ? Rs[c + row * r] : 0.0;
+    }
+  if (check && threadIdx.x == 0) {
+    int bad = 0;
+    if (*fail1 || *fail2) {
+      bad = 1;
+    } else {
+      double md = 0.0;
+      for (uint32_t i = 0; i < r; ++i) md = fmax(md, fabs(Rs[i + i * r]));
+      for (uint32_t i = 0; i < r; ++i)
+        if (fabs(Rs[i + i * r]) <= 1e-13 * md || md == 0.0) {
+          bad = int(i) + 1;
+          break;
+        }
+    }
+    status->degenerate_col = bad;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_cholqr_finish(const double* L1, const double* L2, uint32_t r, const int32_t* fail1,
+                                 const int32_t* fail2, double* rmat, double* rt, uint32_t ldrt,
+                                 int check, DevStatus* status, cudaStream_t st) {
+  cholqr_finish_kernel<<<1, 256, sizeof(double) * r * r, st>>>(L1, L2, r, fail1, fail2, rmat, rt, ldrt,
+                                                               check, status);
+  return cudaGetLastError();
+}
+
+int gram_rm_count(uint64_t rows, int num_sms) {
+  const uint64_t nblk = (rows + 127) / 128;
+  return int(std::max<uint64_t>(1, std::min<uint64_t>(nblk, uint64_t(num_sms))));
+}
+
+cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t ld, double* part,
+                           int num_sms, cudaStream_t st) {
+  const int grid = gram_rm_count(rows, num_sms);
+  const uint32_t ncp = r <= 8 ? 8 : (r + 7) / 8 * 8;
+  switch (ncp) {
+#define TKG_G(N)                                                                          \
+  case N: {                                                                               \
+    const size_t sm = sizeof(double) * 2 * 128 * (N + 4);                                 \
+    cudaFuncSetAttribute(gram_rm_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); \
+    gram_rm_kernel<N><<<grid, 256, sm, st>>>(X, rows, r, ld, part);                        \
+    break;                                                                                \
+  }
+    TKG_G(8) TKG_G(16) TKG_G(24) TKG_G(32) TKG_G(40) TKG_G(48) TKG_G(56) TKG_G(64)
+#undef TKG_G
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+int shrink_count(uint64_t F) { return int((F + kShrinkFibers - 1) / kShrinkFibers); }
+
+cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
+                          const double* rhat, double* out, double* sumsq_part, cudaStream_t st) {
+  const int grid = shrink_count(s * P);
+  shrink_kernel<<<grid, kShrinkThreads, sizeof(double) * r * r, st>>>(R, ld, s, P, r, rhat, out,
+                                                                       sumsq_part);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sumsq_diff(const double* a, const double* b, uint64_t n, double* part,
                               cudaStream_t st) {
@@ -400,19 +599,19 @@ cudaError_t launch_gram_partials(const double* X, uint64_t ld, uint32_t rows, ui
 
 cudaError_t launch_chol(const double* part, int nparts, uint64_t part_ld, int rowstride,
                         uint32_t r, double* G, double* chol, int32_t* flag, DevStatus* status,
-                        cudaStream_t st) {
+                        cudaStream_t st, double floor_rel) {
   chol_kernel<<<1, 256, sizeof(double) * 2 * r * r, st>>>(part, nparts, part_ld, rowstride, r, G,
-                                                          chol, flag, status);
+                                                          chol, flag, status, floor_rel);
   return cudaGetLastError();
 }
 
 cudaError_t launch_row_solve(const double* B, int nparts, uint64_t ldb, uint32_t rows, uint32_t r,
                              const double* chol, double* x_cm, double* xt, uint32_t ldxt,
-                             const int32_t* skip, cudaStream_t st) {
-  const int T = 64;
+                             const int32_t* skip, cudaStream_t st, int forward_only) {
+  const int T = 32;
   const size_t smem = sizeof(double) * (size_t(r) * r + size_t(r) * T);
   row_solve_kernel<<<(rows + T - 1) / T, T, smem, st>>>(B, nparts, ldb, rows, r, chol, x_cm, xt,
-                                                         ldxt, skip);
+                                                         ldxt, skip, forward_only);
   return cudaGetLastError();
 }
 
@@ -427,7 +626,7 @@ cudaError_t launch_qr(const double* Y, int nparts, uint64_t ldy, uint32_t rows, 
 cudaError_t launch_finish_right(const double* fc_gram, int nparts, int nc_stride, uint32_t r,
                                 const double* GL, const double* /*norm_sq*/, double* GR,
                                 double* cholR, DevStatus* status, cudaStream_t st) {
-  finish_right_kernel<<<1, 256, sizeof(double) * 2 * r * r, st>>>(fc_gram, nparts, nc_stride, r,
+  finish_right_kernel<<<1, 1024, sizeof(double) * 2 * r * r, st>>>(fc_gram, nparts, nc_stride, r,
                                                                    GL, GR, cholR, status);
   return cudaGetLastError();
 }
