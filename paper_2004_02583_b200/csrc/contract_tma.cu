@@ -254,26 +254,29 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 // ---------------------------------------------------------------------------
 // FR
 // ---------------------------------------------------------------------------
-template <int NC, int MODE>
+template <int NC, int MODE, bool MCOL>
 struct FrT {
   static constexpr int kIC = 128;   // contraction rows per CTA (8 warps x 16)
   static constexpr int kKB = 32;    // fibers per stage
   static constexpr int kStages = 4;
   static constexpr int kLdA = MODE == kFibI ? 132 : 36;
   static constexpr int kRowsA = MODE == kFibI ? kKB : kIC;
-  static constexpr int kLdM = NC + 4;
+  // M row-major [F][ld]: box (NC+4, 32) -> [32][NC+4];
+  // M column-major (F x r):  box (36, NC)  -> [NC][36]
+  static constexpr int kLdM = MCOL ? 36 : NC + 4;
+  static constexpr int kRowsM = MCOL ? NC : kKB;
   static constexpr int kBytesA = kRowsA * kLdA * 8;
-  static constexpr int kBytesM = kKB * kLdM * 8;
+  static constexpr int kBytesM = kRowsM * kLdM * 8;
   static constexpr int kStageBytes = ((kBytesA + kBytesM) + 127) / 128 * 128;
   static constexpr int kNT = NC / 8;
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes;
 };
 
-template <int NC, int MODE>
+template <int NC, int MODE, bool MCOL>
 __global__ void __launch_bounds__(kThreadsTma, 1)
     fr_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FrTmaArgs a) {
-  using C = FrT<NC, MODE>;
+  using C = FrT<NC, MODE, MCOL>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + C::kStages;
@@ -316,7 +319,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           const uint64_t jl = j - p * a.s;
           tma_3d(st, &tmA, &full[slot], int(jl), i0, int(p));
         }
-        tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, int(j));
+        if (MCOL) tma_2d(st + C::kBytesA, &tmM, &full[slot], int(j), 0);
+        else tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, int(j));
       }
     }
     return;
@@ -355,7 +359,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       }
       double bf[C::kNT];
 #pragma unroll
-      for (int n = 0; n < C::kNT; ++n) bf[n] = Ms[kk * C::kLdM + n * 8 + r8];
+      for (int n = 0; n < C::kNT; ++n)
+        bf[n] = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
 #pragma unroll
       for (int n = 0; n < C::kNT; ++n)
 #pragma unroll
@@ -451,11 +456,11 @@ cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTm
   return cudaGetLastError();
 }
 
-template <int NC, int MODE>
+template <int NC, int MODE, bool MCOL>
 cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, int grid,
                           cudaStream_t st) {
-  using C = FrT<NC, MODE>;
-  auto k = fr_tma_kernel<NC, MODE>;
+  using C = FrT<NC, MODE, MCOL>;
+  auto k = fr_tma_kernel<NC, MODE, MCOL>;
   static bool done = false;
   if (!done) {
     cudaError_t e = set_smem(k, C::kSmem);
@@ -489,8 +494,10 @@ int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt) {
   return -1;
 }
 
-int fr_tma_mode(const FiberView& v, const double* m, uint64_t ldm) {
-  if (!encode_fn() || !aligned16(v.base) || !aligned16(m) || (ldm % 2) != 0) return -1;
+int fr_tma_mode(const FiberView& v, const double* m, uint64_t mj, uint64_t mc) {
+  // M(j, c) = m[j*mj + c*mc]: row-major (mc == 1) or column-major (mj == 1)
+  const uint64_t ld = mc == 1 ? mj : (mj == 1 ? mc : 1);
+  if (!encode_fn() || !aligned16(v.base) || !aligned16(m) || (ld % 2) != 0) return -1;
   if (v.s * v.P >= (1ull << 31)) return -1;
   if (v.s == 1 && v.is_i == 1 && v.is_p % 2 == 0) return kFibI;
   if (v.s % 32 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 && v.P < (1ull << 31)) return kFibJ;
@@ -535,8 +542,10 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
 #undef TKG_FC_CALL
 }
 
-cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t ldm, FrTmaArgs a, int mode,
-                          int num_sms, cudaStream_t st, uint32_t* ranges_used, uint32_t* grid_used) {
+cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, FrTmaArgs a,
+                          int mode, int num_sms, cudaStream_t st, uint32_t* ranges_used,
+                          uint32_t* grid_used) {
+  const bool mcol = mc != 1;
   const uint32_t ncp = pad_nc(a.nc);
   CUtensorMap A, M;
   const uint64_t F = v.s * v.P;
@@ -551,10 +560,15 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t ldm, FrT
     const uint32_t box[3] = {36, 128, 1};
     if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
-  {
+  if (!mcol) {
     const uint64_t dims[2] = {ncp, F};
-    const uint64_t strides[1] = {ldm * 8};
+    const uint64_t strides[1] = {mj * 8};
     const uint32_t box[2] = {ncp + 4, 32};
+    if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
+    const uint64_t dims[2] = {F, a.nc};
+    const uint64_t strides[1] = {mc * 8};
+    const uint32_t box[2] = {36, ncp};
     if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
   }
   a.s = v.s;
@@ -570,8 +584,11 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t ldm, FrT
   if (ranges_used) *ranges_used = a.ranges;
   const int grid = int(a.ranges * a.igroups);
   if (grid_used) *grid_used = grid;
-#define TKG_FR_CALL(N) (mode == kFibI ? fr_tma_launch<N, kFibI>(A, M, a, grid, st) \
-                                      : fr_tma_launch<N, kFibJ>(A, M, a, grid, st))
+#define TKG_FR_CALL(N)                                                                      \
+  (mode == kFibI ? (mcol ? fr_tma_launch<N, kFibI, true>(A, M, a, grid, st)                   \
+                         : fr_tma_launch<N, kFibI, false>(A, M, a, grid, st))                 \
+                 : (mcol ? fr_tma_launch<N, kFibJ, true>(A, M, a, grid, st)                   \
+                         : fr_tma_launch<N, kFibJ, false>(A, M, a, grid, st)))
   TKG_NC_SWITCH(ncp, TKG_FR_CALL)
 #undef TKG_FR_CALL
 }

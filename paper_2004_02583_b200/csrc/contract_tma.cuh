@@ -1,6 +1,6 @@
 // TMA-fed FC / FR kernels (contract_tma.cu). The FC output / FR operand
-// conventions match contract.cuh except that FR's small operand M is
-// row-major [F][ldm] (R and S are kept row-major on the device).
+// conventions match contract.cuh; FR's small operand M may be row-major
+// (R) or column-major (the initializer's S) and is addressed by strides.
 #pragma once
 
 #include <cstdint>
@@ -35,13 +35,15 @@ struct FrTmaArgs {
 
 // -1 when the layout is not covered (the caller uses contract.cu's kernels).
 int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt);
-int fr_tma_mode(const FiberView& v, const double* m, uint64_t ldm);
+int fr_tma_mode(const FiberView& v, const double* m, uint64_t mj, uint64_t mc);
 int fc_tma_grid(const FiberView& v, int num_sms);
 uint32_t fr_tma_ranges(const FiberView& v, int num_sms);
 
 cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, FcTmaArgs a, int mode,
                           int num_sms, cudaStream_t st, int* grid_used);
-cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t ldm, FrTmaArgs a, int mode,
-                          int num_sms, cudaStream_t st, uint32_t* ranges_used, uint32_t* grid_used);
+// M(j, c) = m[j*mj + c*mc]; TMA needs mc == 1 (row-major) or mj == 1 (column-major).
+cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, FrTmaArgs a,
+                          int mode, int num_sms, cudaStream_t st, uint32_t* ranges_used,
+                          uint32_t* grid_used);
 
 }  // namespace tkg

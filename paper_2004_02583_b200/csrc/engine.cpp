@@ -274,28 +274,28 @@ uint32_t Engine::fr_ranges(const FiberView& v, uint32_t nc) {
   return std::max(fr_ranges_for(v, nc, sms_), fr_tma_ranges(v, sms_)) + 4;
 }
 
-uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t nc, double* partial,
-                    double* sumsq_part, bool count_pass, uint32_t* grid_used) {
-  // m is row-major [F][ldm]
+uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, uint32_t nc,
+                    double* partial, double* sumsq_part, bool count_pass, uint32_t* grid_used) {
+  // M(j, c) = m[j*mj + c*mc]
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (profiling_) {
     ev = ev_pair();
     CK(cudaEventRecord(ev.first, st_));
   }
   uint32_t ranges = 0, grid = 0;
-  const int mode = force_v1_ ? -1 : fr_tma_mode(v, m, ldm);
+  const int mode = force_v1_ ? -1 : fr_tma_mode(v, m, mj, mc);
   if (mode >= 0) {
     FrTmaArgs a;
     a.nc = nc;
     a.partial = partial;
     a.sumsq_part = sumsq_part;
-    CK(launch_fr_tma(v, m, ldm, a, mode, sms_, st_, &ranges, &grid));
+    CK(launch_fr_tma(v, m, mj, mc, a, mode, sms_, st_, &ranges, &grid));
   } else {
     FrArgs a;
     a.in = v;
     a.m = m;
-    a.mj = ldm;
-    a.mc = 1;
+    a.mj = mj;
+    a.mc = mc;
     a.nc = nc;
     a.partial = partial;
     a.sumsq_part = sumsq_part;
@@ -382,8 +382,9 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
   for (size_t k = 0; k < items.size(); ++k) {
     const PreGen& g = items[k];
     const uint32_t ncp = pad_nc(g.r);
-    double* d = pre_bufs_[k]->d(g.F * ncp + 8);
-    gen_uniform_on(seed, uint32_t(g.mode), g.F * g.r, d, g.F, ncp, st2_, *pre_y_[k], *pre_st_[k]);
+    double* d = pre_bufs_[k]->d(g.F * g.r + 8);
+    gen_uniform_on(seed, uint32_t(g.mode), g.F * g.r, d, 0, 0, st2_, *pre_y_[k], *pre_st_[k]);
+    (void)ncp;
     CK(cudaEventRecord(pre_ev_[k], st2_));
     pre_[g.mode] = {d, pre_ev_[k], g.F, g.r};
   }
@@ -470,12 +471,12 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       S = pit->second.ptr;
       pre_.erase(pit);
     } else {
-      double* Sg = s_.d(F * ncp + 8);  // row-major [F][ncp]
-      gen_uniform(cfg.seed, uint32_t(mode), F * r, Sg, F, ncp);
+      double* Sg = s_.d(F * r + 8);  // column-major F x r, the reference's storage order
+      gen_uniform(cfg.seed, uint32_t(mode), F * r, Sg);
       S = Sg;
     }
     uint32_t fr_grid = 0;
-    const uint32_t ranges = fr(v, S, ncp, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
+    const uint32_t ranges = fr(v, S, 1, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
     if (!sumsq_known) {  // ||A||^2 fused into the init pass: one partial per CTA
       CK(launch_sum(sq, int(fr_grid), &status_d_->sumsq, st_));
       count_launch();
@@ -521,7 +522,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     if (k == max_iters) break;
     // left update: Y = A R, L = Y G_R^{-1}
     if (status_h_->left_singular) raise(4, singular);
-    const uint32_t ranges = fr(v, R, ncp, r, part, nullptr, true, nullptr);
+    const uint32_t ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr);
     double* Y = qy_.d(I * r);
     CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, Y, st_));
     CK(launch_row_solve(Y, 0, I, uint32_t(I), r, cholR, Lc, nullptr, 0, nullptr, st_));
@@ -789,11 +790,11 @@ void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, ui
   const uint64_t s = sh.stride(mode), F = sh.count() / I;
   const uint32_t ncp = pad_nc(r);
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  double* S = s_.d(F * ncp + 8);
-  gen_uniform(seed, uint32_t(mode), F * r, S, F, ncp);
+  double* S = s_.d(F * r + 8);
+  gen_uniform(seed, uint32_t(mode), F * r, S);
   const uint32_t nranges = fr_ranges(v, r);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const uint32_t ranges = fr(v, S, ncp, r, part, nullptr, false, nullptr);
+  const uint32_t ranges = fr(v, S, 1, F, r, part, nullptr, false, nullptr);
   status_h_->degenerate_col = 0;
   qr_dev(part, int(ranges), ncp, uint32_t(I), r, l_.d(I * r), nullptr, nullptr, 0, true);
   sync();
@@ -810,15 +811,13 @@ void Engine::unfold_times(const double* a, const Shape& sh, int mode, const doub
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
   if (r > kMaxRank) raise(12, "unfold_times: more than 64 columns");
   const double* A = upload(a, sh.count(), false, tensor_, nullptr);
-  double* Mc = work_b_.d(F * r);
-  CK(cudaMemcpyAsync(Mc, m, F * r * sizeof(double), cudaMemcpyHostToDevice, st_));
+  double* M = s_.d(F * r + 8);  // column-major F x r, as given
+  CK(cudaMemcpyAsync(M, m, F * r * sizeof(double), cudaMemcpyHostToDevice, st_));
   const uint32_t ncp = pad_nc(r);
-  double* M = s_.d(F * ncp + 8);  // row-major FR operand
-  CK(launch_pack(Mc, 1, F, uint32_t(F), r, M, ncp, st_));
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
   const uint32_t nranges = fr_ranges(v, r);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const uint32_t ranges = fr(v, M, ncp, r, part, nullptr, false, nullptr);
+  const uint32_t ranges = fr(v, M, 1, F, r, part, nullptr, false, nullptr);
   double* y = misc_.d(I * r);
   CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, y, st_));
   CK(cudaMemcpyAsync(out, y, I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -943,7 +942,7 @@ void Engine::bench_contractions(const double* A, const Shape& sh, int mode, uint
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, false);  // warm-up
-  fr(v, R, ncp, r, part, nullptr, false, nullptr);
+  fr(v, R, ncp, 1, r, part, nullptr, false, nullptr);
   CK(cudaEventRecord(e0, st_));
   for (int k = 0; k < reps; ++k) fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, false);
   CK(cudaEventRecord(e1, st_));
@@ -952,7 +951,7 @@ void Engine::bench_contractions(const double* A, const Shape& sh, int mode, uint
   CK(cudaEventElapsedTime(&ms, e0, e1));
   out_ms[0] = ms / reps;
   CK(cudaEventRecord(e0, st_));
-  for (int k = 0; k < reps; ++k) fr(v, R, ncp, r, part, nullptr, false, nullptr);
+  for (int k = 0; k < reps; ++k) fr(v, R, ncp, 1, r, part, nullptr, false, nullptr);
   CK(cudaEventRecord(e1, st_));
   CK(cudaEventSynchronize(e1));
   CK(cudaEventElapsedTime(&ms, e0, e1));

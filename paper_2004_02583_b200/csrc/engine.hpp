@@ -148,8 +148,8 @@ class Engine {
           const double* diff_ref, int* grid_used, bool count_pass);
   int fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc);
   uint32_t fr_ranges(const FiberView& v, uint32_t nc);
-  uint32_t fr(const FiberView& v, const double* m, uint64_t ldm, uint32_t nc, double* partial,
-              double* sumsq_part, bool count_pass, uint32_t* grid_used);
+  uint32_t fr(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, uint32_t nc,
+              double* partial, double* sumsq_part, bool count_pass, uint32_t* grid_used);
   void sync();
   void qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
               double* rmat, double* rt, uint32_t ldrt, bool check);
