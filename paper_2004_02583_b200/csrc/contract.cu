@@ -44,6 +44,7 @@ struct FcCfg {
 template <int NC, int WF, int MODE>
 __global__ void __launch_bounds__(256, 1) fc_kernel(FcArgs a) {
   using Cfg = FcCfg<NC, WF, MODE>;
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   double* ms = smem;                                    // [kStages][kSub][kLd]
   double* scratch = ms + kStages * Cfg::kStageDoubles;  // [kTF][kLd] output tile (Gram epilogue)
@@ -275,6 +276,7 @@ struct FrCfg {
 template <int NC, int WI, int MODE>
 __global__ void __launch_bounds__(256) fr_kernel(FrArgs a, int wgi, int wgj) {
   using Cfg = FrCfg<NC, WI, MODE>;
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;

@@ -31,6 +31,7 @@ struct FcArgs {
   double* gram_part;      // [grid][NC*NC] (nullable)
   double* sumsq_part;     // [grid] (nullable)
   const double* diff_ref; // nullable: accumulate (diff_ref[o] - out)^2 instead of storing
+  const int32_t* skip = nullptr;  // device flag: return at once when set
 };
 
 struct FrArgs {
@@ -44,6 +45,7 @@ struct FrArgs {
   double* partial;        // [ranges][K][NCP] partial Y per fiber range
   uint32_t ncp;           // padded nc (row stride of partial)
   double* sumsq_part;     // [ranges*igroups] partial sum X^2 (nullable)
+  const int32_t* skip = nullptr;  // device flag: return at once when set
 };
 
 // Host launchers (contract.cu). grid_hint = 0 picks the default persistent grid.

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     fc_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FcTmaArgs a) {
   using C = FcT<NC, MODE>;
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + C::kStages;
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     fr_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FrTmaArgs a) {
   using C = FrT<NC, MODE, MCOL>;
+  if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + C::kStages;

@@ -20,6 +20,7 @@ struct FcTmaArgs {
   uint64_t os_j = 1, os_c = 0, os_p = 0;
   double* sumsq_part = nullptr;                // [grid]
   const double* diff_ref = nullptr;            // diff-norm epilogue instead of a store
+  const int32_t* skip = nullptr;               // device flag: return at once when set
 };
 
 struct FrTmaArgs {
@@ -31,6 +32,7 @@ struct FrTmaArgs {
   double* partial = nullptr;                   // [ranges][K][ncp]
   uint32_t ncp = 0;
   double* sumsq_part = nullptr;                // [ranges*igroups]
+  const int32_t* skip = nullptr;               // device flag: return at once when set
 };
 
 // -1 when the layout is not covered (the caller uses contract.cu's kernels).

@@ -1,0 +1,60 @@
+// Cooperative small dense steps of the ALS sweep (coop.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "als_step.cuh"
+
+namespace tkg {
+
+struct PrepArgs {
+  const double* part = nullptr;  // FR partials [nparts][I][ldp] (from_partials)
+  int nparts = 0;
+  uint32_t ldp = 0;
+  const double* GRinv = nullptr; // r x r
+  int from_partials = 0;
+  uint32_t I = 0, r = 0, ncp = 0;
+  double* Lc = nullptr;          // I x r column-major (read, or written when from_partials)
+  double* GL = nullptr;          // r x r
+  double* GLinv = nullptr;       // r x r
+  double* Mt = nullptr;          // [I][ncp]
+  double* gpart = nullptr;       // [grid][r*r]
+  AlsCtrl* ctrl = nullptr;
+};
+
+struct FinishArgs {
+  const double* R = nullptr;     // row-major [F][ld]
+  uint64_t F = 0, ld = 0;
+  uint32_t r = 0;
+  const double* GL = nullptr;
+  double* GRinv = nullptr;
+  double* gpart = nullptr;       // [grid][ncp*ncp]
+  AlsCtrl* ctrl = nullptr;
+  double* history = nullptr;
+};
+
+struct CholQrArgs {
+  const double* Y = nullptr;     // partials [nparts][I][ldp] or column-major (ld = ldp)
+  int nparts = 0;
+  uint64_t ldp = 0;
+  uint32_t I = 0, r = 0;
+  double* Q = nullptr;           // I x r column-major
+  double* rmat = nullptr;        // r x r (nullable)
+  double* rt = nullptr;          // R^T padded i-major (nullable)
+  uint32_t ldrt = 0;
+  int check = 0;
+  double* gpart = nullptr;       // [grid][r*r]
+  double* L1 = nullptr;          // r*r scratch
+  double* Rinv = nullptr;        // r*r scratch
+  double* work = nullptr;        // 2 doubles
+  AlsCtrl* ctrl = nullptr;       // degenerate_col
+};
+
+int prep_step_grid(uint32_t I);
+int finish_step_grid(uint64_t F, int num_sms);
+cudaError_t launch_prep_step(PrepArgs a, cudaStream_t st);
+cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st);
+cudaError_t launch_cholqr_step(CholQrArgs a, cudaStream_t st);
+
+}  // namespace tkg

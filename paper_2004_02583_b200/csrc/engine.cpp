@@ -7,6 +7,8 @@
 #include <cstring>
 #include <sstream>
 
+#include "als_step.cuh"
+#include "coop.cuh"
 #include "contract_tma.cuh"
 #include "mt_jump.hpp"
 
@@ -187,12 +189,13 @@ void Engine::kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], d
   for (auto& r : recs_) {
     float t = 0;
     CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ev_pool_.push_back(r.a);
+    ev_pool_.push_back(r.b);
+    if (r.cls < 0) continue;  // speculative launch that returned on entry
     stat_ms_[r.cls] += t;
     stat_launch_[r.cls] += 1;
     stat_bytes_[r.cls] += r.bytes;
     stat_flops_[r.cls] += r.flops;
-    ev_pool_.push_back(r.a);
-    ev_pool_.push_back(r.b);
   }
   recs_.clear();
   for (int k = 0; k < 4; ++k) {
@@ -219,7 +222,7 @@ const double* Engine::upload(const double* a, uint64_t n, bool a_dev, DBuf& buf,
 
 void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
                 uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
-                const double* diff_ref, int* grid_used, bool count_pass) {
+                const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip) {
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (profiling_) {
     ev = ev_pair();
@@ -235,6 +238,7 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
     a.os_p = os_p;
     a.sumsq_part = sumsq_part;
     a.diff_ref = diff_ref;
+    a.skip = skip;
     CK(launch_fc_tma(v, mt, ldmt, a, mode, sms_, st_, grid_used));
   } else {
     FcArgs a;
@@ -249,6 +253,7 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
     a.gram_part = nullptr;
     a.sumsq_part = sumsq_part;
     a.diff_ref = diff_ref;
+    a.skip = skip;
     CK(launch_fc(a, sms_, st_, grid_used));
   }
   count_launch();
@@ -275,7 +280,8 @@ uint32_t Engine::fr_ranges(const FiberView& v, uint32_t nc) {
 }
 
 uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, uint32_t nc,
-                    double* partial, double* sumsq_part, bool count_pass, uint32_t* grid_used) {
+                    double* partial, double* sumsq_part, bool count_pass, uint32_t* grid_used,
+                    const int32_t* skip) {
   // M(j, c) = m[j*mj + c*mc]
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (profiling_) {
@@ -289,6 +295,7 @@ uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t mj, uint64_t m
     a.nc = nc;
     a.partial = partial;
     a.sumsq_part = sumsq_part;
+    a.skip = skip;
     CK(launch_fr_tma(v, m, mj, mc, a, mode, sms_, st_, &ranges, &grid));
   } else {
     FrArgs a;
@@ -299,6 +306,7 @@ uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t mj, uint64_t m
     a.nc = nc;
     a.partial = partial;
     a.sumsq_part = sumsq_part;
+    a.skip = skip;
     CK(launch_fr(a, sms_, st_, &ranges, &grid));
   }
   if (grid_used) *grid_used = grid;
@@ -397,32 +405,31 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
 // for the well-conditioned factors ALS produces.
 void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
                     double* rmat, double* rt, uint32_t ldrt, bool check) {
-  const double* Yc = Y;
-  if (nparts > 0) {
-    double* y = qy_.d(uint64_t(I) * r);
-    CK(launch_reduce_partials(Y, nparts, I, uint32_t(ld), r, y, st_));
-    count_launch();
-    Yc = y;
-  } else if (ld != I) {
-    double* y = qy_.d(uint64_t(I) * r);
-    CK(launch_pack(Y, 1, ld, r, I, y, I, st_));  // y[c*I + i] = Y[i + c*ld]
-    count_launch();
-    Yc = y;
-  }
-  const int ng = gram_partials_count(I);
-  double* gp = gram_part_.d(size_t(ng) * r * r);
-  double* L1 = qrl1_.d(size_t(r) * r);
-  double* L2 = qrl2_.d(size_t(r) * r);
-  double* Q1 = qrq1_.d(uint64_t(I) * r);
-  CK(launch_gram_partials(Yc, I, I, r, gp, st_));
-  CK(launch_chol(gp, ng, uint64_t(r) * r, int(r), r, nullptr, L1, &status_d_->qr_fail1, status_d_, st_, 0.0));
-  CK(launch_row_solve(Yc, 0, I, I, r, L1, Q1, nullptr, 0, &status_d_->qr_fail1, st_, 1));
-  CK(launch_gram_partials(Q1, I, I, r, gp, st_));
-  CK(launch_chol(gp, ng, uint64_t(r) * r, int(r), r, nullptr, L2, &status_d_->qr_fail2, status_d_, st_, 0.0));
-  CK(launch_row_solve(Q1, 0, I, I, r, L2, Q, nullptr, 0, &status_d_->qr_fail2, st_, 1));
-  CK(launch_cholqr_finish(L1, L2, r, &status_d_->qr_fail1, &status_d_->qr_fail2, rmat, rt, ldrt,
-                          check ? 1 : 0, status_d_, st_));
-  count_launch(7);
+  CholQrArgs q;
+  q.Y = Y;
+  q.nparts = nparts;
+  q.ldp = ld;
+  q.I = I;
+  q.r = r;
+  q.Q = Q;
+  q.rmat = rmat;
+  q.rt = rt;
+  q.ldrt = ldrt;
+  q.check = check ? 1 : 0;
+  q.gpart = gram_part_.d(size_t(prep_step_grid(I)) * r * r);
+  q.L1 = qrl1_.d(size_t(r) * r);
+  q.Rinv = qrl2_.d(size_t(r) * r);
+  q.work = qrq1_.d(2);
+  q.ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
+  CK(launch_cholqr_step(q, st_));
+  count_launch();
+}
+
+int Engine::qr_degenerate_col() {
+  AlsCtrl h;
+  CK(cudaMemcpyAsync(&h, ctrl_d_.ensure(sizeof(AlsCtrl)), sizeof(AlsCtrl), cudaMemcpyDeviceToHost, st_));
+  sync();
+  return h.degenerate_col;
 }
 
 Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint32_t r,
@@ -449,15 +456,18 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
   const int ngr = gram_rm_count(F, sms_);
   double* grp = fc_gram_.d(size_t(ngr) * ncp * ncp);
-  double* gp = gram_part_.d(size_t(gram_partials_count(uint32_t(I))) * r * r);
   double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
+  double* sumsq = sumsq_d_.d(2);
+  AlsCtrl* ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
+  const int max_iters = std::max(1, cfg.max_iters);
+  double* hist = hist_d_.d(size_t(max_iters));
+  const int32_t* stop = &ctrl->stop;
 
-  status_h_->degenerate_col = 0;
-  // 1. ||A|| and the initial left factor.
+  // 1. ||A|| and the initial left factor (als.cpp:99-120).
   if (cfg.init) {
     if (!sumsq_known) {
       CK(launch_sumsq(A, sh.count(), sq, st_));
-      CK(launch_sum(sq, sumsq_partials_count(sh.count()), &status_d_->sumsq, st_));
+      CK(launch_sum(sq, sumsq_partials_count(sh.count()), sumsq, st_));
       count_launch(2);
     }
     CK(cudaMemcpyAsync(Lc, cfg.init, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
@@ -478,57 +488,110 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     uint32_t fr_grid = 0;
     const uint32_t ranges = fr(v, S, 1, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
     if (!sumsq_known) {  // ||A||^2 fused into the init pass: one partial per CTA
-      CK(launch_sum(sq, int(fr_grid), &status_d_->sumsq, st_));
+      CK(launch_sum(sq, int(fr_grid), sumsq, st_));
       count_launch();
     }
     qr_dev(part, int(ranges), ncp, uint32_t(I), r, Lc, nullptr, nullptr, 0, true);
   }
-  sync();
-  const double norm = std::sqrt(status_h_->sumsq);  // frobenius_norm (tensor_ops.cpp:391-393)
-  if (norm == 0.0) raise(3, "als_low_rank: input tensor has zero norm");
-  if (!cfg.init && status_h_->degenerate_col != 0)
-    raise(6, "als_init: randomized range collapsed at column " + std::to_string(status_h_->degenerate_col) +
-                 " for mode " + std::to_string(mode));
-  out.norm = norm;
+  CK(launch_ctrl_init(ctrl, sumsq, cfg.eta, max_iters, max_iters, cfg.init ? 0 : 1, st_));
+  count_launch();
 
-  // 2. Sweeps (als.cpp:121-160).
-  ModeRep& rep = out.rep;
-  rep.status = 1;
-  double prev = norm;
-  const int max_iters = std::max(1, cfg.max_iters);
+  // 2. Sweeps (als.cpp:121-160), enqueued in batches; kernels of sweeps past
+  //    the stop decision return on entry.
+  int enqueued = 0;
+  int batch = 4;
+  AlsCtrl h;
+  spec_recs_.clear();
+  double* GLinv = cholL;
+  double* GRinv = cholR;
+  double* gpl = gram_part_.d(size_t(prep_step_grid(uint32_t(I))) * r * r);
+  const int nfin = finish_step_grid(F, sms_);
+  double* gpr = fc_gram_.d(size_t(nfin) * ncp * ncp);
+  uint32_t last_ranges = 0;
+  while (true) {
+    const int nb = std::min(batch, max_iters - enqueued);
+    for (int b = 0; b < nb; ++b) {
+      const int k = enqueued + b + 1;  // 1-based sweep
+      PrepArgs pa;
+      pa.part = part;
+      pa.nparts = int(last_ranges);
+      pa.ldp = ncp;
+      pa.GRinv = GRinv;
+      pa.from_partials = k > 1 ? 1 : 0;
+      pa.I = uint32_t(I);
+      pa.r = r;
+      pa.ncp = ncp;
+      pa.Lc = Lc;
+      pa.GL = GL;
+      pa.GLinv = GLinv;
+      pa.Mt = Mt;
+      pa.gpart = gpl;
+      pa.ctrl = ctrl;
+      CK(launch_prep_step(pa, st_));
+      const size_t rec_fc = recs_.size();
+      fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, true, stop);
+      if (profiling_) spec_recs_.push_back({k, 0, rec_fc});
+      FinishArgs fa;
+      fa.R = R;
+      fa.F = F;
+      fa.ld = ncp;
+      fa.r = r;
+      fa.GL = GL;
+      fa.GRinv = GRinv;
+      fa.gpart = gpr;
+      fa.ctrl = ctrl;
+      fa.history = hist;
+      CK(launch_finish_step(fa, sms_, st_));
+      const size_t rec_fr = recs_.size();
+      last_ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr, stop);
+      if (profiling_) spec_recs_.push_back({k, 1, rec_fr});
+      count_launch(2);
+    }
+    enqueued += nb;
+    CK(cudaMemcpyAsync(&h, ctrl, sizeof(AlsCtrl), cudaMemcpyDeviceToHost, st_));
+    sync();
+    if (h.stop || enqueued >= max_iters) break;
+    batch = 8;
+  }
+  (void)GR;
   const std::string singular = mname + ": gram matrix is singular, rank " + std::to_string(r) +
                                " exceeds the numerical rank of the iterate";
-  for (int k = 1; k <= max_iters; ++k) {
-    // right update: G_L, chol, L' = L G_L^{-1} (i-major, padded) -> R = A^T L'
-    CK(launch_gram_partials(Lc, I, uint32_t(I), r, gp, st_));
-    CK(launch_chol(gp, gram_partials_count(uint32_t(I)), uint64_t(r) * r, int(r), r, GL, cholL,
-                   &status_d_->right_singular, status_d_, st_));
-    CK(launch_row_solve(Lc, 0, I, uint32_t(I), r, cholL, nullptr, Mt, ncp, &status_d_->right_singular, st_));
-    count_launch(3);
-    fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, true);
-    CK(launch_gram_rm(R, F, r, ncp, grp, sms_, st_));
-    CK(launch_finish_right(grp, ngr, int(ncp), r, GL, nullptr, GR, cholR, status_d_, st_));
-    count_launch(2);
-    sync();
-    if (status_h_->right_singular) raise(4, singular);
-    const double residual = status_h_->residual;
-    rep.iterations = k;
-    rep.history.push_back(residual);
-    rep.achieved_eta = std::fabs(prev - residual) / norm;
-    if (rep.achieved_eta <= cfg.eta) {
-      rep.status = 0;
-      break;
-    }
-    if (k == max_iters) break;
-    // left update: Y = A R, L = Y G_R^{-1}
-    if (status_h_->left_singular) raise(4, singular);
-    const uint32_t ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr);
-    double* Y = qy_.d(I * r);
-    CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, Y, st_));
-    CK(launch_row_solve(Y, 0, I, uint32_t(I), r, cholR, Lc, nullptr, 0, nullptr, st_));
-    count_launch(2);
-    prev = residual;
+  switch (h.error) {
+    case kAlsErrZeroNorm: raise(3, "als_low_rank: input tensor has zero norm");
+    case kAlsErrDegenerate:
+      raise(6, "als_init: randomized range collapsed at column " + std::to_string(h.degenerate_col) +
+                   " for mode " + std::to_string(mode));
+    case kAlsErrRightSingular:
+    case kAlsErrLeftSingular: raise(4, singular);
+    default: break;
   }
+  // The work counters and the profiling records cover every enqueued pass;
+  // keep the executed ones: FC of sweeps 1..iter, FR of sweeps 1..iter-1
+  // (the stop decision of sweep `iter` skips its left update).
+  {
+    const int fr_run = h.stop ? h.iter - 1 : h.iter;
+    const int skipped = (enqueued - h.iter) + (enqueued - fr_run);
+    const double elems = double(sh.count());
+    const double bytes = 8.0 * (elems + double(F) * r + double(I) * r);
+    passes_ -= uint64_t(skipped);
+    bytes_ -= uint64_t(skipped * bytes);
+    for (const SpecRec& sr : spec_recs_) {
+      const bool ran = sr.kind == 0 ? sr.k <= h.iter : sr.k <= fr_run;
+      if (!ran && sr.rec < recs_.size()) recs_[sr.rec].cls = -1;
+    }
+    spec_recs_.clear();
+  }
+  ModeRep& rep = out.rep;
+  rep.iterations = h.iter;
+  rep.status = h.status;
+  rep.achieved_eta = h.achieved;
+  rep.history.resize(size_t(h.iter));
+  if (h.iter > 0)
+    CK(cudaMemcpyAsync(rep.history.data(), hist, sizeof(double) * h.iter, cudaMemcpyDeviceToHost, st_));
+  sync();
+  out.norm = h.norm;
+  CK(cudaMemcpyAsync(&last_sumsq_, sumsq, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
   return out;
 }
 
@@ -634,7 +697,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     const uint32_t r = uint32_t(ranks[n - 1]);
     const uint64_t I = sh.d[n - 1];
     AlsOut o = run_als(A, sh, n, r, cfg, sumsq_known);
-    if (!sumsq_known) ref_sumsq = status_h_->sumsq;
+    if (!sumsq_known) ref_sumsq = last_sumsq_;
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
     qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
@@ -712,7 +775,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     const uint32_t r = uint32_t(ranks[mode - 1]);
     const uint64_t I = cur.extent(mode), s = cur.stride(mode), F = cur.count() / I, P = F / s;
     AlsOut o = run_als(work, cur, mode, r, cfg, sumsq_known);
-    if (!sumsq_known) ref_sumsq = status_h_->sumsq;
+    if (!sumsq_known) ref_sumsq = last_sumsq_;
     const uint32_t ncp = pad_nc(r);
     U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
     double* RhT = rhatT_.d(size_t(r) * ncp);
@@ -725,7 +788,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     const int nsh = shrink_count(F);
     double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
     CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_));
-    CK(launch_sum(sq, nsh, &status_d_->sumsq, st_));
+    CK(launch_sum(sq, nsh, sumsq_d_.d(2), st_));
     count_launch(2);
     (void)RhT;
     sumsq_known = true;
@@ -797,10 +860,10 @@ void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, ui
   const uint32_t ranges = fr(v, S, 1, F, r, part, nullptr, false, nullptr);
   status_h_->degenerate_col = 0;
   qr_dev(part, int(ranges), ncp, uint32_t(I), r, l_.d(I * r), nullptr, nullptr, 0, true);
-  sync();
-  if (status_h_->degenerate_col != 0)
-    raise(6, "als_init: randomized range collapsed at column " + std::to_string(status_h_->degenerate_col) +
-                 " for mode " + std::to_string(mode));
+  const int bad = qr_degenerate_col();
+  if (bad != 0)
+    raise(6, "als_init: randomized range collapsed at column " + std::to_string(bad) + " for mode " +
+                 std::to_string(mode));
   CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
 }

@@ -145,14 +145,16 @@ class Engine {
   void pregenerate(const std::vector<PreGen>& items, uint64_t seed);
   void fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
           uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
-          const double* diff_ref, int* grid_used, bool count_pass);
+          const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip = nullptr);
   int fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc);
   uint32_t fr_ranges(const FiberView& v, uint32_t nc);
   uint32_t fr(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, uint32_t nc,
-              double* partial, double* sumsq_part, bool count_pass, uint32_t* grid_used);
+              double* partial, double* sumsq_part, bool count_pass, uint32_t* grid_used,
+              const int32_t* skip = nullptr);
   void sync();
   void qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
               double* rmat, double* rt, uint32_t ldrt, bool check);
+  int qr_degenerate_col();
   const double* upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds);
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                                const double* d_core, const std::vector<double*>& d_factors,
@@ -184,7 +186,8 @@ class Engine {
 
   DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
   DBuf fr_part_, fc_gram_, gram_part_, sq_part_, qr_work_, q_, rhat_, rhatT_;
-  DBuf y_seq_, states_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_;
+  DBuf y_seq_, states_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_, sumsq_d_, ctrl_d_, hist_d_;
+  double last_sumsq_ = 0.0;  // ||working tensor||^2 of the last run_als
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   std::vector<DBuf*> factor_bufs_;
   std::map<std::pair<uint64_t, int>, DBuf*> jump_cache_;
@@ -197,6 +200,12 @@ class Engine {
     double bytes, flops;
   };
   std::vector<Rec> recs_;
+  struct SpecRec {
+    int k;       // sweep (1-based)
+    int kind;    // 0 FC (right update), 1 FR (left update)
+    size_t rec;  // index into recs_
+  };
+  std::vector<SpecRec> spec_recs_;
   std::vector<cudaEvent_t> ev_pool_;
   double stat_ms_[4] = {0, 0, 0, 0};
   uint64_t stat_launch_[4] = {0, 0, 0, 0};

@@ -104,7 +104,7 @@ cudaError_t launch_sumsq_diff(const double* a, const double* b, uint64_t n, doub
 // Partial layout: [cta][ncp][ncp] with entry (c1, c2), c1 <= c2 at c1*ncp + c2.
 int gram_rm_count(uint64_t rows, int num_sms);
 cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t ld, double* part,
-                           int num_sms, cudaStream_t st);
+                           int num_sms, cudaStream_t st, const int32_t* skip = nullptr);
 
 // st-HOSVD shrink B_(n) <- R_hat R^T written in tensor layout (hosvd.cpp:176-178):
 // out[jl + c*s + p*s*r] = sum_c' rhat[c + c'*r] * R[(p*s + jl)*ld + c'], plus

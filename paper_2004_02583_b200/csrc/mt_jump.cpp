@@ -239,12 +239,11 @@ std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
 MtPlan mt_plan(uint64_t total) {
   MtPlan p;
   p.total = total;
-  // Enough chunks to fill the GPU for small totals (>= 8192 draws each),
-  // ~64K draws per chunk for large ones, at most 592 (jump cost ~ C).
-  const uint64_t big = (total + 65535) / 65536;
-  const uint64_t small = std::min<uint64_t>(148, (total + 8191) / 8192);
-  uint64_t C = std::max(big, small);
-  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 592));
+  // One warp generates a chunk (~0.3 us per 312 draws) and one chunk costs
+  // one jump (~19937 x 312 bit-word XORs): ~32K draws per chunk balances
+  // the two, capped at 296 chunks (2 per SM).
+  uint64_t C = (total + 32767) / 32768;
+  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 296));
   p.C = static_cast<int>(C);
   p.J = (total + C - 1) / C;
   if (p.J == 0) p.J = 1;

@@ -392,7 +392,9 @@ __global__ void sumsq_diff_kernel(const double* __restrict__ a, const double* __
 // accumulates its upper-triangle 8x8 tiles with DMMA in registers.
 template <int NC>
 __global__ void __launch_bounds__(256) gram_rm_kernel(const double* __restrict__ X, uint64_t rows,
-                                                      uint32_t r, uint64_t ld, double* part) {
+                                                      uint32_t r, uint64_t ld, double* part,
+                                                      const int32_t* skip) {
+  if (skip && *skip) return;
   constexpr int kRows = 128, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2;
   constexpr int kPer = (kTri + 7) / 8;
   extern __shared__ __align__(16) double tile[];  // [2][kRows][kLd]
@@ -552,7 +554,7 @@ int gram_rm_count(uint64_t rows, int num_sms) {
 }
 
 cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t ld, double* part,
-                           int num_sms, cudaStream_t st) {
+                           int num_sms, cudaStream_t st, const int32_t* skip) {
   const int grid = gram_rm_count(rows, num_sms);
   const uint32_t ncp = r <= 8 ? 8 : (r + 7) / 8 * 8;
   switch (ncp) {
@@ -560,7 +562,7 @@ cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t 
   case N: {                                                                               \
     const size_t sm = sizeof(double) * 2 * 128 * (N + 4);                                 \
     cudaFuncSetAttribute(gram_rm_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); \
-    gram_rm_kernel<N><<<grid, 256, sm, st>>>(X, rows, r, ld, part);                        \
+    gram_rm_kernel<N><<<grid, 256, sm, st>>>(X, rows, r, ld, part, skip);                  \
     break;                                                                                \
   }
     TKG_G(8) TKG_G(16) TKG_G(24) TKG_G(32) TKG_G(40) TKG_G(48) TKG_G(56) TKG_G(64)
