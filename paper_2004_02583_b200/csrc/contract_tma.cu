@@ -166,6 +166,13 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const int q = lane & 3;
   const int r8 = lane >> 2;
   double sq_acc = 0.0;
+  // Gram of the output rows (fused epilogue): upper 8x8 tiles (tm <= tn)
+  constexpr bool kGram = NC <= int(kFcGramMaxNc);
+  constexpr int kTri = kGram ? C::kNT * (C::kNT + 1) / 2 : 1;
+  double gacc[kTri][2];
+#pragma unroll
+  for (int t = 0; t < kTri; ++t) gacc[t][0] = gacc[t][1] = 0.0;
+  const bool want_gram = kGram && a.gram_part != nullptr;
   uint32_t it = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t j0 = tile * C::kTF;
@@ -200,6 +207,35 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    // Gram epilogue: G[c1][c2] += sum_rows R[row][c1] R[row][c2] as DMMAs on
+    // fragments rebuilt from the accumulators by shuffles. Fragment t for
+    // rows m*8+k0..+3: lane (r8, q) needs R[m*8+k0+q][t*8+r8], held by lane
+    // 4*(k0+q) + r8/2 as element r8&1 of acc[m][t]. Rows past F are TMA
+    // zero-fill, so they add nothing.
+    if constexpr (kGram) {
+      if (want_gram) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+#pragma unroll
+          for (int k0 = 0; k0 < 8; k0 += 4) {
+            const int src = 4 * (k0 + q) + (r8 >> 1);
+            double fr[C::kNT];
+#pragma unroll
+            for (int t = 0; t < C::kNT; ++t) {
+              const double v0 = __shfl_sync(0xffffffffu, acc[m][t][0], src);
+              const double v1 = __shfl_sync(0xffffffffu, acc[m][t][1], src);
+              fr[t] = (r8 & 1) ? v1 : v0;
+            }
+            int idx = 0;
+#pragma unroll
+            for (int tm = 0; tm < C::kNT; ++tm)
+#pragma unroll
+              for (int tn = tm; tn < C::kNT; ++tn, ++idx) dmma(gacc[idx][0], gacc[idx][1], fr[tm], fr[tn]);
+          }
+        }
+      }
     }
 
     // epilogue straight from registers
@@ -248,6 +284,33 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       double s = 0.0;
       for (int w = 0; w < kCons; ++w) s += red[w];
       a.sumsq_part[blockIdx.x] = s;
+    }
+  }
+  if constexpr (kGram) {
+    if (want_gram) {
+      // every stage has been consumed, so the ring is free: per-warp partials
+      // there, then a fixed-order sum over the 8 warps (deterministic)
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kCons * 32));
+      double* gs = reinterpret_cast<double*>(ring);
+#pragma unroll
+      for (int t = 0; t < kTri; ++t) {
+        gs[(warp * kTri + t) * 64 + lane * 2] = gacc[t][0];
+        gs[(warp * kTri + t) * 64 + lane * 2 + 1] = gacc[t][1];
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kCons * 32));
+      double* out = a.gram_part + size_t(blockIdx.x) * NC * NC;
+      for (int e = threadIdx.x; e < kTri * 64; e += kCons * 32) {
+        double s = 0.0;
+        for (int w = 0; w < kCons; ++w) s += gs[w * kTri * 64 + e];
+        const int t = e / 64, l = (e % 64) / 2, el = e % 2;
+        int tm = 0, rem = t;
+        while (rem >= C::kNT - tm) {
+          rem -= C::kNT - tm;
+          ++tm;
+        }
+        const int tn = tm + rem;
+        out[(tm * 8 + (l >> 2)) * NC + tn * 8 + 2 * (l & 3) + el] = s;
+      }
     }
   }
 }
@@ -416,6 +479,138 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// ---------------------------------------------------------------------------
+// Expansion along the last mode fused with the difference norm:
+//   sq += sum_{j, i} (ref[j + i*F] - sum_c X[j + c*F] U[i + c*Iout])^2
+// (relative_error(t, reconstruct(tk)) without the reconstruction,
+// tensor_ops.cpp:395-440). A CTA keeps the A fragments of a 128-fiber tile
+// of X in registers for all Iout columns; the producer warp streams 32-column
+// blocks of U and of the reference through the TMA ring.
+// ---------------------------------------------------------------------------
+template <int KC>
+struct ExT {
+  static constexpr int kTF = 128, kCB = 32;
+  static constexpr int kLdX = 132, kLdU = 36, kLdR = 132;
+  static constexpr int kStages = KC <= 32 ? 4 : 3;
+  static constexpr int kBytesX = (KC * kLdX * 8 + 127) / 128 * 128;
+  static constexpr int kBytesU = KC * kLdU * 8;
+  static constexpr int kBytesR = kCB * kLdR * 8;
+  static constexpr int kStageBytes = (kBytesU + kBytesR + 127) / 128 * 128;
+  static constexpr size_t kSmem = 1024 + size_t(kBytesX) + size_t(kStages) * kStageBytes;
+};
+
+template <int KC>
+__global__ void __launch_bounds__(kThreadsTma, 1)
+    expand_diff_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmU,
+                           const __grid_constant__ CUtensorMap tmR, uint64_t F, uint32_t Iout,
+                           double* sumsq_part) {
+  using C = ExT<KC>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* xfull = empty + C::kStages;
+  uint64_t* xempty = xfull + 1;
+  double* Xs = reinterpret_cast<double*>(smem_raw + 1024);
+  unsigned char* ring = smem_raw + 1024 + C::kBytesX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t ntiles = (F + C::kTF - 1) / C::kTF;
+  const int nblk = int((Iout + C::kCB - 1) / C::kCB);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCons);
+    }
+    mbar_init(xfull, 1);
+    mbar_init(xempty, kCons);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCons) {
+    if (lane == 0) {
+      prefetch_map(&tmX);
+      prefetch_map(&tmU);
+      prefetch_map(&tmR);
+      uint32_t it = 0, xt = 0;
+      for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++xt) {
+        const int j0 = int(tile * C::kTF);
+        mbar_wait(xempty, (xt & 1) ^ 1);
+        mbar_arrive_expect_tx(xfull, KC * C::kLdX * 8);
+        tma_2d(Xs, &tmX, xfull, j0, 0);
+        for (int b = 0; b < nblk; ++b, ++it) {
+          const int slot = it % C::kStages;
+          const uint32_t ph = (it / C::kStages) & 1;
+          mbar_wait(&empty[slot], ph ^ 1);
+          unsigned char* st = ring + size_t(slot) * C::kStageBytes;
+          mbar_arrive_expect_tx(&full[slot], C::kBytesU + C::kBytesR);
+          tma_2d(st, &tmU, &full[slot], b * C::kCB, 0);
+          tma_2d(st + C::kBytesU, &tmR, &full[slot], j0, b * C::kCB);
+        }
+      }
+    }
+    return;
+  }
+
+  const int q = lane & 3, r8 = lane >> 2;
+  double sq = 0.0;
+  uint32_t it = 0, xt = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++xt) {
+    mbar_wait(xfull, xt & 1);
+    double af[KC / 4][2];
+#pragma unroll
+    for (int t = 0; t < KC / 4; ++t)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) af[t][m] = Xs[(4 * t + q) * C::kLdX + warp * 16 + m * 8 + r8];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xempty);
+    for (int b = 0; b < nblk; ++b, ++it) {
+      const int slot = it % C::kStages;
+      const uint32_t ph = (it / C::kStages) & 1;
+      mbar_wait(&full[slot], ph);
+      const double* Us = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes);
+      const double* Rs = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes + C::kBytesU);
+      double acc[2][4][2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+#pragma unroll
+      for (int t = 0; t < KC / 4; ++t) {
+        double bf[4];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) bf[n] = Us[(4 * t + q) * C::kLdU + n * 8 + r8];
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[t][m], bf[n]);
+      }
+      // rows past F / columns past Iout: TMA zero-fill on both sides
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double d = Rs[(n * 8 + 2 * q + e) * C::kLdR + warp * 16 + m * 8 + r8] - acc[m][n][e];
+            sq = fma(d, d, sq);
+          }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+  }
+  __shared__ double red[kCons];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+  if (lane == 0) red[warp] = sq;
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kCons * 32));
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int w = 0; w < kCons; ++w) s2 += red[w];
+    sumsq_part[blockIdx.x] = s2;
+  }
+}
+
 bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
             const uint32_t* box) {
   auto fn = encode_fn();
@@ -485,6 +680,21 @@ cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTm
     case 64: return CALL(64);               \
     default: return cudaErrorInvalidValue;  \
   }
+
+template <int KC>
+cudaError_t expand_diff_launch(const CUtensorMap& X, const CUtensorMap& U, const CUtensorMap& R,
+                               const ExpandArgs& a, int grid, cudaStream_t st) {
+  using C = ExT<KC>;
+  auto k = expand_diff_tma_kernel<KC>;
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = set_smem(k, C::kSmem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  k<<<grid, kThreadsTma, C::kSmem, st>>>(X, U, R, a.s * a.P, a.Iout, a.sumsq_part);
+  return cudaGetLastError();
+}
 
 }  // namespace
 
@@ -603,6 +813,49 @@ uint32_t fr_tma_ranges(const FiberView& v, int num_sms) {
   ranges = std::min<uint64_t>(ranges, std::max<uint64_t>(1, steps / 4));
   const uint64_t fpr = (steps + ranges - 1) / ranges * 32;
   return uint32_t((F + fpr - 1) / fpr);
+}
+
+bool expand_diff_tma_ok(const ExpandArgs& a) {
+  const uint64_t F = a.s * a.P;
+  return encode_fn() && a.ref && a.P == 1 && a.K >= 1 && a.K <= 64 && F % 2 == 0 && a.Iout % 2 == 0 &&
+         F < (1ull << 31) && aligned16(a.in) && aligned16(a.U) && aligned16(a.ref) && a.sumsq_part;
+}
+
+int expand_diff_tma_grid(uint64_t F, int num_sms) {
+  const uint64_t tiles = (F + 127) / 128;
+  return int(std::max<uint64_t>(1, std::min<uint64_t>(tiles, uint64_t(num_sms))));
+}
+
+cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used) {
+  const uint64_t F = a.s * a.P;
+  const uint32_t kc = a.K <= 8 ? 8 : a.K <= 16 ? 16 : a.K <= 32 ? 32 : 64;
+  CUtensorMap X, U, R;
+  {
+    const uint64_t dims[2] = {F, a.K};
+    const uint64_t strides[1] = {F * 8};
+    const uint32_t box[2] = {132, kc};
+    if (!encode(&X, a.in, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {a.Iout, a.K};
+    const uint64_t strides[1] = {uint64_t(a.Iout) * 8};
+    const uint32_t box[2] = {36, kc};
+    if (!encode(&U, a.U, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {F, a.Iout};
+    const uint64_t strides[1] = {F * 8};
+    const uint32_t box[2] = {132, 32};
+    if (!encode(&R, a.ref, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  const int grid = expand_diff_tma_grid(F, num_sms);
+  if (grid_used) *grid_used = grid;
+  switch (kc) {
+    case 8: return expand_diff_launch<8>(X, U, R, a, grid, st);
+    case 16: return expand_diff_launch<16>(X, U, R, a, grid, st);
+    case 32: return expand_diff_launch<32>(X, U, R, a, grid, st);
+    default: return expand_diff_launch<64>(X, U, R, a, grid, st);
+  }
 }
 
 }  // namespace tkg

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace tkg {
 
@@ -21,7 +22,12 @@ struct FcTmaArgs {
   double* sumsq_part = nullptr;                // [grid]
   const double* diff_ref = nullptr;            // diff-norm epilogue instead of a store
   const int32_t* skip = nullptr;               // device flag: return at once when set
+  double* gram_part = nullptr;                 // [grid][NC*NC] upper tiles of out^T out (NC <= 32)
 };
+
+// NC (padded column count) up to which the FC kernel can fuse the Gram of
+// its output into the epilogue.
+constexpr uint32_t kFcGramMaxNc = 32;
 
 struct FrTmaArgs {
   uint64_t s = 0, P = 0;
@@ -47,5 +53,11 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
 cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, FrTmaArgs a,
                           int mode, int num_sms, cudaStream_t st, uint32_t* ranges_used,
                           uint32_t* grid_used);
+
+// Last-mode expansion fused with the difference norm against a.ref (P == 1,
+// even F and Iout, K <= 64); sumsq_part[grid].
+bool expand_diff_tma_ok(const ExpandArgs& a);
+int expand_diff_tma_grid(uint64_t F, int num_sms);
+cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used);
 
 }  // namespace tkg

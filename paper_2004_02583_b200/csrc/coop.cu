@@ -1,18 +1,27 @@
 // Cooperative (grid-synchronised) small dense steps of the ALS sweep.
 //
-// Each step is one launch whose phases are separated by grid.sync(): row
-// blocks of the I x r factor are processed by many CTAs (32 rows each), the
-// r x r factorizations by CTA 0. The normal-equation solves use the explicit
-// inverse of the r x r Gram matrix (from its Cholesky factor, with the
-// spd_solve pivot floor, kernels.cpp:378-393), so applying it to a row is an
-// r-wide dot product per output instead of a dependent substitution chain.
+// Each step is one persistent launch (one CTA per SM) whose phases are
+// separated by grid.sync(): the split-K partial sums and the Gram partials
+// are reduced by the whole grid, the I x r factor is processed in 32-row
+// blocks by a grid-stride loop, and the r x r factorizations run on CTA 0.
+// The normal-equation solves use the explicit inverse of the r x r Gram
+// matrix (with the spd_solve pivot floor, kernels.cpp:378-393), so applying
+// it to a row is an r-wide dot product per output instead of a dependent
+// substitution chain.
 //
-//   prep_step   : [L = (sum FR partials) G_R^{-1}]  G_L = L^T L  chol  G_L^{-1}
+//   prep_step   : [L = (sum FR partials) G_R^{-1}]  G_L = L^T L  G_L^{-1}
 //                 Mt = L G_L^{-1} (i-major, the FC operand)     (als.cpp:36-50)
-//   finish_step : G_R = R^T R (DMMA), closed-form residual, the stop rule,
-//                 chol(G_R) and G_R^{-1} for the next left update (als.cpp:52-55,136-160)
+//   finish_step : G_R = R^T R (fused into the FC epilogue up to r = 32, else
+//                 a DMMA row pass here), closed-form residual, the stop rule,
+//                 G_R^{-1} for the next left update (als.cpp:52-55,136-160)
 //   cholqr_step : CholQR2 thin QR with R_ii > 0 and the reference's
 //                 degeneracy test (kernels.cpp:303-367, als.cpp:74-86)
+//
+// The r x r kernels on CTA 0 (Cholesky, triangular inverse, Gauss-Jordan
+// inverse) keep each thread's matrix entries in registers; the one row /
+// column every step needs is published to a double-buffered shared vector by
+// its owners, so a step costs one barrier and a few independent loads.
+// Every reduction runs in a fixed order (deterministic results).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -25,175 +34,407 @@ namespace cg = cooperative_groups;
 
 namespace tkg {
 
+#ifdef TKG_PHASE_TIMING
+__device__ unsigned long long g_phase_ns[64];
+#define PHASE(k)                                                                            \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                              \
+      unsigned long long t_;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      g_phase_ns[k] = t_;                                                                   \
+    }                                                                                       \
+  } while (0)
+#else
+#define PHASE(k) \
+  do {           \
+  } while (0)
+#endif
+
 namespace {
 
-constexpr int kRowsB = 32;     // factor rows per CTA
+constexpr int kRB = 32;        // factor rows per block
 constexpr int kThreads = 256;
+constexpr int kMaxR = 64;
+constexpr int kGE = (kMaxR * kMaxR + kThreads - 1) / kThreads;  // Gram entries per thread
 
-// Lower Cholesky of G (column-major r x r) into L; floor_rel as spd_solve.
-// Returns failing column + 1 or 0. One CTA.
-__device__ int chol_cta(const double* G, double* L, uint32_t r, double floor_rel, double* piv_out) {
-  __shared__ double floor_s, piv_s;
-  __shared__ int fail_s;
-  if (threadIdx.x == 0) {
-    double md = 0.0;
-    for (uint32_t i = 0; i < r; ++i) md = fmax(md, G[i + i * r]);
-    floor_s = floor_rel * md;
-    fail_s = 0;
+// entries of an r x r matrix per thread
+__host__ __device__ constexpr int ke_for(int r) { return (r * r + kThreads - 1) / kThreads; }
+
+// ---- one-CTA dense kernels (CTA 0), register-resident -------------------------------
+// Thread t owns the column-major entries e = t + k*kThreads (k < KE); entries
+// past r*r get the dummy index (r, r), which every step treats as a no-op
+// owner of slot r of the shared vectors (sized kMaxR + 1).
+template <int KE>
+struct Owned {
+  double v[KE];
+  int i[KE], j[KE];
+  __device__ explicit Owned(uint32_t r) {
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      const uint32_t e = threadIdx.x + t * kThreads;
+      const bool ok = e < r * r;
+      i[t] = ok ? int(e % r) : int(r);
+      j[t] = ok ? int(e / r) : int(r);
+      v[t] = 0.0;
+    }
   }
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) L[e] = 0.0;
+  __device__ bool valid(int t, uint32_t r) const { return i[t] < int(r); }
+};
+
+// Lower Cholesky factor of G (column-major, smem) into L (smem): right-looking
+// updates of the unscaled Schur complement; column k+1 is published once its
+// last update (step k) is done. Positivity is the only pivot test (CholQR).
+// Returns the failing column + 1 or 0.
+template <int KE>
+__device__ int chol_reg(const double* G, double* L, uint32_t r) {
+  __shared__ double cb[2][kMaxR + 1];
+  __shared__ double dg[kMaxR + 1];
+  Owned<KE> o(r);
+#pragma unroll
+  for (int t = 0; t < KE; ++t) {
+    if (o.valid(t, r) && o.i[t] >= o.j[t]) o.v[t] = G[o.i[t] + o.j[t] * r];
+    if (o.j[t] == 0) cb[0][o.i[t]] = o.v[t];
+  }
+  __syncthreads();
+  int fail = 0;
+  for (uint32_t k = 0; k < r; ++k) {
+    const double* c = cb[k & 1];
+    double* cn = cb[(k + 1) & 1];
+    const double p = c[k];  // uniform across the CTA
+    if (!(p > 0.0)) {
+      fail = int(k) + 1;
+      break;
+    }
+    if (threadIdx.x == 0) dg[k] = p;
+    const double inv = __drcp_rn(p);
+    double ci[KE], cj[KE];
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      ci[t] = c[o.i[t]];
+      cj[t] = c[o.j[t]];
+    }
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      const int i = o.i[t], j = o.j[t];
+      if (j > int(k) && i >= j) o.v[t] = fma(-ci[t] * inv, cj[t], o.v[t]);
+      if (j == int(k) + 1) cn[i] = o.v[t];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    __syncthreads();
+    return fail;
+  }
+#pragma unroll
+  for (int t = 0; t < KE; ++t) {
+    if (!o.valid(t, r)) continue;
+    const int i = o.i[t], j = o.j[t];
+    const double d = sqrt(dg[j]);
+    L[i + j * r] = i > j ? o.v[t] / d : (i == j ? d : 0.0);
+  }
+  __syncthreads();
+  return 0;
+}
+
+// X = L^{-1} (lower) by right-looking forward substitution on the identity:
+// row k, final up to its 1/L_kk scale after step k-1, updates the rows below.
+template <int KE>
+__device__ void tri_inv_reg(const double* L, double* X, uint32_t r) {
+  __shared__ double rb[2][kMaxR + 1];
+  Owned<KE> o(r);
+#pragma unroll
+  for (int t = 0; t < KE; ++t) {
+    o.v[t] = o.i[t] == o.j[t] ? 1.0 : 0.0;
+    if (o.i[t] == 0) rb[0][o.j[t]] = o.v[t];
+  }
+  __syncthreads();
+  for (uint32_t k = 0; k + 1 < r; ++k) {
+    const double* u = rb[k & 1];
+    double* un = rb[(k + 1) & 1];
+    const double rk = __drcp_rn(L[k + k * r]);
+    double lik[KE], ukc[KE];
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      lik[t] = L[min(o.i[t], int(r) - 1) + k * r];
+      ukc[t] = u[o.j[t]];
+    }
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      const int i = o.i[t], c = o.j[t];
+      if (i > int(k) && c <= int(k) && i < int(r)) o.v[t] = fma(-lik[t] * rk, ukc[t], o.v[t]);
+      if (i == int(k) + 1) un[c] = o.v[t];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < KE; ++t) {
+    if (!o.valid(t, r)) continue;
+    const int i = o.i[t], c = o.j[t];
+    X[i + c * r] = i >= c ? o.v[t] / L[i + i * r] : 0.0;
+  }
+  __syncthreads();
+}
+
+// Inverse of the SPD matrix G (column-major, smem) by Gauss-Jordan elimination
+// without pivoting into out (smem). The pivot of step k is the Schur
+// complement diagonal, i.e. the Cholesky pivot, tested with spd_solve's floor
+// (pivot <= floor_rel * max diag fails, kernels.cpp:378-393). Row k and
+// column k of the current matrix are published by their owners. Returns the
+// failing column + 1 (pivot in *piv_out) or 0.
+template <int KE>
+__device__ int gj_inv_reg(const double* G, double* out, uint32_t r, double floor_rel, double* piv_out) {
+  __shared__ double rowb[2][kMaxR + 1], colb[2][kMaxR + 1];
+  Owned<KE> o(r);
+  double md = 0.0;
+  for (uint32_t i = 0; i < r; ++i) md = fmax(md, G[i + i * r]);
+  const double floor_v = floor_rel * md;
+#pragma unroll
+  for (int t = 0; t < KE; ++t) {
+    if (o.valid(t, r)) o.v[t] = G[o.i[t] + o.j[t] * r];
+    if (o.i[t] == 0) rowb[0][o.j[t]] = o.v[t];
+    if (o.j[t] == 0) colb[0][o.i[t]] = o.v[t];
+  }
   __syncthreads();
   for (uint32_t k = 0; k < r; ++k) {
-    if (threadIdx.x == 0) {
-      double pivot = G[k + k * r];
-      for (uint32_t p = 0; p < k; ++p) pivot -= L[k + p * r] * L[k + p * r];
-      if (pivot <= floor_s || !(pivot > 0.0)) {
-        fail_s = int(k) + 1;
-        piv_s = pivot;
-      } else {
-        L[k + k * r] = sqrt(pivot);
+    const double* rw = rowb[k & 1];
+    const double* cl = colb[k & 1];
+    double* rwn = rowb[(k + 1) & 1];
+    double* cln = colb[(k + 1) & 1];
+    const double p = rw[k];  // uniform across the CTA
+    if (!(p > floor_v) || !(p > 0.0)) {
+      if (piv_out && threadIdx.x == 0) *piv_out = p;
+      __syncthreads();
+      return int(k) + 1;
+    }
+    const double ip = __drcp_rn(p);
+    double aik[KE], akj[KE];
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      aik[t] = cl[o.i[t]];
+      akj[t] = rw[o.j[t]];
+    }
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      const int i = o.i[t], j = o.j[t];
+      const double old = o.v[t];
+      double v;
+      if (i == int(k)) v = j == int(k) ? ip : old * ip;
+      else if (j == int(k)) v = -old * ip;
+      else v = fma(-aik[t] * ip, akj[t], old);
+      o.v[t] = v;
+      if (i == int(k) + 1) rwn[j] = v;
+      if (j == int(k) + 1) cln[i] = v;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < KE; ++t)
+    if (o.valid(t, r)) out[o.i[t] + o.j[t] * r] = o.v[t];
+  __syncthreads();
+  return 0;
+}
+
+// ---- grid-wide reductions -----------------------------------------------------------
+
+// Gs (global, column-major r x r, symmetric) = sum over k of
+// part[k*pld + a*rs + b] for a <= b: one warp per entry, lanes over k, a
+// fixed xor tree (lane 0's sum is the result).
+__device__ void reduce_gram_grid(const double* part, int nparts, uint64_t pld, uint32_t rs, uint32_t r,
+                                 double* Gs) {
+  const uint32_t wpb = blockDim.x >> 5;
+  const uint32_t nw = gridDim.x * wpb;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t ntri = r * (r + 1) / 2;
+  for (uint32_t t = blockIdx.x * wpb + (threadIdx.x >> 5); t < ntri; t += nw) {
+    uint32_t a = 0, rem = t;
+    while (rem >= r - a) {
+      rem -= r - a;
+      ++a;
+    }
+    const uint32_t b = a + rem;
+    const double* p = part + size_t(a) * rs + b;
+    double s = 0.0;
+    for (int k = int(lane); k < nparts; k += 32) s += p[size_t(k) * pld];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) {
+      Gs[a + b * r] = s;
+      Gs[b + a * r] = s;
+    }
+  }
+}
+
+// part[0][i][c] = sum_k part[k][i][c] (c < r), in place. G = 2^g lanes share
+// an entry (as many as the grid affords, <= 32): lane `sub` sums k = sub,
+// sub + G, ... in order, then a fixed xor tree over the G lanes.
+__device__ void reduce_partials_grid(double* part, int nparts, uint32_t I, uint32_t ldp, uint32_t r) {
+  const uint64_t n = uint64_t(I) * r;
+  const uint64_t stride = uint64_t(I) * ldp;
+  const uint64_t T = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t G = 1;
+  while (G < 32 && uint64_t(2 * G) * n <= T && int(2 * G) <= nparts) G *= 2;
+  const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t sub = uint32_t(gt % G);
+  for (uint64_t e = gt / G;; e += T / G) {
+    const bool act = e < n;
+    if (!__any_sync(0xffffffffu, act)) break;
+    double s = 0.0;
+    double* p = nullptr;
+    if (act) {
+      const uint64_t i = e / r, c = e % r;
+      p = part + i * ldp + c;
+      int k = int(sub);
+      for (; k + 7 * int(G) < nparts; k += 8 * int(G)) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = p[size_t(k + u * int(G)) * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
       }
+      for (; k < nparts; k += int(G)) s += p[size_t(k) * stride];
     }
-    __syncthreads();
-    if (fail_s) break;
-    const double dkk = L[k + k * r];
-    for (uint32_t i = k + 1 + threadIdx.x; i < r; i += blockDim.x) {
-      double acc = G[i + k * r];
-      for (uint32_t p = 0; p < k; ++p) acc -= L[i + p * r] * L[k + p * r];
-      L[i + k * r] = acc / dkk;
-    }
-    __syncthreads();
+    for (uint32_t off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (act && sub == 0) p[0] = s;
   }
-  if (piv_out && fail_s && threadIdx.x == 0) *piv_out = piv_s;
-  const int f = fail_s;
-  __syncthreads();
-  return f;
 }
 
-// Linv = L^{-1} (lower), column c by forward substitution on e_c. One CTA.
-__device__ void tri_inv_cta(const double* L, double* Linv, uint32_t r) {
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) Linv[e] = 0.0;
-  __syncthreads();
-  for (uint32_t c = threadIdx.x; c < r; c += blockDim.x) {
-    for (uint32_t a = c; a < r; ++a) {
-      double acc = a == c ? 1.0 : 0.0;
-      for (uint32_t p = c; p < a; ++p) acc -= L[a + p * r] * Linv[p + c * r];
-      Linv[a + c * r] = acc / L[a + a * r];
+// ---- row-block helpers ---------------------------------------------------------------
+
+// X[row][c] (pitch ld) = rows i0.. of a row-major or column-major I x r
+// matrix with leading dimension ld_src.
+__device__ void load_rows(const double* src, bool row_major, uint64_t ld_src, uint32_t i0, uint32_t nrow,
+                          uint32_t r, double* X, uint32_t ld) {
+  if (row_major) {
+    for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
+      const uint32_t row = e / r, c = e % r;
+      X[row * ld + c] = src[uint64_t(i0 + row) * ld_src + c];
+    }
+  } else {
+    for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
+      const uint32_t row = e % nrow, c = e / nrow;
+      X[row * ld + c] = src[(i0 + row) + uint64_t(c) * ld_src];
     }
   }
-  __syncthreads();
 }
 
-// Ginv = L^{-T} L^{-1} (symmetric, column-major). One CTA.
-__device__ void spd_inv_cta(const double* Linv, double* Ginv, uint32_t r) {
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const uint32_t a = e % r, c = e / r;
-    const uint32_t k0 = max(a, c);
-    double s = 0.0;
-    for (uint32_t k = k0; k < r; ++k) s += Linv[k + a * r] * Linv[k + c * r];
-    Ginv[e] = s;
-  }
-  __syncthreads();
-}
-
-// Upper-triangle Gram partial of the CTA's rows (rows x r, row-major in smem,
-// pitch ld): part[(a, b)] at a*r + b for a <= b.
-__device__ void rows_gram(const double* X, uint32_t nrow, uint32_t r, uint32_t ld, double* part) {
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const uint32_t a = e / r, b = e % r;
-    double s = 0.0;
-    if (a <= b)
-      for (uint32_t row = 0; row < nrow; ++row) s += X[row * ld + a] * X[row * ld + b];
-    part[e] = s;
+__device__ void store_rows_cm(const double* X, uint32_t ld, uint32_t i0, uint32_t nrow, uint32_t r,
+                              double* dst, uint64_t ld_dst) {
+  for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
+    const uint32_t row = e % nrow, c = e / nrow;
+    dst[(i0 + row) + uint64_t(c) * ld_dst] = X[row * ld + c];
   }
 }
 
-// G (column-major, symmetric) = sum_k part[k] (upper entries, fixed order).
-__device__ void reduce_gram(const double* part, int nparts, uint64_t pld, uint32_t rowstride, uint32_t r,
-                            double* G) {
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const uint32_t i = e % r, j = e / r;
-    const uint32_t a = min(i, j), b = max(i, j);
-    const double* p = part + size_t(a) * rowstride + b;
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < nparts; ++k) s += p[size_t(k) * pld];
-    G[e] = s;
-  }
-  __syncthreads();
-}
-
-// out[row][c] = sum_k X[row][k] M[k + c*r]  (rows in smem, pitch ld)
-__device__ void rows_mul(const double* X, uint32_t nrow, uint32_t r, uint32_t ld, const double* M,
+// out[row][c] = sum_k X[row][k] Mr[k*r + c]  (rows in smem with pitch ld; Mr
+// row-major so that a warp's consecutive c read consecutive banks)
+__device__ void rows_mul(const double* X, uint32_t nrow, uint32_t r, uint32_t ld, const double* Mr,
                          double* out, uint32_t ldo) {
   for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
     const uint32_t row = e / r, c = e % r;
     double s = 0.0;
-    for (uint32_t k = 0; k < r; ++k) s = fma(X[row * ld + k], M[k + c * r], s);
+    for (uint32_t k = 0; k < r; ++k) s = fma(X[row * ld + k], Mr[k * r + c], s);
     out[row * ldo + c] = s;
   }
 }
 
+// Mr[k*r + c] = M(k, c) for a column-major r x r M in global memory.
+__device__ void load_mat_rm(const double* M, double* Mr, uint32_t r) {
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const uint32_t k = e / r, c = e % r;
+    Mr[e] = M[k + c * r];
+  }
+  __syncthreads();
+}
+
+__device__ void load_mat(const double* src, double* dst, uint32_t n) {
+  for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
+  __syncthreads();
+}
+
+// Per-thread Gram accumulators: entry e = tid + t*blockDim (a = e / r,
+// b = e % r, a <= b) over the CTA's row blocks.
+struct GramAcc {
+  double g[kGE];
+  __device__ void zero() {
+#pragma unroll
+    for (int t = 0; t < kGE; ++t) g[t] = 0.0;
+  }
+  __device__ void add(const double* X, uint32_t nrow, uint32_t r, uint32_t ld) {
+#pragma unroll
+    for (int t = 0; t < kGE; ++t) {
+      const uint32_t e = threadIdx.x + t * blockDim.x;
+      if (e < r * r) {
+        const uint32_t a = e / r, b = e % r;
+        if (a <= b) {
+          double s = g[t];
+          for (uint32_t row = 0; row < nrow; ++row) s = fma(X[row * ld + a], X[row * ld + b], s);
+          g[t] = s;
+        }
+      }
+    }
+  }
+  __device__ void store(double* part, uint32_t r) const {
+#pragma unroll
+    for (int t = 0; t < kGE; ++t) {
+      const uint32_t e = threadIdx.x + t * blockDim.x;
+      if (e < r * r) part[e] = g[t];
+    }
+  }
+};
+
 // ---- prep_step -------------------------------------------------------------------
+template <int KE>
 __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
   cg::grid_group grid = cg::this_grid();
   AlsCtrl* ctrl = a.ctrl;
   if (ctrl->stop) return;  // uniform: nobody writes stop before the first grid.sync
   extern __shared__ double sm[];
-  const uint32_t r = a.r, ld = r + 1;
-  double* X = sm;                        // [kRowsB][ld]
-  double* M = X + kRowsB * ld;           // r*r
-  double* W = M + r * r;                 // r*r (CTA 0 scratch)
-  double* W2 = W + r * r;                // r*r
-  const uint32_t i0 = blockIdx.x * kRowsB;
-  const uint32_t nrow = i0 < a.I ? min(uint32_t(kRowsB), a.I - i0) : 0;
+  const uint32_t r = a.r, ld = r + 1, I = a.I;
+  double* X = sm;                 // [kRB][ld]
+  double* X2 = X + kRB * ld;      // [kRB][ld]
+  double* M = X2 + kRB * ld;      // r*r
+  double* W = M + r * r;          // r*r (CTA 0 scratch)
+  const uint32_t nblk = (I + kRB - 1) / kRB;
 
-  // Phase 1: the CTA's rows of L, and their Gram partial
-  if (a.from_partials) {
-    for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) M[e] = a.GRinv[e];
-    double* Y = W;  // reuse as [kRowsB][ld] only if it fits: use X for Y, compute into W2? keep simple:
-    (void)Y;
-    for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-      const uint32_t row = e / r, c = e % r;
-      const double* p = a.part + size_t(i0 + row) * a.ldp + c;
-      double s = 0.0;
-#pragma unroll 4
-      for (int k = 0; k < a.nparts; ++k) s += p[size_t(k) * a.I * a.ldp];
-      X[row * ld + c] = s;
-    }
-    __syncthreads();
-    // L rows = Y rows G_R^{-1}; written back over X through a register pass
-    double vals[8];
-    uint32_t cnt = 0;
-    for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-      const uint32_t row = e / r, c = e % r;
-      double s = 0.0;
-      for (uint32_t k = 0; k < r; ++k) s = fma(X[row * ld + k], M[k + c * r], s);
-      vals[cnt++] = s;
-    }
-    __syncthreads();
-    cnt = 0;
-    for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-      const uint32_t row = e / r, c = e % r;
-      X[row * ld + c] = vals[cnt];
-      a.Lc[(i0 + row) + uint64_t(c) * a.I] = vals[cnt];
-      ++cnt;
-    }
-  } else {
-    for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-      const uint32_t row = e % nrow, c = e / nrow;
-      X[row * ld + c] = a.Lc[(i0 + row) + uint64_t(c) * a.I];
-    }
+  // Phase A: sum of the FR partials into slot 0
+  if (a.from_partials && a.nparts > 1) {
+    reduce_partials_grid(a.part, a.nparts, I, a.ldp, r);
+    grid.sync();
   }
-  __syncthreads();
-  rows_gram(X, nrow, r, ld, a.gpart + size_t(blockIdx.x) * r * r);
+  // Phase B: L rows (from partials: Y G_R^{-1}, kept row-major in slot 0 and
+  // written to Lc), and their Gram partial
+  if (a.from_partials) load_mat_rm(a.GRinv, M, r);
+  GramAcc g;
+  g.zero();
+  for (uint32_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const uint32_t i0 = b * kRB, nrow = min(uint32_t(kRB), I - i0);
+    if (a.from_partials) {
+      load_rows(a.part, true, a.ldp, i0, nrow, r, X, ld);
+      __syncthreads();
+      rows_mul(X, nrow, r, ld, M, X2, ld);
+      __syncthreads();
+      for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
+        const uint32_t row = e / r, c = e % r;
+        a.part[uint64_t(i0 + row) * a.ldp + c] = X2[row * ld + c];
+      }
+      store_rows_cm(X2, ld, i0, nrow, r, a.Lc, I);
+    } else {
+      load_rows(a.Lc, false, I, i0, nrow, r, X2, ld);
+      __syncthreads();
+    }
+    g.add(X2, nrow, r, ld);
+    __syncthreads();
+  }
+  g.store(a.gpart + size_t(blockIdx.x) * r * r, r);
+  grid.sync();
+  reduce_gram_grid(a.gpart, gridDim.x, uint64_t(r) * r, r, r, a.gs);
   grid.sync();
 
-  // Phase 2 (CTA 0): G_L, Cholesky with the spd_solve floor, G_L^{-1}
+  // Phase C (CTA 0): G_L, its inverse with the spd_solve pivot floor
   if (blockIdx.x == 0) {
-    reduce_gram(a.gpart, gridDim.x, uint64_t(r) * r, r, r, M);
+    load_mat(a.gs, M, r * r);
     double piv = 0.0;
-    const int fail = chol_cta(M, W, r, 1e-13, &piv);
+    const int fail = gj_inv_reg<KE>(M, W, r, 1e-13, &piv);
     if (fail) {
       if (threadIdx.x == 0) {
         ctrl->error = kAlsErrRightSingular;
@@ -201,24 +442,30 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
         ctrl->stop = 1;
       }
     } else {
-      for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.GL[e] = M[e];
-      tri_inv_cta(W, W2, r);
-      spd_inv_cta(W2, M, r);
-      for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.GLinv[e] = M[e];
+      for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+        a.GL[e] = M[e];
+        a.GLinv[e] = W[e];
+      }
     }
   }
   grid.sync();
   if (ctrl->stop) return;
 
-  // Phase 3: Mt rows = L rows G_L^{-1}, padded to ncp
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) M[e] = a.GLinv[e];
-  __syncthreads();
-  for (uint32_t e = threadIdx.x; e < nrow * a.ncp; e += blockDim.x) {
-    const uint32_t row = e / a.ncp, c = e % a.ncp;
-    double s = 0.0;
-    if (c < r)
-      for (uint32_t k = 0; k < r; ++k) s = fma(X[row * ld + k], M[k + c * r], s);
-    a.Mt[uint64_t(i0 + row) * a.ncp + c] = s;
+  // Phase D: Mt rows = L rows G_L^{-1}, padded to ncp
+  load_mat_rm(a.GLinv, M, r);
+  for (uint32_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const uint32_t i0 = b * kRB, nrow = min(uint32_t(kRB), I - i0);
+    if (a.from_partials) load_rows(a.part, true, a.ldp, i0, nrow, r, X, ld);
+    else load_rows(a.Lc, false, I, i0, nrow, r, X, ld);
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < nrow * a.ncp; e += blockDim.x) {
+      const uint32_t row = e / a.ncp, c = e % a.ncp;
+      double s = 0.0;
+      if (c < r)
+        for (uint32_t k = 0; k < r; ++k) s = fma(X[row * ld + k], M[k * r + c], s);
+      a.Mt[uint64_t(i0 + row) * a.ncp + c] = s;
+    }
+    __syncthreads();
   }
 }
 
@@ -235,8 +482,9 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
   const uint32_t r = a.r;
 
-  // Phase 1: Gram partial of the CTA's contiguous row range of R (row-major [F][ld])
-  {
+  // Phase 1 (R^T R not fused into FC): Gram partial of the CTA's contiguous
+  // row range of R (row-major [F][ld])
+  if (a.gram_nparts == 0) {
     double acc[kPer][2];
     int tm[kPer], tn[kPer];
 #pragma unroll
@@ -284,18 +532,21 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
       out[c1 * NC + c2] = acc[k][0];
       out[c1 * NC + c2 + 1] = acc[k][1];
     }
+    grid.sync();
   }
+  reduce_gram_grid(a.gpart, a.gram_nparts ? a.gram_nparts : int(gridDim.x), uint64_t(NC) * NC, NC, r,
+                   a.gs);
   grid.sync();
   if (blockIdx.x != 0) return;
 
   // Phase 2 (CTA 0): residual, stop rule, G_R^{-1}
   double* G = sm;
-  double* L = G + r * r;
-  double* Li = L + r * r;
+  double* Gi = G + r * r;
   __syncthreads();
-  reduce_gram(a.gpart, gridDim.x, uint64_t(NC) * NC, NC, r, G);
+  load_mat(a.gs, G, r * r);
   __shared__ double hi_s[32], lo_s[32];
   if (threadIdx.x < 32) {
+    // compensated trace(G_L G_R) (als.cpp:136-141)
     double s = 0.0, c = 0.0;
     for (uint32_t e = threadIdx.x; e < r * r; e += 32) {
       const double p = a.GL[e] * G[e];
@@ -341,7 +592,7 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
   __syncthreads();
   if (!cont_s) return;
   double piv = 0.0;
-  const int fail = chol_cta(G, L, r, 1e-13, &piv);
+  const int fail = gj_inv_reg<ke_for(NC)>(G, Gi, r, 1e-13, &piv);
   if (fail) {
     if (threadIdx.x == 0) {
       ctrl->error = kAlsErrLeftSingular;
@@ -350,77 +601,94 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
     }
     return;
   }
-  tri_inv_cta(L, Li, r);
-  spd_inv_cta(Li, G, r);
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.GRinv[e] = G[e];
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.GRinv[e] = Gi[e];
 }
 
 // ---- cholqr_step -------------------------------------------------------------------
+template <int KE>
 __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
-  const uint32_t r = a.r, ld = r + 1;
-  double* X = sm;                 // [kRowsB][ld] rows of Y, then Q1
-  double* M = X + kRowsB * ld;    // r*r
+  const uint32_t r = a.r, ld = r + 1, I = a.I;
+  double* X = sm;                 // [kRB][ld]
+  double* X2 = X + kRB * ld;      // [kRB][ld]
+  double* M = X2 + kRB * ld;      // r*r
   double* W = M + r * r;          // r*r
   double* W2 = W + r * r;         // r*r
-  double* X2 = W2 + r * r;        // [kRowsB][ld]
-  __shared__ int fail_s;
-  const uint32_t i0 = blockIdx.x * kRowsB;
-  const uint32_t nrow = i0 < a.I ? min(uint32_t(kRowsB), a.I - i0) : 0;
+  const uint32_t nblk = (I + kRB - 1) / kRB;
+  const bool rm = a.nparts > 0;   // Y as row-major partials (summed into slot 0)
+  PHASE(0);
 
-  // Phase 1: rows of Y, Gram partial
-  for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-    const uint32_t row = e / r, c = e % r;
-    double v;
-    if (a.nparts > 0) {
-      const double* p = a.Y + size_t(i0 + row) * a.ldp + c;
-      v = 0.0;
-#pragma unroll 4
-      for (int k = 0; k < a.nparts; ++k) v += p[size_t(k) * a.I * a.ldp];
-    } else {
-      v = a.Y[(i0 + row) + uint64_t(c) * a.ldp];
-    }
-    X[row * ld + c] = v;
+  // Phase 1: Y rows, Gram partial
+  if (a.nparts > 1) {
+    reduce_partials_grid(a.Y, a.nparts, I, uint32_t(a.ldp), r);
+    grid.sync();
   }
-  __syncthreads();
-  rows_gram(X, nrow, r, ld, a.gpart + size_t(blockIdx.x) * r * r);
+  PHASE(1);
+  GramAcc g;
+  g.zero();
+  for (uint32_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const uint32_t i0 = b * kRB, nrow = min(uint32_t(kRB), I - i0);
+    load_rows(a.Y, rm, a.ldp, i0, nrow, r, X, ld);
+    __syncthreads();
+    g.add(X, nrow, r, ld);
+    __syncthreads();
+  }
+  g.store(a.gpart + size_t(blockIdx.x) * r * r, r);
   grid.sync();
+  PHASE(2);
+  reduce_gram_grid(a.gpart, gridDim.x, uint64_t(r) * r, r, r, a.gs);
+  grid.sync();
+  PHASE(3);
   // Phase 2 (CTA 0): chol (no floor), R1^{-1} = (L1^{-1})^T
   if (blockIdx.x == 0) {
-    reduce_gram(a.gpart, gridDim.x, uint64_t(r) * r, r, r, M);
-    const int fail = chol_cta(M, W, r, 0.0, nullptr);
-    if (threadIdx.x == 0) a.work[0] = fail;  // shared with the other CTAs
+    load_mat(a.gs, M, r * r);
+    const int fail = chol_reg<KE>(M, W, r);
+    PHASE(4);
+    if (threadIdx.x == 0) a.work[0] = fail;
     if (!fail) {
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.L1[e] = W[e];
-      tri_inv_cta(W, W2, r);  // L1^{-1} (lower)
+      tri_inv_reg<KE>(W, W2, r);  // L1^{-1} (lower)
+      PHASE(5);
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.Rinv[e] = W2[e];
     }
   }
   grid.sync();
-  if (threadIdx.x == 0) fail_s = int(a.work[0]);
-  __syncthreads();
-  if (!fail_s) {
-    // Phase 3: Q1 rows = Y rows R1^{-1}: Q1[c] = sum_k Y[k] Linv[c + k*r] (R1^{-1} = Linv^T)
-    for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-      const uint32_t i = e % r, j = e / r;
-      M[i + j * r] = a.Rinv[j + i * r];  // M = Linv^T
+  PHASE(6);
+  const int fail1 = int(a.work[0]);
+  if (!fail1) {
+    // Phase 3: Q1 rows = Y rows R1^{-1} (into Q), Gram partial of Q1;
+    // R1^{-1}(k, c) = L1^{-1}(c, k), i.e. the row-major operand is Rinv itself
+    load_mat(a.Rinv, M, r * r);
+    g.zero();
+    for (uint32_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+      const uint32_t i0 = b * kRB, nrow = min(uint32_t(kRB), I - i0);
+      load_rows(a.Y, rm, a.ldp, i0, nrow, r, X, ld);
+      __syncthreads();
+      rows_mul(X, nrow, r, ld, M, X2, ld);
+      __syncthreads();
+      store_rows_cm(X2, ld, i0, nrow, r, a.Q, I);
+      g.add(X2, nrow, r, ld);
+      __syncthreads();
     }
-    __syncthreads();
-    rows_mul(X, nrow, r, ld, M, X2, ld);
-    __syncthreads();
-    rows_gram(X2, nrow, r, ld, a.gpart + size_t(blockIdx.x) * r * r);
+    g.store(a.gpart + size_t(blockIdx.x) * r * r, r);
+    grid.sync();
+    PHASE(7);
+    reduce_gram_grid(a.gpart, gridDim.x, uint64_t(r) * r, r, r, a.gs);
   }
   grid.sync();
+  PHASE(8);
   // Phase 4 (CTA 0): second factorization, R = R2 R1, degeneracy
   if (blockIdx.x == 0) {
-    int fail = fail_s;
+    int fail = fail1;
     if (!fail) {
-      reduce_gram(a.gpart, gridDim.x, uint64_t(r) * r, r, r, M);
-      fail = chol_cta(M, W, r, 0.0, nullptr);
+      load_mat(a.gs, M, r * r);
+      fail = chol_reg<KE>(M, W, r);
+      PHASE(9);
     }
     if (!fail) {
-      tri_inv_cta(W, W2, r);  // L2^{-1}
+      tri_inv_reg<KE>(W, W2, r);  // L2^{-1}
+      PHASE(10);
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.Rinv[e] = W2[e];
       // R = R2 R1 = L2^T L1^T
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
@@ -454,28 +722,36 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
     }
   }
   grid.sync();
-  if (a.work[1] != 0.0 || fail_s) return;
-  // Phase 5: Q rows = Q1 rows R2^{-1}
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const uint32_t i = e % r, j = e / r;
-    M[i + j * r] = a.Rinv[j + i * r];
+  PHASE(11);
+  if (a.work[1] != 0.0 || fail1) return;
+  // Phase 5: Q rows = Q1 rows R2^{-1} (row-major operand = Rinv, as above)
+  load_mat(a.Rinv, M, r * r);
+  for (uint32_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const uint32_t i0 = b * kRB, nrow = min(uint32_t(kRB), I - i0);
+    load_rows(a.Q, false, I, i0, nrow, r, X, ld);
+    __syncthreads();
+    rows_mul(X, nrow, r, ld, M, X2, ld);
+    __syncthreads();
+    store_rows_cm(X2, ld, i0, nrow, r, a.Q, I);
+    __syncthreads();
   }
-  __syncthreads();
-  for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
-    const uint32_t row = e / r, c = e % r;
-    double s = 0.0;
-    for (uint32_t k = 0; k < r; ++k) s = fma(X2[row * ld + k], M[k + c * r], s);
-    a.Q[(i0 + row) + uint64_t(c) * a.I] = s;
-  }
+  PHASE(12);
 }
 
 template <class K>
-cudaError_t coop_launch(K kernel, int grid, size_t smem, void* args, cudaStream_t st) {
+cudaError_t coop_launch(K kernel, int want, int num_sms, size_t smem, void* args, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) {
     cudaGetLastError();
     return e;
   }
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+  if (e != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return e != cudaSuccess ? e : cudaErrorCooperativeLaunchTooLarge;
+  }
+  const int grid = std::max(1, std::min(want, occ * num_sms));
   void* params[] = {args};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kernel), dim3(grid), dim3(kThreads), params,
                                   smem, st);
@@ -483,36 +759,51 @@ cudaError_t coop_launch(K kernel, int grid, size_t smem, void* args, cudaStream_
   return e;
 }
 
+size_t rows_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 3 * size_t(r) * r); }
+
 }  // namespace
 
-int prep_step_grid(uint32_t I) { return int((I + kRowsB - 1) / kRowsB); }
+int coop_partials_cap(int num_sms) { return num_sms * (2048 / kThreads); }
+
 int finish_step_grid(uint64_t F, int num_sms) {
   return int(std::max<uint64_t>(1, std::min<uint64_t>((F + 63) / 64, uint64_t(num_sms))));
 }
 
-cudaError_t launch_prep_step(PrepArgs a, cudaStream_t st) {
-  const uint32_t r = a.r, ld = r + 1;
-  const size_t smem = sizeof(double) * (kRowsB * ld + 3 * size_t(r) * r);
-  return coop_launch(prep_step_kernel, prep_step_grid(a.I), smem, &a, st);
+#define TKG_KE_SWITCH(r, CALL) \
+  if ((r) <= 16) return CALL(1); \
+  if ((r) <= 32) return CALL(4); \
+  if ((r) <= 48) return CALL(9); \
+  return CALL(16);
+
+cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st) {
+#define TKG_P(KE) coop_launch(prep_step_kernel<KE>, num_sms, num_sms, rows_smem(a.r), &a, st)
+  TKG_KE_SWITCH(a.r, TKG_P)
+#undef TKG_P
 }
 
 cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
-  const int grid = finish_step_grid(a.F, num_sms);
+  const uint32_t ntri = a.r * (a.r + 1) / 2;
+  const int want = a.gram_nparts ? int(std::min<uint32_t>(uint32_t(num_sms), (ntri + 7) / 8))
+                                 : finish_step_grid(a.F, num_sms);
   const uint32_t ncp = a.r <= 8 ? 8 : (a.r + 7) / 8 * 8;
-  const size_t smem = sizeof(double) * std::max<size_t>(64 * (ncp + 4), 3 * size_t(a.r) * a.r);
+  const size_t smem = sizeof(double) * std::max<size_t>(64 * (ncp + 4), 2 * size_t(a.r) * a.r);
   switch (ncp) {
 #define TKG_F(N) \
-  case N: return coop_launch(finish_step_kernel<N>, grid, smem, &a, st);
+  case N: return coop_launch(finish_step_kernel<N>, want, num_sms, smem, &a, st);
     TKG_F(8) TKG_F(16) TKG_F(24) TKG_F(32) TKG_F(40) TKG_F(48) TKG_F(56) TKG_F(64)
 #undef TKG_F
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_cholqr_step(CholQrArgs a, cudaStream_t st) {
-  const uint32_t r = a.r, ld = r + 1;
-  const size_t smem = sizeof(double) * (2 * kRowsB * ld + 3 * size_t(r) * r);
-  return coop_launch(cholqr_step_kernel, prep_step_grid(a.I), smem, &a, st);
+cudaError_t launch_cholqr_step(CholQrArgs a, int num_sms, cudaStream_t st) {
+#define TKG_Q(KE) coop_launch(cholqr_step_kernel<KE>, num_sms, num_sms, rows_smem(a.r), &a, st)
+  TKG_KE_SWITCH(a.r, TKG_Q)
+#undef TKG_Q
 }
+
+#ifdef TKG_PHASE_TIMING
+void phase_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_phase_ns, sizeof(g_phase_ns)); }
+#endif
 
 }  // namespace tkg

@@ -9,7 +9,8 @@
 namespace tkg {
 
 struct PrepArgs {
-  const double* part = nullptr;  // FR partials [nparts][I][ldp] (from_partials)
+  double* part = nullptr;        // FR partials [nparts][I][ldp] (from_partials; summed
+                                 // into slot 0, which then holds L row-major)
   int nparts = 0;
   uint32_t ldp = 0;
   const double* GRinv = nullptr; // r x r
@@ -20,6 +21,7 @@ struct PrepArgs {
   double* GLinv = nullptr;       // r x r
   double* Mt = nullptr;          // [I][ncp]
   double* gpart = nullptr;       // [grid][r*r]
+  double* gs = nullptr;          // r x r scratch (reduced Gram)
   AlsCtrl* ctrl = nullptr;
 };
 
@@ -30,12 +32,16 @@ struct FinishArgs {
   const double* GL = nullptr;
   double* GRinv = nullptr;
   double* gpart = nullptr;       // [grid][ncp*ncp]
+  double* gs = nullptr;          // r x r scratch (reduced Gram)
   AlsCtrl* ctrl = nullptr;
   double* history = nullptr;
+  int gram_nparts = 0;           // > 0: gpart already holds this many Gram partials
+                                 // (fused into the FC epilogue); one CTA, no R pass
 };
 
 struct CholQrArgs {
-  const double* Y = nullptr;     // partials [nparts][I][ldp] or column-major (ld = ldp)
+  double* Y = nullptr;           // partials [nparts][I][ldp] (summed into slot 0) or
+                                 // column-major (ld = ldp, nparts 0, not written)
   int nparts = 0;
   uint64_t ldp = 0;
   uint32_t I = 0, r = 0;
@@ -45,16 +51,18 @@ struct CholQrArgs {
   uint32_t ldrt = 0;
   int check = 0;
   double* gpart = nullptr;       // [grid][r*r]
+  double* gs = nullptr;          // r x r scratch (reduced Gram)
   double* L1 = nullptr;          // r*r scratch
   double* Rinv = nullptr;        // r*r scratch
   double* work = nullptr;        // 2 doubles
   AlsCtrl* ctrl = nullptr;       // degenerate_col
 };
 
-int prep_step_grid(uint32_t I);
+// Upper bound on the grid of any launch below (sizes the gpart buffers).
+int coop_partials_cap(int num_sms);
 int finish_step_grid(uint64_t F, int num_sms);
-cudaError_t launch_prep_step(PrepArgs a, cudaStream_t st);
+cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st);
 cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st);
-cudaError_t launch_cholqr_step(CholQrArgs a, cudaStream_t st);
+cudaError_t launch_cholqr_step(CholQrArgs a, int num_sms, cudaStream_t st);
 
 }  // namespace tkg

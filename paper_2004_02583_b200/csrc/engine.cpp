@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -18,6 +20,15 @@ namespace {
 
 using Clock = std::chrono::steady_clock;
 double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+// TKG_TRACE=1: host timestamps (us) of the orchestration points on stderr.
+const bool g_trace = std::getenv("TKG_TRACE") != nullptr;
+Clock::time_point g_trace_t0;
+void trace(const char* what, int a = -1) {
+  if (!g_trace) return;
+  std::fprintf(stderr, "[tkg] %9.1f us  %s %d\n",
+               std::chrono::duration<double, std::micro>(Clock::now() - g_trace_t0).count(), what, a);
+}
 
 int category_of(int subtype) {
   switch (subtype) {
@@ -180,6 +191,21 @@ std::pair<cudaEvent_t, cudaEvent_t> Engine::ev_pair() {
   return {a, b};
 }
 
+std::pair<cudaEvent_t, cudaEvent_t> Engine::small_begin() {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (profiling_) {
+    ev = ev_pair();
+    CK(cudaEventRecord(ev.first, st_));
+  }
+  return ev;
+}
+
+void Engine::small_end(std::pair<cudaEvent_t, cudaEvent_t> ev) {
+  if (!profiling_) return;
+  CK(cudaEventRecord(ev.second, st_));
+  record(kClsSmall, ev.first, ev.second, 0.0, 0.0);
+}
+
 void Engine::record(int cls, cudaEvent_t a, cudaEvent_t b, double bytes, double flops) {
   recs_.push_back({cls, a, b, bytes, flops});
 }
@@ -222,7 +248,8 @@ const double* Engine::upload(const double* a, uint64_t n, bool a_dev, DBuf& buf,
 
 void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
                 uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
-                const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip) {
+                const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip,
+                double* gram_part) {
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (profiling_) {
     ev = ev_pair();
@@ -239,6 +266,7 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
     a.sumsq_part = sumsq_part;
     a.diff_ref = diff_ref;
     a.skip = skip;
+    a.gram_part = gram_part;
     CK(launch_fc_tma(v, mt, ldmt, a, mode, sms_, st_, grid_used));
   } else {
     FcArgs a;
@@ -250,7 +278,7 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
     a.os_c = os_c;
     a.os_p = os_p;
     a.nc = nc;
-    a.gram_part = nullptr;
+    a.gram_part = gram_part;
     a.sumsq_part = sumsq_part;
     a.diff_ref = diff_ref;
     a.skip = skip;
@@ -406,7 +434,7 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
 void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
                     double* rmat, double* rt, uint32_t ldrt, bool check) {
   CholQrArgs q;
-  q.Y = Y;
+  q.Y = const_cast<double*>(Y);  // written only when nparts > 1 (partials summed in place)
   q.nparts = nparts;
   q.ldp = ld;
   q.I = I;
@@ -416,12 +444,15 @@ void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32
   q.rt = rt;
   q.ldrt = ldrt;
   q.check = check ? 1 : 0;
-  q.gpart = gram_part_.d(size_t(prep_step_grid(I)) * r * r);
+  q.gpart = gram_part_.d(size_t(coop_partials_cap(sms_)) * r * r);
+  q.gs = gs_.d(size_t(r) * r);
   q.L1 = qrl1_.d(size_t(r) * r);
   q.Rinv = qrl2_.d(size_t(r) * r);
   q.work = qrq1_.d(2);
   q.ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
-  CK(launch_cholqr_step(q, st_));
+  const auto ev = small_begin();
+  CK(launch_cholqr_step(q, sms_, st_));
+  small_end(ev);
   count_launch();
 }
 
@@ -495,6 +526,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   }
   CK(launch_ctrl_init(ctrl, sumsq, cfg.eta, max_iters, max_iters, cfg.init ? 0 : 1, st_));
   count_launch();
+  trace("init enqueued", mode);
 
   // 2. Sweeps (als.cpp:121-160), enqueued in batches; kernels of sweeps past
   //    the stop decision return on entry.
@@ -504,8 +536,11 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   spec_recs_.clear();
   double* GLinv = cholL;
   double* GRinv = cholR;
-  double* gpl = gram_part_.d(size_t(prep_step_grid(uint32_t(I))) * r * r);
-  const int nfin = finish_step_grid(F, sms_);
+  double* gpl = gram_part_.d(size_t(coop_partials_cap(sms_)) * r * r);
+  double* gs = gs_.d(size_t(r) * r);
+  // Gram of R: fused into the FC epilogue up to ncp 32, else a row pass inside finish_step
+  const bool fused_gram = ncp <= kFcGramMaxNc;
+  const int nfin = std::max(finish_step_grid(F, sms_), fc_grid(v, Mt, ncp, r));
   double* gpr = fc_gram_.d(size_t(nfin) * ncp * ncp);
   uint32_t last_ranges = 0;
   while (true) {
@@ -526,10 +561,21 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       pa.GLinv = GLinv;
       pa.Mt = Mt;
       pa.gpart = gpl;
+      pa.gs = gs;
       pa.ctrl = ctrl;
-      CK(launch_prep_step(pa, st_));
+      {
+        const size_t rec = recs_.size();
+        const auto ev = small_begin();
+        CK(launch_prep_step(pa, sms_, st_));
+        small_end(ev);
+        trace("  prep launched", k);
+        if (profiling_) spec_recs_.push_back({k, 0, rec});
+      }
       const size_t rec_fc = recs_.size();
-      fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, true, stop);
+      int fc_used = 0;
+      fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, true, stop,
+         fused_gram ? gpr : nullptr);
+      trace("  fc launched", k);
       if (profiling_) spec_recs_.push_back({k, 0, rec_fc});
       FinishArgs fa;
       fa.R = R;
@@ -539,17 +585,29 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       fa.GL = GL;
       fa.GRinv = GRinv;
       fa.gpart = gpr;
+      fa.gs = gs;
       fa.ctrl = ctrl;
       fa.history = hist;
-      CK(launch_finish_step(fa, sms_, st_));
+      fa.gram_nparts = fused_gram ? fc_used : 0;
+      {
+        const size_t rec = recs_.size();
+        const auto ev = small_begin();
+        CK(launch_finish_step(fa, sms_, st_));
+        small_end(ev);
+        trace("  finish launched", k);
+        if (profiling_) spec_recs_.push_back({k, 0, rec});
+      }
       const size_t rec_fr = recs_.size();
       last_ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr, stop);
+      trace("  fr launched", k);
       if (profiling_) spec_recs_.push_back({k, 1, rec_fr});
       count_launch(2);
     }
     enqueued += nb;
     CK(cudaMemcpyAsync(&h, ctrl, sizeof(AlsCtrl), cudaMemcpyDeviceToHost, st_));
+    trace("batch enqueued", enqueued);
     sync();
+    trace("batch synced", h.iter);
     if (h.stop || enqueued >= max_iters) break;
     batch = 8;
   }
@@ -592,6 +650,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   out.norm = h.norm;
   CK(cudaMemcpyAsync(&last_sumsq_, sumsq, sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
+  trace("als done", mode);
   return out;
 }
 
@@ -655,14 +714,19 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
     ea.U = d_factors[n - 1];
     ea.Iout = uint32_t(Iout);
     if (last) {
-      nsq = expand_grid(F, sms_);
-      sq = sq_part_.d(size_t(std::max(4096, nsq)));
+      sq = sq_part_.d(size_t(std::max(4096, std::max(expand_grid(F, sms_), sms_))));
       ea.ref = A;
       ea.sumsq_part = sq;
     } else {
       ea.out = bufs[which]->d(nxt.count());
     }
-    CK(launch_expand(ea, sms_, st_, nullptr));
+    if (last && !force_v1_ && expand_diff_tma_ok(ea)) {
+      nsq = expand_diff_tma_grid(F, sms_);
+      CK(launch_expand_diff_tma(ea, sms_, st_, nullptr));
+    } else {
+      if (last) nsq = expand_grid(F, sms_);
+      CK(launch_expand(ea, sms_, st_, nullptr));
+    }
     count_launch();
     src = ea.out;
     cur = nxt;
@@ -685,11 +749,13 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   std::vector<double*> U(sh.N);
   begin_timed();
   const auto t0 = Clock::now();
+  g_trace_t0 = t0;
   {
     std::vector<PreGen> items;
     for (int n = 2; n <= sh.N; ++n) items.push_back({n, sh.count() / sh.d[n - 1], uint32_t(ranks[n - 1])});
     pregenerate(items, cfg.seed);
   }
+  trace("pregenerate enqueued");
   bool sumsq_known = false;
   double ref_sumsq = 0.0;
   for (int n = 1; n <= sh.N; ++n) {
@@ -702,6 +768,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
     qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
     sync();
+    trace("mode done (qr synced)", n);
     o.rep.seconds = since(tm);
     rep->per_mode.push_back(o.rep);
   }
@@ -711,6 +778,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
   core_chain(A, sh, ranks, U, core_buf);
   sync();
+  trace("core synced");
   rep->seconds = since(t0);
   rep->launches = launches_;
   rep->passes = passes_;
@@ -727,6 +795,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   const auto tr = Clock::now();
   rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
   rep->residual_seconds = since(tr);
+  trace("residual synced");
 }
 
 void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,

@@ -145,7 +145,8 @@ class Engine {
   void pregenerate(const std::vector<PreGen>& items, uint64_t seed);
   void fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
           uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
-          const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip = nullptr);
+          const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip = nullptr,
+          double* gram_part = nullptr);
   int fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc);
   uint32_t fr_ranges(const FiberView& v, uint32_t nc);
   uint32_t fr(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, uint32_t nc,
@@ -163,6 +164,8 @@ class Engine {
                   const std::vector<double*>& d_factors, double* d_core);
   void begin_timed();
   void count_launch(int n = 1) { launches_ += n; }
+  std::pair<cudaEvent_t, cudaEvent_t> small_begin();
+  void small_end(std::pair<cudaEvent_t, cudaEvent_t> ev);
   void record(int cls, cudaEvent_t a, cudaEvent_t b, double bytes, double flops);
   std::pair<cudaEvent_t, cudaEvent_t> ev_pair();
 
@@ -185,7 +188,7 @@ class Engine {
   DevStatus* status_d_ = nullptr;
 
   DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
-  DBuf fr_part_, fc_gram_, gram_part_, sq_part_, qr_work_, q_, rhat_, rhatT_;
+  DBuf fr_part_, fc_gram_, gram_part_, gs_, sq_part_, qr_work_, q_, rhat_, rhatT_;
   DBuf y_seq_, states_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_, sumsq_d_, ctrl_d_, hist_d_;
   double last_sumsq_ = 0.0;  // ||working tensor||^2 of the last run_als
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;

@@ -4,9 +4,11 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <random>
+#include <thread>
 
 namespace tkg {
 
@@ -204,15 +206,13 @@ const std::vector<uint64_t>& mt_charpoly() {
   return P;
 }
 
-std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
+namespace {
+
+// base^e mod P by square-and-multiply.
+std::vector<uint64_t> powmod(const std::vector<uint64_t>& base_in, uint64_t e) {
   const int W = kPolyWords;
-  std::vector<uint64_t> out(size_t(count) * W, 0);
-  if (count <= 0) return out;
-  // x^J mod P by square-and-multiply.
-  std::vector<uint64_t> base(W, 0), acc(W, 0), tmp(W);
-  base[0] = 2;  // x
+  std::vector<uint64_t> base = base_in, acc(W, 0), tmp(W);
   acc[0] = 1;
-  uint64_t e = J;
   while (e) {
     if (e & 1) {
       mulmod(acc.data(), base.data(), tmp.data());
@@ -224,26 +224,50 @@ std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
       base = tmp;
     }
   }
-  // out[c] = (x^J)^c
-  out[0] = 1;
-  std::vector<uint64_t> cur(W, 0);
-  cur[0] = 1;
-  for (int c = 1; c < count; ++c) {
-    mulmod(cur.data(), acc.data(), tmp.data());
-    cur = tmp;
-    std::copy(cur.begin(), cur.end(), out.begin() + size_t(c) * W);
-  }
+  return acc;
+}
+
+}  // namespace
+
+std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
+  const int W = kPolyWords;
+  std::vector<uint64_t> out(size_t(count) * W, 0);
+  if (count <= 0) return out;
+  std::vector<uint64_t> x(W, 0);
+  x[0] = 2;  // x
+  const std::vector<uint64_t> xj = powmod(x, J);
+  // out[c] = (x^J)^c: contiguous segments of c on host threads, each started
+  // by its own exponentiation (a few ms per product of two degree-19937
+  // polynomials, so a 300-entry table is worth splitting).
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nseg = std::max(1, std::min<int>(int(hw), count / 8));
+  const int per = (count + nseg - 1) / nseg;
+  auto seg = [&](int s) {
+    const int c0 = s * per, c1 = std::min(count, c0 + per);
+    if (c0 >= c1) return;
+    std::vector<uint64_t> cur = powmod(xj, uint64_t(c0)), tmp(W);
+    std::copy(cur.begin(), cur.end(), out.begin() + size_t(c0) * W);
+    for (int c = c0 + 1; c < c1; ++c) {
+      mulmod(cur.data(), xj.data(), tmp.data());
+      cur.swap(tmp);
+      std::copy(cur.begin(), cur.end(), out.begin() + size_t(c) * W);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int s = 1; s < nseg; ++s) th.emplace_back(seg, s);
+  seg(0);
+  for (auto& t : th) t.join();
   return out;
 }
 
 MtPlan mt_plan(uint64_t total) {
   MtPlan p;
   p.total = total;
-  // One warp generates a chunk (~0.3 us per 312 draws) and one chunk costs
-  // one jump (~19937 x 312 bit-word XORs): ~32K draws per chunk balances
-  // the two, capped at 296 chunks (2 per SM).
-  uint64_t C = (total + 32767) / 32768;
-  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 296));
+  // A chunk costs one jump (19937 x 312 bit-word XORs, ~0.35 us of the whole
+  // GPU) and J/312 twists of one warp (~0.4 us each, latency-bound): the sum
+  // T/(312 C) * 0.4 + 0.35 C is smallest near C = sqrt(T / 256).
+  uint64_t C = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(total) / 256.0)));
+  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 1184));
   p.C = static_cast<int>(C);
   p.J = (total + C - 1) / C;
   if (p.J == 0) p.J = 1;

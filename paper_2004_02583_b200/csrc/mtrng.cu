@@ -1,9 +1,10 @@
 // Device side of the MT19937-64 jump-ahead (see mt_jump.hpp): chunk states
-// by GF(2) XOR-sums over the raw sequence, then one CTA per chunk generates
+// by GF(2) XOR-sums over the raw sequence, then one warp per chunk generates
 // its J draws with the standard twist (in-place semantics of
 // std::mersenne_twister_engine) and writes uniform01 values
 // ((y >> 11) * 2^-53, rng.hpp:19-21) straight into S (storage order, or
 // transposed into the row-major FR operand layout).
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -35,17 +36,15 @@ __device__ __forceinline__ double to_uniform01(uint64_t z) {
 // y[i0 + 10L .. i0 + 10L + 18] loaded once serve all 10 bits x 10 outputs
 // (the XOR-sum is a Hankel product), so shared-memory traffic is ~5x lower
 // than one load per (bit, word). Partial sums are combined with atomicXor.
-constexpr int kJumpSplit = 8;
 constexpr int kJW = 10;  // words per lane
 
 __global__ void __launch_bounds__(32) mt_jump_kernel(const uint64_t* __restrict__ y,
                                                      const uint64_t* __restrict__ polys,
-                                                     uint64_t* __restrict__ states) {
+                                                     uint64_t* __restrict__ states, int wpp) {
   extern __shared__ uint64_t ys[];
   const int c = blockIdx.x;
   const int part = blockIdx.y;
   const int lane = threadIdx.x;
-  const int wpp = (kPolyWords + kJumpSplit - 1) / kJumpSplit;
   const int w0 = part * wpp;
   const int w1 = min(kPolyWords, w0 + wpp);
   if (w0 >= w1) return;
@@ -87,75 +86,95 @@ __global__ void __launch_bounds__(32) mt_jump_kernel(const uint64_t* __restrict_
   }
 }
 
-// One warp per chunk (4 chunks per CTA): the 312-word state lives in shared
-// memory; each twist is two independent 156-wide phases (read, __syncwarp,
-// write) plus the wrap word, with in-place std::mersenne_twister_engine
-// semantics; outputs are written coalesced in storage order.
+// One warp per chunk with the 312-word state in registers: word j = 32*s + L
+// lives in slot s of lane L (slot 9 only for L < 24). A twist (in-place
+// std::mersenne_twister_engine semantics) is
+//   new[j] = twist(old[j], old[j+1], old[j+156])   j < 156
+//   new[j] = twist(old[j], old[j+1], new[j-156])   156 <= j < 311
+//   new[311] = twist(old[311], new[0], new[155])
+// with the neighbours fetched by warp shuffles: j+1 is lane L+1 (lane 0's
+// next slot for L = 31), j+156 = 32(s+4) + L+28 and j-156 = 32(s-5) + L+4, so
+// each source lane sends the slot its reader needs. No shared memory, no
+// barriers; the ten words of a slot are written as one coalesced row.
 constexpr int kGenWarps = 4;
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  return static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(v), src));
+}
 
 __global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* __restrict__ states,
                                                                int C, uint64_t J, uint64_t total,
                                                                double* __restrict__ out, uint64_t F,
                                                                uint64_t ld) {
-  __shared__ uint64_t mts[kGenWarps][kMtN];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, L = threadIdx.x & 31;
   const int c = blockIdx.x * kGenWarps + warp;
   if (c >= C) return;
-  uint64_t* mt = mts[warp];
   const uint64_t start = uint64_t(c) * J;
   const uint64_t end = min(start + J, total);
-  for (int k = lane; k < kMtN; k += 32) mt[k] = states[size_t(c) * kMtN + k];
-  __syncwarp();
+  uint64_t w[10];
+#pragma unroll
+  for (int s = 0; s < 10; ++s) {
+    const int j = 32 * s + L;
+    w[s] = j < kMtN ? states[size_t(c) * kMtN + j] : 0ull;
+  }
+  const int nxt = (L + 1) & 31, far = (L + 28) & 31, back = (L + 4) & 31;
   uint64_t pos = start;
   while (true) {
     if (ld == 0) {
-      for (int k = lane; k < kMtN; k += 32)
-        if (pos + k < end) out[pos + k] = to_uniform01(mt[k]);
+      if (pos + kMtN <= end) {
+#pragma unroll
+        for (int s = 0; s < 10; ++s)
+          if (s < 9 || L < 24) out[pos + 32 * s + L] = to_uniform01(w[s]);
+      } else {
+#pragma unroll
+        for (int s = 0; s < 10; ++s) {
+          const uint64_t j = 32 * s + L;
+          if ((s < 9 || L < 24) && pos + j < end) out[pos + j] = to_uniform01(w[s]);
+        }
+      }
     } else {
       const uint64_t c0 = pos / F;
       const uint64_t j0 = pos - c0 * F;
-      for (int k = lane; k < kMtN; k += 32) {
-        if (pos + k >= end) continue;
+#pragma unroll
+      for (int s = 0; s < 10; ++s) {
+        const uint64_t k = 32 * s + L;
+        if (!(s < 9 || L < 24) || pos + k >= end) continue;
         uint64_t j = j0 + k, col = c0;
         if (j >= F) {
           col += j / F;
           j %= F;
         }
-        out[j * ld + col] = to_uniform01(mt[k]);
+        out[j * ld + col] = to_uniform01(w[s]);
       }
     }
     pos += kMtN;
     if (pos >= end) break;
-    uint64_t nv[5];
-    // i = 0..155: reads old i, i+1, i+156
+    // phase A: j = 32s + L < 156 (s <= 4; s = 4 for L < 28)
+    uint64_t na[5];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const int i = lane + 32 * r;
-      nv[r] = i < 156 ? twist(mt[i], mt[i + 1], mt[i + 156]) : 0ull;
+    for (int s = 0; s < 5; ++s) {
+      const uint64_t v1 = shfl64(L == 0 ? w[s + 1] : w[s], nxt);
+      const uint64_t v2 = shfl64(L >= 28 ? w[s + 4] : w[s + 5], far);
+      na[s] = twist(w[s], v1, v2);
     }
-    __syncwarp();
+    // phase B: 156 <= j < 311 (s = 4 for L >= 28, s = 5..9)
+    uint64_t nb[10];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const int i = lane + 32 * r;
-      if (i < 156) mt[i] = nv[r];
+    for (int s = 4; s < 10; ++s) {
+      const uint64_t v1 = shfl64(L == 0 ? w[s < 9 ? s + 1 : 9] : w[s], nxt);
+      const int ia = s - 4 < 4 ? s - 4 : 4, ib = s - 5 > 0 ? s - 5 : 0;
+      const uint64_t v3 = shfl64(s == 4 ? na[0] : (L < 4 ? na[ia] : na[ib]), back);
+      nb[s] = twist(w[s], v1, v3);
     }
-    __syncwarp();
-    // i = 156..310: reads old i, i+1 and new i-156
+    // j = 311 (lane 23, slot 9)
+    const uint64_t n0 = shfl64(na[0], 0), n155 = shfl64(na[4], 27);
+    const uint64_t n311 = twist(w[9], n0, n155);
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const int i = 156 + lane + 32 * r;
-      nv[r] = i < 311 ? twist(mt[i], mt[i + 1], mt[i - 156]) : 0ull;
-    }
-    __syncwarp();
+    for (int s = 0; s < 4; ++s) w[s] = na[s];
+    w[4] = L < 28 ? na[4] : nb[4];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const int i = 156 + lane + 32 * r;
-      if (i < 311) mt[i] = nv[r];
-    }
-    __syncwarp();
-    // i = 311: reads old 311, new 0 and new 155
-    if (lane == 0) mt[311] = twist(mt[311], mt[0], mt[155]);
-    __syncwarp();
+    for (int s = 5; s < 9; ++s) w[s] = nb[s];
+    w[9] = L < 23 ? nb[9] : (L == 23 ? n311 : 0ull);
   }
 }
 
@@ -165,9 +184,12 @@ cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C
                              uint64_t* d_states, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_states, 0, sizeof(uint64_t) * size_t(C) * kMtN, st);
   if (e != cudaSuccess) return e;
-  const int wpp = (kPolyWords + kJumpSplit - 1) / kJumpSplit;
+  // enough warps to fill the machine (~16 per SM), at least 5 words per warp
+  const int parts = std::max(4, std::min(64, (2368 + C - 1) / C));
+  const int wpp = (kPolyWords + parts - 1) / parts;
+  const int nparts = (kPolyWords + wpp - 1) / wpp;
   const size_t smem = sizeof(uint64_t) * (size_t(wpp) * 64 + 32 * kJW + kJW);
-  mt_jump_kernel<<<dim3(C, kJumpSplit), 32, smem, st>>>(d_y, d_polys, d_states);
+  mt_jump_kernel<<<dim3(C, nparts), 32, smem, st>>>(d_y, d_polys, d_states, wpp);
   return cudaGetLastError();
 }
 
