@@ -13,8 +13,10 @@ inside the timed region).
 
   python bench.py [--config 3] [--steps K] [--warmup W] [--gpus N] [--impl b200|reference]
 
-Under torchrun (N > 1) every rank decomposes its own tensor (replicas, weak
-scaling); the sharded multi-GPU path is not part of this build yet.
+Under torchrun (N > 1) the ranks decompose ONE tensor of the config's shape
+split along its last mode (paper_2004_02583_b200.dist, NCCL): strong
+scaling, `value` = the step's algorithmic bytes / the max-over-ranks step
+time.
 """
 from __future__ import annotations
 
@@ -288,19 +290,48 @@ def reference_arm(args, c, world, rank):
 # ---- B200 arm ------------------------------------------------------------------------
 def b200_arm(args, c, world, rank, local):
     import paper_2004_02583_b200 as tk
-    ctx = tk.Context(local)
-    dims, ranks = c["dims"], c["ranks"]
-    n = int(np.prod(dims))
-    host, host_buf = make_tensor(c, dims, pinned=True)
+    from paper_2004_02583_b200 import dist as tkd
     import torch
+    dims, ranks = c["dims"], c["ranks"]
+    sharded = world > 1 or args.shard
+    if sharded:
+        # one rank per GPU, tensor split along its last mode (BASELINE north star)
+        uid = tkd.broadcast_unique_id(rank) if world > 1 else tkd.nccl_unique_id()
+        sc = tkd.ShardedContext.nccl(local, rank, world, uid)
+        ctx = sc.ctx
+        b0, nl = tkd.shard_range(dims[-1], rank, world)
+    else:
+        ctx = tk.Context(local)
+        b0, nl = 0, dims[-1]
+    ldims = list(dims[:-1]) + [nl]
+    n = int(np.prod(ldims))
+    host_buf = torch.empty(n, dtype=torch.float64, pin_memory=True)
+
+    def combine(sq):  # per-slice sums of every rank's slab (exact: x + 0)
+        if world == 1:
+            return sq
+        import torch.distributed as dist
+        full = torch.zeros((dims[-1], 2), dtype=torch.float64,
+                           device=f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu")
+        full[b0:b0 + nl] = torch.from_numpy(sq).to(full.device)
+        dist.all_reduce(full)
+        return full.cpu().numpy()
+
+    tk.synth_tucker_slab(dims, ranks, c["alpha"], c["nu"], c["seed"], b0, nl, out=host_buf.numpy(),
+                         combine=combine)
+    host = host_buf.numpy().reshape(ldims, order="F")
     dev = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
-    dev.copy_(host_buf if host_buf is not None else torch.from_numpy(host.reshape(-1, order="F")))
+    dev.copy_(host_buf)
     torch.cuda.synchronize()
-    dt = tk.DeviceTensor.from_torch(dev, dims)
+    dt = tk.DeviceTensor.from_torch(dev, ldims)
     eng = tk.FactorEngine.with_als(tk.AlsConfig(eta=c["eta"], max_iters=MAX_ITERS, seed=ALS_SEED))
     flush = n * 8 < 4 * L2_BYTES
 
     def call(x):
+        if sharded:
+            if c["kind"] == "t":
+                return sc.t_hosvd(x, dims, tk.Truncation(ranks), eng)
+            return sc.st_hosvd(x, dims, tk.Truncation(ranks), None, eng)
         if c["kind"] == "t":
             return ctx.t_hosvd(x, tk.Truncation(ranks), eng)
         return ctx.st_hosvd(x, tk.Truncation(ranks), None, eng)
@@ -330,7 +361,8 @@ def b200_arm(args, c, world, rank, local):
     per_mode = [(m.mode, m.als.iterations) for m in rep.per_mode]
     nbytes = step_bytes(c["kind"], dims, ranks, per_mode)
     nflops = step_flops(c["kind"], dims, ranks, per_mode)
-    value = world * nbytes / (ms_step * 1e-3) / 1e9
+    # the whole job decomposes ONE tensor of the config's shape (strong scaling)
+    value = nbytes / (ms_step * 1e-3) / 1e9
 
     # end-to-end through the API with the pinned host tensor
     for _ in range(1):
@@ -342,8 +374,9 @@ def b200_arm(args, c, world, rank, local):
         _, rep_e = call(host)
         e2e_ms += ctx.timer_stop()
     e2e_ms = max_over_ranks(e2e_ms, world) / args.steps
-    h2d = n * 8
-    d2h = 8 * (int(np.prod(ranks)) + sum(dims[k] * ranks[k] for k in range(len(dims))))
+    # job totals: every rank uploads its slab and reads back core + factors
+    h2d = int(np.prod(dims)) * 8
+    d2h = world * 8 * (int(np.prod(ranks)) + sum(dims[k] * ranks[k] for k in range(len(dims))))
 
     if rank != 0:
         return 0
@@ -385,16 +418,18 @@ def b200_arm(args, c, world, rank, local):
         "metric": f"ALS-sweep effective HBM GB/s ({workload_name(c)})",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Tucker model, SURVEY §8(d); counter-based generator csrc/synth.cpp)",
         "config": {"workload": workload_name(c), "config_id": args.config,
-                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "parallelism": (f"shard{world} along mode {len(dims)} (NCCL allreduce of the I_n x R_n / "
+                                   f"R_n x R_n partials, one all-to-all for the last mode)"
+                                   if sharded else "single GPU"),
                    "l2": "flushed between steps" if flush else "tensor larger than L2 (%.1f GiB)" % (n * 8 / 2**30),
                    "iterations": per_mode},
         "time_to_solution_s": rep.seconds,
-        "tflops": world * nflops / (ms_step * 1e-3) / 1e12,
+        "tflops": nflops / (ms_step * 1e-3) / 1e12,
         "relative_residual": rep.relative_residual,
-        "e2e": {"value": world * nbytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+        "e2e": {"value": nbytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -414,6 +449,8 @@ def main():
     p.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--shard", action="store_true",
+                   help="use the sharded (NCCL) path even on one GPU")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     c = CONFIGS[args.config]

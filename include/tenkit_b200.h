@@ -124,6 +124,38 @@ int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
                  const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
                  tkg_error* err);
 
+/* ---- Sharded decomposition (one context per GPU, tensor split along its
+ * last mode; BASELINE north star). The reference is single-process; these
+ * entry points keep t_hosvd / st_hosvd's arguments and results (core and
+ * factors replicated on every rank, identical to the single-GPU result of
+ * the whole tensor) and add the slab this rank holds. */
+typedef struct tkg_local_group tkg_local_group;
+
+/* 128-byte NCCL unique id (create on one rank, broadcast to the others).
+ * NCCL is loaded at run time (dlopen libnccl.so.2). */
+int tkg_nccl_unique_id(void* out128, tkg_error* err);
+/* Attach an NCCL communicator (rank of world) to ctx; collectives run on
+ * the context's stream. */
+int tkg_comm_init_nccl(tkg_ctx* ctx, int rank, int world, const void* unique_id128, tkg_error* err);
+/* In-process group: `world` contexts driven by `world` host threads of one
+ * process (host-synchronous collectives; tests on a single device). */
+int tkg_local_group_create(int world, tkg_local_group** out, tkg_error* err);
+void tkg_local_group_destroy(tkg_local_group* g);
+int tkg_comm_init_local(tkg_ctx* ctx, tkg_local_group* g, int rank, tkg_error* err);
+/* Balanced split of an extent: rank holds [begin, begin + len). */
+int tkg_shard_range(uint64_t extent, int rank, int world, uint64_t* begin, uint64_t* len);
+/* a: this rank's slab dims[0..N-2] x [slab_begin, slab_begin + slab_len) of
+ * the last mode (column-major, host or device), slab = tkg_shard_range of
+ * dims[N-1]; dims: the GLOBAL shape. */
+int tkg_t_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                        uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
+                        const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
+                        tkg_error* err);
+int tkg_st_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                         uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
+                         const uint32_t* mode_order, const tkg_als_config* cfg, double* core, double* factors,
+                         tkg_report* report, tkg_error* err);
+
 /* Stable ascending-rank order (Proposition 1). out: order entries. */
 int tkg_select_order(int32_t order, const uint64_t* dims, const uint64_t* ranks, uint32_t* out,
                      tkg_error* err);

@@ -9,7 +9,7 @@ from .tenkit import (AlsConfig, AlsReport, Context, DecompositionReport, Degener
                      NoConvergenceError, RankTooLargeError, SingularGramError, Truncation,
                      TuckerTensor, UnsupportedError, ZeroReferenceError, als_init, als_low_rank,
                      default_context, frobenius_norm, gram, mode_n_product, reduced_qr,
-                     relative_error, select_order, st_hosvd, synth_tucker, t_hosvd, unfold_t_times,
+                     relative_error, select_order, st_hosvd, synth_tucker, synth_tucker_slab, t_hosvd, unfold_t_times,
                      unfold_times)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -64,6 +64,18 @@ SIGNATURES = [
                                C.POINTER(TkgAlsConfig), _dp, _dp, C.POINTER(TkgReport),
                                C.POINTER(TkgError)]),
     ("tkg_select_order", C.c_int, [C.c_int32, _u64p, _u64p, _u32p, C.POINTER(TkgError)]),
+    ("tkg_nccl_unique_id", C.c_int, [C.c_void_p, C.POINTER(TkgError)]),
+    ("tkg_comm_init_nccl", C.c_int, [_ctxp, C.c_int, C.c_int, C.c_void_p, C.POINTER(TkgError)]),
+    ("tkg_local_group_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(TkgError)]),
+    ("tkg_local_group_destroy", None, [C.c_void_p]),
+    ("tkg_comm_init_local", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.POINTER(TkgError)]),
+    ("tkg_shard_range", C.c_int, [C.c_uint64, C.c_int, C.c_int, _u64p, _u64p]),
+    ("tkg_t_hosvd_sharded", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint64, C.c_uint64,
+                                      _u64p, C.POINTER(TkgAlsConfig), _dp, _dp, C.POINTER(TkgReport),
+                                      C.POINTER(TkgError)]),
+    ("tkg_st_hosvd_sharded", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint64, C.c_uint64,
+                                       _u64p, _u32p, C.POINTER(TkgAlsConfig), _dp, _dp, C.POINTER(TkgReport),
+                                       C.POINTER(TkgError)]),
     ("tkg_als_low_rank", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint32,
                                    C.c_uint64, C.POINTER(TkgAlsConfig), _dp, _dp,
                                    C.POINTER(TkgModeReport), C.POINTER(TkgError)]),
@@ -130,6 +142,14 @@ def synth_lib():
             h.tkg_synth_tucker.restype = C.c_int
             h.tkg_synth_tucker.argtypes = [C.c_int, _u64p, _u64p, C.c_double, C.c_double,
                                            C.c_uint64, _dp]
+            h.tkg_synth_tucker_slab.restype = C.c_int
+            h.tkg_synth_tucker_slab.argtypes = [C.c_int, _u64p, _u64p, C.c_double, C.c_uint64,
+                                                C.c_uint64, C.c_uint64, _dp, _dp]
+            h.tkg_synth_add_noise.restype = C.c_int
+            h.tkg_synth_add_noise.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                              C.c_double, _dp]
+            h.tkg_synth_noise_scale.restype = C.c_double
+            h.tkg_synth_noise_scale.argtypes = [C.c_uint64, _dp, C.c_double]
             _synth = h
         return _synth
 

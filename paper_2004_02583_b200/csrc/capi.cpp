@@ -3,6 +3,7 @@
 // like the reference's exception taxonomy (errors.hpp:10-77), and never
 // lets a C++ exception cross the ABI.
 #include <cstring>
+#include <memory>
 #include <new>
 #include <string>
 #include <vector>
@@ -12,6 +13,10 @@
 
 struct tkg_ctx {
   tkg::Engine* eng;
+};
+
+struct tkg_local_group {
+  std::shared_ptr<tkg::LocalGroup> g;
 };
 
 namespace {
@@ -151,6 +156,73 @@ int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, 
     tkg::DecompRep rep;
     eng(ctx).st_hosvd(a, a_on_device != 0, sh, rk, mode_order ? &mo : nullptr, make_cfg(cfg), core,
                       factors, &rep);
+    fill_report(rep, order, report);
+  });
+}
+
+int tkg_nccl_unique_id(void* out128, tkg_error* err) {
+  return guarded(err, [&] {
+    if (!tkg::nccl_unique_id(out128)) tkg::raise(TKG_E_CUDA, "NCCL (libnccl.so.2) could not be loaded");
+  });
+}
+
+int tkg_comm_init_nccl(tkg_ctx* ctx, int rank, int world, const void* unique_id128, tkg_error* err) {
+  return guarded(err, [&] {
+    if (world < 1 || rank < 0 || rank >= world) tkg::raise(TKG_E_DIMENSION_MISMATCH, "comm: bad rank / world");
+    eng(ctx).set_comm(tkg::make_nccl_comm(unique_id128, rank, world));
+  });
+}
+
+int tkg_local_group_create(int world, tkg_local_group** out, tkg_error* err) {
+  return guarded(err, [&] {
+    if (world < 1) tkg::raise(TKG_E_DIMENSION_MISMATCH, "local group: world must be >= 1");
+    *out = new tkg_local_group{tkg::make_local_group(world)};
+  });
+}
+
+void tkg_local_group_destroy(tkg_local_group* g) { delete g; }
+
+int tkg_comm_init_local(tkg_ctx* ctx, tkg_local_group* g, int rank, tkg_error* err) {
+  return guarded(err, [&] {
+    if (!g || rank < 0 || rank >= tkg::local_group_world(*g->g)) tkg::raise(TKG_E_DIMENSION_MISMATCH, "comm: bad rank / group");
+    eng(ctx).set_comm(tkg::make_local_comm(g->g, rank));
+  });
+}
+
+int tkg_shard_range(uint64_t extent, int rank, int world, uint64_t* begin, uint64_t* len) {
+  if (world < 1 || rank < 0 || rank >= world) return 1;
+  const tkg::ShardRange r = tkg::shard_range(extent, rank, world);
+  *begin = r.begin;
+  *len = r.len;
+  return 0;
+}
+
+int tkg_t_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                        uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
+                        const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
+                        tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    tkg::DecompRep rep;
+    eng(ctx).t_hosvd_sharded(a, a_on_device != 0, sh, slab_begin, slab_len, rk, make_cfg(cfg), core, factors,
+                             &rep);
+    fill_report(rep, order, report);
+  });
+}
+
+int tkg_st_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                         uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
+                         const uint32_t* mode_order, const tkg_als_config* cfg, double* core, double* factors,
+                         tkg_report* report, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    std::vector<int> mo;
+    if (mode_order) mo.assign(mode_order, mode_order + order);
+    tkg::DecompRep rep;
+    eng(ctx).st_hosvd_sharded(a, a_on_device != 0, sh, slab_begin, slab_len, rk, mode_order ? &mo : nullptr,
+                              make_cfg(cfg), core, factors, &rep);
     fill_report(rep, order, report);
   });
 }

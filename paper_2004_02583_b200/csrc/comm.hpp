@@ -1,0 +1,52 @@
+// Collectives of the sharded decomposition (one process or thread per GPU).
+//
+// The tensor is sharded along its last mode (BASELINE north star); the ALS
+// of every other mode keeps its fiber rows local and combines only the
+// I_n x R_n left-update partial sums, the R_n x R_n Gram matrix of the right
+// factor and ||A||^2 with a sum-allreduce. The last mode is re-sharded once
+// by an all-to-all (alltoallv) so that its fibers become local too.
+//
+//  * NcclComm  : NCCL over NVLink/NVSwitch, loaded with dlopen (the library
+//                links no NCCL; inside a torch process this resolves to the
+//                NCCL torch already loaded). Stream-ordered on the engine's
+//                stream, so collectives interleave with the speculative
+//                sweep batches without host synchronisation.
+//  * LocalComm : ranks that are host threads of one process (tests on one
+//                GPU): host barriers + device copies; synchronous.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+
+#include <cuda_runtime.h>
+
+namespace tkg {
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  // buf[0..n) <- sum over ranks (identical bits on every rank)
+  virtual void allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
+  // to rank q: scount[q] doubles at sendbuf + soff[q]; from rank q:
+  // rcount[q] doubles into recvbuf + roff[q]
+  virtual void alltoallv(const double* sendbuf, const size_t* scount, const size_t* soff, double* recvbuf,
+                         const size_t* rcount, const size_t* roff, cudaStream_t st) = 0;
+
+ protected:
+  int rank_ = 0, world_ = 1;
+};
+
+// false when libnccl.so.2 cannot be loaded
+bool nccl_available();
+bool nccl_unique_id(void* out128);
+std::unique_ptr<Comm> make_nccl_comm(const void* unique_id128, int rank, int world);
+
+struct LocalGroup;
+std::shared_ptr<LocalGroup> make_local_group(int world);
+int local_group_world(const LocalGroup& g);
+std::unique_ptr<Comm> make_local_comm(const std::shared_ptr<LocalGroup>& g, int rank);
+
+}  // namespace tkg

@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
 
   // Phase 1 (R^T R not fused into FC): Gram partial of the CTA's contiguous
   // row range of R (row-major [F][ld])
-  if (a.gram_nparts == 0) {
+  if (a.gram_nparts == 0 && a.mode != 2) {
     double acc[kPer][2];
     int tm[kPer], tn[kPer];
 #pragma unroll
@@ -532,11 +532,14 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
       out[c1 * NC + c2] = acc[k][0];
       out[c1 * NC + c2 + 1] = acc[k][1];
     }
+    if (a.mode == 1) return;
     grid.sync();
   }
-  reduce_gram_grid(a.gpart, a.gram_nparts ? a.gram_nparts : int(gridDim.x), uint64_t(NC) * NC, NC, r,
-                   a.gs);
-  grid.sync();
+  if (a.mode != 2) {
+    reduce_gram_grid(a.gpart, a.gram_nparts ? a.gram_nparts : int(gridDim.x), uint64_t(NC) * NC, NC, r,
+                     a.gs);
+    grid.sync();
+  }
   if (blockIdx.x != 0) return;
 
   // Phase 2 (CTA 0): residual, stop rule, G_R^{-1}
@@ -783,8 +786,9 @@ cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st) {
 
 cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
   const uint32_t ntri = a.r * (a.r + 1) / 2;
-  const int want = a.gram_nparts ? int(std::min<uint32_t>(uint32_t(num_sms), (ntri + 7) / 8))
-                                 : finish_step_grid(a.F, num_sms);
+  const int want = a.mode == 2 ? 1
+                   : a.gram_nparts ? int(std::min<uint32_t>(uint32_t(num_sms), (ntri + 7) / 8))
+                                   : finish_step_grid(a.F, num_sms);
   const uint32_t ncp = a.r <= 8 ? 8 : (a.r + 7) / 8 * 8;
   const size_t smem = sizeof(double) * std::max<size_t>(64 * (ncp + 4), 2 * size_t(a.r) * a.r);
   switch (ncp) {

@@ -36,7 +36,10 @@ struct FinishArgs {
   AlsCtrl* ctrl = nullptr;
   double* history = nullptr;
   int gram_nparts = 0;           // > 0: gpart already holds this many Gram partials
-                                 // (fused into the FC epilogue); one CTA, no R pass
+                                 // (fused into the FC epilogue), no R pass
+  int mode = 0;                  // 0 full step; 1 only the R^T R partials of the R pass
+                                 // (gpart[grid], see finish_step_grid); 2 only the CTA-0
+                                 // part from the reduced Gram in gs (sharded runs)
 };
 
 struct CholQrArgs {

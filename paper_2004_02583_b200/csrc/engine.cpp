@@ -48,7 +48,6 @@ constexpr int kMtSeqPadded = kPolyWords * 64 + kMtN;  // jump kernel reads this 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) raise(11, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
-#define CK(x) check_cuda((x), #x)
 
 // ---- Shape (shape.cpp:11-45) -------------------------------------------------
 uint64_t Shape::count() const {
@@ -147,6 +146,7 @@ Engine::~Engine() {
   for (auto* b : pre_bufs_) delete b;
   for (auto* b : pre_y_) delete b;
   for (auto* b : pre_st_) delete b;
+  for (auto* b : pre_ids_) delete b;
   for (auto ev : pre_ev_) cudaEventDestroy(ev);
   cudaEventDestroy(pre_gate_);
   if (status_h_) cudaFreeHost(status_h_);
@@ -353,10 +353,13 @@ uint32_t Engine::fr(const FiberView& v, const double* m, uint64_t mj, uint64_t m
   return ranges;
 }
 
-// S (n doubles) = uniform01 draws of seeded_engine(seed, stream), on device,
-// enqueued on `st` with its own sequence/state buffers.
-void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F,
-                            uint64_t ld, cudaStream_t st, DBuf& ybuf, DBuf& sbuf) {
+// S = uniform01 draws 0..n-1 of seeded_engine(seed, stream), on device,
+// enqueued on `st` with its own sequence/state buffers. With a shard window
+// only the draws of the shard's fibers are kept (see MtWindow), and when
+// those form one position range per column only the chunks that meet them
+// are jumped to and generated.
+void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win,
+                            cudaStream_t st, DBuf& ybuf, DBuf& sbuf, DBuf& cbuf) {
   if (n == 0) return;
   if (mt_charpoly().empty()) raise(11, "MT19937-64 characteristic polynomial check failed");
   const MtPlan plan = mt_plan(n);
@@ -378,15 +381,34 @@ void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* 
   uint64_t* d_y = ybuf.u(kMtSeqPadded);
   // pageable source: the copy is staged before cudaMemcpyAsync returns
   CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st));
-  uint64_t* d_states = sbuf.u(size_t(plan.C) * kMtN);
+  int nchunks = plan.C;
+  const int* d_ids = nullptr;
+  if (win.nloc > 0 && win.Fg == win.Plo * win.Gsm) {
+    const uint64_t a0 = win.o0 * win.Plo, a1 = (win.o0 + win.nloc) * win.Plo;
+    const uint64_t ncol = n / win.Fg;
+    std::vector<int> ids;
+    for (int c = 0; c < plan.C; ++c) {
+      const uint64_t p0 = uint64_t(c) * plan.J, p1 = std::min(n, p0 + plan.J);
+      bool hit = false;
+      for (uint64_t col = p0 / win.Fg; col <= (p1 - 1) / win.Fg && col < ncol && !hit; ++col)
+        hit = std::max(p0, col * win.Fg + a0) < std::min(p1, col * win.Fg + a1);
+      if (hit) ids.push_back(c);
+    }
+    nchunks = int(ids.size());
+    if (nchunks == 0) return;
+    int* d = static_cast<int*>(cbuf.ensure(ids.size() * sizeof(int)));
+    CK(cudaMemcpyAsync(d, ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    d_ids = d;
+  }
+  uint64_t* d_states = sbuf.u(size_t(nchunks) * kMtN);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   const bool prof = profiling_ && st == st_;
   if (prof) {
     ev = ev_pair();
     CK(cudaEventRecord(ev.first, st));
   }
-  CK(launch_mt_states(d_y, polys->u(0) /*existing*/, plan.C, d_states, st));
-  CK(launch_mt_generate(d_states, plan.C, plan.J, n, d_out, F, ld, st));
+  CK(launch_mt_states(d_y, polys->u(0) /*existing*/, nchunks, d_ids, d_states, st));
+  CK(launch_mt_generate(d_states, nchunks, d_ids, plan.J, n, d_out, win, st));
   count_launch(3);  // memset + jump + generate
   if (prof) {
     CK(cudaEventRecord(ev.second, st));
@@ -394,9 +416,8 @@ void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* 
   }
 }
 
-void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F,
-                         uint64_t ld) {
-  gen_uniform_on(seed, stream, n, d_out, F, ld, st_, y_seq_, states_);
+void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win) {
+  gen_uniform_on(seed, stream, n, d_out, win, st_, y_seq_, states_, chunk_ids_);
 }
 
 // The initializer streams depend only on (seed, mode, fibers, rank), not on
@@ -409,6 +430,7 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
     pre_bufs_.push_back(new DBuf());
     pre_y_.push_back(new DBuf());
     pre_st_.push_back(new DBuf());
+    pre_ids_.push_back(new DBuf());
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     pre_ev_.push_back(ev);
@@ -417,10 +439,9 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
   CK(cudaStreamWaitEvent(st2_, pre_gate_, 0));
   for (size_t k = 0; k < items.size(); ++k) {
     const PreGen& g = items[k];
-    const uint32_t ncp = pad_nc(g.r);
     double* d = pre_bufs_[k]->d(g.F * g.r + 8);
-    gen_uniform_on(seed, uint32_t(g.mode), g.F * g.r, d, 0, 0, st2_, *pre_y_[k], *pre_st_[k]);
-    (void)ncp;
+    const uint64_t total = (g.win.nloc ? g.win.Fg : g.F) * g.r;
+    gen_uniform_on(seed, uint32_t(g.mode), total, d, g.win, st2_, *pre_y_[k], *pre_st_[k], *pre_ids_[k]);
     CK(cudaEventRecord(pre_ev_[k], st2_));
     pre_[g.mode] = {d, pre_ev_[k], g.F, g.r};
   }
@@ -456,6 +477,15 @@ void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32
   count_launch();
 }
 
+// Sharded runs: Y = sum of this shard's FR partials (into slot 0), summed
+// over the shards; returns the new partial count (1).
+uint32_t Engine::reduce_left_partials(double* part, uint32_t nparts, uint32_t I, uint32_t ncp, uint32_t r) {
+  CK(launch_reduce_slot0(part, int(nparts), I, ncp, r, st_));
+  count_launch();
+  dist_->allreduce_sum(part, size_t(I) * ncp, st_);
+  return 1;
+}
+
 int Engine::qr_degenerate_col() {
   AlsCtrl h;
   CK(cudaMemcpyAsync(&h, ctrl_d_.ensure(sizeof(AlsCtrl)), sizeof(AlsCtrl), cudaMemcpyDeviceToHost, st_));
@@ -464,7 +494,7 @@ int Engine::qr_degenerate_col() {
 }
 
 Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint32_t r,
-                               const AlsCfg& cfg, bool sumsq_known) {
+                               const AlsCfg& cfg, bool sumsq_known, const MtWindow& win) {
   const uint64_t I = sh.extent(mode);
   const uint64_t s = sh.stride(mode);
   const uint64_t F = sh.count() / I;
@@ -485,8 +515,6 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   double* cholR = cholR_.d(kMaxRank * kMaxRank);
   const uint32_t nranges = fr_ranges(v, r);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const int ngr = gram_rm_count(F, sms_);
-  double* grp = fc_gram_.d(size_t(ngr) * ncp * ncp);
   double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
   double* sumsq = sumsq_d_.d(2);
   AlsCtrl* ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
@@ -500,6 +528,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       CK(launch_sumsq(A, sh.count(), sq, st_));
       CK(launch_sum(sq, sumsq_partials_count(sh.count()), sumsq, st_));
       count_launch(2);
+      if (dist_) dist_->allreduce_sum(sumsq, 1, st_);
     }
     CK(cudaMemcpyAsync(Lc, cfg.init, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
   } else {
@@ -513,15 +542,17 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       pre_.erase(pit);
     } else {
       double* Sg = s_.d(F * r + 8);  // column-major F x r, the reference's storage order
-      gen_uniform(cfg.seed, uint32_t(mode), F * r, Sg);
+      gen_uniform(cfg.seed, uint32_t(mode), (win.nloc ? win.Fg : F) * r, Sg, win);
       S = Sg;
     }
     uint32_t fr_grid = 0;
-    const uint32_t ranges = fr(v, S, 1, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
+    uint32_t ranges = fr(v, S, 1, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
     if (!sumsq_known) {  // ||A||^2 fused into the init pass: one partial per CTA
       CK(launch_sum(sq, int(fr_grid), sumsq, st_));
       count_launch();
+      if (dist_) dist_->allreduce_sum(sumsq, 1, st_);
     }
+    if (dist_) ranges = reduce_left_partials(part, ranges, uint32_t(I), ncp, r);
     qr_dev(part, int(ranges), ncp, uint32_t(I), r, Lc, nullptr, nullptr, 0, true);
   }
   CK(launch_ctrl_init(ctrl, sumsq, cfg.eta, max_iters, max_iters, cfg.init ? 0 : 1, st_));
@@ -592,6 +623,18 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       {
         const size_t rec = recs_.size();
         const auto ev = small_begin();
+        if (dist_) {
+          // R^T R over this shard's fibers, summed over the shards, then the step
+          int nparts = fc_used;
+          if (!fused_gram) {
+            fa.mode = 1;
+            CK(launch_finish_step(fa, sms_, st_));
+            nparts = finish_step_grid(F, sms_);
+          }
+          CK(launch_gram_reduce(gpr, nparts, uint64_t(ncp) * ncp, ncp, r, gs, st_));
+          dist_->allreduce_sum(gs, size_t(r) * r, st_);
+          fa.mode = 2;
+        }
         CK(launch_finish_step(fa, sms_, st_));
         small_end(ev);
         trace("  finish launched", k);
@@ -599,6 +642,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       }
       const size_t rec_fr = recs_.size();
       last_ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr, stop);
+      if (dist_) last_ranges = reduce_left_partials(part, last_ranges, uint32_t(I), ncp, r);
       trace("  fr launched", k);
       if (profiling_) spec_recs_.push_back({k, 1, rec_fr});
       count_launch(2);
@@ -734,6 +778,7 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
   }
   double* out = misc2_.d(1);
   CK(launch_sum(sq, nsq, out, st_));
+  if (dist_) dist_->allreduce_sum(out, 1, st_);
   double diff_sq = 0.0;
   CK(cudaMemcpyAsync(&diff_sq, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
@@ -752,7 +797,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   g_trace_t0 = t0;
   {
     std::vector<PreGen> items;
-    for (int n = 2; n <= sh.N; ++n) items.push_back({n, sh.count() / sh.d[n - 1], uint32_t(ranks[n - 1])});
+    for (int n = 2; n <= sh.N; ++n) items.push_back({n, sh.count() / sh.d[n - 1], uint32_t(ranks[n - 1]), MtWindow()});
     pregenerate(items, cfg.seed);
   }
   trace("pregenerate enqueued");
@@ -798,25 +843,25 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   trace("residual synced");
 }
 
+// select_order, or the caller's order validated as checked_order (hosvd.cpp:30-50)
+std::vector<int> checked_order(const Shape& sh, const std::vector<uint64_t>& ranks, const std::vector<int>* order_in) {
+  if (!order_in) return select_order(ranks);
+  if (order_in->size() != size_t(sh.N))
+    raise(1, "st_hosvd: order has " + std::to_string(order_in->size()) + " entries for an order-" +
+                 std::to_string(sh.N) + " tensor");
+  std::vector<bool> seen(sh.N, false);
+  for (int m : *order_in) {
+    if (m < 1 || m > sh.N || seen[m - 1]) raise(1, "st_hosvd: order is not a permutation of 1.." + std::to_string(sh.N));
+    seen[m - 1] = true;
+  }
+  return *order_in;
+}
+
 void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
                       const std::vector<int>* order_in, const AlsCfg& cfg, double* core,
                       double* factors, DecompRep* rep) {
   validate_truncation(sh, ranks);
-  std::vector<int> order;
-  if (!order_in) {
-    order = select_order(ranks);
-  } else {  // checked_order (hosvd.cpp:30-50)
-    if (order_in->size() != size_t(sh.N))
-      raise(1, "st_hosvd: order has " + std::to_string(order_in->size()) + " entries for an order-" +
-                   std::to_string(sh.N) + " tensor");
-    std::vector<bool> seen(sh.N, false);
-    for (int m : *order_in) {
-      if (m < 1 || m > sh.N || seen[m - 1])
-        raise(1, "st_hosvd: order is not a permutation of 1.." + std::to_string(sh.N));
-      seen[m - 1] = true;
-    }
-    order = *order_in;
-  }
+  const std::vector<int> order = checked_order(sh, ranks, order_in);
   *rep = DecompRep();
   const double* A = upload(a, sh.count(), a_dev, tensor_, &rep->h2d_seconds);
   while (factor_bufs_.size() < size_t(sh.N)) factor_bufs_.push_back(new DBuf());
@@ -834,7 +879,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     Shape w = sh;
     for (size_t k = 0; k < order.size(); ++k) {
       const int m = order[k];
-      if (k > 0) items.push_back({m, w.count() / w.d[m - 1], uint32_t(ranks[m - 1])});
+      if (k > 0) items.push_back({m, w.count() / w.d[m - 1], uint32_t(ranks[m - 1]), MtWindow()});
       w.d[m - 1] = ranks[m - 1];
     }
     pregenerate(items, cfg.seed);

@@ -8,8 +8,10 @@
 // while every pass over the tensor and every small solve runs on the GPU.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -17,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include "comm.hpp"
 #include "kernels.cuh"
 
 namespace tkg {
@@ -29,6 +32,7 @@ struct Error : std::runtime_error {
 
 [[noreturn]] void raise(int subtype, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
+#define CK(x) ::tkg::check_cuda((x), #x)
 
 struct Shape {
   int N = 0;
@@ -101,6 +105,18 @@ class Engine {
   void als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r, uint64_t seed,
                 double* l_out);
 
+  // Sharded drivers (engine_dist.cpp): `a` is this rank's slab [begin,
+  // begin + len) of the last mode of the global shape G (shard_range split);
+  // core / factors / report come back replicated on every rank.
+  void set_comm(std::unique_ptr<Comm> c);
+  bool has_comm() const { return comm_ != nullptr; }
+  void t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t begin, uint64_t len,
+                       const std::vector<uint64_t>& ranks, const AlsCfg& cfg, double* core, double* factors,
+                       DecompRep* rep);
+  void st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t begin, uint64_t len,
+                        const std::vector<uint64_t>& ranks, const std::vector<int>* order, const AlsCfg& cfg,
+                        double* core, double* factors, DecompRep* rep);
+
   // Primitives (host in/out).
   void unfold_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r, double* out);
   void unfold_t_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r, double* out);
@@ -131,16 +147,17 @@ class Engine {
   // left in l_, R (F x r) in r_. sumsq_known: status_->sumsq already holds
   // ||A||^2 of this tensor.
   AlsOut run_als(const double* A, const Shape& sh, int mode, uint32_t r, const AlsCfg& cfg,
-                 bool sumsq_known);
-  // ld == 0: storage order; else S (F x r col-major draw order) written row-major [F][ld]
-  void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F = 0,
-                   uint64_t ld = 0);
-  void gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, uint64_t F,
-                      uint64_t ld, cudaStream_t st, DBuf& ybuf, DBuf& sbuf);
+                 bool sumsq_known, const MtWindow& win = MtWindow());
+  uint32_t reduce_left_partials(double* part, uint32_t nparts, uint32_t I, uint32_t ncp, uint32_t r);
+  // draws 0..n-1 in storage order, or a shard's window of them (MtWindow)
+  void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win = MtWindow());
+  void gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win,
+                      cudaStream_t st, DBuf& ybuf, DBuf& sbuf, DBuf& cbuf);
   struct PreGen {
     int mode;
-    uint64_t F;
+    uint64_t F;  // local fibers
     uint32_t r;
+    MtWindow win;
   };
   void pregenerate(const std::vector<PreGen>& items, uint64_t seed);
   void fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
@@ -164,6 +181,12 @@ class Engine {
                   const std::vector<double*>& d_factors, double* d_core);
   void begin_timed();
   void count_launch(int n = 1) { launches_ += n; }
+  void reshard(const double* src, const Shape& G, int from, int to, double* dst);
+  void check_shard(const Shape& G, uint64_t begin, uint64_t len);
+  void dist_core_and_residual(const double* A, const Shape& L, uint64_t k0, const Shape& G,
+                              const std::vector<uint64_t>& ranks, std::vector<double*>& U, double* core_buf,
+                              bool compute_core, double ref_sumsq, DecompRep* rep, double* core_host,
+                              double* factors_host, std::chrono::steady_clock::time_point t0);
   std::pair<cudaEvent_t, cudaEvent_t> small_begin();
   void small_end(std::pair<cudaEvent_t, cudaEvent_t> ev);
   void record(int cls, cudaEvent_t a, cudaEvent_t b, double bytes, double flops);
@@ -182,14 +205,14 @@ class Engine {
     uint32_t r;
   };
   std::map<int, PreS> pre_;
-  std::vector<DBuf*> pre_bufs_, pre_y_, pre_st_;
+  std::vector<DBuf*> pre_bufs_, pre_y_, pre_st_, pre_ids_;
   std::vector<cudaEvent_t> pre_ev_;
   DevStatus* status_h_ = nullptr;
   DevStatus* status_d_ = nullptr;
 
   DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
   DBuf fr_part_, fc_gram_, gram_part_, gs_, sq_part_, qr_work_, q_, rhat_, rhatT_;
-  DBuf y_seq_, states_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_, sumsq_d_, ctrl_d_, hist_d_;
+  DBuf y_seq_, states_, chunk_ids_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_, sumsq_d_, ctrl_d_, hist_d_;
   double last_sumsq_ = 0.0;  // ||working tensor||^2 of the last run_als
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   std::vector<DBuf*> factor_bufs_;
@@ -218,7 +241,18 @@ class Engine {
   uint64_t launches_ = 0;
   uint64_t passes_ = 0;
   uint64_t bytes_ = 0;
+
+  std::unique_ptr<Comm> comm_;
+  Comm* dist_ = nullptr;  // set while a sharded driver runs: run_als sums over ranks
+  DBuf send_, recv_, reshard_, uslab_;
 };
+
+struct ShardRange {
+  uint64_t begin = 0, len = 0;
+};
+// balanced split of `extent` over `world` ranks
+ShardRange shard_range(uint64_t extent, int rank, int world);
+std::vector<int> checked_order(const Shape& sh, const std::vector<uint64_t>& ranks, const std::vector<int>* order);
 
 std::vector<int> select_order(const std::vector<uint64_t>& ranks);
 void validate_truncation(const Shape& sh, const std::vector<uint64_t>& ranks);

@@ -26,12 +26,20 @@ struct DevStatus {
 };
 
 // ---- MT19937-64 (mtrng.cu) -------------------------------------------------
-cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C,
+// Chunk c of J draws starts at position c*J; d_chunk_ids (nullable) lists the
+// C chunks to compute (states and outputs are indexed by list slot).
+cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C, const int* d_chunk_ids,
                              uint64_t* d_states, cudaStream_t st);
-// ld == 0: out[idx] (storage order); ld > 0: out[(idx % F)*ld + idx / F],
-// i.e. the column-major F x r matrix S written row-major (the FR operand layout).
-cudaError_t launch_mt_generate(const uint64_t* d_states, int C, uint64_t J, uint64_t total,
-                               double* d_out, uint64_t F, uint64_t ld, cudaStream_t st);
+// nloc == 0: out[pos] (storage order). Otherwise the stream is the
+// column-major Fg x r matrix S of a mode whose fibers j decompose as
+// j = jlo + Plo*(ism + Gsm*jhi), ism the index along the sharded mode; one
+// shard keeps ism in [o0, o0 + nloc), stored as its own local fiber order
+// jlo + Plo*((ism - o0) + nloc*jhi), column c at c * (Fg / Gsm * nloc).
+struct MtWindow {
+  uint64_t Fg = 0, Plo = 1, Gsm = 1, o0 = 0, nloc = 0;
+};
+cudaError_t launch_mt_generate(const uint64_t* d_states, int C, const int* d_chunk_ids, uint64_t J,
+                               uint64_t total, double* d_out, MtWindow win, cudaStream_t st);
 
 // ---- small dense LA (smallla.cu) -------------------------------------------
 // part[b] = upper triangle of X_b^T X_b over row blocks of X (rows x r, col-major, ld).
@@ -51,21 +59,7 @@ cudaError_t launch_chol(const double* part, int nparts, uint64_t part_ld, int pa
                         uint32_t r, double* G, double* chol, int32_t* flag, DevStatus* status,
                         cudaStream_t st, double floor_rel = 1e-13);
 
-// Row-wise SPD solve X(i,:) = B(i,:) G^{-1} via the Cholesky factor, with
-// forward/back substitution in the order of spd_solve (kernels.cpp:398-415).
-// B is either the sum of `nparts` partials part[k][i][ldp] (FR output) or a
-// column-major matrix (nparts == 0: B[i + c*ldb]).
-// Output: column-major X (x_cm, ld = rows) and/or i-major padded Xt (xt, ldxt).
-// forward_only: X(i,:)^T = L^{-1} B(i,:)^T (the CholQR step Q = Y R^{-1}, R = L^T).
-cudaError_t launch_row_solve(const double* B, int nparts, uint64_t ldb_or_ldp, uint32_t rows,
-                             uint32_t r, const double* chol, double* x_cm, double* xt,
-                             uint32_t ldxt, const int32_t* skip_flag, cudaStream_t st,
-                             int forward_only = 0);
 
-// CholQR2 epilogue: R = L2^T L1^T, degeneracy test, optional R / R^T outputs.
-cudaError_t launch_cholqr_finish(const double* L1, const double* L2, uint32_t r, const int32_t* fail1,
-                                 const int32_t* fail2, double* rmat, double* rt, uint32_t ldrt,
-                                 int check, DevStatus* status, cudaStream_t st);
 
 // Householder thin QR (kernels.cpp:303-367, R_ii >= 0) of Y (rows x r), where
 // Y = sum of `nparts` FR partials [k][i][ldp] (or a column-major matrix when
@@ -77,12 +71,6 @@ cudaError_t launch_qr(const double* Y, int nparts, uint64_t ldy_or_ldp, uint32_t
                       double* q, double* rmat, double* rt, uint32_t ldrt, double* work,
                       int check_degenerate, DevStatus* status, cudaStream_t st);
 
-// Closed-form residual step after the right update (als.cpp:36-44,52-55):
-// G_R = reduce(FC Gram partials), trace(G_L G_R) (compensated), residual,
-// and chol(G_R) for the left update (flag on failure).
-cudaError_t launch_finish_right(const double* fc_gram, int nparts, int nc_stride, uint32_t r,
-                                const double* GL, const double* norm_sq, double* GR,
-                                double* cholR, DevStatus* status, cudaStream_t st);
 
 // out[0] = sum of `n` partials in fixed order (into status->sumsq when dst null).
 cudaError_t launch_sum(const double* partials, int n, double* dst, cudaStream_t st);
@@ -99,12 +87,6 @@ cudaError_t launch_sumsq(const double* x, uint64_t n, double* part, cudaStream_t
 cudaError_t launch_sumsq_diff(const double* a, const double* b, uint64_t n, double* part,
                               cudaStream_t st);
 
-// Upper-triangle Gram partials of a row-major [rows][ld] matrix with r
-// columns (gram(R), matrix.cpp:90-126), one partial per CTA, DMMA tiles.
-// Partial layout: [cta][ncp][ncp] with entry (c1, c2), c1 <= c2 at c1*ncp + c2.
-int gram_rm_count(uint64_t rows, int num_sms);
-cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t ld, double* part,
-                           int num_sms, cudaStream_t st, const int32_t* skip = nullptr);
 
 // st-HOSVD shrink B_(n) <- R_hat R^T written in tensor layout (hosvd.cpp:176-178):
 // out[jl + c*s + p*s*r] = sum_c' rhat[c + c'*r] * R[(p*s + jl)*ld + c'], plus
@@ -131,5 +113,20 @@ cudaError_t launch_expand(const ExpandArgs& a, int num_sms, cudaStream_t st, int
 // Y = sum of FR partials, written column-major (rows x r).
 cudaError_t launch_reduce_partials(const double* part, int nparts, uint32_t rows, uint32_t ldp,
                                    uint32_t r, double* y, cudaStream_t st);
+
+// ---- sharded decomposition (smallla.cu) -------------------------------------
+cudaError_t launch_add(double* dst, const double* src, size_t n, cudaStream_t st);
+// part[0][i][c] = sum over the nparts FR partials [k][I][ldp] (c < r), in place.
+cudaError_t launch_reduce_slot0(double* part, int nparts, uint32_t I, uint32_t ldp, uint32_t r, cudaStream_t st);
+// G (column-major r x r) = sum_k part[k*pld + a*rs + b] (upper entries a <= b).
+cudaError_t launch_gram_reduce(const double* part, int nparts, uint64_t pld, uint32_t rs, uint32_t r, double* G,
+                               cudaStream_t st);
+struct BoxCopy {
+  int N = 0;
+  uint64_t box[16] = {0};
+  uint64_t src_stride[16] = {0}, dst_stride[16] = {0};
+  uint64_t src_base = 0, dst_base = 0;
+};
+cudaError_t launch_copy_box(const double* src, double* dst, const BoxCopy& b, cudaStream_t st);
 
 }  // namespace tkg

@@ -2,8 +2,8 @@
 // by GF(2) XOR-sums over the raw sequence, then one warp per chunk generates
 // its J draws with the standard twist (in-place semantics of
 // std::mersenne_twister_engine) and writes uniform01 values
-// ((y >> 11) * 2^-53, rng.hpp:19-21) straight into S (storage order, or
-// transposed into the row-major FR operand layout).
+// ((y >> 11) * 2^-53, rng.hpp:19-21) straight into S (storage order, or the
+// window of one shard's fibers).
 #include <algorithm>
 #include <cstdint>
 
@@ -40,9 +40,11 @@ constexpr int kJW = 10;  // words per lane
 
 __global__ void __launch_bounds__(32) mt_jump_kernel(const uint64_t* __restrict__ y,
                                                      const uint64_t* __restrict__ polys,
-                                                     uint64_t* __restrict__ states, int wpp) {
+                                                     uint64_t* __restrict__ states, int wpp,
+                                                     const int* __restrict__ chunk_ids) {
   extern __shared__ uint64_t ys[];
-  const int c = blockIdx.x;
+  const int slot = blockIdx.x;
+  const int c = chunk_ids ? chunk_ids[slot] : slot;
   const int part = blockIdx.y;
   const int lane = threadIdx.x;
   const int w0 = part * wpp;
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(32) mt_jump_kernel(const uint64_t* __restrict_
   for (int k = 0; k < kJW; ++k) {
     const int t = kJW * lane + k;
     if (t < kMtN)
-      atomicXor(reinterpret_cast<unsigned long long*>(states + size_t(c) * kMtN + t),
+      atomicXor(reinterpret_cast<unsigned long long*>(states + size_t(slot) * kMtN + t),
                 static_cast<unsigned long long>(acc[k]));
   }
 }
@@ -104,23 +106,24 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
 
 __global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* __restrict__ states,
                                                                int C, uint64_t J, uint64_t total,
-                                                               double* __restrict__ out, uint64_t F,
-                                                               uint64_t ld) {
+                                                               double* __restrict__ out, MtWindow win,
+                                                               const int* __restrict__ chunk_ids) {
   const int warp = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int c = blockIdx.x * kGenWarps + warp;
-  if (c >= C) return;
+  const int slot = blockIdx.x * kGenWarps + warp;
+  if (slot >= C) return;
+  const int c = chunk_ids ? chunk_ids[slot] : slot;
   const uint64_t start = uint64_t(c) * J;
   const uint64_t end = min(start + J, total);
   uint64_t w[10];
 #pragma unroll
   for (int s = 0; s < 10; ++s) {
     const int j = 32 * s + L;
-    w[s] = j < kMtN ? states[size_t(c) * kMtN + j] : 0ull;
+    w[s] = j < kMtN ? states[size_t(slot) * kMtN + j] : 0ull;
   }
   const int nxt = (L + 1) & 31, far = (L + 28) & 31, back = (L + 4) & 31;
   uint64_t pos = start;
   while (true) {
-    if (ld == 0) {
+    if (win.nloc == 0) {
       if (pos + kMtN <= end) {
 #pragma unroll
         for (int s = 0; s < 10; ++s)
@@ -133,18 +136,23 @@ __global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* 
         }
       }
     } else {
-      const uint64_t c0 = pos / F;
-      const uint64_t j0 = pos - c0 * F;
+      // shard window (see MtWindow)
+      const uint64_t c0 = pos / win.Fg;
+      const uint64_t j0 = pos - c0 * win.Fg;
+      const uint64_t Fl = win.Fg / win.Gsm * win.nloc;
 #pragma unroll
       for (int s = 0; s < 10; ++s) {
         const uint64_t k = 32 * s + L;
         if (!(s < 9 || L < 24) || pos + k >= end) continue;
         uint64_t j = j0 + k, col = c0;
-        if (j >= F) {
-          col += j / F;
-          j %= F;
+        if (j >= win.Fg) {
+          col += j / win.Fg;
+          j %= win.Fg;
         }
-        out[j * ld + col] = to_uniform01(w[s]);
+        const uint64_t jlo = j % win.Plo, t = j / win.Plo;
+        const uint64_t ism = t % win.Gsm, jhi = t / win.Gsm;
+        if (ism >= win.o0 && ism < win.o0 + win.nloc)
+          out[jlo + win.Plo * ((ism - win.o0) + win.nloc * jhi) + col * Fl] = to_uniform01(w[s]);
       }
     }
     pos += kMtN;
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* 
 
 }  // namespace
 
-cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C,
+cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C, const int* d_chunk_ids,
                              uint64_t* d_states, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_states, 0, sizeof(uint64_t) * size_t(C) * kMtN, st);
   if (e != cudaSuccess) return e;
@@ -189,14 +197,14 @@ cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C
   const int wpp = (kPolyWords + parts - 1) / parts;
   const int nparts = (kPolyWords + wpp - 1) / wpp;
   const size_t smem = sizeof(uint64_t) * (size_t(wpp) * 64 + 32 * kJW + kJW);
-  mt_jump_kernel<<<dim3(C, nparts), 32, smem, st>>>(d_y, d_polys, d_states, wpp);
+  mt_jump_kernel<<<dim3(C, nparts), 32, smem, st>>>(d_y, d_polys, d_states, wpp, d_chunk_ids);
   return cudaGetLastError();
 }
 
-cudaError_t launch_mt_generate(const uint64_t* d_states, int C, uint64_t J, uint64_t total,
-                               double* d_out, uint64_t F, uint64_t ld, cudaStream_t st) {
-  mt_gen_kernel<<<(C + kGenWarps - 1) / kGenWarps, 32 * kGenWarps, 0, st>>>(d_states, C, J, total,
-                                                                           d_out, F, ld);
+cudaError_t launch_mt_generate(const uint64_t* d_states, int C, const int* d_chunk_ids, uint64_t J,
+                               uint64_t total, double* d_out, MtWindow win, cudaStream_t st) {
+  mt_gen_kernel<<<(C + kGenWarps - 1) / kGenWarps, 32 * kGenWarps, 0, st>>>(d_states, C, J, total, d_out,
+                                                                           win, d_chunk_ids);
   return cudaGetLastError();
 }
 

@@ -1,8 +1,8 @@
-// Small dense kernels of the ALS step (r <= 64, I_n <= a few thousand):
-// Gram partials, Cholesky with the reference's pivot floor, row-wise SPD
-// solves, Householder QR with the reference's sign convention, and the
-// closed-form residual. They run on-device so a sweep never round-trips
-// through the host except for the one status read that decides the stop.
+// Small dense kernels outside the ALS sweep (the sweep's own small steps are
+// in coop.cu): Gram partials + Cholesky with the reference's pivot floor
+// (gram / spd_solve primitives), Householder QR with the reference's sign
+// convention (reduced_qr primitive), fixed-order sums, sums of squares, the
+// st-HOSVD shrink, and operand packing.
 #include <algorithm>
 #include <cmath>
 
@@ -105,52 +105,6 @@ __global__ void chol_kernel(const double* __restrict__ part, int nparts, uint64_
     if (G) G[e] = Gs[e];
     chol[e] = Ls[e];
   }
-}
-
-// ---- row-wise SPD solve ------------------------------------------------------
-__global__ void row_solve_kernel(const double* __restrict__ B, int nparts, uint64_t ldb,
-                                 uint32_t rows, uint32_t r, const double* __restrict__ chol,
-                                 double* x_cm, double* xt, uint32_t ldxt, const int32_t* skip,
-                                 int forward_only) {
-  if (skip && *skip) return;
-  extern __shared__ double sm[];
-  double* Ls = sm;                 // r*r
-  double* xs = sm + r * r;         // [r][blockDim]
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) Ls[e] = chol[e];
-  __syncthreads();
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows) return;
-  const uint32_t T = blockDim.x, t = threadIdx.x;
-  for (uint32_t c = 0; c < r; ++c) {
-    double b;
-    if (nparts > 0) {
-      b = 0.0;
-      for (int k = 0; k < nparts; ++k) b += B[(size_t(k) * rows + i) * ldb + c];
-    } else {
-      b = B[i + uint64_t(c) * ldb];
-    }
-    xs[c * T + t] = b;
-  }
-  // Forward substitution L y = b, then L^T x = y (kernels.cpp:401-415).
-  for (uint32_t a = 0; a < r; ++a) {
-    double acc = xs[a * T + t];
-    for (uint32_t p = 0; p < a; ++p) acc -= Ls[a + p * r] * xs[p * T + t];
-    xs[a * T + t] = acc / Ls[a + a * r];
-  }
-  if (!forward_only) {
-    for (uint32_t a = r; a-- > 0;) {
-      double acc = xs[a * T + t];
-      for (uint32_t p = a + 1; p < r; ++p) acc -= Ls[p + a * r] * xs[p * T + t];
-      xs[a * T + t] = acc / Ls[a + a * r];
-    }
-  }
-  for (uint32_t c = 0; c < r; ++c) {
-    const double v = xs[c * T + t];
-    if (x_cm) x_cm[i + uint64_t(c) * rows] = v;
-    if (xt) xt[uint64_t(i) * ldxt + c] = v;
-  }
-  if (xt)
-    for (uint32_t c = r; c < ldxt; ++c) xt[uint64_t(i) * ldxt + c] = 0.0;
 }
 
 // ---- Householder QR (kernels.cpp:303-367) ----------------------------------
@@ -283,55 +237,6 @@ __global__ void __launch_bounds__(1024) qr_kernel(const double* __restrict__ Y, 
   }
 }
 
-// ---- closed-form residual (als.cpp:18-25,52-55) -----------------------------
-__global__ void finish_right_kernel(const double* __restrict__ fc_gram, int nparts, int nc,
-                                    uint32_t r, const double* __restrict__ GL, double* GR,
-                                    double* cholR, DevStatus* status) {
-  extern __shared__ double sm[];
-  double* Gs = sm;
-  double* Ls = sm + r * r;
-  reduce_upper(fc_gram, nparts, uint64_t(nc) * nc, nc, r, Gs);
-  __syncthreads();
-  // trace(G_L G_R) = sum_ij GL(i,j) GR(i,j), compensated (TwoSum) per lane
-  // then combined in a fixed tree.
-  __shared__ double hi_s[32], lo_s[32];
-  if (threadIdx.x < 32) {
-    double s = 0.0, c = 0.0;
-    for (uint32_t e = threadIdx.x; e < r * r; e += 32) {
-      double p = GL[e] * Gs[e];
-      double pe = fma(GL[e], Gs[e], -p);
-      double t, err;
-      two_sum(s, p, t, err);
-      s = t;
-      c += err + pe;
-    }
-    hi_s[threadIdx.x] = s;
-    lo_s[threadIdx.x] = c;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0, c = 0.0;
-    for (int k = 0; k < 32; ++k) {
-      double t, err;
-      two_sum(s, hi_s[k], t, err);
-      s = t;
-      c += err + lo_s[k];
-    }
-    const double tr = s + c;
-    const double norm = sqrt(status->sumsq);  // frobenius_norm (tensor_ops.cpp:391-393)
-    const double norm_sq = norm * norm;       // als.cpp:106
-    status->trace = tr;
-    status->residual = sqrt(fmax(0.0, norm_sq - tr));
-  }
-  __syncthreads();
-  block_chol(Gs, Ls, r, &status->left_singular, status);
-  __syncthreads();
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-    GR[e] = Gs[e];
-    cholR[e] = Ls[e];
-  }
-}
-
 __global__ void sum_kernel(const double* __restrict__ p, int n, double* dst) {
   __shared__ double red[32];
   // fixed-shape tree: thread t sums p[t], p[t+T], ... then a fixed warp tree
@@ -386,90 +291,6 @@ __global__ void sumsq_diff_kernel(const double* __restrict__ a, const double* __
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// ---- Gram of a row-major matrix on the tensor pipe ----------------------------
-// Each CTA owns a contiguous row range, streams 128-row blocks through a
-// double-buffered cp.async ring (row pitch NC+4 = 4 mod 16 doubles) and
-// accumulates its upper-triangle 8x8 tiles with DMMA in registers.
-template <int NC>
-__global__ void __launch_bounds__(256) gram_rm_kernel(const double* __restrict__ X, uint64_t rows,
-                                                      uint32_t r, uint64_t ld, double* part,
-                                                      const int32_t* skip) {
-  if (skip && *skip) return;
-  constexpr int kRows = 128, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2;
-  constexpr int kPer = (kTri + 7) / 8;
-  extern __shared__ __align__(16) double tile[];  // [2][kRows][kLd]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
-  double acc[kPer][2];
-  int tm[kPer], tn[kPer];
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    acc[k][0] = acc[k][1] = 0.0;
-    int tt = warp + 8 * k, mt = 0;
-    if (tt < kTri) {
-      int rem = tt;
-      while (rem >= kNT - mt) { rem -= kNT - mt; ++mt; }
-      tm[k] = mt;
-      tn[k] = mt + rem;
-    } else {
-      tm[k] = tn[k] = -1;
-    }
-  }
-  const uint64_t nblk = (rows + kRows - 1) / kRows;
-  const uint64_t per = (nblk + gridDim.x - 1) / gridDim.x;
-  const uint64_t b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
-  const bool vec = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (NC % 2 == 0);
-  auto load = [&](uint64_t b, int buf) {
-    double* t = tile + buf * kRows * kLd;
-    const uint64_t r0 = b * kRows;
-    if (vec) {
-      for (int e = threadIdx.x; e < kRows * (NC / 2); e += blockDim.x) {
-        const int row = e / (NC / 2), c = (e % (NC / 2)) * 2;
-        const uint64_t gr = r0 + row;
-        if (gr < rows) cp_async16(t + row * kLd + c, X + gr * ld + c);
-        else { t[row * kLd + c] = 0.0; t[row * kLd + c + 1] = 0.0; }
-      }
-    } else {
-      for (int e = threadIdx.x; e < kRows * NC; e += blockDim.x) {
-        const int row = e / NC, c = e % NC;
-        const uint64_t gr = r0 + row;
-        t[row * kLd + c] = gr < rows ? X[gr * ld + c] : 0.0;
-      }
-    }
-    cp_async_commit();
-  };
-  if (b0 < b1) load(b0, 0);
-  for (uint64_t b = b0; b < b1; ++b) {
-    const int buf = int((b - b0) & 1);
-    if (b + 1 < b1) {
-      load(b + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* t = tile + buf * kRows * kLd;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      if (tm[k] < 0) continue;
-#pragma unroll 8
-      for (int k0 = 0; k0 < kRows; k0 += 4) {
-        const double* rp = t + (k0 + q) * kLd;
-        dmma(acc[k][0], acc[k][1], rp[tm[k] * 8 + r8], rp[tn[k] * 8 + r8]);
-      }
-    }
-    __syncthreads();
-  }
-  // columns >= r hold whatever the padding held; the consumer reads c < r only
-  double* out = part + size_t(blockIdx.x) * NC * NC;
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    if (tm[k] < 0) continue;
-    const int c1 = tm[k] * 8 + r8, c2 = tn[k] * 8 + 2 * q;
-    out[c1 * NC + c2] = acc[k][0];
-    out[c1 * NC + c2 + 1] = acc[k][1];
-  }
-}
-
 // ---- st-HOSVD shrink ---------------------------------------------------------
 constexpr int kShrinkThreads = 256;
 constexpr int kShrinkFibers = 4096;  // fibers per CTA
@@ -502,75 +323,73 @@ __global__ void __launch_bounds__(kShrinkThreads) shrink_kernel(
 
 // R = R2 R1 with R_k = L_k^T (CholQR2), the reference's degeneracy test on
 // diag(R) (als.cpp:74-86), and optional outputs R (col-major) / R^T padded.
-__global__ void cholqr_finish_kernel(const double* __restrict__ L1, const double* __restrict__ L2,
-                                     uint32_t r, const int32_t* fail1, const int32_t* fail2,
-                                     double* rmat, double* rt, uint32_t ldrt, int check,
-                                     DevStatus* status) {
-  extern __shared__ double Rs[];
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
-    const uint32_t i = e % r, j = e / r;
-    double acc = 0.0;
-    if (i <= j)
-      for (uint32_t k = i; k <= j; ++k) acc += L2[k + i * r] * L1[j + k * r];  // R2[i][k] R1[k][j]
-    Rs[e] = acc;
-    if (rmat) rmat[e] = acc;
+
+// ---- sharded-decomposition helpers -------------------------------------------------
+__global__ void add_kernel(double* __restrict__ dst, const double* __restrict__ src, size_t n) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
+// part[0][i][c] = sum_k part[k][i][c] (c < r), in place; 8 lanes per entry,
+// each over k = sub, sub + 8, ... in order, then a fixed xor tree.
+__global__ void reduce_slot0_kernel(double* __restrict__ part, int nparts, uint32_t I, uint32_t ldp, uint32_t r) {
+  const uint64_t n = uint64_t(I) * r;
+  const uint64_t e = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 8;
+  const int sub = threadIdx.x & 7;
+  const bool act = e < n;
+  double s = 0.0;
+  double* p = nullptr;
+  if (act) {
+    p = part + (e / r) * ldp + (e % r);
+    const uint64_t stride = uint64_t(I) * ldp;
+    for (int k = sub; k < nparts; k += 8) s += p[size_t(k) * stride];
   }
-  __syncthreads();
-  if (rt)
-    for (uint32_t e = threadIdx.x; e < r * ldrt; e += blockDim.x) {
-      const uint32_t row = e / ldrt, c = e % ldrt;  // rt[c'][c] = R[c][c']
-      rt[e] = c < r ? Rs[c + row * r] : 0.0;
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (act && sub == 0) p[0] = s;
+}
+
+// G (column-major r x r, symmetric) = sum_k part[k*pld + a*rs + b], a <= b;
+// one warp per entry (lanes over k, fixed xor tree).
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int nparts, uint64_t pld, uint32_t rs,
+                                   uint32_t r, double* __restrict__ G) {
+  const uint32_t t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  if (t >= r * (r + 1) / 2) return;
+  uint32_t a = 0, rem = t;
+  while (rem >= r - a) {
+    rem -= r - a;
+    ++a;
+  }
+  const uint32_t b = a + rem;
+  const double* p = part + size_t(a) * rs + b;
+  double s = 0.0;
+  for (int k = int(lane); k < nparts; k += 32) s += p[size_t(k) * pld];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) {
+    G[a + b * r] = s;
+    G[b + a * r] = s;
+  }
+}
+
+// N-d box copy between column-major tensors (strides in elements).
+__global__ void copy_box_kernel(const double* __restrict__ src, double* __restrict__ dst, BoxCopy b,
+                                uint64_t total) {
+  for (uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t rem = idx, so = b.src_base, dof = b.dst_base;
+    for (int k = 0; k < b.N; ++k) {
+      const uint64_t c = rem % b.box[k];
+      rem /= b.box[k];
+      so += c * b.src_stride[k];
+      dof += c * b.dst_stride[k];
     }
-  if (check && threadIdx.x == 0) {
-    int bad = 0;
-    if (*fail1 || *fail2) {
-      bad = 1;
-    } else {
-      double md = 0.0;
-      for (uint32_t i = 0; i < r; ++i) md = fmax(md, fabs(Rs[i + i * r]));
-      for (uint32_t i = 0; i < r; ++i)
-        if (fabs(Rs[i + i * r]) <= 1e-13 * md || md == 0.0) {
-          bad = int(i) + 1;
-          break;
-        }
-    }
-    status->degenerate_col = bad;
+    dst[dof] = src[so];
   }
 }
 
 }  // namespace
-
-cudaError_t launch_cholqr_finish(const double* L1, const double* L2, uint32_t r, const int32_t* fail1,
-                                 const int32_t* fail2, double* rmat, double* rt, uint32_t ldrt,
-                                 int check, DevStatus* status, cudaStream_t st) {
-  cholqr_finish_kernel<<<1, 256, sizeof(double) * r * r, st>>>(L1, L2, r, fail1, fail2, rmat, rt, ldrt,
-                                                               check, status);
-  return cudaGetLastError();
-}
-
-int gram_rm_count(uint64_t rows, int num_sms) {
-  const uint64_t nblk = (rows + 127) / 128;
-  return int(std::max<uint64_t>(1, std::min<uint64_t>(nblk, uint64_t(num_sms))));
-}
-
-cudaError_t launch_gram_rm(const double* X, uint64_t rows, uint32_t r, uint64_t ld, double* part,
-                           int num_sms, cudaStream_t st, const int32_t* skip) {
-  const int grid = gram_rm_count(rows, num_sms);
-  const uint32_t ncp = r <= 8 ? 8 : (r + 7) / 8 * 8;
-  switch (ncp) {
-#define TKG_G(N)                                                                          \
-  case N: {                                                                               \
-    const size_t sm = sizeof(double) * 2 * 128 * (N + 4);                                 \
-    cudaFuncSetAttribute(gram_rm_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); \
-    gram_rm_kernel<N><<<grid, 256, sm, st>>>(X, rows, r, ld, part, skip);                  \
-    break;                                                                                \
-  }
-    TKG_G(8) TKG_G(16) TKG_G(24) TKG_G(32) TKG_G(40) TKG_G(48) TKG_G(56) TKG_G(64)
-#undef TKG_G
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
-}
 
 int shrink_count(uint64_t F) { return int((F + kShrinkFibers - 1) / kShrinkFibers); }
 
@@ -607,29 +426,11 @@ cudaError_t launch_chol(const double* part, int nparts, uint64_t part_ld, int ro
   return cudaGetLastError();
 }
 
-cudaError_t launch_row_solve(const double* B, int nparts, uint64_t ldb, uint32_t rows, uint32_t r,
-                             const double* chol, double* x_cm, double* xt, uint32_t ldxt,
-                             const int32_t* skip, cudaStream_t st, int forward_only) {
-  const int T = 32;
-  const size_t smem = sizeof(double) * (size_t(r) * r + size_t(r) * T);
-  row_solve_kernel<<<(rows + T - 1) / T, T, smem, st>>>(B, nparts, ldb, rows, r, chol, x_cm, xt,
-                                                         ldxt, skip, forward_only);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_qr(const double* Y, int nparts, uint64_t ldy, uint32_t rows, uint32_t r,
                       double* q, double* rmat, double* rt, uint32_t ldrt, double* work,
                       int check_degenerate, DevStatus* status, cudaStream_t st) {
   qr_kernel<<<1, 1024, 0, st>>>(Y, nparts, ldy, rows, r, q, rmat, rt, ldrt, work,
                                 check_degenerate, status);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_finish_right(const double* fc_gram, int nparts, int nc_stride, uint32_t r,
-                                const double* GL, const double* /*norm_sq*/, double* GR,
-                                double* cholR, DevStatus* status, cudaStream_t st) {
-  finish_right_kernel<<<1, 1024, sizeof(double) * 2 * r * r, st>>>(fc_gram, nparts, nc_stride, r,
-                                                                   GL, GR, cholR, status);
   return cudaGetLastError();
 }
 
@@ -658,6 +459,36 @@ cudaError_t launch_reduce_partials(const double* part, int nparts, uint32_t rows
                                    uint32_t r, double* y, cudaStream_t st) {
   const uint64_t n = uint64_t(rows) * r;
   reduce_partials_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, nparts, rows, ldp, r, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add(double* dst, const double* src, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int grid = int(std::min<size_t>((n + 255) / 256, 4096));
+  add_kernel<<<grid, 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_slot0(double* part, int nparts, uint32_t I, uint32_t ldp, uint32_t r, cudaStream_t st) {
+  if (nparts <= 1) return cudaSuccess;
+  const uint64_t threads = uint64_t(I) * r * 8;
+  reduce_slot0_kernel<<<int((threads + 255) / 256), 256, 0, st>>>(part, nparts, I, ldp, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_reduce(const double* part, int nparts, uint64_t pld, uint32_t rs, uint32_t r, double* G,
+                               cudaStream_t st) {
+  const uint32_t ntri = r * (r + 1) / 2;
+  gram_reduce_kernel<<<(ntri + 7) / 8, 256, 0, st>>>(part, nparts, pld, rs, r, G);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_box(const double* src, double* dst, const BoxCopy& b, cudaStream_t st) {
+  uint64_t total = 1;
+  for (int k = 0; k < b.N; ++k) total *= b.box[k];
+  if (total == 0) return cudaSuccess;
+  const int grid = int(std::min<uint64_t>((total + 255) / 256, 148 * 16));
+  copy_box_kernel<<<grid, 256, 0, st>>>(src, dst, b, total);
   return cudaGetLastError();
 }
 

@@ -90,16 +90,21 @@ void expand(const double* in, uint64_t s, uint64_t R, uint64_t P, const double* 
 
 extern "C" {
 
-// Writes prod(dims) doubles into `out` (column-major). Returns 0 on success.
-int tkg_synth_tucker(int order, const uint64_t* dims, const uint64_t* ranks, double alpha,
-                     double nu, uint64_t seed, double* out) {
+// Phase 1 of the generator for the slab [k0, k0 + nloc) of the last mode:
+// out (column-major, dims with the last extent nloc) = A0 = G x_1 Q_1 ...
+// x_N Q_N restricted to the slab, and slice_sq[2*t] / slice_sq[2*t+1] the
+// sums of A0^2 and of the noise e^2 over last-mode slice k0 + t (summed in
+// a fixed order inside the slice, so any split of the tensor gives the same
+// per-slice numbers). Returns 0 on success.
+int tkg_synth_tucker_slab(int order, const uint64_t* dims, const uint64_t* ranks, double alpha, uint64_t seed,
+                          uint64_t k0, uint64_t nloc, double* out, double* slice_sq) {
   if (order < 1 || order > 16) return 1;
-  uint64_t total = 1, core = 1;
+  uint64_t core = 1;
   for (int n = 0; n < order; ++n) {
     if (ranks[n] < 1 || ranks[n] > dims[n]) return 1;
-    total *= dims[n];
     core *= ranks[n];
   }
+  if (k0 + nloc > dims[order - 1] || nloc == 0) return 1;
   // core
   std::vector<double> cur(core);
   {
@@ -115,52 +120,91 @@ int tkg_synth_tucker(int order, const uint64_t* dims, const uint64_t* ranks, dou
       cur[k] = normal_at(key, k) * scale;
     }
   }
-  // A0 = G x_1 Q_1 ... x_N Q_N (the last expansion writes into `out`)
+  // A0 slab = G x_1 Q_1 ... x_N Q_N[k0 : k0 + nloc, :] (the last expansion writes into `out`)
   std::vector<uint64_t> shp(ranks, ranks + order);
   std::vector<double> nxt;
   for (int n = 0; n < order; ++n) {
+    const bool last = n == order - 1;
     std::vector<double> Q(dims[n] * ranks[n]);
     orthonormal(stream_key(seed, 1 + n), dims[n], ranks[n], Q.data());
+    uint64_t I = dims[n];
+    if (last) {  // rows k0 .. k0 + nloc of Q_N
+      std::vector<double> Qs(nloc * ranks[n]);
+      for (uint64_t c = 0; c < ranks[n]; ++c)
+        for (uint64_t i = 0; i < nloc; ++i) Qs[i + c * nloc] = Q[k0 + i + c * dims[n]];
+      Q.swap(Qs);
+      I = nloc;
+    }
     uint64_t s = 1, P = 1;
     for (int m = 0; m < n; ++m) s *= shp[m];
     for (int m = n + 1; m < order; ++m) P *= shp[m];
     double* dst;
-    if (n == order - 1) {
+    if (last) {
       dst = out;
     } else {
-      nxt.assign(s * dims[n] * P, 0.0);
+      nxt.assign(s * I * P, 0.0);
       dst = nxt.data();
     }
-    expand(cur.data(), s, ranks[n], P, Q.data(), dims[n], dst);
-    shp[n] = dims[n];
-    if (n != order - 1) cur.swap(nxt);
+    expand(cur.data(), s, ranks[n], P, Q.data(), I, dst);
+    shp[n] = I;
+    if (!last) cur.swap(nxt);
   }
-  // noise, rescaled to nu * ||A0||_F exactly
+  // per-slice sums of A0^2 and of the noise e^2 (noise index = global element index)
+  const uint64_t slice = [&] {
+    uint64_t v = 1;
+    for (int n = 0; n + 1 < order; ++n) v *= dims[n];
+    return v;
+  }();
   const uint64_t key = stream_key(seed, 1000);
-  const uint64_t chunk = 1u << 20;
-  const int64_t nch = int64_t((total + chunk - 1) / chunk);
-  std::vector<double> pa(nch), pe(nch);
-#pragma omp parallel for schedule(static)
-  for (int64_t c = 0; c < nch; ++c) {  // fixed chunks: thread-count invariant sums
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t t = 0; t < int64_t(nloc); ++t) {
     double sa = 0.0, se = 0.0;
-    const uint64_t hi = std::min<uint64_t>(total, uint64_t(c + 1) * chunk);
-    for (uint64_t k = uint64_t(c) * chunk; k < hi; ++k) {
-      const double e = normal_at(key, k);
-      sa += out[k] * out[k];
+    const double* o = out + uint64_t(t) * slice;
+    const uint64_t g0 = (k0 + uint64_t(t)) * slice;
+    for (uint64_t k = 0; k < slice; ++k) {
+      const double e = normal_at(key, g0 + k);
+      sa += o[k] * o[k];
       se += e * e;
     }
-    pa[c] = sa;
-    pe[c] = se;
+    slice_sq[2 * t] = sa;
+    slice_sq[2 * t + 1] = se;
   }
-  double a0 = 0.0, ee = 0.0;
-  for (int64_t c = 0; c < nch; ++c) {
-    a0 += pa[c];
-    ee += pe[c];
-  }
-  const double scale = (ee > 0.0) ? nu * std::sqrt(a0) / std::sqrt(ee) : 0.0;
-#pragma omp parallel for schedule(static)
-  for (int64_t k = 0; k < int64_t(total); ++k) out[k] += scale * normal_at(key, uint64_t(k));
   return 0;
+}
+
+// Phase 2: out += scale * e over the slab, scale = nu * ||A0||_F / ||e||_F
+// from the sums of all slices of the tensor (tkg_synth_noise_scale).
+int tkg_synth_add_noise(int order, const uint64_t* dims, uint64_t seed, uint64_t k0, uint64_t nloc, double scale,
+                        double* out) {
+  if (order < 1 || order > 16) return 1;
+  uint64_t slice = 1;
+  for (int n = 0; n + 1 < order; ++n) slice *= dims[n];
+  const uint64_t key = stream_key(seed, 1000);
+  const uint64_t g0 = k0 * slice, total = nloc * slice;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < int64_t(total); ++k) out[k] += scale * normal_at(key, g0 + uint64_t(k));
+  return 0;
+}
+
+// nu * sqrt(sum A0^2) / sqrt(sum e^2) over all I_N slices, summed in slice order.
+double tkg_synth_noise_scale(uint64_t nslices, const double* slice_sq, double nu) {
+  double a0 = 0.0, ee = 0.0;
+  for (uint64_t t = 0; t < nslices; ++t) {
+    a0 += slice_sq[2 * t];
+    ee += slice_sq[2 * t + 1];
+  }
+  return ee > 0.0 ? nu * std::sqrt(a0) / std::sqrt(ee) : 0.0;
+}
+
+// The whole tensor (prod(dims) doubles, column-major). Returns 0 on success.
+int tkg_synth_tucker(int order, const uint64_t* dims, const uint64_t* ranks, double alpha, double nu,
+                     uint64_t seed, double* out) {
+  if (order < 1 || order > 16) return 1;
+  const uint64_t IN = dims[order - 1];
+  std::vector<double> sq(2 * IN);
+  int rc = tkg_synth_tucker_slab(order, dims, ranks, alpha, seed, 0, IN, out, sq.data());
+  if (rc) return rc;
+  return tkg_synth_add_noise(order, dims, seed, 0, IN, tkg_synth_noise_scale(IN, sq.data(), nu), out);
 }
 
 }  // extern "C"

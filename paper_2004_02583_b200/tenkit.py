@@ -503,3 +503,32 @@ def synth_tucker(dims, ranks, alpha: float, nu: float, seed: int, out: Optional[
     if rc != 0:
         raise DimensionMismatchError("synth_tucker: invalid dims/ranks")
     return out
+
+
+def synth_tucker_slab(dims, ranks, alpha: float, nu: float, seed: int, begin: int, length: int,
+                      out: Optional[np.ndarray] = None, combine=None):
+    """Slab [begin, begin+length) of the last mode of synth_tucker(dims, ...),
+    bit-identical to the same slice of the whole tensor. The noise scale
+    needs per-slice sums from every slab: `combine(sums)` receives this
+    slab's (length, 2) array and returns the (I_N, 2) array of all slices
+    (e.g. an all-gather across ranks); None = this slab is the whole tensor."""
+    dims = [int(d) for d in dims]
+    sl = list(dims[:-1]) + [int(length)]
+    n = int(np.prod(sl))
+    if out is None:
+        out = np.empty(n)
+    assert out.size == n and out.dtype == np.float64
+    h = _lib.synth_lib()
+    sq = np.zeros((int(length), 2))
+    dp = C.POINTER(C.c_double)
+    rc = h.tkg_synth_tucker_slab(len(dims), _lib.u64(dims), _lib.u64(ranks), float(alpha), int(seed),
+                                 int(begin), int(length), out.ctypes.data_as(dp), sq.ctypes.data_as(dp))
+    if rc != 0:
+        raise DimensionMismatchError("synth_tucker_slab: invalid dims/ranks/slab")
+    allsq = np.ascontiguousarray(combine(sq) if combine is not None else sq, dtype=np.float64)
+    if allsq.shape != (dims[-1], 2):
+        raise DimensionMismatchError("synth_tucker_slab: combine must return (I_N, 2) slice sums")
+    scale = h.tkg_synth_noise_scale(dims[-1], allsq.ctypes.data_as(dp), float(nu))
+    h.tkg_synth_add_noise(len(dims), _lib.u64(dims), int(seed), int(begin), int(length), scale,
+                          out.ctypes.data_as(dp))
+    return out
