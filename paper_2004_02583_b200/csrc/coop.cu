@@ -475,10 +475,10 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
   cg::grid_group grid = cg::this_grid();
   AlsCtrl* ctrl = a.ctrl;
   if (ctrl->stop) return;
-  constexpr int kRows = 64, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2;
+  constexpr int kRows = 64, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2, kStg = 3;
   constexpr int kPer = (kTri + 7) / 8;
   extern __shared__ __align__(16) double sm[];
-  double* tile = sm;  // [kRows][kLd]
+  double* tile = sm;  // [kStg][kRows][kLd]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
   const uint32_t r = a.r;
 
@@ -503,27 +503,43 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
     const uint64_t nblk = (a.F + kRows - 1) / kRows;
     const uint64_t per = (nblk + gridDim.x - 1) / gridDim.x;
     const uint64_t b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
-    for (uint64_t b = b0; b < b1; ++b) {
-      __syncthreads();
+    // kStg-deep cp.async ring of 64-row blocks of R
+    auto issue = [&](uint64_t b, int slot) {
+      double* t = tile + size_t(slot) * kRows * kLd;
       for (int e = threadIdx.x; e < kRows * (NC / 2); e += blockDim.x) {
         const int row = e / (NC / 2), c = (e % (NC / 2)) * 2;
         const uint64_t gr = b * kRows + row;
-        double2 v = make_double2(0.0, 0.0);
-        if (gr < a.F) v = *reinterpret_cast<const double2*>(a.R + gr * a.ld + c);
-        tile[row * kLd + c] = v.x;
-        tile[row * kLd + c + 1] = v.y;
+        if (gr < a.F) {
+          cp_async16(t + row * kLd + c, a.R + gr * a.ld + c);
+        } else {
+          t[row * kLd + c] = 0.0;
+          t[row * kLd + c + 1] = 0.0;
+        }
       }
-      __syncthreads();
+    };
+#pragma unroll
+    for (int i = 0; i < kStg - 1; ++i) {
+      if (b0 + i < b1) issue(b0 + i, i);
+      cp_async_commit();
+    }
+    for (uint64_t b = b0; b < b1; ++b) {
+      cp_async_wait<kStg - 2>();
+      __syncthreads();  // block b landed everywhere; slot (b-1) is free
+      const int slot = int((b - b0) % kStg);
+      if (b + kStg - 1 < b1) issue(b + kStg - 1, int((b - b0 + kStg - 1) % kStg));
+      cp_async_commit();
+      const double* t = tile + size_t(slot) * kRows * kLd;
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
         if (tm[k] < 0) continue;
 #pragma unroll 8
         for (int k0 = 0; k0 < kRows; k0 += 4) {
-          const double* rp = tile + (k0 + q) * kLd;
+          const double* rp = t + (k0 + q) * kLd;
           dmma(acc[k][0], acc[k][1], rp[tm[k] * 8 + r8], rp[tn[k] * 8 + r8]);
         }
       }
     }
+    cp_async_wait<0>();
     double* out = a.gpart + size_t(blockIdx.x) * NC * NC;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
@@ -790,7 +806,7 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
                    : a.gram_nparts ? int(std::min<uint32_t>(uint32_t(num_sms), (ntri + 7) / 8))
                                    : finish_step_grid(a.F, num_sms);
   const uint32_t ncp = a.r <= 8 ? 8 : (a.r + 7) / 8 * 8;
-  const size_t smem = sizeof(double) * std::max<size_t>(64 * (ncp + 4), 2 * size_t(a.r) * a.r);
+  const size_t smem = sizeof(double) * std::max<size_t>(3 * 64 * (ncp + 4), 2 * size_t(a.r) * a.r);
   switch (ncp) {
 #define TKG_F(N) \
   case N: return coop_launch(finish_step_kernel<N>, want, num_sms, smem, &a, st);

@@ -292,29 +292,82 @@ __global__ void sumsq_diff_kernel(const double* __restrict__ a, const double* __
 }
 
 // ---- st-HOSVD shrink ---------------------------------------------------------
+// working <- tensorize(R_hat R^T) (hosvd.cpp:176-178): out(jl, c, p) =
+// sum_k R[j][k] R_hat(c, k) for every fiber j = jl + p*s, i.e. a tall-skinny
+// F x r x r product. A CTA takes 128-fiber tiles of R (row-major [F][ld],
+// one contiguous block), runs DMMA against R_hat^T held in shared memory,
+// stages the r x 128 result in shared memory and writes each output column
+// as one coalesced run of fibers; ||out||^2 per CTA.
 constexpr int kShrinkThreads = 256;
-constexpr int kShrinkFibers = 4096;  // fibers per CTA
+constexpr int kShrinkTile = 128;
 
-__global__ void __launch_bounds__(kShrinkThreads) shrink_kernel(
+template <int NC>
+__global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
     const double* __restrict__ R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
     const double* __restrict__ rhat, double* __restrict__ out, double* sumsq_part) {
-  extern __shared__ double rh[];  // r x r column-major
+  constexpr int kLd = NC + 4;            // fragment rows 4 (mod 16) apart
+  constexpr int kLdO = kShrinkTile + 4;
+  extern __shared__ __align__(16) double sm[];
+  double* Rs = sm;                       // [128][kLd]; reused as Os [NC][kLdO]
+  double* Bs = sm + kShrinkTile * kLd;   // [NC][kLd]: Bs[k][c] = R_hat(c, k)
   __shared__ double red[32];
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) rh[e] = rhat[e];
-  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
+  for (int e = threadIdx.x; e < NC * NC; e += blockDim.x) {
+    const int k = e / NC, c = e % NC;
+    Bs[k * kLd + c] = (k < int(r) && c < int(r)) ? rhat[c + k * r] : 0.0;
+  }
   const uint64_t F = s * P;
-  const uint64_t f0 = uint64_t(blockIdx.x) * kShrinkFibers;
-  const uint64_t f1 = min(F, f0 + kShrinkFibers);
+  const uint64_t ntiles = (F + kShrinkTile - 1) / kShrinkTile;
   double sq = 0.0;
-  for (uint64_t j = f0 + threadIdx.x; j < f1; j += blockDim.x) {
-    const uint64_t p = j / s, jl = j - p * s;
-    const double* row = R + j * ld;
-    double* o = out + jl + p * s * r;
-    for (uint32_t c = 0; c < r; ++c) {
-      double acc = 0.0;
-      for (uint32_t k = 0; k < r; ++k) acc = fma(rh[c + k * r], row[k], acc);
-      o[uint64_t(c) * s] = acc;
-      sq = fma(acc, acc, sq);
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t j0 = tile * kShrinkTile;
+    const int nf = int(F - j0 < uint64_t(kShrinkTile) ? F - j0 : uint64_t(kShrinkTile));
+    __syncthreads();  // previous tile's readers of Rs / Os are done
+    for (int e = threadIdx.x; e < kShrinkTile * (NC / 2); e += blockDim.x) {
+      const int row = e / (NC / 2), c = (e % (NC / 2)) * 2;
+      double2 v = make_double2(0.0, 0.0);
+      if (row < nf) v = *reinterpret_cast<const double2*>(R + (j0 + row) * ld + c);
+      Rs[row * kLd + c] = c < int(r) ? v.x : 0.0;  // R's padding columns are never written
+      Rs[row * kLd + c + 1] = c + 1 < int(r) ? v.y : 0.0;
+    }
+    __syncthreads();
+    double acc[2][NC / 8][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < NC / 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < NC / 4; ++t) {
+      const int kk = 4 * t + q;
+      double af[2], bf[NC / 8];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) af[m] = Rs[(warp * 16 + m * 8 + r8) * kLd + kk];
+#pragma unroll
+      for (int n = 0; n < NC / 8; ++n) bf[n] = Bs[kk * kLd + n * 8 + r8];
+#pragma unroll
+      for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+        for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+    }
+    __syncthreads();  // Rs becomes the staging buffer Os
+    double* Os = Rs;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < NC / 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int f = warp * 16 + m * 8 + r8, c = n * 8 + 2 * q + e;
+          Os[c * kLdO + f] = acc[m][n][e];
+        }
+    __syncthreads();
+    for (int e = threadIdx.x; e < int(r) * kShrinkTile; e += blockDim.x) {
+      const int c = e / kShrinkTile, f = e % kShrinkTile;
+      if (f >= nf) continue;
+      const uint64_t j = j0 + f, p = j / s, jl = j - p * s;
+      const double v = Os[c * kLdO + f];
+      out[jl + uint64_t(c) * s + p * s * r] = v;
+      sq = fma(v, v, sq);
     }
   }
   sq = block_sum(sq, red);
@@ -391,14 +444,30 @@ __global__ void copy_box_kernel(const double* __restrict__ src, double* __restri
 
 }  // namespace
 
-int shrink_count(uint64_t F) { return int((F + kShrinkFibers - 1) / kShrinkFibers); }
+int shrink_count(uint64_t F) {
+  const uint64_t tiles = (F + kShrinkTile - 1) / kShrinkTile;
+  return int(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 2 * 148)));
+}
 
 cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
                           const double* rhat, double* out, double* sumsq_part, cudaStream_t st) {
   const int grid = shrink_count(s * P);
-  shrink_kernel<<<grid, kShrinkThreads, sizeof(double) * r * r, st>>>(R, ld, s, P, r, rhat, out,
-                                                                       sumsq_part);
-  return cudaGetLastError();
+  const uint32_t nc = r <= 8 ? 8 : (r + 7) / 8 * 8;
+#define TKG_S(N)                                                                                    \
+  if (nc == N) {                                                                                    \
+    const size_t smem = sizeof(double) * (size_t(kShrinkTile) * (N + 4) + size_t(N) * (N + 4));     \
+    cudaError_t e = cudaFuncSetAttribute(shrink_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         int(smem));                                                \
+    if (e != cudaSuccess) {                                                                         \
+      cudaGetLastError();                                                                           \
+      return e;                                                                                     \
+    }                                                                                               \
+    shrink_kernel<N><<<grid, kShrinkThreads, smem, st>>>(R, ld, s, P, r, rhat, out, sumsq_part);   \
+    return cudaGetLastError();                                                                      \
+  }
+  TKG_S(8) TKG_S(16) TKG_S(24) TKG_S(32) TKG_S(40) TKG_S(48) TKG_S(56) TKG_S(64)
+#undef TKG_S
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_sumsq_diff(const double* a, const double* b, uint64_t n, double* part,
