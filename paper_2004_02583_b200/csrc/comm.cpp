@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the library is loaded with dlopen
 
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -119,15 +120,22 @@ struct LocalGroup {
   double* sum = nullptr;  // device scratch (grow-only)
   size_t sum_n = 0;
 
+  bool failed = false;
+
+  // A rank that throws never arrives: the others give up after 120 s (and
+  // every later barrier of the group fails at once) instead of hanging.
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
+    if (failed) raise(11, "LocalComm: a peer rank failed");
     const uint64_t g = gen;
     if (++arrived == world) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+    } else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || failed; }) || failed) {
+      failed = true;
+      cv.notify_all();
+      raise(11, "LocalComm: barrier timed out (a peer rank failed or diverged)");
     }
   }
   ~LocalGroup() {
@@ -143,6 +151,7 @@ class LocalComm final : public Comm {
     rank_ = rank;
     world_ = g_->world;
   }
+  bool shares_device() const override { return true; }
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
     check_cuda(cudaStreamSynchronize(st), "LocalComm sync");
     g_->bufs[rank_] = buf;

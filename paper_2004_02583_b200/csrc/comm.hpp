@@ -28,6 +28,8 @@ class Comm {
   virtual ~Comm() = default;
   int rank() const { return rank_; }
   int world() const { return world_; }
+  // ranks share one device (in-process group)
+  virtual bool shares_device() const { return false; }
   // buf[0..n) <- sum over ranks (identical bits on every rank)
   virtual void allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
   // to rank q: scount[q] doubles at sendbuf + soff[q]; from rank q:

@@ -16,9 +16,10 @@
 //
 // Geometries (see common.cuh for the FiberView vocabulary):
 //   FC kFibI : s == 1, contraction index contiguous  (mode 1)     A box 36 x 128
-//   FC kFibJ : s % 128 == 0, fibers contiguous         (modes > 1)  A box 132 x 16
+//   FC kFibJ : s even, s % 128 == 0 or s >= 1024      (modes > 1)  A box 132 x 32
 //   FR kFibI : s == 1                                               A box 132 x 32
-//   FR kFibJ : s % 32 == 0                                           A box 36 x 128
+//   FR kFibJ : s even, s % 32 == 0 or s >= 128                      A box 68 x 128
+// kFibJ tiles / chunks stay inside one panel p (TMA zero-fills past s).
 // Other layouts use the register-streaming kernels in contract.cu.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -96,8 +97,8 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
 template <int NC, int MODE>
 struct FcT {
   static constexpr int kTF = 128;                       // fibers per tile (8 warps x 16)
-  static constexpr int kKB = MODE == kFibI ? 32 : 16;   // contraction indices per stage
-  static constexpr int kStages = MODE == kFibI ? 4 : 6;
+  static constexpr int kKB = 32;                         // contraction indices per stage
+  static constexpr int kStages = 4;
   static constexpr int kLdA = MODE == kFibI ? 36 : 132; // padded inner extent of the A box
   static constexpr int kRowsA = MODE == kFibI ? kTF : kKB;
   static constexpr int kLdM = NC + 4;
@@ -122,7 +123,10 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint64_t F = a.s * a.P;
-  const uint64_t ntiles = (F + C::kTF - 1) / C::kTF;
+  // kFibJ tiles never cross a panel: tile t covers fibers jl0 .. jl0+127 of
+  // panel p (rows past s are TMA zero-fill and are not stored)
+  const uint64_t tpp = MODE == kFibJ ? (a.s + C::kTF - 1) / C::kTF : 1;
+  const uint64_t ntiles = MODE == kFibJ ? tpp * a.P : (F + C::kTF - 1) / C::kTF;
   const int nkb = int((a.K + C::kKB - 1) / C::kKB);
 
   if (threadIdx.x == 0) {
@@ -141,6 +145,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       prefetch_map(&tmM);
       uint32_t it = 0;
       for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t tp = tile / tpp, jl0 = (tile - tp * tpp) * C::kTF;
         const uint64_t j0 = tile * C::kTF;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int slot = it % C::kStages;
@@ -151,9 +156,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           if (MODE == kFibI) {
             tma_2d(st, &tmA, &full[slot], kb * C::kKB, int(j0));
           } else {
-            const uint64_t p = j0 / a.s;
-            const uint64_t jl = j0 - p * a.s;
-            tma_3d(st, &tmA, &full[slot], int(jl), kb * C::kKB, int(p));
+            tma_3d(st, &tmA, &full[slot], int(jl0), kb * C::kKB, int(tp));
           }
           tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, kb * C::kKB);
         }
@@ -175,6 +178,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const bool want_gram = kGram && a.gram_part != nullptr;
   uint32_t it = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t tp = tile / tpp, jl0 = (tile - tp * tpp) * C::kTF;
     const uint64_t j0 = tile * C::kTF;
     double acc[2][C::kNT][2];
 #pragma unroll
@@ -241,10 +245,17 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     // epilogue straight from registers
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-      const uint64_t j = j0 + warp * 16 + m * 8 + r8;
-      if (j >= F) continue;
-      const uint64_t p = j / a.s;
-      const uint64_t jl = j - p * a.s;
+      uint64_t p, jl;
+      if (MODE == kFibJ) {
+        p = tp;
+        jl = jl0 + warp * 16 + m * 8 + r8;
+        if (jl >= a.s) continue;
+      } else {
+        const uint64_t j = j0 + warp * 16 + m * 8 + r8;
+        if (j >= F) continue;
+        p = j / a.s;
+        jl = j - p * a.s;
+      }
       const int64_t base = int64_t(jl * a.os_j + p * a.os_p);
 #pragma unroll
       for (int n = 0; n < C::kNT; ++n) {
@@ -321,13 +332,15 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 template <int NC, int MODE, bool MCOL>
 struct FrT {
   static constexpr int kIC = 128;   // contraction rows per CTA (8 warps x 16)
-  static constexpr int kKB = 32;    // fibers per stage
-  static constexpr int kStages = 4;
-  static constexpr int kLdA = MODE == kFibI ? 132 : 36;
+  // fibers per stage: kFibJ boxes read kKB+4 contiguous fibers of 128 rows,
+  // so longer runs per row (64) and a double-buffered ring
+  static constexpr int kKB = MODE == kFibI ? 32 : 64;
+  static constexpr int kStages = MODE == kFibI ? 4 : 2;
+  static constexpr int kLdA = MODE == kFibI ? 132 : kKB + 4;
   static constexpr int kRowsA = MODE == kFibI ? kKB : kIC;
-  // M row-major [F][ld]: box (NC+4, 32) -> [32][NC+4];
-  // M column-major (F x r):  box (36, NC)  -> [NC][36]
-  static constexpr int kLdM = MCOL ? 36 : NC + 4;
+  // M row-major [F][ld]: box (NC+4, kKB) -> [kKB][NC+4];
+  // M column-major (F x r):  box (kKB+4, NC)  -> [NC][kKB+4]
+  static constexpr int kLdM = MCOL ? kKB + 4 : NC + 4;
   static constexpr int kRowsM = MCOL ? NC : kKB;
   static constexpr int kBytesA = kRowsA * kLdA * 8;
   static constexpr int kBytesM = kRowsM * kLdM * 8;
@@ -354,8 +367,17 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const uint32_t ig = blockIdx.x % a.igroups;
   const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
   const uint64_t f1 = min(F, f0 + a.fibers_per_range);
-  const int nkb = f1 > f0 ? int((f1 - f0 + C::kKB - 1) / C::kKB) : 0;
   const int i0 = int(ig) * C::kIC;
+  // fiber chunks of up to kKB that never cross a panel (kFibJ): the chunk
+  // starting at j holds min(kKB, end of j's panel or of the range - j) fibers
+  auto chunk_len = [&](uint64_t j) -> int {
+    uint64_t end = f1;
+    if (MODE == kFibJ) {
+      const uint64_t pe = (j / a.s + 1) * a.s;
+      end = pe < end ? pe : end;
+    }
+    return end - j < uint64_t(C::kKB) ? int(end - j) : C::kKB;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -370,12 +392,12 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     if (lane == 0) {
       prefetch_map(&tmA);
       prefetch_map(&tmM);
-      for (int kb = 0; kb < nkb; ++kb) {
+      int kb = 0;
+      for (uint64_t j = f0; j < f1; j += chunk_len(j), ++kb) {
         const int slot = kb % C::kStages;
         const uint32_t ph = (kb / C::kStages) & 1;
         mbar_wait(&empty[slot], ph ^ 1);
         unsigned char* st = ring + size_t(slot) * C::kStageBytes;
-        const uint64_t j = f0 + uint64_t(kb) * C::kKB;
         mbar_arrive_expect_tx(&full[slot], C::kBytesA + C::kBytesM);
         if (MODE == kFibI) {
           tma_2d(st, &tmA, &full[slot], i0, int(j));
@@ -401,15 +423,16 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   double sq_acc = 0.0;
   const bool want_sq = a.sumsq_part != nullptr;
 
-  for (int kb = 0; kb < nkb; ++kb) {
+  int kb = 0;
+  for (uint64_t j = f0; j < f1; ++kb) {
     const int slot = kb % C::kStages;
     const uint32_t ph = (kb / C::kStages) & 1;
     mbar_wait(&full[slot], ph);
     const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes);
     const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes + C::kBytesA);
-    // Fibers past f1 in the last stage belong to the next range: drop them.
-    const uint64_t left = f1 - (f0 + uint64_t(kb) * C::kKB);
-    const int kvalid = left < uint64_t(C::kKB) ? int(left) : C::kKB;
+    // fibers past the chunk (next panel / next range) are dropped
+    const int kvalid = chunk_len(j);
+    j += kvalid;
 #pragma unroll
     for (int t = 0; t < C::kKB / 4; ++t) {
       const int kk = 4 * t + q;
@@ -702,7 +725,10 @@ int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt) {
   if (!encode_fn() || !aligned16(v.base) || !aligned16(mt) || (ldmt % 2) != 0) return -1;
   if (v.s * v.P >= (1ull << 31) || v.K >= (1u << 31)) return -1;
   if (v.s == 1 && v.is_i == 1 && v.is_p % 2 == 0) return kFibI;
-  if (v.s % 128 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 && v.P < (1ull << 31)) return kFibJ;
+  // panel-local 128-fiber tiles: cheap when s is a multiple of 128 or large
+  if ((v.s % 128 == 0 || v.s >= 1024) && v.s % 2 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 &&
+      v.P < (1ull << 31))
+    return kFibJ;
   return -1;
 }
 
@@ -712,7 +738,10 @@ int fr_tma_mode(const FiberView& v, const double* m, uint64_t mj, uint64_t mc) {
   if (!encode_fn() || !aligned16(v.base) || !aligned16(m) || (ld % 2) != 0) return -1;
   if (v.s * v.P >= (1ull << 31)) return -1;
   if (v.s == 1 && v.is_i == 1 && v.is_p % 2 == 0) return kFibI;
-  if (v.s % 32 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 && v.P < (1ull << 31)) return kFibJ;
+  // panel-local 32-fiber chunks: cheap when s is a multiple of 32 or large
+  if ((v.s % 32 == 0 || v.s >= 128) && v.s % 2 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 &&
+      v.P < (1ull << 31))
+    return kFibJ;
   return -1;
 }
 
@@ -725,7 +754,7 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
                           int num_sms, cudaStream_t st, int* grid_used) {
   const uint32_t ncp = pad_nc(a.nc);
   CUtensorMap A, M;
-  const int KB = mode == kFibI ? 32 : 16;
+  const int KB = 32;
   if (mode == kFibI) {
     const uint64_t dims[2] = {v.K, v.s * v.P};
     const uint64_t strides[1] = {v.is_p * 8};
@@ -734,7 +763,7 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
   } else {
     const uint64_t dims[3] = {v.s, v.K, v.P};
     const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
-    const uint32_t box[3] = {132, 16, 1};
+    const uint32_t box[3] = {132, 32, 1};
     if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
@@ -769,18 +798,19 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
   } else {
     const uint64_t dims[3] = {v.s, v.K, v.P};
     const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
-    const uint32_t box[3] = {36, 128, 1};
+    const uint32_t box[3] = {68, 128, 1};
     if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
+  const uint32_t kb = mode == kFibI ? 32 : 64;
   if (!mcol) {
     const uint64_t dims[2] = {ncp, F};
     const uint64_t strides[1] = {mj * 8};
-    const uint32_t box[2] = {ncp + 4, 32};
+    const uint32_t box[2] = {ncp + 4, kb};
     if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
   } else {
     const uint64_t dims[2] = {F, a.nc};
     const uint64_t strides[1] = {mc * 8};
-    const uint32_t box[2] = {36, ncp};
+    const uint32_t box[2] = {kb + 4, ncp};
     if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
   }
   a.s = v.s;

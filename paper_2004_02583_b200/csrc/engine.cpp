@@ -472,7 +472,7 @@ void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32
   q.work = qrq1_.d(2);
   q.ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
   const auto ev = small_begin();
-  CK(launch_cholqr_step(q, sms_, st_));
+  coop_launch([&] { CK(launch_cholqr_step(q, sms_, st_)); });
   small_end(ev);
   count_launch();
 }
@@ -597,7 +597,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       {
         const size_t rec = recs_.size();
         const auto ev = small_begin();
-        CK(launch_prep_step(pa, sms_, st_));
+        coop_launch([&] { CK(launch_prep_step(pa, sms_, st_)); });
         small_end(ev);
         trace("  prep launched", k);
         if (profiling_) spec_recs_.push_back({k, 0, rec});
@@ -628,14 +628,14 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
           int nparts = fc_used;
           if (!fused_gram) {
             fa.mode = 1;
-            CK(launch_finish_step(fa, sms_, st_));
+            coop_launch([&] { CK(launch_finish_step(fa, sms_, st_)); });
             nparts = finish_step_grid(F, sms_);
           }
           CK(launch_gram_reduce(gpr, nparts, uint64_t(ncp) * ncp, ncp, r, gs, st_));
           dist_->allreduce_sum(gs, size_t(r) * r, st_);
           fa.mode = 2;
         }
-        CK(launch_finish_step(fa, sms_, st_));
+        coop_launch([&] { CK(launch_finish_step(fa, sms_, st_)); });
         small_end(ev);
         trace("  finish launched", k);
         if (profiling_) spec_recs_.push_back({k, 0, rec});

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -182,6 +183,20 @@ class Engine {
   void begin_timed();
   void count_launch(int n = 1) { launches_ += n; }
   void reshard(const double* src, const Shape& G, int from, int to, double* dst);
+  // Cooperative (grid.sync) launches. Ranks of an in-process group share one
+  // device: two partially resident cooperative grids could wait on each
+  // other, so there they run one at a time (process-wide lock, synchronised).
+  template <class F>
+  void coop_launch(F&& launch) {
+    if (comm_ && comm_->shares_device()) {
+      std::lock_guard<std::mutex> g(coop_mutex());
+      launch();
+      check_cuda(cudaStreamSynchronize(st_), "coop sync");
+    } else {
+      launch();
+    }
+  }
+  static std::mutex& coop_mutex();
   void check_shard(const Shape& G, uint64_t begin, uint64_t len);
   void dist_core_and_residual(const double* A, const Shape& L, uint64_t k0, const Shape& G,
                               const std::vector<uint64_t>& ranks, std::vector<double*>& U, double* core_buf,

@@ -61,6 +61,11 @@ ShardRange shard_range(uint64_t extent, int rank, int world) {
 
 void Engine::set_comm(std::unique_ptr<Comm> c) { comm_ = std::move(c); }
 
+std::mutex& Engine::coop_mutex() {
+  static std::mutex m;
+  return m;
+}
+
 // dst (sharded along `to`) <- src (sharded along `from`) of the global shape
 // G: pack one box per destination, one alltoallv, unpack one box per source.
 void Engine::reshard(const double* src, const Shape& G, int from, int to, double* dst) {

@@ -33,14 +33,14 @@ def run_ranks(world, fn):
         except BaseException as e:  # noqa: BLE001 - reported below
             errs.append((r, e))
 
-    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
     for t in th:
         t.start()
     for t in th:
-        t.join(timeout=240)
-    assert not any(t.is_alive() for t in th), "a rank did not finish"
+        t.join(timeout=200)
     if errs:
-        raise errs[0][1]
+        raise RuntimeError("; ".join(f"rank {r}: {type(e).__name__}: {e}" for r, e in errs)) from errs[0][1]
+    assert not any(t.is_alive() for t in th), "a rank did not finish" 
     for c in ctxs:
         c.close()
     return out

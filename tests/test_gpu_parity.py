@@ -17,7 +17,9 @@ from parity import assert_parity, compare_decompositions, ortho_defect, principa
 pytestmark = pytest.mark.gpu
 
 SHAPES = [[7], [6, 8], [3, 4, 5], [4, 3, 2, 5], [3, 2, 4, 2, 3], [40, 30, 20], [300, 9, 5],
-          [5, 3, 700], [64, 33, 17], [10, 96, 7], [17, 4, 6, 5]]
+          [5, 3, 700], [64, 33, 17], [10, 96, 7], [17, 4, 6, 5],
+          # panel-local TMA tiles (s not a multiple of 32 / 128): s = 1500, 200, 1360
+          [30, 50, 20], [200, 6, 4], [34, 40, 3]]
 
 
 def rel(a, b):
