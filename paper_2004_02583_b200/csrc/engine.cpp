@@ -140,6 +140,8 @@ Engine::~Engine() {
     cudaEventDestroy(r.b);
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto e : mode_ev_) cudaEventDestroy(e);
+  if (stage_h_) cudaFreeHost(stage_h_);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
   cudaStreamSynchronize(st2_);
@@ -493,8 +495,37 @@ int Engine::qr_degenerate_col() {
   return h.degenerate_col;
 }
 
+void Engine::stage_reserve(int modes, int max_iters) {
+  const size_t n = size_t(std::max(1, modes)) * size_t(std::max(1, max_iters) + 1);
+  if (n > stage_n_) {
+    sync();  // no copy into the old buffer is pending
+    if (stage_h_) cudaFreeHost(stage_h_);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_h_), n * sizeof(double), cudaHostAllocDefault));
+    stage_n_ = n;
+  }
+  stage_iters_ = std::max(1, max_iters);
+  while (mode_ev_.size() < size_t(2 * std::max(1, modes))) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    mode_ev_.push_back(e);
+  }
+}
+
+void Engine::collect(AlsOut& o, ModeRep& dst) const {
+  dst = o.rep;
+  dst.history.assign(o.hist_host, o.hist_host + o.rep.iterations);
+}
+
+void Engine::mode_begin(int k) { CK(cudaEventRecord(mode_ev_[2 * k], st_)); }
+void Engine::mode_end(int k) { CK(cudaEventRecord(mode_ev_[2 * k + 1], st_)); }
+double Engine::mode_seconds(int k) {
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, mode_ev_[2 * k], mode_ev_[2 * k + 1]));
+  return ms * 1e-3;
+}
+
 Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint32_t r,
-                               const AlsCfg& cfg, bool sumsq_known, const MtWindow& win) {
+                               const AlsCfg& cfg, bool sumsq_known, const MtWindow& win, int slot) {
   const uint64_t I = sh.extent(mode);
   const uint64_t s = sh.stride(mode);
   const uint64_t F = sh.count() / I;
@@ -687,13 +718,15 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   rep.iterations = h.iter;
   rep.status = h.status;
   rep.achieved_eta = h.achieved;
-  rep.history.resize(size_t(h.iter));
-  if (h.iter > 0)
-    CK(cudaMemcpyAsync(rep.history.data(), hist, sizeof(double) * h.iter, cudaMemcpyDeviceToHost, st_));
-  sync();
   out.norm = h.norm;
-  CK(cudaMemcpyAsync(&last_sumsq_, sumsq, sizeof(double), cudaMemcpyDeviceToHost, st_));
-  sync();
+  if (stage_n_ < size_t(slot + 1) * size_t(stage_iters_ + 1) || stage_iters_ < max_iters)
+    stage_reserve(slot + 1, max_iters);
+  double* hs = stage_h_ + size_t(slot) * size_t(stage_iters_ + 1);
+  if (h.iter > 0)
+    CK(cudaMemcpyAsync(hs, hist, sizeof(double) * h.iter, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(hs + stage_iters_, sumsq, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  out.hist_host = hs;
+  out.sumsq_host = hs + stage_iters_;
   trace("als done", mode);
   return out;
 }
@@ -734,8 +767,7 @@ void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint
 // the difference norm (relative_error(t, reconstruct(tk)), hosvd.cpp:123,189).
 double Engine::relative_residual_dev(const double* A, const Shape& sh,
                                      const std::vector<uint64_t>& ranks, const double* d_core,
-                                     const std::vector<double*>& d_factors, double ref_sumsq) {
-  if (ref_sumsq == 0.0) raise(3, "relative_error: reference tensor has zero norm");
+                                     const std::vector<double*>& d_factors, const double* ref_sumsq_host) {
   Shape cur;
   cur.N = sh.N;
   for (int k = 0; k < sh.N; ++k) cur.d[k] = ranks[k];
@@ -782,6 +814,8 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
   double diff_sq = 0.0;
   CK(cudaMemcpyAsync(&diff_sq, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
+  const double ref_sumsq = *ref_sumsq_host;
+  if (ref_sumsq == 0.0) raise(3, "relative_error: reference tensor has zero norm");
   return std::sqrt(diff_sq / ref_sumsq);
 }
 
@@ -801,21 +835,19 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     pregenerate(items, cfg.seed);
   }
   trace("pregenerate enqueued");
+  stage_reserve(sh.N, cfg.max_iters);
   bool sumsq_known = false;
-  double ref_sumsq = 0.0;
+  std::vector<AlsOut> outs;
   for (int n = 1; n <= sh.N; ++n) {
-    const auto tm = Clock::now();
     const uint32_t r = uint32_t(ranks[n - 1]);
     const uint64_t I = sh.d[n - 1];
-    AlsOut o = run_als(A, sh, n, r, cfg, sumsq_known);
-    if (!sumsq_known) ref_sumsq = last_sumsq_;
+    mode_begin(n - 1);
+    outs.push_back(run_als(A, sh, n, r, cfg, sumsq_known, MtWindow(), n - 1));
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
     qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
-    sync();
-    trace("mode done (qr synced)", n);
-    o.rep.seconds = since(tm);
-    rep->per_mode.push_back(o.rep);
+    mode_end(n - 1);
+    trace("mode done", n);
   }
   Shape cs;
   cs.N = sh.N;
@@ -824,6 +856,12 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   core_chain(A, sh, ranks, U, core_buf);
   sync();
   trace("core synced");
+  for (int n = 0; n < sh.N; ++n) {
+    rep->per_mode.emplace_back();
+    collect(outs[n], rep->per_mode.back());
+    rep->per_mode.back().seconds = mode_seconds(n);
+  }
+  const double* ref_sumsq = outs[0].sumsq_host;
   rep->seconds = since(t0);
   rep->launches = launches_;
   rep->passes = passes_;
@@ -873,7 +911,6 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
   DBuf* bufs[2] = {&work_a_, &work_b_};
   int which = 0;
   bool sumsq_known = false;
-  double ref_sumsq = 0.0;
   {
     std::vector<PreGen> items;
     Shape w = sh;
@@ -884,12 +921,14 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     }
     pregenerate(items, cfg.seed);
   }
+  stage_reserve(sh.N, cfg.max_iters);
+  std::vector<AlsOut> outs;
   for (int mode : order) {
-    const auto tm = Clock::now();
+    const int k = int(outs.size());
     const uint32_t r = uint32_t(ranks[mode - 1]);
     const uint64_t I = cur.extent(mode), s = cur.stride(mode), F = cur.count() / I, P = F / s;
-    AlsOut o = run_als(work, cur, mode, r, cfg, sumsq_known);
-    if (!sumsq_known) ref_sumsq = last_sumsq_;
+    mode_begin(k);
+    outs.push_back(run_als(work, cur, mode, r, cfg, sumsq_known, MtWindow(), k));
     const uint32_t ncp = pad_nc(r);
     U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
     double* RhT = rhatT_.d(size_t(r) * ncp);
@@ -906,9 +945,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     count_launch(2);
     (void)RhT;
     sumsq_known = true;
-    sync();
-    o.rep.seconds = since(tm);
-    rep->per_mode.push_back(o.rep);
+    mode_end(k);
     work = dst;
     cur = nxt;
     which ^= 1;
@@ -917,6 +954,12 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
   double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
   CK(cudaMemcpyAsync(core_buf, work, cs.count() * sizeof(double), cudaMemcpyDeviceToDevice, st_));
   sync();
+  for (size_t k = 0; k < outs.size(); ++k) {
+    rep->per_mode.emplace_back();
+    collect(outs[k], rep->per_mode.back());
+    rep->per_mode.back().seconds = mode_seconds(int(k));
+  }
+  const double* ref_sumsq = outs[0].sumsq_host;
   rep->seconds = since(t0);
   rep->launches = launches_;
   rep->passes = passes_;
@@ -945,7 +988,6 @@ void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode
   const double* A = upload(a, sh.count(), a_dev, tensor_, nullptr);
   if (cfg.init && r > kMaxRank) raise(12, "rank above the supported 64");
   AlsOut o = run_als(A, sh, mode, r, cfg, false);
-  *rep = o.rep;
   const uint64_t F = sh.count() / I;
   CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   if (r_out) {  // R is row-major [F][ncp] on the device; the API returns column-major F x r
@@ -955,6 +997,7 @@ void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode
     CK(cudaMemcpyAsync(r_out, rc, F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   }
   sync();
+  collect(o, *rep);
 }
 
 void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,

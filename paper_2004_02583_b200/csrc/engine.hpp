@@ -141,14 +141,25 @@ class Engine {
 
  private:
   struct AlsOut {
-    ModeRep rep;
+    ModeRep rep;          // history filled by collect() after the next sync
     double norm = 0.0;
+    const double* hist_host = nullptr;   // pinned staging, rep.iterations values
+    const double* sumsq_host = nullptr;  // pinned staging: ||working tensor||^2
   };
+  // Host-visible results of the decomposition drivers are staged in pinned
+  // memory with asynchronous copies and read after the driver's single final
+  // synchronisation (one slot of max_iters + 1 doubles per mode), and the
+  // per-mode times are CUDA events on the stream.
+  void stage_reserve(int modes, int max_iters);
+  void collect(AlsOut& o, ModeRep& dst) const;
+  void mode_begin(int k);
+  void mode_end(int k);
+  double mode_seconds(int k);
   // Runs als_low_rank on a device-resident tensor; L (col-major I x r) is
   // left in l_, R (F x r) in r_. sumsq_known: status_->sumsq already holds
   // ||A||^2 of this tensor.
   AlsOut run_als(const double* A, const Shape& sh, int mode, uint32_t r, const AlsCfg& cfg,
-                 bool sumsq_known, const MtWindow& win = MtWindow());
+                 bool sumsq_known, const MtWindow& win = MtWindow(), int slot = 0);
   uint32_t reduce_left_partials(double* part, uint32_t nparts, uint32_t I, uint32_t ncp, uint32_t r);
   // draws 0..n-1 in storage order, or a shard's window of them (MtWindow)
   void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win = MtWindow());
@@ -175,9 +186,10 @@ class Engine {
               double* rmat, double* rt, uint32_t ldrt, bool check);
   int qr_degenerate_col();
   const double* upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds);
+  // ref_sumsq_host: pinned ||A||^2, read after the function's own sync
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                                const double* d_core, const std::vector<double*>& d_factors,
-                               double ref_sumsq);
+                               const double* ref_sumsq_host);
   void core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                   const std::vector<double*>& d_factors, double* d_core);
   void begin_timed();
@@ -200,7 +212,7 @@ class Engine {
   void check_shard(const Shape& G, uint64_t begin, uint64_t len);
   void dist_core_and_residual(const double* A, const Shape& L, uint64_t k0, const Shape& G,
                               const std::vector<uint64_t>& ranks, std::vector<double*>& U, double* core_buf,
-                              bool compute_core, double ref_sumsq, DecompRep* rep, double* core_host,
+                              bool compute_core, std::vector<AlsOut>& outs, DecompRep* rep, double* core_host,
                               double* factors_host, std::chrono::steady_clock::time_point t0);
   std::pair<cudaEvent_t, cudaEvent_t> small_begin();
   void small_end(std::pair<cudaEvent_t, cudaEvent_t> ev);
@@ -228,7 +240,10 @@ class Engine {
   DBuf tensor_, work_a_, work_b_, s_, r_, l_, mt_, gl_, gr_, cholL_, cholR_;
   DBuf fr_part_, fc_gram_, gram_part_, gs_, sq_part_, qr_work_, q_, rhat_, rhatT_;
   DBuf y_seq_, states_, chunk_ids_, misc_, misc2_, flush_, qy_, qrl1_, qrl2_, qrq1_, sumsq_d_, ctrl_d_, hist_d_;
-  double last_sumsq_ = 0.0;  // ||working tensor||^2 of the last run_als
+  double* stage_h_ = nullptr;  // pinned
+  size_t stage_n_ = 0;
+  int stage_iters_ = 0;
+  std::vector<cudaEvent_t> mode_ev_;
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   std::vector<DBuf*> factor_bufs_;
   std::map<std::pair<uint64_t, int>, DBuf*> jump_cache_;

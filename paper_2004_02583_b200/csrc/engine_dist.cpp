@@ -150,8 +150,8 @@ void Engine::check_shard(const Shape& G, uint64_t begin, uint64_t len) {
 // mode: the TTM chain over the local slab with U_N's slab rows, summed.
 void Engine::dist_core_and_residual(const double* A, const Shape& L, uint64_t k0, const Shape& G,
                                     const std::vector<uint64_t>& ranks, std::vector<double*>& U,
-                                    double* core_buf, bool compute_core, double ref_sumsq, DecompRep* rep,
-                                    double* core_host, double* factors_host, Clock::time_point t0) {
+                                    double* core_buf, bool compute_core, std::vector<AlsOut>& outs,
+                                    DecompRep* rep, double* core_host, double* factors_host, Clock::time_point t0) {
   const int N = G.N;
   const uint64_t nloc = L.d[N - 1];
   const uint32_t rN = uint32_t(ranks[N - 1]);
@@ -169,6 +169,11 @@ void Engine::dist_core_and_residual(const double* A, const Shape& L, uint64_t k0
   }
   sync();
   rep->seconds = since(t0);
+  for (size_t k = 0; k < outs.size(); ++k) {
+    rep->per_mode.emplace_back();
+    collect(outs[k], rep->per_mode.back());
+    rep->per_mode.back().seconds = mode_seconds(int(k));
+  }
   rep->launches = launches_;
   rep->passes = passes_;
   rep->bytes = bytes_;
@@ -183,7 +188,7 @@ void Engine::dist_core_and_residual(const double* A, const Shape& L, uint64_t k0
   sync();
   rep->d2h_seconds = since(td);
   const auto tr = Clock::now();
-  rep->relative_residual = relative_residual_dev(A, L, ranks, core_buf, Us, ref_sumsq);
+  rep->relative_residual = relative_residual_dev(A, L, ranks, core_buf, Us, outs[0].sumsq_host);
   rep->residual_seconds = since(tr);
 }
 
@@ -221,10 +226,11 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
     }
     pregenerate(items, cfg.seed);
   }
+  stage_reserve(N, cfg.max_iters);
   bool sumsq_known = false;
-  double ref_sumsq = 0.0;
+  std::vector<AlsOut> outs;
   for (int n = 1; n <= N; ++n) {
-    const auto tm = Clock::now();
+    mode_begin(n - 1);
     const uint32_t r = uint32_t(ranks[n - 1]);
     const uint64_t I = G.d[n - 1];
     const double* An = A;
@@ -239,20 +245,17 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
       }
       Ln = &LB;
     }
-    AlsOut o = run_als(An, *Ln, n, r, cfg, sumsq_known, window(n));
-    if (!sumsq_known) ref_sumsq = last_sumsq_;
+    outs.push_back(run_als(An, *Ln, n, r, cfg, sumsq_known, window(n), n - 1));
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
     qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
-    sync();
-    o.rep.seconds = since(tm);
-    rep->per_mode.push_back(o.rep);
+    mode_end(n - 1);
   }
   Shape cs;
   cs.N = N;
   for (int k = 0; k < N; ++k) cs.d[k] = ranks[k];
   double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
-  dist_core_and_residual(A, L, k0, G, ranks, U, core_buf, true, ref_sumsq, rep, core, factors, t0);
+  dist_core_and_residual(A, L, k0, G, ranks, U, core_buf, true, outs, rep, core, factors, t0);
 }
 
 void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t k0, uint64_t nloc,
@@ -326,11 +329,13 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
   DBuf* bufs[2] = {&work_a_, &work_b_};
   int which = 0;
   bool sumsq_known = false;
-  double ref_sumsq = 0.0;
   int sm = N;
   Shape Gw = G;
+  stage_reserve(N, cfg.max_iters);
+  std::vector<AlsOut> outs;
   for (const Step& st : plan) {
-    const auto tm = Clock::now();
+    const int k = int(outs.size());
+    mode_begin(k);
     const int mode = st.mode;
     if (st.move) {
       const Shape Lnew = local_shape(Gw, st.sm);
@@ -344,8 +349,7 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
     const Shape Lw = local_shape(Gw, sm);
     const uint32_t r = uint32_t(ranks[mode - 1]);
     const uint64_t I = Gw.d[mode - 1], s = Lw.stride(mode), F = Lw.count() / I, P = F / s;
-    AlsOut o = run_als(work, Lw, mode, r, cfg, sumsq_known, window(st));
-    if (!sumsq_known) ref_sumsq = last_sumsq_;
+    outs.push_back(run_als(work, Lw, mode, r, cfg, sumsq_known, window(st), k));
     const uint32_t ncp = pad_nc(r);
     U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
     double* RhT = rhatT_.d(size_t(r) * ncp);
@@ -361,9 +365,7 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
     count_launch(2);
     comm_->allreduce_sum(sumsq_d_.d(2), 1, st_);
     sumsq_known = true;
-    sync();
-    o.rep.seconds = since(tm);
-    rep->per_mode.push_back(o.rep);
+    mode_end(k);
     work = dst;
     Gw.d[mode - 1] = r;
     which ^= 1;
@@ -390,7 +392,7 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
     count_launch();
   }
   comm_->allreduce_sum(core_buf, cs.count(), st_);
-  dist_core_and_residual(A, L, k0, G, ranks, U, core_buf, false, ref_sumsq, rep, core, factors, t0);
+  dist_core_and_residual(A, L, k0, G, ranks, U, core_buf, false, outs, rep, core, factors, t0);
 }
 
 }  // namespace tkg
