@@ -98,11 +98,12 @@ template <int NC, int MODE>
 struct FcT {
   static constexpr int kTF = 128;                       // fibers per tile (8 warps x 16)
   static constexpr int kKB = 32;                         // contraction indices per stage
-  static constexpr int kStages = 4;
+  static constexpr int kStages = MODE == kFibS ? 3 : 4;
   static constexpr int kLdA = MODE == kFibI ? 36 : 132; // padded inner extent of the A box
   static constexpr int kRowsA = MODE == kFibI ? kTF : kKB;
   static constexpr int kLdM = NC + 4;
-  static constexpr int kBytesA = kRowsA * kLdA * 8;
+  // kFibS: the A box is {sb, 32, pc} with pc*sb <= 160 (runtime size)
+  static constexpr int kBytesA = MODE == kFibS ? kKB * 160 * 8 : kRowsA * kLdA * 8;
   static constexpr int kBytesM = kKB * kLdM * 8;
   static constexpr int kStageBytes = ((kBytesA + kBytesM) + 127) / 128 * 128;
   static constexpr int kNT = NC / 8;
@@ -126,8 +127,13 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   // kFibJ tiles never cross a panel: tile t covers fibers jl0 .. jl0+127 of
   // panel p (rows past s are TMA zero-fill and are not stored)
   const uint64_t tpp = MODE == kFibJ ? (a.s + C::kTF - 1) / C::kTF : 1;
-  const uint64_t ntiles = MODE == kFibJ ? tpp * a.P : (F + C::kTF - 1) / C::kTF;
+  // kFibS tiles are a.pc whole panels (a.pc * s <= 128 fibers)
+  const uint64_t ntiles = MODE == kFibJ   ? tpp * a.P
+                          : MODE == kFibS ? (a.P + a.pc - 1) / a.pc
+                                          : (F + C::kTF - 1) / C::kTF;
   const int nkb = int((a.K + C::kKB - 1) / C::kKB);
+  const int stage_bytes = MODE == kFibS ? int(a.stage_bytes) : C::kStageBytes;
+  const int bytes_a = MODE == kFibS ? int(a.bytes_a) : C::kBytesA;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -151,14 +157,16 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           const int slot = it % C::kStages;
           const uint32_t ph = (it / C::kStages) & 1;
           mbar_wait(&empty[slot], ph ^ 1);
-          unsigned char* st = ring + size_t(slot) * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[slot], C::kBytesA + C::kBytesM);
+          unsigned char* st = ring + size_t(slot) * stage_bytes;
+          mbar_arrive_expect_tx(&full[slot], bytes_a + C::kBytesM);
           if (MODE == kFibI) {
             tma_2d(st, &tmA, &full[slot], kb * C::kKB, int(j0));
-          } else {
+          } else if (MODE == kFibJ) {
             tma_3d(st, &tmA, &full[slot], int(jl0), kb * C::kKB, int(tp));
+          } else {
+            tma_3d(st, &tmA, &full[slot], 0, kb * C::kKB, int(tile * a.pc));
           }
-          tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, kb * C::kKB);
+          tma_2d(st + bytes_a, &tmM, &full[slot], 0, kb * C::kKB);
         }
       }
     }
@@ -168,6 +176,19 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   // ---------------- consumers ----------------
   const int q = lane & 3;
   const int r8 = lane >> 2;
+  // kFibS: tile row m is fiber jl = m % s of panel m / s of the tile; its A
+  // column kk sits at (panel*kKB + kk)*sb + jl
+  int offS[2] = {0, 0};
+  bool okS[2] = {true, true};
+  if (MODE == kFibS) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int row = warp * 16 + m * 8 + r8;
+      const int pcm = row / int(a.s), jl = row - pcm * int(a.s);
+      okS[m] = pcm < int(a.pc);
+      offS[m] = okS[m] ? (pcm * C::kKB) * int(a.sb) + jl : 0;
+    }
+  }
   double sq_acc = 0.0;
   // Gram of the output rows (fused epilogue): upper 8x8 tiles (tm <= tn)
   constexpr bool kGram = NC <= int(kFcGramMaxNc);
@@ -190,8 +211,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       const int slot = it % C::kStages;
       const uint32_t ph = (it / C::kStages) & 1;
       mbar_wait(&full[slot], ph);
-      const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes);
-      const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes + C::kBytesA);
+      const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes);
+      const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes + bytes_a);
 #pragma unroll
       for (int t = 0; t < C::kKB / 4; ++t) {
         const int kk = 4 * t + q;
@@ -199,7 +220,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           const int row = warp * 16 + m * 8 + r8;
-          af[m] = MODE == kFibI ? As[row * C::kLdA + kk] : As[kk * C::kLdA + row];
+          if (MODE == kFibS) af[m] = okS[m] ? As[offS[m] + kk * int(a.sb)] : 0.0;
+          else af[m] = MODE == kFibI ? As[row * C::kLdA + kk] : As[kk * C::kLdA + row];
         }
         double bf[C::kNT];
 #pragma unroll
@@ -250,6 +272,13 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         p = tp;
         jl = jl0 + warp * 16 + m * 8 + r8;
         if (jl >= a.s) continue;
+      } else if (MODE == kFibS) {
+        if (!okS[m]) continue;
+        const int row = warp * 16 + m * 8 + r8;
+        const uint64_t pcm = uint64_t(row) / a.s;
+        p = tile * a.pc + pcm;
+        jl = uint64_t(row) - pcm * a.s;
+        if (p >= a.P) continue;
       } else {
         const uint64_t j = j0 + warp * 16 + m * 8 + r8;
         if (j >= F) continue;
@@ -334,6 +363,7 @@ struct FrT {
   static constexpr int kIC = 128;   // contraction rows per CTA (8 warps x 16)
   // fibers per stage: kFibJ boxes read kKB+4 contiguous fibers of 128 rows,
   // so longer runs per row (64) and a double-buffered ring
+  // kFibS (short panels): a chunk is pc whole panels, kf = pc*s <= 64 fibers
   static constexpr int kKB = MODE == kFibI ? 32 : 64;
   static constexpr int kStages = MODE == kFibI ? 4 : 2;
   static constexpr int kLdA = MODE == kFibI ? 132 : kKB + 4;
@@ -342,7 +372,7 @@ struct FrT {
   // M column-major (F x r):  box (kKB+4, NC)  -> [NC][kKB+4]
   static constexpr int kLdM = MCOL ? kKB + 4 : NC + 4;
   static constexpr int kRowsM = MCOL ? NC : kKB;
-  static constexpr int kBytesA = kRowsA * kLdA * 8;
+  static constexpr int kBytesA = MODE == kFibS ? kIC * 64 * 8 : kRowsA * kLdA * 8;  // kFibS: max
   static constexpr int kBytesM = kRowsM * kLdM * 8;
   static constexpr int kStageBytes = ((kBytesA + kBytesM) + 127) / 128 * 128;
   static constexpr int kNT = NC / 8;
@@ -370,14 +400,21 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const int i0 = int(ig) * C::kIC;
   // fiber chunks of up to kKB that never cross a panel (kFibJ): the chunk
   // starting at j holds min(kKB, end of j's panel or of the range - j) fibers
+  // kFibS: ranges are whole panels and chunks a.kf = a.pc * s fibers, so a
+  // chunk is a.pc whole panels (the last one of a range may be shorter)
+  const int kmax = MODE == kFibS ? int(a.kf) : C::kKB;
   auto chunk_len = [&](uint64_t j) -> int {
     uint64_t end = f1;
     if (MODE == kFibJ) {
       const uint64_t pe = (j / a.s + 1) * a.s;
       end = pe < end ? pe : end;
     }
-    return end - j < uint64_t(C::kKB) ? int(end - j) : C::kKB;
+    return end - j < uint64_t(kmax) ? int(end - j) : kmax;
   };
+  const int stage_bytes = MODE == kFibS ? int(a.stage_bytes) : C::kStageBytes;
+  const int bytes_a = MODE == kFibS ? int(a.bytes_a) : C::kBytesA;
+  const int bytes_m = MODE == kFibS ? int(a.bytes_m) : C::kBytesM;
+  const int ldm = MODE == kFibS && MCOL ? int(a.ldm) : C::kLdM;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -397,8 +434,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         const int slot = kb % C::kStages;
         const uint32_t ph = (kb / C::kStages) & 1;
         mbar_wait(&empty[slot], ph ^ 1);
-        unsigned char* st = ring + size_t(slot) * C::kStageBytes;
-        mbar_arrive_expect_tx(&full[slot], C::kBytesA + C::kBytesM);
+        unsigned char* st = ring + size_t(slot) * stage_bytes;
+        mbar_arrive_expect_tx(&full[slot], bytes_a + bytes_m);
         if (MODE == kFibI) {
           tma_2d(st, &tmA, &full[slot], i0, int(j));
         } else {
@@ -406,8 +443,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           const uint64_t jl = j - p * a.s;
           tma_3d(st, &tmA, &full[slot], int(jl), i0, int(p));
         }
-        if (MCOL) tma_2d(st + C::kBytesA, &tmM, &full[slot], int(j), 0);
-        else tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, int(j));
+        if (MCOL) tma_2d(st + bytes_a, &tmM, &full[slot], int(j), 0);
+        else tma_2d(st + bytes_a, &tmM, &full[slot], 0, int(j));
       }
     }
     return;
@@ -422,14 +459,23 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
   double sq_acc = 0.0;
   const bool want_sq = a.sumsq_part != nullptr;
+  // kFibS: fiber kk of a chunk is jl = kk % s of panel kk / s; its A rows sit
+  // at ((kk / s)*128 + row)*s + jl
+  int koff[C::kKB / 4];
+#pragma unroll
+  for (int t = 0; t < C::kKB / 4; ++t) {
+    const int kk = 4 * t + q;
+    const int pc = MODE == kFibS ? kk / int(a.s) : 0;
+    koff[t] = MODE == kFibS ? pc * C::kIC * int(a.s) + (kk - pc * int(a.s)) : 0;
+  }
 
   int kb = 0;
   for (uint64_t j = f0; j < f1; ++kb) {
     const int slot = kb % C::kStages;
     const uint32_t ph = (kb / C::kStages) & 1;
     mbar_wait(&full[slot], ph);
-    const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes);
-    const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes + C::kBytesA);
+    const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes);
+    const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes + bytes_a);
     // fibers past the chunk (next panel / next range) are dropped
     const int kvalid = chunk_len(j);
     j += kvalid;
@@ -441,14 +487,22 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 #pragma unroll
       for (int m = 0; m < 2; ++m) {
         const int row = warp * 16 + m * 8 + r8;
-        const double v = MODE == kFibI ? As[kk * C::kLdA + row] : As[row * C::kLdA + kk];
+        double v;
+        if (MODE == kFibS) v = kok ? As[koff[t] + row * int(a.s)] : 0.0;
+        else v = MODE == kFibI ? As[kk * C::kLdA + row] : As[row * C::kLdA + kk];
         af[m] = kok ? v : 0.0;
         if (want_sq) sq_acc = fma(af[m], af[m], sq_acc);
       }
       double bf[C::kNT];
 #pragma unroll
-      for (int n = 0; n < C::kNT; ++n)
-        bf[n] = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
+      for (int n = 0; n < C::kNT; ++n) {
+        if (MODE == kFibS) {  // rows past the chunk are not loaded: keep them finite
+          const double v = MCOL ? Ms[(n * 8 + r8) * ldm + kk] : Ms[kk * C::kLdM + n * 8 + r8];
+          bf[n] = kok ? v : 0.0;
+        } else {
+          bf[n] = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
+        }
+      }
 #pragma unroll
       for (int n = 0; n < C::kNT; ++n)
 #pragma unroll
@@ -725,11 +779,9 @@ int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt) {
   if (!encode_fn() || !aligned16(v.base) || !aligned16(mt) || (ldmt % 2) != 0) return -1;
   if (v.s * v.P >= (1ull << 31) || v.K >= (1u << 31)) return -1;
   if (v.s == 1 && v.is_i == 1 && v.is_p % 2 == 0) return kFibI;
-  // panel-local 128-fiber tiles: cheap when s is a multiple of 128 or large
-  if ((v.s % 128 == 0 || v.s >= 1024) && v.s % 2 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 &&
-      v.P < (1ull << 31))
-    return kFibJ;
-  return -1;
+  if (v.s % 2 != 0 || v.is_i % 2 != 0 || v.is_p % 2 != 0 || v.P >= (1ull << 31)) return -1;
+  // panel-local 128-fiber tiles for long panels, whole-panel tiles for short ones
+  return v.s >= 128 ? kFibJ : kFibS;
 }
 
 int fr_tma_mode(const FiberView& v, const double* m, uint64_t mj, uint64_t mc) {
@@ -738,12 +790,32 @@ int fr_tma_mode(const FiberView& v, const double* m, uint64_t mj, uint64_t mc) {
   if (!encode_fn() || !aligned16(v.base) || !aligned16(m) || (ld % 2) != 0) return -1;
   if (v.s * v.P >= (1ull << 31)) return -1;
   if (v.s == 1 && v.is_i == 1 && v.is_p % 2 == 0) return kFibI;
-  // panel-local 32-fiber chunks: cheap when s is a multiple of 32 or large
-  if ((v.s % 32 == 0 || v.s >= 128) && v.s % 2 == 0 && v.is_i % 2 == 0 && v.is_p % 2 == 0 &&
-      v.P < (1ull << 31))
-    return kFibJ;
-  return -1;
+  if (v.s % 2 != 0 || v.is_i % 2 != 0 || v.is_p % 2 != 0 || v.P >= (1ull << 31)) return -1;
+  // panel-local 64-fiber chunks for long panels, whole-panel chunks for short ones
+  return (v.s % 32 == 0 || v.s >= 64) ? kFibJ : kFibS;
 }
+
+namespace {
+
+// kFibS FC: panels per tile and the padded inner box extent (4 mod 16
+// doubles when that costs at most a quarter more)
+void fc_short_geometry(uint64_t s, uint32_t* pc, uint32_t* sb) {
+  *pc = uint32_t(128 / s);
+  uint32_t b = uint32_t(s) + uint32_t((4 + 16 - s % 16) % 16);
+  *sb = (b <= s + s / 4) ? b : uint32_t(s);
+}
+
+// kFibS FR: panels per chunk (kf = pc * s <= 64 fibers) and the panel ranges
+void fr_short_geometry(const FiberView& v, int num_sms, uint32_t* pc, uint64_t* ppr, uint32_t* ranges) {
+  *pc = uint32_t(64 / v.s);
+  const uint32_t igroups = (v.K + 127) / 128;
+  uint64_t r = std::max<uint64_t>(1, uint64_t(num_sms) / igroups);
+  r = std::min<uint64_t>(r, std::max<uint64_t>(1, v.P / (4 * *pc)));
+  *ppr = (v.P + r - 1) / r;
+  *ranges = uint32_t((v.P + *ppr - 1) / *ppr);
+}
+
+}  // namespace
 
 int fc_tma_grid(const FiberView& v, int num_sms) {
   const uint64_t tiles = (v.s * v.P + 127) / 128;
@@ -760,11 +832,19 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
     const uint64_t strides[1] = {v.is_p * 8};
     const uint32_t box[2] = {36, 128};
     if (!encode(&A, v.base, 2, dims, strides, box)) return cudaErrorInvalidValue;
-  } else {
+  } else if (mode == kFibJ) {
     const uint64_t dims[3] = {v.s, v.K, v.P};
     const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
     const uint32_t box[3] = {132, 32, 1};
     if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
+    fc_short_geometry(v.s, &a.pc, &a.sb);
+    const uint64_t dims[3] = {v.s, v.K, v.P};
+    const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
+    const uint32_t box[3] = {a.sb, 32, a.pc};
+    if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
+    a.bytes_a = 32u * a.pc * a.sb * 8u;
+    a.stage_bytes = (a.bytes_a + 32u * (ncp + 4) * 8u + 127u) / 128u * 128u;
   }
   {
     const uint64_t dims[2] = {ncp, v.K};
@@ -777,8 +857,9 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
   a.K = v.K;
   const int grid = fc_tma_grid(v, num_sms);
   if (grid_used) *grid_used = grid;
-#define TKG_FC_CALL(N) (mode == kFibI ? fc_tma_launch<N, kFibI>(A, M, a, grid, st) \
-                                      : fc_tma_launch<N, kFibJ>(A, M, a, grid, st))
+#define TKG_FC_CALL(N) (mode == kFibI   ? fc_tma_launch<N, kFibI>(A, M, a, grid, st) \
+                        : mode == kFibJ ? fc_tma_launch<N, kFibJ>(A, M, a, grid, st) \
+                                        : fc_tma_launch<N, kFibS>(A, M, a, grid, st))
   TKG_NC_SWITCH(ncp, TKG_FC_CALL)
 #undef TKG_FC_CALL
 }
@@ -795,13 +876,27 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
     const uint64_t strides[1] = {v.is_p * 8};
     const uint32_t box[2] = {132, 32};
     if (!encode(&A, v.base, 2, dims, strides, box)) return cudaErrorInvalidValue;
-  } else {
+  } else if (mode == kFibJ) {
     const uint64_t dims[3] = {v.s, v.K, v.P};
     const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
     const uint32_t box[3] = {68, 128, 1};
     if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
+    uint64_t ppr = 0;
+    uint32_t nr = 0;
+    fr_short_geometry(v, num_sms, &a.pc, &ppr, &nr);
+    a.kf = a.pc * uint32_t(v.s);
+    a.panels_per_range = ppr;
+    const uint64_t dims[3] = {v.s, v.K, v.P};
+    const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
+    const uint32_t box[3] = {uint32_t(v.s), 128, a.pc};
+    if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
+    a.bytes_a = a.pc * 128u * uint32_t(v.s) * 8u;
+    a.ldm = a.kf + 4;
+    a.bytes_m = mcol ? ncp * a.ldm * 8u : a.kf * (ncp + 4) * 8u;
+    a.stage_bytes = (a.bytes_a + a.bytes_m + 127u) / 128u * 128u;
   }
-  const uint32_t kb = mode == kFibI ? 32 : 64;
+  const uint32_t kb = mode == kFibI ? 32 : mode == kFibJ ? 64 : a.kf;
   if (!mcol) {
     const uint64_t dims[2] = {ncp, F};
     const uint64_t strides[1] = {mj * 8};
@@ -818,24 +913,37 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
   a.K = v.K;
   a.ncp = ncp;
   a.igroups = (v.K + 127) / 128;
-  const uint64_t steps = (F + 31) / 32;
-  uint64_t ranges = std::max<uint64_t>(1, uint64_t(num_sms) / a.igroups);
-  ranges = std::min<uint64_t>(ranges, std::max<uint64_t>(1, steps / 4));
-  a.fibers_per_range = (steps + ranges - 1) / ranges * 32;
-  a.ranges = uint32_t((F + a.fibers_per_range - 1) / a.fibers_per_range);
+  if (mode == kFibS) {  // whole-panel ranges
+    a.fibers_per_range = a.panels_per_range * v.s;
+    a.ranges = uint32_t((v.P + a.panels_per_range - 1) / a.panels_per_range);
+  } else {
+    const uint64_t steps = (F + 31) / 32;
+    uint64_t ranges = std::max<uint64_t>(1, uint64_t(num_sms) / a.igroups);
+    ranges = std::min<uint64_t>(ranges, std::max<uint64_t>(1, steps / 4));
+    a.fibers_per_range = (steps + ranges - 1) / ranges * 32;
+    a.ranges = uint32_t((F + a.fibers_per_range - 1) / a.fibers_per_range);
+  }
   if (ranges_used) *ranges_used = a.ranges;
   const int grid = int(a.ranges * a.igroups);
   if (grid_used) *grid_used = grid;
 #define TKG_FR_CALL(N)                                                                      \
-  (mode == kFibI ? (mcol ? fr_tma_launch<N, kFibI, true>(A, M, a, grid, st)                   \
-                         : fr_tma_launch<N, kFibI, false>(A, M, a, grid, st))                 \
-                 : (mcol ? fr_tma_launch<N, kFibJ, true>(A, M, a, grid, st)                   \
-                         : fr_tma_launch<N, kFibJ, false>(A, M, a, grid, st)))
+  (mode == kFibI   ? (mcol ? fr_tma_launch<N, kFibI, true>(A, M, a, grid, st)                 \
+                           : fr_tma_launch<N, kFibI, false>(A, M, a, grid, st))               \
+   : mode == kFibJ ? (mcol ? fr_tma_launch<N, kFibJ, true>(A, M, a, grid, st)                 \
+                           : fr_tma_launch<N, kFibJ, false>(A, M, a, grid, st))               \
+                   : (mcol ? fr_tma_launch<N, kFibS, true>(A, M, a, grid, st)                 \
+                           : fr_tma_launch<N, kFibS, false>(A, M, a, grid, st)))
   TKG_NC_SWITCH(ncp, TKG_FR_CALL)
 #undef TKG_FR_CALL
 }
 
 uint32_t fr_tma_ranges(const FiberView& v, int num_sms) {
+  if (v.s > 1 && v.s < 64 && v.s % 32 != 0) {  // kFibS (when that mode is chosen)
+    uint32_t pc = 0, nr = 0;
+    uint64_t ppr = 0;
+    fr_short_geometry(v, num_sms, &pc, &ppr, &nr);
+    return nr;
+  }
   const uint64_t F = v.s * v.P;
   const uint32_t igroups = (v.K + 127) / 128;
   const uint64_t steps = (F + 31) / 32;
@@ -858,7 +966,7 @@ int expand_diff_tma_grid(uint64_t F, int num_sms) {
 
 cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used) {
   const uint64_t F = a.s * a.P;
-  const uint32_t kc = a.K <= 8 ? 8 : a.K <= 16 ? 16 : a.K <= 32 ? 32 : 64;
+  const uint32_t kc = (a.K + 7) / 8 * 8;  // K padded to the DMMA k granularity used here
   CUtensorMap X, U, R;
   {
     const uint64_t dims[2] = {F, a.K};
@@ -883,7 +991,11 @@ cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_
   switch (kc) {
     case 8: return expand_diff_launch<8>(X, U, R, a, grid, st);
     case 16: return expand_diff_launch<16>(X, U, R, a, grid, st);
+    case 24: return expand_diff_launch<24>(X, U, R, a, grid, st);
     case 32: return expand_diff_launch<32>(X, U, R, a, grid, st);
+    case 40: return expand_diff_launch<40>(X, U, R, a, grid, st);
+    case 48: return expand_diff_launch<48>(X, U, R, a, grid, st);
+    case 56: return expand_diff_launch<56>(X, U, R, a, grid, st);
     default: return expand_diff_launch<64>(X, U, R, a, grid, st);
   }
 }

@@ -11,7 +11,7 @@
 
 namespace tkg {
 
-enum TmaMode { kFibI = 0, kFibJ = 1 };
+enum TmaMode { kFibI = 0, kFibJ = 1, kFibS = 2 };
 
 struct FcTmaArgs {
   uint64_t s = 0, P = 0;
@@ -23,6 +23,9 @@ struct FcTmaArgs {
   const double* diff_ref = nullptr;            // diff-norm epilogue instead of a store
   const int32_t* skip = nullptr;               // device flag: return at once when set
   double* gram_part = nullptr;                 // [grid][NC*NC] upper tiles of out^T out (NC <= 32)
+  // kFibS (short panels): a tile is pc whole panels (pc*s <= 128 fibers), the
+  // A box {sb, 32, pc} (sb >= s, TMA zero-fills past s); runtime stage sizes
+  uint32_t pc = 1, sb = 0, bytes_a = 0, stage_bytes = 0;
 };
 
 // NC (padded column count) up to which the FC kernel can fuse the Gram of
@@ -39,6 +42,10 @@ struct FrTmaArgs {
   uint32_t ncp = 0;
   double* sumsq_part = nullptr;                // [ranges*igroups]
   const int32_t* skip = nullptr;               // device flag: return at once when set
+  // kFibS (short panels): a chunk is pc whole panels (kf = pc*s <= 64 fibers),
+  // ranges are panel ranges; A box {s, 128, pc}; runtime sizes
+  uint32_t pc = 1, kf = 0, bytes_a = 0, bytes_m = 0, stage_bytes = 0, ldm = 0;
+  uint64_t panels_per_range = 0;
 };
 
 // -1 when the layout is not covered (the caller uses contract.cu's kernels).
