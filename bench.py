@@ -399,7 +399,8 @@ def b200_arm(args, c, world, rank, local):
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["hbm_src"]}
     roof.update({"kernel": {"fc": "FC fiber contraction (right update A_(n)^T L', TTM)",
                             "fr": "FR fiber reduction (left update A_(n) R, init A_(n) S)"}[cls],
-                 "traffic": ncu_traffic(args.config), "launch_ms": per_launch_ms,
+                 "traffic": (ncu_traffic(args.config) or {}).get("dram_bytes_per_launch"),
+                 "traffic_source": ncu_traffic(args.config), "launch_ms": per_launch_ms,
                  "arith_intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge,
                  "share_of_step": st["ms"] / (ms_step * args.steps),
                  "hbm_frac_of_dominant": (st["bytes"] / (st["ms"] * 1e-3) / 1e9) / peaks["hbm_gbs"],

@@ -457,7 +457,9 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-  double sq_acc = 0.0;
+  // ||A||^2 of the init pass in 4 independent chains (a single chain of
+  // dependent DFMAs between the DMMAs stalls the warp's in-order issue)
+  double sq_acc[4] = {0.0, 0.0, 0.0, 0.0};
   const bool want_sq = a.sumsq_part != nullptr;
   // kFibS: fiber kk of a chunk is jl = kk % s of panel kk / s; its A rows sit
   // at ((kk / s)*128 + row)*s + jl
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         if (MODE == kFibS) v = kok ? As[koff[t] + row * int(a.s)] : 0.0;
         else v = MODE == kFibI ? As[kk * C::kLdA + row] : As[row * C::kLdA + kk];
         af[m] = kok ? v : 0.0;
-        if (want_sq) sq_acc = fma(af[m], af[m], sq_acc);
+        if (want_sq) sq_acc[(t & 1) * 2 + m] = fma(af[m], af[m], sq_acc[(t & 1) * 2 + m]);
       }
       double bf[C::kNT];
 #pragma unroll
@@ -526,9 +528,10 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   }
   if (want_sq) {
     __shared__ double red[kCons];
+    double sq = (sq_acc[0] + sq_acc[1]) + (sq_acc[2] + sq_acc[3]);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq_acc += __shfl_xor_sync(0xffffffffu, sq_acc, off);
-    if (lane == 0) red[warp] = sq_acc;
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[warp] = sq;
     asm volatile("bar.sync 1, %0;\n" ::"n"(kCons * 32));
     if (threadIdx.x == 0) {
       double s = 0.0;

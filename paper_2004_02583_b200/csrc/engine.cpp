@@ -385,7 +385,7 @@ void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* 
   CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st));
   int nchunks = plan.C;
   const int* d_ids = nullptr;
-  if (win.nloc > 0 && win.Fg == win.Plo * win.Gsm) {
+  if (win.nloc > 0 && win.Gsm > 1 && win.Fg == win.Plo * win.Gsm) {
     const uint64_t a0 = win.o0 * win.Plo, a1 = (win.o0 + win.nloc) * win.Plo;
     const uint64_t ncol = n / win.Fg;
     std::vector<int> ids;
@@ -418,6 +418,17 @@ void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* 
   }
 }
 
+// The initializer S of a mode (F local fibers), column-major F x r: the
+// whole stream in storage order, or a shard's window of it. (A row-major
+// [F][ld] S would need scattered 8-byte writes from the generator; the FR
+// kernel reads the column-major operand at the same speed.)
+MtWindow Engine::s_window(MtWindow win, uint64_t F, uint64_t ld) {
+  (void)F;
+  if (win.nloc == 0) return win;
+  win.ld = ld;
+  return mt_window_finish(win);
+}
+
 void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win) {
   gen_uniform_on(seed, stream, n, d_out, win, st_, y_seq_, states_, chunk_ids_);
 }
@@ -443,7 +454,8 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
     const PreGen& g = items[k];
     double* d = pre_bufs_[k]->d(g.F * g.r + 8);
     const uint64_t total = (g.win.nloc ? g.win.Fg : g.F) * g.r;
-    gen_uniform_on(seed, uint32_t(g.mode), total, d, g.win, st2_, *pre_y_[k], *pre_st_[k], *pre_ids_[k]);
+    gen_uniform_on(seed, uint32_t(g.mode), total, d, s_window(g.win, g.F, 0), st2_, *pre_y_[k], *pre_st_[k],
+                   *pre_ids_[k]);
     CK(cudaEventRecord(pre_ev_[k], st2_));
     pre_[g.mode] = {d, pre_ev_[k], g.F, g.r};
   }
@@ -573,7 +585,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       pre_.erase(pit);
     } else {
       double* Sg = s_.d(F * r + 8);  // column-major F x r, the reference's storage order
-      gen_uniform(cfg.seed, uint32_t(mode), (win.nloc ? win.Fg : F) * r, Sg, win);
+      gen_uniform(cfg.seed, uint32_t(mode), (win.nloc ? win.Fg : F) * r, Sg, s_window(win, F, 0));
       S = Sg;
     }
     uint32_t fr_grid = 0;

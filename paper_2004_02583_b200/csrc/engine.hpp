@@ -163,6 +163,7 @@ class Engine {
   uint32_t reduce_left_partials(double* part, uint32_t nparts, uint32_t I, uint32_t ncp, uint32_t r);
   // draws 0..n-1 in storage order, or a shard's window of them (MtWindow)
   void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win = MtWindow());
+  static MtWindow s_window(MtWindow win, uint64_t F, uint64_t ld);
   void gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win,
                       cudaStream_t st, DBuf& ybuf, DBuf& sbuf, DBuf& cbuf);
   struct PreGen {

@@ -35,9 +35,29 @@ cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C
 // j = jlo + Plo*(ism + Gsm*jhi), ism the index along the sharded mode; one
 // shard keeps ism in [o0, o0 + nloc), stored as its own local fiber order
 // jlo + Plo*((ism - o0) + nloc*jhi), column c at c * (Fg / Gsm * nloc).
+// ld > 0: the kept draws are written row-major, element (local fiber, c) at
+// [fiber*ld + c] (the FR operand layout), instead of column-major.
+// Whole tensor: Gsm = 1, o0 = 0, nloc = 1, Plo = Fg (mt_window_all).
 struct MtWindow {
-  uint64_t Fg = 0, Plo = 1, Gsm = 1, o0 = 0, nloc = 0;
+  uint64_t Fg = 0, Plo = 1, Gsm = 1, o0 = 0, nloc = 0, ld = 0;
+  double inv_fg = 0.0, inv_plo = 0.0, inv_gsm = 0.0;  // set by mt_window_finish
 };
+inline MtWindow mt_window_finish(MtWindow w) {
+  w.inv_fg = w.Fg ? 1.0 / double(w.Fg) : 0.0;
+  w.inv_plo = w.Plo ? 1.0 / double(w.Plo) : 0.0;
+  w.inv_gsm = w.Gsm ? 1.0 / double(w.Gsm) : 0.0;
+  return w;
+}
+inline MtWindow mt_window_all(uint64_t F, uint64_t ld) {
+  MtWindow w;
+  w.Fg = F;
+  w.Plo = F;
+  w.Gsm = 1;
+  w.o0 = 0;
+  w.nloc = 1;
+  w.ld = ld;
+  return mt_window_finish(w);
+}
 cudaError_t launch_mt_generate(const uint64_t* d_states, int C, const int* d_chunk_ids, uint64_t J,
                                uint64_t total, double* d_out, MtWindow win, cudaStream_t st);
 

@@ -100,6 +100,15 @@ __global__ void __launch_bounds__(32) mt_jump_kernel(const uint64_t* __restrict_
 // barriers; the ten words of a slot are written as one coalesced row.
 constexpr int kGenWarps = 4;
 
+// n / d for n < 2^51 from a double reciprocal plus one correction step.
+__device__ __forceinline__ uint64_t fast_div(uint64_t n, uint64_t d, double inv) {
+  uint64_t q = static_cast<uint64_t>(static_cast<double>(n) * inv);
+  const int64_t r = static_cast<int64_t>(n - q * d);
+  if (r < 0) --q;
+  else if (static_cast<uint64_t>(r) >= d) ++q;
+  return q;
+}
+
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(v), src));
 }
@@ -136,8 +145,8 @@ __global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* 
         }
       }
     } else {
-      // shard window (see MtWindow)
-      const uint64_t c0 = pos / win.Fg;
+      // S window (see MtWindow): position c*Fg + j -> column c, fiber j
+      const uint64_t c0 = fast_div(pos, win.Fg, win.inv_fg);
       const uint64_t j0 = pos - c0 * win.Fg;
       const uint64_t Fl = win.Fg / win.Gsm * win.nloc;
 #pragma unroll
@@ -145,14 +154,19 @@ __global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* 
         const uint64_t k = 32 * s + L;
         if (!(s < 9 || L < 24) || pos + k >= end) continue;
         uint64_t j = j0 + k, col = c0;
-        if (j >= win.Fg) {
-          col += j / win.Fg;
-          j %= win.Fg;
+        while (j >= win.Fg) {
+          j -= win.Fg;
+          ++col;
         }
-        const uint64_t jlo = j % win.Plo, t = j / win.Plo;
-        const uint64_t ism = t % win.Gsm, jhi = t / win.Gsm;
-        if (ism >= win.o0 && ism < win.o0 + win.nloc)
-          out[jlo + win.Plo * ((ism - win.o0) + win.nloc * jhi) + col * Fl] = to_uniform01(w[s]);
+        uint64_t loc = j;
+        if (win.Gsm > 1) {  // a shard: keep its own fibers, in its local order
+          const uint64_t t = fast_div(j, win.Plo, win.inv_plo);
+          const uint64_t jhi = fast_div(t, win.Gsm, win.inv_gsm);
+          const uint64_t ism = t - jhi * win.Gsm;
+          if (ism < win.o0 || ism >= win.o0 + win.nloc) continue;
+          loc = (j - t * win.Plo) + win.Plo * ((ism - win.o0) + win.nloc * jhi);
+        }
+        out[win.ld ? loc * win.ld + col : loc + col * Fl] = to_uniform01(w[s]);
       }
     }
     pos += kMtN;
