@@ -227,7 +227,10 @@ def test_exact_recovery(ctx, ref, sequential):
 
 @pytest.mark.parametrize("sequential", [False, True])
 @pytest.mark.parametrize("dims,ranks", [([9, 8, 7], [3, 2, 4]), ([20, 18, 16], [5, 4, 3]),
-                                        ([12, 10, 8, 6], [3, 3, 2, 2]), ([40, 30, 20], [10, 10, 5])])
+                                        ([12, 10, 8, 6], [3, 3, 2, 2]), ([40, 30, 20], [10, 10, 5]),
+                                        # ranks > 32: the R^T R row pass (finish_step) and r x r
+                                        # factorizations with 9 / 16 entries per thread
+                                        ([90, 80, 70], [40, 33, 50]), ([96, 80, 72], [64, 60, 36])])
 def test_hosvd_matches_reference(ctx, ref, sequential, dims, ranks):
     t = random_tensor(ref, dims, 3 + len(dims))
     t = t + 5 * _tucker_exact(ref, dims, ranks, 77)
