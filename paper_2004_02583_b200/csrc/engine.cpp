@@ -437,6 +437,12 @@ void Engine::gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_o
 // the data: generate those of every mode after the first on a second stream
 // while the first modes' sweeps run (the RNG kernels fit beside the
 // contraction kernels' shared-memory footprint).
+void Engine::defer_pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
+  pre_.clear();
+  pending_pre_ = items;
+  pending_seed_ = seed;
+}
+
 void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
   pre_.clear();
   while (pre_bufs_.size() < items.size()) {
@@ -601,6 +607,13 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   CK(launch_ctrl_init(ctrl, sumsq, cfg.eta, max_iters, max_iters, cfg.init ? 0 : 1, st_));
   count_launch();
   trace("init enqueued", mode);
+  // the initializer streams of the later modes are prepared on the host and
+  // queued on the side stream once this mode's first kernels are queued
+  if (!pending_pre_.empty()) {
+    std::vector<PreGen> items;
+    items.swap(pending_pre_);
+    pregenerate(items, pending_seed_);
+  }
 
   // 2. Sweeps (als.cpp:121-160), enqueued in batches; kernels of sweeps past
   //    the stop decision return on entry.
@@ -844,7 +857,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   {
     std::vector<PreGen> items;
     for (int n = 2; n <= sh.N; ++n) items.push_back({n, sh.count() / sh.d[n - 1], uint32_t(ranks[n - 1]), MtWindow()});
-    pregenerate(items, cfg.seed);
+    defer_pregenerate(items, cfg.seed);
   }
   trace("pregenerate enqueued");
   stage_reserve(sh.N, cfg.max_iters);
@@ -931,7 +944,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
       if (k > 0) items.push_back({m, w.count() / w.d[m - 1], uint32_t(ranks[m - 1]), MtWindow()});
       w.d[m - 1] = ranks[m - 1];
     }
-    pregenerate(items, cfg.seed);
+    defer_pregenerate(items, cfg.seed);
   }
   stage_reserve(sh.N, cfg.max_iters);
   std::vector<AlsOut> outs;

@@ -173,6 +173,10 @@ class Engine {
     MtWindow win;
   };
   void pregenerate(const std::vector<PreGen>& items, uint64_t seed);
+  // run by the first run_als of the decomposition after its init is queued
+  void defer_pregenerate(const std::vector<PreGen>& items, uint64_t seed);
+  std::vector<PreGen> pending_pre_;
+  uint64_t pending_seed_ = 0;
   void fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc, double* out,
           uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
           const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip = nullptr,

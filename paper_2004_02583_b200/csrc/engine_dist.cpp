@@ -224,7 +224,7 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
       const Shape& Ln = n < N ? L : LB;
       items.push_back({n, Ln.count() / Ln.d[n - 1], uint32_t(ranks[n - 1]), window(n)});
     }
-    pregenerate(items, cfg.seed);
+    defer_pregenerate(items, cfg.seed);
   }
   stage_reserve(N, cfg.max_iters);
   bool sumsq_known = false;
@@ -323,7 +323,7 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
       items.push_back({plan[k].mode, Lw.count() / Lw.d[plan[k].mode - 1], uint32_t(ranks[plan[k].mode - 1]),
                        window(plan[k])});
     }
-    pregenerate(items, cfg.seed);
+    defer_pregenerate(items, cfg.seed);
   }
   const double* work = A;
   DBuf* bufs[2] = {&work_a_, &work_b_};

@@ -133,10 +133,37 @@ void mulmod(const uint64_t* a, const uint64_t* b, uint64_t* r) {
 
 }  // namespace
 
+// The seeded state is formed as std::mersenne_twister_engine::seed(Sseq&)
+// does ([rand.eng.mers]: 2 x 32-bit words of seed_seq::generate per state
+// word, and the all-zero fix-up), and the raw words are produced by the
+// engine's own recurrence in the in-place order -- no tempering, so nothing
+// to invert. Checked bitwise against std::mt19937_64 by the tests.
 void mt_raw_sequence(uint64_t seed, uint32_t stream, uint64_t* y, int n) {
   std::seed_seq seq{static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), stream};
-  std::mt19937_64 eng(seq);
-  for (int k = 0; k < n; ++k) y[k] = untemper(eng());
+  uint32_t a[2 * kMtN];
+  seq.generate(a, a + 2 * kMtN);
+  uint64_t x[kMtN];
+  for (int i = 0; i < kMtN; ++i) x[i] = uint64_t(a[2 * i]) | (uint64_t(a[2 * i + 1]) << 32);
+  {
+    bool zero = (x[0] & 0xFFFFFFFF80000000ull) == 0;
+    for (int i = 1; i < kMtN && zero; ++i) zero = x[i] == 0;
+    if (zero) x[0] = 1ull << 63;
+  }
+  constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull;
+  constexpr uint64_t kMatA = 0xB5026F5AA96619E9ull;
+  auto tw = [&](uint64_t cur, uint64_t nxt, uint64_t far) {
+    const uint64_t v = (cur & kUpper) | (nxt & kLower);
+    return far ^ (v >> 1) ^ ((0ull - (v & 1ull)) & kMatA);
+  };
+  int k = 0;
+  while (k < n) {
+    for (int i = 0; i < kMtN - 156; ++i) x[i] = tw(x[i], x[i + 1], x[i + 156]);
+    for (int i = kMtN - 156; i < kMtN - 1; ++i) x[i] = tw(x[i], x[i + 1], x[i - (kMtN - 156)]);
+    x[kMtN - 1] = tw(x[kMtN - 1], x[0], x[155]);
+    const int m = std::min(kMtN, n - k);
+    std::memcpy(y + k, x, sizeof(uint64_t) * size_t(m));
+    k += m;
+  }
 }
 
 const std::vector<uint64_t>& mt_charpoly() {
