@@ -764,12 +764,13 @@ void Engine::begin_timed() {
 
 // multi_mode_product(t, {U_n^T}) in ascending mode order (hosvd.cpp:115-121).
 void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
-                        const std::vector<double*>& d_factors, double* d_core) {
+                        const std::vector<double*>& d_factors, double* d_core, int last_mode) {
   Shape cur = sh;
   const double* src = A;
   DBuf* bufs[2] = {&work_a_, &work_b_};
   int which = 0;
-  for (int n = 1; n <= sh.N; ++n) {
+  const int nlast = last_mode > 0 ? last_mode : sh.N;
+  for (int n = 1; n <= nlast; ++n) {
     const uint64_t I = cur.extent(n), s = cur.stride(n), F = cur.count() / I, P = F / s;
     const uint32_t r = uint32_t(ranks[n - 1]);
     const uint32_t ncp = pad_nc(r);
@@ -778,9 +779,9 @@ void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint
     count_launch();
     Shape nxt = cur;
     nxt.d[n - 1] = r;
-    double* dst = (n == sh.N) ? d_core : bufs[which]->d(nxt.count());
+    double* dst = (n == nlast) ? d_core : bufs[which]->d(nxt.count());
     FiberView v{src, s, P, uint32_t(I), s, s * I};
-    fc(v, Mt, ncp, r, dst, 1, s, s * r, nullptr, nullptr, nullptr, n == 1);
+    fc(v, Mt, ncp, r, dst, 1, s, s * r, nullptr, nullptr, nullptr, n == 1 && last_mode == 0);
     src = dst;
     cur = nxt;
     which ^= 1;
@@ -870,7 +871,11 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     outs.push_back(run_als(A, sh, n, r, cfg, sumsq_known, MtWindow(), n - 1));
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
-    qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
+    if (n < sh.N) {
+      qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
+    } else {  // keep R_hat of the last mode for the core
+      qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], rhat_.d(r * r), nullptr, 0, false);
+    }
     mode_end(n - 1);
     trace("mode done", n);
   }
@@ -878,7 +883,24 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   cs.N = sh.N;
   for (int k = 0; k < sh.N; ++k) cs.d[k] = ranks[k];
   double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
-  core_chain(A, sh, ranks, U, core_buf);
+  // core = A x_1 U_1^T ... x_N U_N^T (hosvd.cpp:115-121). The last mode's
+  // factor comes from the final consistent pair (L = U_N R_hat, R = A_(N)^T L
+  // (L^T L)^{-1}), so A_(N)^T U_N = R R_hat^T exactly: the first contraction
+  // of the chain is the st-HOSVD shrink of R (hosvd.cpp:176-178) instead of
+  // another pass over A, and the remaining TTMs run on the r_N-extent tensor.
+  {
+    const int N = sh.N;
+    const uint32_t rN = uint32_t(ranks[N - 1]), ncpN = pad_nc(rN);
+    const uint64_t IN = sh.d[N - 1], sN = sh.stride(N), FN = sh.count() / IN;
+    Shape T = sh;
+    T.d[N - 1] = rN;
+    double* Tbuf = N == 1 ? core_buf : core_t_.d(T.count());
+    const int nsh = shrink_count(FN);
+    double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
+    CK(launch_shrink(r_.d(FN * ncpN + 8), ncpN, sN, 1, rN, rhat_.d(rN * rN), Tbuf, sq, st_));
+    count_launch();
+    if (N > 1) core_chain(Tbuf, T, ranks, U, core_buf, N - 1);
+  }
   sync();
   trace("core synced");
   for (int n = 0; n < sh.N; ++n) {

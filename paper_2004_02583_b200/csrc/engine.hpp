@@ -195,8 +195,9 @@ class Engine {
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                                const double* d_core, const std::vector<double*>& d_factors,
                                const double* ref_sumsq_host);
+  // TTMs of modes 1..last_mode (0 = all) with U_n^T, ascending (hosvd.cpp:115-121)
   void core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
-                  const std::vector<double*>& d_factors, double* d_core);
+                  const std::vector<double*>& d_factors, double* d_core, int last_mode = 0);
   void begin_timed();
   void count_launch(int n = 1) { launches_ += n; }
   void reshard(const double* src, const Shape& G, int from, int to, double* dst);
@@ -279,7 +280,7 @@ class Engine {
 
   std::unique_ptr<Comm> comm_;
   Comm* dist_ = nullptr;  // set while a sharded driver runs: run_als sums over ranks
-  DBuf send_, recv_, reshard_, uslab_;
+  DBuf send_, recv_, reshard_, uslab_, uslab2_, core_t_;
 };
 
 struct ShardRange {

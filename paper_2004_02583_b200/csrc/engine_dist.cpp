@@ -248,14 +248,37 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
     outs.push_back(run_als(An, *Ln, n, r, cfg, sumsq_known, window(n), n - 1));
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
-    qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
+    qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], n == N ? rhat_.d(r * r) : nullptr, nullptr, 0, false);
     mode_end(n - 1);
   }
   Shape cs;
   cs.N = N;
   for (int k = 0; k < N; ++k) cs.d[k] = ranks[k];
   double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
-  dist_core_and_residual(A, L, k0, G, ranks, U, core_buf, true, outs, rep, core, factors, t0);
+  // core: A x_N U_N^T = tensorize(R_hat R^T) of the final pair (see
+  // Engine::t_hosvd), here on this rank's fibers of mode N (the tensor is
+  // sharded along mode N-1 at that point), then the TTMs of modes 1..N-1 with
+  // U_{N-1}'s rows of this shard, summed over ranks
+  {
+    const uint32_t rN = uint32_t(ranks[N - 1]), ncpN = pad_nc(rN);
+    const uint64_t FN = LB.count() / LB.d[N - 1];
+    Shape T = LB;
+    T.d[N - 1] = rN;
+    double* Tbuf = core_t_.d(T.count());
+    const int nsh = shrink_count(FN);
+    double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
+    CK(launch_shrink(r_.d(FN * ncpN + 8), ncpN, LB.stride(N), 1, rN, rhat_.d(rN * rN), Tbuf, sq, st_));
+    count_launch();
+    const uint32_t rM = uint32_t(ranks[N - 2]);
+    double* uM = uslab2_.d(bN.len * rM);
+    CK(cudaMemcpy2DAsync(uM, bN.len * sizeof(double), U[N - 2] + bN.begin, G.d[N - 2] * sizeof(double),
+                         bN.len * sizeof(double), rM, cudaMemcpyDeviceToDevice, st_));
+    std::vector<double*> Us = U;
+    Us[N - 2] = uM;
+    core_chain(Tbuf, T, ranks, Us, core_buf, N - 1);
+    comm_->allreduce_sum(core_buf, cs.count(), st_);
+  }
+  dist_core_and_residual(A, L, k0, G, ranks, U, core_buf, false, outs, rep, core, factors, t0);
 }
 
 void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t k0, uint64_t nloc,
