@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   }
 
   const int q = lane & 3, r8 = lane >> 2;
-  double sq = 0.0;
+  double sqv[4] = {0.0, 0.0, 0.0, 0.0};  // independent chains (see the FR init pass)
   uint32_t it = 0, xt = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++xt) {
     mbar_wait(xfull, xt & 1);
@@ -673,13 +673,14 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double d = Rs[(n * 8 + 2 * q + e) * C::kLdR + warp * 16 + m * 8 + r8] - acc[m][n][e];
-            sq = fma(d, d, sq);
+            sqv[(n & 1) * 2 + e] = fma(d, d, sqv[(n & 1) * 2 + e]);
           }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
   }
   __shared__ double red[kCons];
+  double sq = (sqv[0] + sqv[1]) + (sqv[2] + sqv[3]);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
   if (lane == 0) red[warp] = sq;
