@@ -11,6 +11,10 @@
 // st-HOSVD shrink.
 #pragma once
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -72,5 +76,27 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 // read as DMMA B fragments: 4 consecutive rows must land 4 doubles apart
 // modulo the 16-double bank window, i.e. ld = 4 (mod 16).
 __host__ __device__ constexpr int smem_ld(int nc) { return nc + ((4 - nc) % 16 + 16) % 16; }
+
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (never
+// lowers it): several host threads sharing a device (in-process ranks) may
+// launch one kernel with different sizes, and a per-call set could lower the
+// limit under another thread's launch.
+template <class K>
+inline cudaError_t raise_smem_limit(K kernel, size_t bytes) {
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, size_t> cur;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(m);
+  size_t& c = cur[{reinterpret_cast<const void*>(kernel), dev}];
+  if (bytes <= c) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
+  c = bytes;
+  return cudaSuccess;
+}
 
 }  // namespace tkg

@@ -479,16 +479,8 @@ cudaError_t fc_launch_t(const FcArgs& a, int grid, cudaStream_t st) {
   constexpr int WF = fc_wf<NC>();
   using Cfg = FcCfg<NC, WF, MODE>;
   auto k = fc_kernel<NC, WF, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(Cfg::kSmem));
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return e;
-    }
-    attr_set = true;
-  }
+  cudaError_t e = raise_smem_limit(k, Cfg::kSmem);
+  if (e != cudaSuccess) return e;
   k<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(a);
   return cudaGetLastError();
 }
@@ -524,11 +516,8 @@ cudaError_t fr_launch_t(const FrArgs& a, int wgi, int wgj, cudaStream_t st) {
   const size_t ring = sizeof(double) * kStages * size_t(kSub * wgj) * FrCfg<NC, WI, MODE>::kLd;
   const size_t red = sizeof(double) * size_t(wgj) * rows_cta * NC;
   const size_t smem = std::max(ring, red);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return e;
-  }
+  cudaError_t e = raise_smem_limit(k, smem);
+  if (e != cudaSuccess) return e;
   const int grid = int(a.ranges * a.igroups);
   k<<<grid, 32 * wgi * wgj, smem, st>>>(a, wgi, wgj);
   return cudaGetLastError();

@@ -714,9 +714,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 template <class K>
 cudaError_t set_smem(K k, size_t bytes) {
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-  if (e != cudaSuccess) cudaGetLastError();
-  return e;
+  return raise_smem_limit(k, bytes);
 }
 
 template <int NC, int MODE>
@@ -724,12 +722,8 @@ cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTm
                           cudaStream_t st) {
   using C = FcT<NC, MODE>;
   auto k = fc_tma_kernel<NC, MODE>;
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = set_smem(k, C::kSmem);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  cudaError_t e = set_smem(k, C::kSmem);
+  if (e != cudaSuccess) return e;
   k<<<grid, kThreadsTma, C::kSmem, st>>>(A, M, a);
   return cudaGetLastError();
 }
@@ -739,12 +733,8 @@ cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTm
                           cudaStream_t st) {
   using C = FrT<NC, MODE, MCOL>;
   auto k = fr_tma_kernel<NC, MODE, MCOL>;
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = set_smem(k, C::kSmem);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  cudaError_t e = set_smem(k, C::kSmem);
+  if (e != cudaSuccess) return e;
   k<<<grid, kThreadsTma, C::kSmem, st>>>(A, M, a);
   return cudaGetLastError();
 }
@@ -767,12 +757,8 @@ cudaError_t expand_diff_launch(const CUtensorMap& X, const CUtensorMap& U, const
                                const ExpandArgs& a, int grid, cudaStream_t st) {
   using C = ExT<KC>;
   auto k = expand_diff_tma_kernel<KC>;
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = set_smem(k, C::kSmem);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  cudaError_t e = set_smem(k, C::kSmem);
+  if (e != cudaSuccess) return e;
   k<<<grid, kThreadsTma, C::kSmem, st>>>(X, U, R, a.s * a.P, a.Iout, a.sumsq_part);
   return cudaGetLastError();
 }

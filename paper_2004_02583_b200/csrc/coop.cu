@@ -759,11 +759,8 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
 
 template <class K>
 cudaError_t coop_launch(K kernel, int want, int num_sms, size_t smem, void* args, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return e;
-  }
+  cudaError_t e = raise_smem_limit(kernel, smem);
+  if (e != cudaSuccess) return e;
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
   if (e != cudaSuccess || occ < 1) {

@@ -188,9 +188,8 @@ cudaError_t launch_expand(const ExpandArgs& a, int num_sms, cudaStream_t st, int
   if (kc <= N) {                                                                                \
     const size_t smem = sizeof(double) * (size_t(N) * kLdT + 2 * size_t(N) * kLdU +           \
                                           (a.ref ? 2 * size_t(kCB) * kLdR : 0));             \
-    cudaError_t e = cudaFuncSetAttribute(expand_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         int(smem));                                            \
-    if (e != cudaSuccess) { cudaGetLastError(); return e; }                                     \
+    cudaError_t e = raise_smem_limit(expand_kernel<N>, smem);                                 \
+    if (e != cudaSuccess) return e;                                                             \
     expand_kernel<N><<<grid, 256, smem, st>>>(a);                                               \
     return cudaGetLastError();                                                                  \
   }

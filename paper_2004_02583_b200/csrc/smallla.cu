@@ -456,12 +456,8 @@ cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, 
 #define TKG_S(N)                                                                                    \
   if (nc == N) {                                                                                    \
     const size_t smem = sizeof(double) * (size_t(kShrinkTile) * (N + 4) + size_t(N) * (N + 4));     \
-    cudaError_t e = cudaFuncSetAttribute(shrink_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         int(smem));                                                \
-    if (e != cudaSuccess) {                                                                         \
-      cudaGetLastError();                                                                           \
-      return e;                                                                                     \
-    }                                                                                               \
+    cudaError_t e = raise_smem_limit(shrink_kernel<N>, smem);                                       \
+    if (e != cudaSuccess) return e;                                                                 \
     shrink_kernel<N><<<grid, kShrinkThreads, smem, st>>>(R, ld, s, P, r, rhat, out, sumsq_part);   \
     return cudaGetLastError();                                                                      \
   }
