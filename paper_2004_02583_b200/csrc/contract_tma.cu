@@ -365,7 +365,10 @@ struct FrT {
   // so longer runs per row (64) and a double-buffered ring
   // kFibS (short panels): a chunk is pc whole panels, kf = pc*s <= 64 fibers
   static constexpr int kKB = MODE == kFibI ? 32 : 64;
-  static constexpr int kStages = MODE == kFibI ? 4 : 2;
+  // kFibI with NC <= 32: two CTAs per SM with two stages each (a grid of
+  // exactly 2 x #SMs = ranges x row groups fills every SM; one CTA per SM
+  // left SMs idle when #SMs is not a multiple of the row-group count)
+  static constexpr int kStages = MODE == kFibI ? (NC <= 32 ? 2 : 4) : 2;
   static constexpr int kLdA = MODE == kFibI ? 132 : kKB + 4;
   static constexpr int kRowsA = MODE == kFibI ? kKB : kIC;
   // M row-major [F][ld]: box (NC+4, kKB) -> [kKB][NC+4];
@@ -380,7 +383,7 @@ struct FrT {
 };
 
 template <int NC, int MODE, bool MCOL>
-__global__ void __launch_bounds__(kThreadsTma, 1)
+__global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 : 1)
     fr_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FrTmaArgs a) {
   using C = FrT<NC, MODE, MCOL>;
@@ -393,17 +396,15 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint64_t F = a.s * a.P;
-  const uint32_t range = blockIdx.x / a.igroups;
-  const uint32_t ig = blockIdx.x % a.igroups;
-  const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
-  const uint64_t f1 = min(F, f0 + a.fibers_per_range);
-  const int i0 = int(ig) * C::kIC;
+  // persistent CTAs: work item = (fiber range, row group); the ring runs on
+  // across items
+  const uint32_t items = a.ranges * a.igroups;
   // fiber chunks of up to kKB that never cross a panel (kFibJ): the chunk
   // starting at j holds min(kKB, end of j's panel or of the range - j) fibers
   // kFibS: ranges are whole panels and chunks a.kf = a.pc * s fibers, so a
   // chunk is a.pc whole panels (the last one of a range may be shorter)
   const int kmax = MODE == kFibS ? int(a.kf) : C::kKB;
-  auto chunk_len = [&](uint64_t j) -> int {
+  auto chunk_len = [&](uint64_t j, uint64_t f1) -> int {
     uint64_t end = f1;
     if (MODE == kFibJ) {
       const uint64_t pe = (j / a.s + 1) * a.s;
@@ -430,7 +431,12 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       prefetch_map(&tmA);
       prefetch_map(&tmM);
       int kb = 0;
-      for (uint64_t j = f0; j < f1; j += chunk_len(j), ++kb) {
+      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const uint32_t range = item / a.igroups, ig = item % a.igroups;
+        const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
+        const uint64_t f1 = min(F, f0 + a.fibers_per_range);
+        const int i0 = int(ig) * C::kIC;
+      for (uint64_t j = f0; j < f1; j += chunk_len(j, f1), ++kb) {
         const int slot = kb % C::kStages;
         const uint32_t ph = (kb / C::kStages) & 1;
         mbar_wait(&empty[slot], ph ^ 1);
@@ -446,17 +452,13 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         if (MCOL) tma_2d(st + bytes_a, &tmM, &full[slot], int(j), 0);
         else tma_2d(st + bytes_a, &tmM, &full[slot], 0, int(j));
       }
+      }
     }
     return;
   }
 
   const int q = lane & 3;
   const int r8 = lane >> 2;
-  double acc[2][C::kNT][2];
-#pragma unroll
-  for (int m = 0; m < 2; ++m)
-#pragma unroll
-    for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
   // ||A||^2 of the init pass in 4 independent chains (a single chain of
   // dependent DFMAs between the DMMAs stalls the warp's in-order issue)
   double sq_acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -472,6 +474,16 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   }
 
   int kb = 0;
+  for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+  const uint32_t range = item / a.igroups, ig = item % a.igroups;
+  const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
+  const uint64_t f1 = min(F, f0 + a.fibers_per_range);
+  const int i0 = int(ig) * C::kIC;
+  double acc[2][C::kNT][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
   for (uint64_t j = f0; j < f1; ++kb) {
     const int slot = kb % C::kStages;
     const uint32_t ph = (kb / C::kStages) & 1;
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes);
     const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes + bytes_a);
     // fibers past the chunk (next panel / next range) are dropped
-    const int kvalid = chunk_len(j);
+    const int kvalid = chunk_len(j, f1);
     j += kvalid;
 #pragma unroll
     for (int t = 0; t < C::kKB / 4; ++t) {
@@ -526,6 +538,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       *reinterpret_cast<double2*>(dst + c) = make_double2(acc[m][n][0], acc[m][n][1]);
     }
   }
+  }  // item
   if (want_sq) {
     __shared__ double red[kCons];
     double sq = (sq_acc[0] + sq_acc[1]) + (sq_acc[2] + sq_acc[3]);
@@ -799,7 +812,7 @@ void fc_short_geometry(uint64_t s, uint32_t* pc, uint32_t* sb) {
 void fr_short_geometry(const FiberView& v, int num_sms, uint32_t* pc, uint64_t* ppr, uint32_t* ranges) {
   *pc = uint32_t(64 / v.s);
   const uint32_t igroups = (v.K + 127) / 128;
-  uint64_t r = std::max<uint64_t>(1, uint64_t(num_sms) / igroups);
+  uint64_t r = std::max<uint64_t>(1, uint64_t(num_sms) * 2 / igroups);
   r = std::min<uint64_t>(r, std::max<uint64_t>(1, v.P / (4 * *pc)));
   *ppr = (v.P + r - 1) / r;
   *ranges = uint32_t((v.P + *ppr - 1) / *ppr);
@@ -908,13 +921,18 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
     a.ranges = uint32_t((v.P + a.panels_per_range - 1) / a.panels_per_range);
   } else {
     const uint64_t steps = (F + 31) / 32;
-    uint64_t ranges = std::max<uint64_t>(1, uint64_t(num_sms) / a.igroups);
+    // one work item per CTA slot; two per SM when the row-group count does
+    // not divide the SM count (persistent CTAs then stay busy)
+    const int per_sm = (mode == kFibI && ncp <= 32) ? 2 : 1;
+    const uint64_t items_per_sm = (num_sms % a.igroups == 0) ? per_sm : 2;
+    uint64_t ranges = std::max<uint64_t>(1, uint64_t(num_sms) * items_per_sm / a.igroups);
     ranges = std::min<uint64_t>(ranges, std::max<uint64_t>(1, steps / 4));
     a.fibers_per_range = (steps + ranges - 1) / ranges * 32;
     a.ranges = uint32_t((F + a.fibers_per_range - 1) / a.fibers_per_range);
   }
   if (ranges_used) *ranges_used = a.ranges;
-  const int grid = int(a.ranges * a.igroups);
+  const int ctas_per_sm = (mode == kFibI && ncp <= 32) ? 2 : 1;
+  const int grid = int(std::min<uint64_t>(uint64_t(a.ranges) * a.igroups, uint64_t(num_sms) * ctas_per_sm));
   if (grid_used) *grid_used = grid;
 #define TKG_FR_CALL(N)                                                                      \
   (mode == kFibI   ? (mcol ? fr_tma_launch<N, kFibI, true>(A, M, a, grid, st)                 \
@@ -937,7 +955,7 @@ uint32_t fr_tma_ranges(const FiberView& v, int num_sms) {
   const uint64_t F = v.s * v.P;
   const uint32_t igroups = (v.K + 127) / 128;
   const uint64_t steps = (F + 31) / 32;
-  uint64_t ranges = std::max<uint64_t>(1, uint64_t(num_sms) / igroups);
+  uint64_t ranges = std::max<uint64_t>(1, uint64_t(num_sms) * 2 / igroups);  // upper bound (buffer sizing)
   ranges = std::min<uint64_t>(ranges, std::max<uint64_t>(1, steps / 4));
   const uint64_t fpr = (steps + ranges - 1) / ranges * 32;
   return uint32_t((F + fpr - 1) / fpr);
