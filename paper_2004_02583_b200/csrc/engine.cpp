@@ -364,7 +364,7 @@ void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* 
                             cudaStream_t st, DBuf& ybuf, DBuf& sbuf, DBuf& cbuf) {
   if (n == 0) return;
   if (mt_charpoly().empty()) raise(11, "MT19937-64 characteristic polynomial check failed");
-  const MtPlan plan = mt_plan(n);
+  const MtPlan plan = mt_plan(n, st != st_);
   const auto key = std::make_pair(plan.J, plan.C);
   DBuf* polys = nullptr;
   auto it = jump_cache_.find(key);

@@ -287,7 +287,7 @@ std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
   return out;
 }
 
-MtPlan mt_plan(uint64_t total) {
+MtPlan mt_plan(uint64_t total, bool side) {
   MtPlan p;
   p.total = total;
   // A chunk costs one jump (19937 x 312 bit-word XORs, ~0.35 us of the whole
@@ -295,6 +295,10 @@ MtPlan mt_plan(uint64_t total) {
   // T/(312 C) * 0.4 + 0.35 C is smallest near C = sqrt(T / 256).
   uint64_t C = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(total) / 256.0)));
   C = std::max<uint64_t>(1, std::min<uint64_t>(C, 1184));
+  // streams generated on the side stream, behind the sweeps of earlier modes,
+  // are not latency-critical: a quarter of the chunks (a quarter of the jump
+  // work competing with the sweeps for the SMs) and 4x longer chunks
+  if (side) C = std::max<uint64_t>(1, C / 4);
   p.C = static_cast<int>(C);
   p.J = (total + C - 1) / C;
   if (p.J == 0) p.J = 1;

@@ -44,6 +44,7 @@ struct MtPlan {
   uint64_t J;
   int C;
 };
-MtPlan mt_plan(uint64_t total_draws);
+// side: generated off the critical path (fewer, longer chunks)
+MtPlan mt_plan(uint64_t total_draws, bool side = false);
 
 }  // namespace tkg
