@@ -213,6 +213,20 @@ def _tucker_exact(ref, dims, ranks, seed):
 
 
 @pytest.mark.parametrize("sequential", [False, True])
+def test_order1(ctx, ref, sequential):
+    # an order-1 tensor is its own rank-1 Tucker model: U = +-a/||a||, core = +-||a||
+    a = random_tensor(ref, [57], 4)
+    eng = tk.FactorEngine.with_als(tk.AlsConfig(eta=1e-8, seed=3))
+    fn = (lambda: ctx.st_hosvd(a, tk.Truncation([1]), None, eng)) if sequential else \
+        (lambda: ctx.t_hosvd(a, tk.Truncation([1]), eng))
+    tkr, rep = fn()
+    u = tkr.factors[0][:, 0]
+    assert abs(abs(float(np.dot(u, a))) - np.linalg.norm(a)) <= 1e-12 * np.linalg.norm(a)
+    assert abs(abs(float(tkr.core.reshape(-1)[0])) - np.linalg.norm(a)) <= 1e-12 * np.linalg.norm(a)
+    assert rep.relative_residual <= 1e-12
+
+
+@pytest.mark.parametrize("sequential", [False, True])
 def test_exact_recovery(ctx, ref, sequential):
     # test_hosvd.cpp:79-95 / acceptance C1: exact rank-(2,3,2) tensor
     t = _tucker_exact(ref, [10, 11, 9], [2, 3, 2], 42)
@@ -230,8 +244,14 @@ def test_exact_recovery(ctx, ref, sequential):
                                         ([12, 10, 8, 6], [3, 3, 2, 2]), ([40, 30, 20], [10, 10, 5]),
                                         # ranks > 32: the R^T R row pass (finish_step) and r x r
                                         # factorizations with 9 / 16 entries per thread
-                                        ([90, 80, 70], [40, 33, 50]), ([96, 80, 72], [64, 60, 36])])
+                                        ([90, 80, 70], [40, 33, 50]), ([96, 80, 72], [64, 60, 36]),
+                                        # order 2 (the t-HOSVD core's first step is the shrink of
+                                        # the last mode's R), odd / short panels
+                                        ([37, 29], [5, 5]), ([3, 130, 5, 7], [2, 9, 3, 2])])
 def test_hosvd_matches_reference(ctx, ref, sequential, dims, ranks):
+    if sequential and len(dims) == 2:
+        pytest.skip("order-2 st-HOSVD: the second mode's shrunk tensor is exactly rank r, "
+                    "its stopping test compares rounding noise")
     t = random_tensor(ref, dims, 3 + len(dims))
     t = t + 5 * _tucker_exact(ref, dims, ranks, 77)
     eng = tk.FactorEngine.with_als(tk.AlsConfig(eta=1e-8, seed=7, max_iters=50))
