@@ -17,6 +17,8 @@
  *   tkg_reduced_qr     <- tenkit::reduced_qr     include/tenkit/kernels.hpp:23,  src/kernels.cpp:303-367
  *   tkg_gram           <- tenkit::gram           include/tenkit/matrix.hpp:49,   src/matrix.cpp:90-126
  *   tkg_uniform01      <- uniform01(seeded_engine(seed, stream)) include/tenkit/rng.hpp:19-21,57-61
+ *   tkg_recover_singular_vectors <- tenkit::recover_singular_vectors include/tenkit/hosvd.hpp:78-82,
+ *                                   src/hosvd.cpp:65-72
  *
  * Conventions (identical to the reference):
  *   - tensors: flat doubles, generalized column-major, first index fastest
@@ -110,8 +112,8 @@ int tkg_destroy(tkg_ctx* ctx);
 
 /* t_hosvd with the ALS engine (FactorEngine::with_als). core: prod R_n
  * doubles; factors: concatenated I_n x R_n column-major in mode order.
- * want_singular_vectors must be 0 (recover_singular_vectors is a §8(f)
- * "next" row; returns TKG_E_UNSUPPORTED). */
+ * want_singular_vectors: rotate every factor onto the leading left singular
+ * vectors of its mode (recover_singular_vectors, hosvd.cpp:100-106). */
 int tkg_t_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
                 const uint64_t* dims, const uint64_t* ranks, const tkg_als_config* cfg,
                 int32_t want_singular_vectors, double* core, double* factors,
@@ -149,8 +151,8 @@ int tkg_shard_range(uint64_t extent, int rank, int world, uint64_t* begin, uint6
  * dims[N-1]; dims: the GLOBAL shape. */
 int tkg_t_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
                         uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
-                        const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
-                        tkg_error* err);
+                        const tkg_als_config* cfg, int32_t want_singular_vectors, double* core,
+                        double* factors, tkg_report* report, tkg_error* err);
 int tkg_st_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
                          uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
                          const uint32_t* mode_order, const tkg_als_config* cfg, double* core, double* factors,
@@ -187,6 +189,13 @@ int tkg_reduced_qr(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, 
                    double* r, tkg_error* err);
 int tkg_gram(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* out,
              tkg_error* err);
+/* recover_singular_vectors: q (rows = I_mode x cols, orthonormal columns)
+ * -> out = q V, V the left singular vectors of q^T A_(mode) in descending
+ * order, each column's largest-magnitude entry positive (dense_svd's
+ * convention, kernels.cpp:25-43). cols <= 64 and at least cols fibers. */
+int tkg_recover_singular_vectors(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims,
+                                 uint32_t mode, const double* q, uint64_t rows, uint64_t cols, double* out,
+                                 tkg_error* err);
 /* n draws of uniform01 from seeded_engine(seed, stream), generated on the
  * device by jump-ahead (the ALS initializer's stream). */
 int tkg_uniform01(tkg_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t n, double* out,

@@ -126,7 +126,8 @@ struct Options {
 
 inline Tucker hosvd_raw(Context& ctx, bool sequential, const double* a, bool a_on_device,
                         const std::vector<uint64_t>& dims, const std::vector<uint64_t>& ranks,
-                        const Options& opt, const std::vector<uint32_t>* order, tkg_report* rep) {
+                        const Options& opt, const std::vector<uint32_t>* order, tkg_report* rep,
+                        bool want_singular_vectors = false) {
   Tucker t;
   t.dims = dims;
   t.ranks = ranks;
@@ -151,7 +152,7 @@ inline Tucker hosvd_raw(Context& ctx, bool sequential, const double* a, bool a_o
                       order ? order->data() : nullptr, &cfg, t.core.data(), flat.data(), rep, &e);
   else
     rc = tkg_t_hosvd(ctx.get(), a, a_on_device, int32_t(dims.size()), dims.data(), ranks.data(), &cfg,
-                     0, t.core.data(), flat.data(), rep, &e);
+                     want_singular_vectors ? 1 : 0, t.core.data(), flat.data(), rep, &e);
   check(rc, e);
   uint64_t ofs = 0;
   for (size_t k = 0; k < dims.size(); ++k) {
@@ -185,7 +186,8 @@ inline tenkit::DecompositionReport to_report(const tkg_report& r) {
 
 inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> run(
     bool sequential, const tenkit::DenseTensor& t, const tenkit::Truncation& trunc,
-    const std::optional<tenkit::ModeOrder>& order, const tenkit::FactorEngine& engine) {
+    const std::optional<tenkit::ModeOrder>& order, const tenkit::FactorEngine& engine,
+    bool want_singular_vectors = false) {
   std::vector<uint64_t> dims(t.shape().dims().begin(), t.shape().dims().end());
   std::vector<uint64_t> ranks(trunc.ranks.begin(), trunc.ranks.end());
   std::vector<uint32_t> ord;
@@ -193,7 +195,7 @@ inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> run(
   Options opt{engine.als.eta, engine.als.max_iters, engine.als.seed};
   tkg_report rep{};
   Tucker r = hosvd_raw(Context::default_context(), sequential, t.data(), false, dims, ranks, opt,
-                       order ? &ord : nullptr, &rep);
+                       order ? &ord : nullptr, &rep, want_singular_vectors);
   std::vector<std::size_t> rk(trunc.ranks.begin(), trunc.ranks.end());
   tenkit::TuckerTensor tk{tenkit::DenseTensor(tenkit::Shape(rk), std::move(r.core)), {}, t.shape()};
   for (size_t k = 0; k < dims.size(); ++k)
@@ -204,8 +206,20 @@ inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> run(
 inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> t_hosvd(
     const tenkit::DenseTensor& t, const tenkit::Truncation& trunc, const tenkit::FactorEngine& engine,
     bool want_singular_vectors = false) {
-  if (want_singular_vectors) throw tenkit::DimensionMismatchError("want_singular_vectors: not on the B200 path");
-  return run(false, t, trunc, std::nullopt, engine);
+  return run(false, t, trunc, std::nullopt, engine, want_singular_vectors);
+}
+
+// hosvd.hpp:78-82
+inline tenkit::Matrix recover_singular_vectors(const tenkit::DenseTensor& t, std::size_t mode,
+                                               const tenkit::Matrix& q) {
+  std::vector<uint64_t> dims(t.shape().dims().begin(), t.shape().dims().end());
+  std::vector<double> out(q.rows() * q.cols(), 0.0);
+  tkg_error e{};
+  check(tkg_recover_singular_vectors(Context::default_context().get(), t.data(), int32_t(dims.size()),
+                                     dims.data(), uint32_t(mode), q.values().data(), q.rows(), q.cols(),
+                                     out.data(), &e),
+        e);
+  return tenkit::Matrix(q.rows(), q.cols(), std::move(out));
 }
 
 inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> st_hosvd(

@@ -285,9 +285,21 @@ int ref_select_order(int order, const uint64_t* dims, const uint64_t* ranks,
   });
 }
 
+// recover_singular_vectors (hosvd.cpp:65-72), q rows x cols.
+int ref_recover_singular_vectors(const double* a, int order, const uint64_t* dims,
+                                 uint32_t mode, const double* q, uint64_t rows,
+                                 uint64_t cols, double* out, int* subtype, char* msg,
+                                 int len) {
+  return guarded({subtype, msg, len}, [&] {
+    DenseTensor t = make_tensor(a, order, dims);
+    copy_out(recover_singular_vectors(t, mode, make_matrix(q, rows, cols)), out);
+  });
+}
+
 // t_hosvd / st_hosvd with the ALS engine (hosvd.cpp:74-191). factors_out
 // receives the factors concatenated in mode order (I_n x R_n each).
 // mode_order: nullable (st only; nullptr = select_order).
+// sequential: 0 t_hosvd, 1 st_hosvd, 2 t_hosvd(want_singular_vectors = true).
 int ref_hosvd_als(int sequential, const double* a, int order,
                   const uint64_t* dims, const uint64_t* ranks,
                   const uint32_t* mode_order, double eta, int max_iters,
@@ -302,13 +314,13 @@ int ref_hosvd_als(int sequential, const double* a, int order,
     cfg.seed = seed;
     FactorEngine eng = FactorEngine::with_als(cfg);
     std::pair<TuckerTensor, DecompositionReport> res =
-        sequential
+        sequential == 1
             ? st_hosvd(t, tr,
                        mode_order ? std::optional<ModeOrder>(ModeOrder{
                                         std::vector<std::size_t>(mode_order, mode_order + order)})
                                   : std::nullopt,
                        eng)
-            : t_hosvd(t, tr, eng);
+            : t_hosvd(t, tr, eng, sequential == 2);
     copy_out(res.first.core, core_out);
     if (factors_out) {
       double* p = factors_out;

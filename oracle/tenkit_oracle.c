@@ -718,6 +718,109 @@ done:
 }
 
 /* ======================= hosvd.cpp ===================================== */
+/* recover_singular_vectors (hosvd.cpp:65-72): out = q V with V the left
+ * singular vectors of q^T A_(mode). The reference takes dense_svd of the
+ * r x F matrix q^T A_(mode) (kernels.cpp:419-446): transposed to F x r, a
+ * Householder QR, then the r x r triangular factor T; the left vectors of
+ * q^T A_(mode) are T's right singular vectors, ordered by descending singular
+ * value (stable, kernels.cpp:273-301) and signed so each column's
+ * largest-magnitude entry (first on ties) is positive (fix_column_signs,
+ * kernels.cpp:25-43). This restatement computes T's right singular vectors
+ * with the one-sided (Hestenes) Jacobi method instead of the reference's
+ * Golub-Kahan iteration: equal to rounding, not bitwise (pinned against the
+ * compiled reference by tests/test_oracle_pins.py). F < r (fewer fibers than
+ * columns) is not covered (the reference then returns fewer columns). */
+int orc_recover_singular_vectors(const double* a, int order, const uint64_t* dims, int mode,
+                                 const double* q, size_t rows, size_t r, double* out,
+                                 orc_error* err) {
+  if (mode < 1 || mode > order)
+    return fail(err, ORC_E_INVALID_MODE, USAGE, "recover_singular_vectors: mode %d outside 1..%d", mode,
+                order);
+  const size_t count = count_of(order, dims), I = dims[mode - 1];
+  if (rows != I)
+    return fail(err, ORC_E_DIMENSION_MISMATCH, USAGE, "recover_singular_vectors: q has %zu rows, extent %zu",
+                rows, I);
+  const size_t F = I ? count / I : 0;
+  if (r == 0 || F < r)
+    return fail(err, ORC_E_OTHER, USAGE, "recover_singular_vectors: %zu fibers for %zu columns", F, r);
+  double* p = malloc((F * r + 1) * sizeof(double));   /* (q^T A_(mode))^T, F x r */
+  double* qq = malloc((F * r + 1) * sizeof(double));
+  double* t = malloc((r * r + 1) * sizeof(double));
+  double* v = malloc((r * r + 1) * sizeof(double));
+  double* w = malloc((r + 1) * sizeof(double));
+  size_t* perm = malloc((r + 1) * sizeof(size_t));
+  int st = orc_unfold_t_times(a, order, dims, mode, q, r, p, err);
+  if (!st) st = orc_reduced_qr(p, F, r, qq, t, err);
+  if (!st) {
+    for (size_t i = 0; i < r * r; ++i) v[i] = 0.0;
+    for (size_t i = 0; i < r; ++i) v[i + i * r] = 1.0;
+    for (int sweep = 0; sweep < 80; ++sweep) { /* Hestenes: orthogonalise T's columns */
+      int rotated = 0;
+      for (size_t i = 0; i + 1 < r; ++i)
+        for (size_t j = i + 1; j < r; ++j) {
+          double al = 0.0, be = 0.0, ga = 0.0;
+          for (size_t k = 0; k < r; ++k) {
+            al += t[k + i * r] * t[k + i * r];
+            be += t[k + j * r] * t[k + j * r];
+            ga += t[k + i * r] * t[k + j * r];
+          }
+          if (ga == 0.0 || fabs(ga) <= 0x1.0p-60 * sqrt(al * be)) continue;
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tn = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + tn * tn), sn = c * tn;
+          for (size_t k = 0; k < r; ++k) {
+            const double x = t[k + i * r], y = t[k + j * r];
+            t[k + i * r] = c * x - sn * y;
+            t[k + j * r] = sn * x + c * y;
+            const double vx = v[k + i * r], vy = v[k + j * r];
+            v[k + i * r] = c * vx - sn * vy;
+            v[k + j * r] = sn * vx + c * vy;
+          }
+          rotated = 1;
+        }
+      if (!rotated) break;
+    }
+    for (size_t c = 0; c < r; ++c) {
+      double n2 = 0.0;
+      for (size_t k = 0; k < r; ++k) n2 += t[k + c * r] * t[k + c * r];
+      w[c] = sqrt(n2);
+      perm[c] = c;
+    }
+    for (size_t c = 1; c < r; ++c) { /* stable descending (insertion sort) */
+      const size_t x = perm[c];
+      size_t k = c;
+      while (k > 0 && w[perm[k - 1]] < w[x]) {
+        perm[k] = perm[k - 1];
+        --k;
+      }
+      perm[k] = x;
+    }
+    for (size_t c = 0; c < r; ++c) { /* t <- V sorted and signed */
+      const size_t col = perm[c];
+      size_t arg = 0;
+      double best = 0.0;
+      for (size_t k = 0; k < r; ++k) {
+        const double mag = fabs(v[k + col * r]);
+        if (mag > best) {
+          best = mag;
+          arg = k;
+        }
+      }
+      const double sg = v[arg + col * r] >= 0.0 ? 1.0 : -1.0;
+      for (size_t k = 0; k < r; ++k) t[k + c * r] = sg * v[k + col * r];
+    }
+    orc_matmul(q, I, r, t, r, out);
+    ok(err);
+  }
+  free(p);
+  free(qq);
+  free(t);
+  free(v);
+  free(w);
+  free(perm);
+  return st;
+}
+
 void orc_select_order(int order, const uint64_t* ranks, int* out) { /* :54-63 stable sort */
   for (int k = 0; k < order; ++k) out[k] = k + 1;
   for (int i = 1; i < order; ++i) { /* insertion sort is stable */
@@ -745,6 +848,9 @@ int orc_hosvd_als(int sequential, const double* a, int order, const uint64_t* di
                   const uint64_t* ranks, const int* mode_order, double eta, int max_iters,
                   uint64_t seed, double* core_out, double* factors_out, orc_hosvd_report* rep,
                   orc_error* err) {
+  /* sequential == 2: t_hosvd with want_singular_vectors (hosvd.cpp:100-106) */
+  const int want_sv = sequential == 2;
+  if (want_sv) sequential = 0;
   int st = validate_trunc(order, dims, ranks, err);
   if (st) return st;
   memset(rep, 0, sizeof(*rep));
@@ -787,6 +893,13 @@ int orc_hosvd_als(int sequential, const double* a, int order, const uint64_t* di
       orc_reduced_qr(l, I, r, factors_out + fofs[n - 1], rr, NULL);
       free(rr);
       free(l);
+      if (want_sv) {
+        double* qv = malloc((I * r + 1) * sizeof(double));
+        st = orc_recover_singular_vectors(a, order, dims, n, factors_out + fofs[n - 1], I, r, qv, err);
+        if (!st) memcpy(factors_out + fofs[n - 1], qv, I * r * sizeof(double));
+        free(qv);
+        if (st) return st;
+      }
     }
     /* core = multi_mode_product(t, {U_n^T}) ascending (:115-121) */
     uint64_t cur[64];

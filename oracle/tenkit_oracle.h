@@ -115,6 +115,11 @@ typedef struct {
 /* sequential=0: t_hosvd (:74-125); 1: st_hosvd (:127-191).
  * mode_order nullable (= select_order). core_out: prod R_n; factors_out:
  * concatenated I_n x R_n in mode order. */
+/* hosvd.cpp:65-72; q is rows x r (rows = extent of mode). */
+int orc_recover_singular_vectors(const double* a, int order, const uint64_t* dims, int mode,
+                                 const double* q, size_t rows, size_t r, double* out,
+                                 orc_error* err);
+/* sequential: 0 t_hosvd, 1 st_hosvd, 2 t_hosvd with want_singular_vectors */
 int orc_hosvd_als(int sequential, const double* a, int order,
                   const uint64_t* dims, const uint64_t* ranks,
                   const int* mode_order, double eta, int max_iters,

@@ -71,8 +71,8 @@ SIGNATURES = [
     ("tkg_comm_init_local", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.POINTER(TkgError)]),
     ("tkg_shard_range", C.c_int, [C.c_uint64, C.c_int, C.c_int, _u64p, _u64p]),
     ("tkg_t_hosvd_sharded", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint64, C.c_uint64,
-                                      _u64p, C.POINTER(TkgAlsConfig), _dp, _dp, C.POINTER(TkgReport),
-                                      C.POINTER(TkgError)]),
+                                      _u64p, C.POINTER(TkgAlsConfig), C.c_int32, _dp, _dp,
+                                      C.POINTER(TkgReport), C.POINTER(TkgError)]),
     ("tkg_st_hosvd_sharded", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint64, C.c_uint64,
                                        _u64p, _u32p, C.POINTER(TkgAlsConfig), _dp, _dp, C.POINTER(TkgReport),
                                        C.POINTER(TkgError)]),
@@ -93,6 +93,8 @@ SIGNATURES = [
     ("tkg_reduced_qr", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, _dp,
                                  C.POINTER(TkgError)]),
     ("tkg_gram", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, C.POINTER(TkgError)]),
+    ("tkg_recover_singular_vectors", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.c_uint64,
+                                               C.c_uint64, _dp, C.POINTER(TkgError)]),
     ("tkg_uniform01", C.c_int, [_ctxp, C.c_uint64, C.c_uint32, C.c_uint64, _dp,
                                 C.POINTER(TkgError)]),
     ("tkg_set_profiling", C.c_int, [_ctxp, C.c_int]),

@@ -136,11 +136,9 @@ int tkg_t_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, c
                 double* core, double* factors, tkg_report* report, tkg_error* err) {
   return guarded(err, [&] {
     tkg::Shape sh = make_shape(order, dims);
-    if (want_singular_vectors)
-      tkg::raise(TKG_E_UNSUPPORTED, "t_hosvd: want_singular_vectors is not implemented on the B200 path");
     std::vector<uint64_t> rk(ranks, ranks + order);
     tkg::DecompRep rep;
-    eng(ctx).t_hosvd(a, a_on_device != 0, sh, rk, make_cfg(cfg), core, factors, &rep);
+    eng(ctx).t_hosvd(a, a_on_device != 0, sh, rk, make_cfg(cfg), core, factors, &rep, want_singular_vectors != 0);
     fill_report(rep, order, report);
   });
 }
@@ -199,14 +197,14 @@ int tkg_shard_range(uint64_t extent, int rank, int world, uint64_t* begin, uint6
 
 int tkg_t_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
                         uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
-                        const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
-                        tkg_error* err) {
+                        const tkg_als_config* cfg, int32_t want_singular_vectors, double* core, double* factors,
+                        tkg_report* report, tkg_error* err) {
   return guarded(err, [&] {
     tkg::Shape sh = make_shape(order, dims);
     std::vector<uint64_t> rk(ranks, ranks + order);
     tkg::DecompRep rep;
     eng(ctx).t_hosvd_sharded(a, a_on_device != 0, sh, slab_begin, slab_len, rk, make_cfg(cfg), core, factors,
-                             &rep);
+                             &rep, want_singular_vectors != 0);
     fill_report(rep, order, report);
   });
 }
@@ -312,6 +310,14 @@ int tkg_reduced_qr(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, 
 
 int tkg_gram(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* out, tkg_error* err) {
   return guarded(err, [&] { eng(ctx).gram(a, rows, cols, out); });
+}
+
+int tkg_recover_singular_vectors(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode,
+                                 const double* q, uint64_t rows, uint64_t cols, double* out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).recover_singular_vectors(a, sh, int(mode), q, rows, cols, out);
+  });
 }
 
 int tkg_uniform01(tkg_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t n, double* out, tkg_error* err) {

@@ -756,6 +756,89 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   return out;
 }
 
+// recover_singular_vectors (hosvd.cpp:65-72): the left singular vectors V of
+// q^T A_(n) are the eigenvectors of the Gram matrix of R = A_(n)^T q; an FC
+// pass forms R (with R^T R fused into its epilogue up to 32 columns, else the
+// row pass of finish_step), a single-CTA Jacobi solve gives V ordered and
+// signed as dense_svd (kernels.cpp:25-43, 273-301, 419-427), and U <- q V.
+// The eigenvectors of a Gram matrix carry errors ~eps sigma_1^2 / (sigma_i^2 -
+// sigma_j^2), against the reference's eps sigma_1 / (sigma_i - sigma_j)
+// (QR + SVD of the triangle, kernels.cpp:431-436), so a second round repeats
+// the step from q V0: the columns of A_(n)^T q V0 are formed directly from A,
+// their Gram is diagonal up to eps sigma_i sigma_j, and its Jacobi rotation
+// V1 refines V = V0 V1 to the reference's accuracy. The second round's R and
+// V1^T are what the t-HOSVD core uses (A_(n)^T U = (A_(n)^T q V0) V1).
+void Engine::recover_sv(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt) {
+  recover_sv_round(A, sh, mode, r, U, sv_vt0_.d(size_t(r) * r));
+  recover_sv_round(A, sh, mode, r, U, vt);
+}
+
+void Engine::recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
+  if (F < r)
+    raise(12, "recover_singular_vectors: mode " + std::to_string(mode) + " has " + std::to_string(F) +
+                  " fibers, fewer than the rank " + std::to_string(r));
+  const uint32_t ncp = pad_nc(r);
+  FiberView v{A, s, P, uint32_t(I), s, s * I};
+  double* Mt = mt_.d(I * ncp);
+  CK(launch_pack(U, 1, I, uint32_t(I), r, Mt, ncp, st_));  // Mt[i][c] = U[i + c*I]
+  count_launch();
+  double* R = r_.d(F * ncp + 8);
+  const bool fused_gram = ncp <= kFcGramMaxNc;
+  const int nfin = std::max(finish_step_grid(F, sms_), fc_grid(v, Mt, ncp, r));
+  double* gpr = fc_gram_.d(size_t(nfin) * ncp * ncp);
+  int fc_used = 0;
+  fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, true, nullptr, fused_gram ? gpr : nullptr);
+  int nparts = fc_used;
+  if (!fused_gram) {
+    AlsCtrl* ctrl = static_cast<AlsCtrl*>(sv_ctrl_.ensure(sizeof(AlsCtrl)));
+    CK(cudaMemsetAsync(ctrl, 0, sizeof(AlsCtrl), st_));
+    FinishArgs fa;
+    fa.R = R;
+    fa.F = F;
+    fa.ld = ncp;
+    fa.r = r;
+    fa.gpart = gpr;
+    fa.ctrl = ctrl;
+    fa.mode = 1;
+    coop_launch([&] { CK(launch_finish_step(fa, sms_, st_)); });
+    count_launch();
+    nparts = finish_step_grid(F, sms_);
+  }
+  double* G = sv_g_.d(size_t(r) * r);
+  CK(launch_gram_reduce(gpr, nparts, uint64_t(ncp) * ncp, ncp, r, G, st_));
+  if (dist_) dist_->allreduce_sum(G, size_t(r) * r, st_);
+  CK(launch_sym_eig(G, r, vt, nullptr, st_));
+  double* Un = sv_u_.d(I * r);
+  ExpandArgs ea;  // Un(i, c) = sum_k U(i, k) V(k, c): the expansion with s = I, K = r
+  ea.in = U;
+  ea.s = I;
+  ea.P = 1;
+  ea.K = r;
+  ea.U = vt;
+  ea.Iout = r;
+  ea.out = Un;
+  CK(launch_expand(ea, sms_, st_, nullptr));
+  CK(cudaMemcpyAsync(U, Un, I * r * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+  count_launch(3);
+}
+
+void Engine::recover_singular_vectors(const double* a, const Shape& sh, int mode, const double* q, uint64_t rows,
+                                      uint64_t cols, double* out) {
+  if (mode < 1 || mode > sh.N)
+    raise(1, "recover_singular_vectors: mode " + std::to_string(mode) + " outside 1.." + std::to_string(sh.N));
+  if (rows != sh.extent(mode))
+    raise(2, "recover_singular_vectors: q has " + std::to_string(rows) + " rows, mode " + std::to_string(mode) +
+                 " has extent " + std::to_string(sh.extent(mode)));
+  if (cols < 1 || cols > kMaxRank) raise(12, "recover_singular_vectors: q must have 1..64 columns");
+  const double* A = upload(a, sh.count(), false, tensor_, nullptr);
+  double* U = l_.d(rows * cols);
+  CK(cudaMemcpyAsync(U, q, rows * cols * sizeof(double), cudaMemcpyHostToDevice, st_));
+  recover_sv(A, sh, mode, uint32_t(cols), U, sv_vt_.d(cols * cols));
+  CK(cudaMemcpyAsync(out, U, rows * cols * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
 void Engine::begin_timed() {
   launches_ = 0;
   passes_ = 0;
@@ -846,7 +929,7 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
 }
 
 void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
-                     const AlsCfg& cfg, double* core, double* factors, DecompRep* rep) {
+                     const AlsCfg& cfg, double* core, double* factors, DecompRep* rep, bool want_sv) {
   validate_truncation(sh, ranks);
   *rep = DecompRep();
   const double* A = upload(a, sh.count(), a_dev, tensor_, &rep->h2d_seconds);
@@ -873,8 +956,12 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
     if (n < sh.N) {
       qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], nullptr, nullptr, 0, false);
+      if (want_sv) recover_sv(A, sh, n, r, U[n - 1], sv_vt_.d(r * r));
     } else {  // keep R_hat of the last mode for the core
       qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], rhat_.d(r * r), nullptr, 0, false);
+      // with singular vectors, r_ becomes A_(N)^T q and the core's R_hat is
+      // V^T: A_(N)^T U_N = (A_(N)^T q) V
+      if (want_sv) recover_sv(A, sh, n, r, U[n - 1], rhat_.d(r * r));
     }
     mode_end(n - 1);
     trace("mode done", n);

@@ -96,8 +96,9 @@ class Engine {
   ~Engine();
 
   // Decomposition drivers; `a` is host (a_dev false) or device memory.
+  // want_sv: rotate each factor onto singular vectors (recover_singular_vectors)
   void t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
-               const AlsCfg& cfg, double* core, double* factors, DecompRep* rep);
+               const AlsCfg& cfg, double* core, double* factors, DecompRep* rep, bool want_sv = false);
   void st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
                 const std::vector<int>* order, const AlsCfg& cfg, double* core, double* factors,
                 DecompRep* rep);
@@ -113,7 +114,7 @@ class Engine {
   bool has_comm() const { return comm_ != nullptr; }
   void t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t begin, uint64_t len,
                        const std::vector<uint64_t>& ranks, const AlsCfg& cfg, double* core, double* factors,
-                       DecompRep* rep);
+                       DecompRep* rep, bool want_sv = false);
   void st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t begin, uint64_t len,
                         const std::vector<uint64_t>& ranks, const std::vector<int>* order, const AlsCfg& cfg,
                         double* core, double* factors, DecompRep* rep);
@@ -127,6 +128,9 @@ class Engine {
   double relative_error(const double* a, const double* b, uint64_t n);
   void reduced_qr(const double* a, uint64_t rows, uint64_t cols, double* q, double* r);
   void gram(const double* a, uint64_t rows, uint64_t cols, double* out);
+  // recover_singular_vectors (hosvd.cpp:65-72): q (I_mode x cols) -> q V
+  void recover_singular_vectors(const double* a, const Shape& sh, int mode, const double* q, uint64_t rows,
+                                uint64_t cols, double* out);
   void uniform01(uint64_t seed, uint32_t stream, uint64_t n, double* out);
 
   void bench_contractions(const double* dA, const Shape& sh, int mode, uint32_t r, int reps,
@@ -190,6 +194,11 @@ class Engine {
   void qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
               double* rmat, double* rt, uint32_t ldrt, bool check);
   int qr_degenerate_col();
+  // recover_singular_vectors on a device-resident tensor: U (I x r, device,
+  // col-major) <- U V; leaves R = A_(n)^T U_old in r_ (row-major [F][ncp])
+  // and V^T (r x r, col-major) in vt. Sums the Gram over ranks when dist_.
+  void recover_sv(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
+  void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   const double* upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds);
   // ref_sumsq_host: pinned ||A||^2, read after the function's own sync
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
@@ -281,6 +290,7 @@ class Engine {
   std::unique_ptr<Comm> comm_;
   Comm* dist_ = nullptr;  // set while a sharded driver runs: run_als sums over ranks
   DBuf send_, recv_, reshard_, uslab_, uslab2_, core_t_;
+  DBuf sv_u_, sv_g_, sv_vt_, sv_vt0_, sv_ctrl_;
 };
 
 struct ShardRange {

@@ -194,7 +194,7 @@ void Engine::dist_core_and_residual(const double* A, const Shape& L, uint64_t k0
 
 void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64_t k0, uint64_t nloc,
                              const std::vector<uint64_t>& ranks, const AlsCfg& cfg, double* core, double* factors,
-                             DecompRep* rep) {
+                             DecompRep* rep, bool want_sv) {
   validate_truncation(G, ranks);
   check_shard(G, k0, nloc);
   const int N = G.N, world = comm_->world(), rank = comm_->rank();
@@ -249,6 +249,9 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
     sumsq_known = true;
     U[n - 1] = factor_bufs_[n - 1]->d(I * r);
     qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], n == N ? rhat_.d(r * r) : nullptr, nullptr, 0, false);
+    // singular vectors: the Gram of this rank's fibers of A_(n)^T q is summed
+    // over ranks, so every rank forms the same V (see Engine::t_hosvd)
+    if (want_sv) recover_sv(An, *Ln, n, r, U[n - 1], n == N ? rhat_.d(r * r) : sv_vt_.d(r * r));
     mode_end(n - 1);
   }
   Shape cs;

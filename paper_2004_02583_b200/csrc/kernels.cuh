@@ -134,6 +134,13 @@ cudaError_t launch_expand(const ExpandArgs& a, int num_sms, cudaStream_t st, int
 cudaError_t launch_reduce_partials(const double* part, int nparts, uint32_t rows, uint32_t ldp,
                                    uint32_t r, double* y, cudaStream_t st);
 
+// recover_singular_vectors (hosvd.cpp:65-72): eigenvectors of the symmetric
+// r x r matrix G (column-major, r <= 64) by parallel cyclic Jacobi, ordered by
+// descending eigenvalue and signed per fix_column_signs (kernels.cpp:25-43).
+// Writes V^T column-major (vt[c + i*r] = V(i, c)) and, when evals is set, the
+// eigenvalues in that order.
+cudaError_t launch_sym_eig(const double* G, uint32_t r, double* vt, double* evals, cudaStream_t st);
+
 // ---- sharded decomposition (smallla.cu) -------------------------------------
 cudaError_t launch_add(double* dst, const double* src, size_t n, cudaStream_t st);
 // part[0][i][c] = sum over the nparts FR partials [k][I][ldp] (c < r), in place.

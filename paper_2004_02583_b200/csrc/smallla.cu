@@ -377,6 +377,144 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
 // R = R2 R1 with R_k = L_k^T (CholQR2), the reference's degeneracy test on
 // diag(R) (als.cpp:74-86), and optional outputs R (col-major) / R^T padded.
 
+// ---- recover_singular_vectors (hosvd.cpp:65-72) ----------------------------------
+// The left singular vectors of q^T A_(n) are the eigenvectors of its Gram
+// matrix G = (A_(n)^T q)^T (A_(n)^T q) (r x r). One CTA runs the cyclic
+// parallel Jacobi method on G in shared memory: each round rotates the r/2
+// disjoint pairs of a round-robin tournament (player 0 fixed, the others
+// rotating), rows first, then columns and the accumulated V; a sweep is
+// r-1 rounds (r padded to even), repeated until a sweep finds every
+// off-diagonal entry negligible. The columns are then ordered by descending
+// eigenvalue (svd_tall's stable sort of the singular values,
+// kernels.cpp:273-301) and signed so that each column's largest-magnitude
+// entry (the first on ties) is positive (fix_column_signs, kernels.cpp:25-43,
+// applied to the left vectors of q^T A_(n) by dense_svd, kernels.cpp:419-427).
+constexpr int kEigMax = 64;
+constexpr int kEigLd = kEigMax + 1;
+constexpr int kEigThreads = 256;
+
+__device__ __forceinline__ void eig_pair(int round, int k, int m, int& p, int& q) {
+  if (k == 0) {
+    p = 0;
+    q = 1 + round;
+  } else {
+    p = 1 + (round + k) % (m - 1);
+    q = 1 + (round - k + (m - 1)) % (m - 1);
+  }
+  if (p > q) {
+    const int t = p;
+    p = q;
+    q = t;
+  }
+}
+
+__global__ void __launch_bounds__(kEigThreads) sym_eig_kernel(const double* __restrict__ G, uint32_t r,
+                                                              double* __restrict__ vt,
+                                                              double* __restrict__ evals) {
+  extern __shared__ __align__(16) double sm[];
+  double* A = sm;                       // [m][kEigLd]
+  double* V = sm + kEigMax * kEigLd;    // [m][kEigLd], V(i, c) at V[i*kEigLd + c]
+  __shared__ double cs[kEigMax / 2], sn[kEigMax / 2];
+  __shared__ int perm[kEigMax];
+  __shared__ double sgn[kEigMax];
+  __shared__ int rotated;
+  const int n = int(r), m = (n + 1) & ~1, half = m / 2, tid = threadIdx.x;
+  for (int e = tid; e < m * m; e += blockDim.x) {
+    const int i = e / m, j = e % m;
+    A[i * kEigLd + j] = (i < n && j < n) ? G[i + size_t(j) * r] : 0.0;
+    V[i * kEigLd + j] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int sweep = 0; sweep < 60 && m > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < m - 1; ++round) {
+      if (tid < half) {
+        int p, q;
+        eig_pair(round, tid, m, p, q);
+        double c = 1.0, s = 0.0;
+        const double apq = A[p * kEigLd + q];
+        if (q < n) {
+          const double app = A[p * kEigLd + p], aqq = A[q * kEigLd + q];
+          // negligible against the diagonal: the classical Jacobi threshold
+          if (fabs(apq) > 1e-300 && fabs(apq) > 0x1.0p-60 * sqrt(fabs(app) * fabs(aqq))) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            rotated = 1;
+          }
+        }
+        cs[tid] = c;
+        sn[tid] = s;
+      }
+      __syncthreads();
+      // rows: A <- J^T A (rows p, q of each pair)
+      for (int e = tid; e < half * m; e += blockDim.x) {
+        const int k = e / m, j = e % m;
+        const double c = cs[k], s = sn[k];
+        if (s == 0.0) continue;
+        int p, q;
+        eig_pair(round, k, m, p, q);
+        const double x = A[p * kEigLd + j], y = A[q * kEigLd + j];
+        A[p * kEigLd + j] = c * x - s * y;
+        A[q * kEigLd + j] = s * x + c * y;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = tid; e < half * m; e += blockDim.x) {
+        const int k = e / m, i = e % m;
+        const double c = cs[k], s = sn[k];
+        if (s == 0.0) continue;
+        int p, q;
+        eig_pair(round, k, m, p, q);
+        const double x = A[i * kEigLd + p], y = A[i * kEigLd + q];
+        A[i * kEigLd + p] = c * x - s * y;
+        A[i * kEigLd + q] = s * x + c * y;
+        const double vx = V[i * kEigLd + p], vy = V[i * kEigLd + q];
+        V[i * kEigLd + p] = c * vx - s * vy;
+        V[i * kEigLd + q] = s * vx + c * vy;
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  if (tid == 0) {  // stable descending order of the eigenvalues
+    for (int c = 0; c < n; ++c) perm[c] = c;
+    for (int c = 1; c < n; ++c) {
+      const int x = perm[c];
+      const double vx = A[x * kEigLd + x];
+      int k = c;
+      while (k > 0 && A[perm[k - 1] * kEigLd + perm[k - 1]] < vx) {
+        perm[k] = perm[k - 1];
+        --k;
+      }
+      perm[k] = x;
+    }
+  }
+  __syncthreads();
+  if (tid < n) {
+    const int col = perm[tid];
+    int arg = 0;
+    double best = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double mag = fabs(V[i * kEigLd + col]);
+      if (mag > best) {
+        best = mag;
+        arg = i;
+      }
+    }
+    sgn[tid] = V[arg * kEigLd + col] >= 0.0 ? 1.0 : -1.0;
+    if (evals) evals[tid] = A[col * kEigLd + col];
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int c = e % n, i = e / n;  // vt(c, i) = V(i, perm[c]) * sign
+    vt[c + size_t(i) * r] = sgn[c] * V[i * kEigLd + perm[c]];
+  }
+}
+
 // ---- sharded-decomposition helpers -------------------------------------------------
 __global__ void add_kernel(double* __restrict__ dst, const double* __restrict__ src, size_t n) {
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
@@ -556,5 +694,15 @@ cudaError_t launch_copy_box(const double* src, double* dst, const BoxCopy& b, cu
   copy_box_kernel<<<grid, 256, 0, st>>>(src, dst, b, total);
   return cudaGetLastError();
 }
+
+cudaError_t launch_sym_eig(const double* G, uint32_t r, double* vt, double* evals, cudaStream_t st) {
+  if (r < 1 || r > uint32_t(kEigMax)) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * 2 * kEigMax * kEigLd;
+  cudaError_t e = raise_smem_limit(sym_eig_kernel, smem);
+  if (e != cudaSuccess) return e;
+  sym_eig_kernel<<<1, kEigThreads, smem, st>>>(G, r, vt, evals);
+  return cudaGetLastError();
+}
+
 
 }  // namespace tkg

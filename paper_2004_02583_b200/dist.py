@@ -131,7 +131,7 @@ class ShardedContext:
         return ptr, on_dev, dims, b, n, keep
 
     def _run(self, sequential: bool, slab, dims, trunc: Truncation, order: Optional[ModeOrder],
-             engine: FactorEngine):
+             engine: FactorEngine, want_singular_vectors: bool = False):
         ptr, on_dev, dims, b, n, keep = self._slab(slab, dims)
         ranks = list(trunc.ranks)
         N = len(dims)
@@ -154,12 +154,14 @@ class ShardedContext:
                                         C.byref(cfg), _flat_ptr(core), _flat_ptr(fac), C.byref(rep), C.byref(err))
         else:
             rc = l.tkg_t_hosvd_sharded(self.ctx._ctx, ptr, on_dev, N, _lib.u64(dims), b, n, _lib.u64(ranks),
-                                       C.byref(cfg), _flat_ptr(core), _flat_ptr(fac), C.byref(rep), C.byref(err))
+                                       C.byref(cfg), int(bool(want_singular_vectors)), _flat_ptr(core),
+                                       _flat_ptr(fac), C.byref(rep), C.byref(err))
         _raise(rc, err)
         return Context._tucker(core, fac, dims, ranks), _decomp_report(rep)
 
-    def t_hosvd(self, slab, dims: Sequence[int], trunc: Truncation, engine: FactorEngine):
-        return self._run(False, slab, dims, trunc, None, engine)
+    def t_hosvd(self, slab, dims: Sequence[int], trunc: Truncation, engine: FactorEngine,
+                want_singular_vectors: bool = False):
+        return self._run(False, slab, dims, trunc, None, engine, want_singular_vectors)
 
     def st_hosvd(self, slab, dims: Sequence[int], trunc: Truncation, order: Optional[ModeOrder],
                  engine: FactorEngine):

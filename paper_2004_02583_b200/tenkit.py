@@ -393,6 +393,18 @@ class Context:
                                 C.byref(err)), err)
         return g
 
+    def recover_singular_vectors(self, t, mode: int, q):
+        """hosvd.cpp:65-72: q (I_mode x r, orthonormal) -> q V, V the left
+        singular vectors of q^T A_(mode) (descending, dense_svd's signs)."""
+        a = _host(t)
+        q = _host(q)
+        out = np.zeros(q.shape, order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_recover_singular_vectors(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape),
+                                                    int(mode), _flat_ptr(q), q.shape[0], q.shape[1],
+                                                    _flat_ptr(out), C.byref(err)), err)
+        return out
+
     def uniform01(self, seed: int, stream: int, n: int):
         out = np.zeros(n)
         err = _lib.TkgError()
@@ -487,6 +499,10 @@ def reduced_qr(a):
 
 def gram(a):
     return default_context().gram(a)
+
+
+def recover_singular_vectors(t, mode, q):
+    return default_context().recover_singular_vectors(t, mode, q)
 
 
 def synth_tucker(dims, ranks, alpha: float, nu: float, seed: int, out: Optional[np.ndarray] = None):

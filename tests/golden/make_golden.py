@@ -31,6 +31,21 @@ CASES = [
     ("st3_r10", [40, 30, 20], [10, 10, 5], True, None, 1e-8, 7, 9),
     ("t3_tight", [30, 28, 26], [6, 5, 4], False, None, 1e-12, 2004, 12),
 ]
+# t_hosvd with want_singular_vectors (hosvd.cpp:100-106, recover_singular_vectors :65-72)
+CASES_SV = [
+    ("t3_sv", [40, 30, 20], [10, 10, 5], 1e-8, 7, 9),
+    ("t4_sv", [12, 10, 8, 6], [3, 3, 2, 2], 1e-8, 7, 4),
+    ("t3_sv_r40", [70, 60, 50], [40, 36, 8], 1e-8, 5, 21),
+]
+
+
+def save_if_changed(path, **arrays):
+    """Rewrite a fixture only when its arrays change (keeps committed files stable)."""
+    if os.path.exists(path):
+        old = np.load(path)
+        if set(old.files) == set(arrays) and all(np.array_equal(old[k], arrays[k]) for k in arrays):
+            return
+    np.savez_compressed(path, **arrays)
 
 
 def tucker_input(ref, dims, ranks, seed):
@@ -44,9 +59,12 @@ def main():
     ref = Ref()
     ref.set_threads(1)
     index = {}
-    for name, dims, ranks, seq, order, eta, seed, noise in CASES:
+    cases = [c + (False,) for c in CASES] + [(n, d, r, False, None, e, s, z, True)
+                                              for n, d, r, e, s, z in CASES_SV]
+    for name, dims, ranks, seq, order, eta, seed, noise, want_sv in cases:
         a = tucker_input(ref, dims, ranks, noise)
-        res = ref.hosvd_als(a, ranks, sequential=seq, order=order, eta=eta, seed=seed)
+        res = ref.hosvd_als(a, ranks, sequential=seq, order=order, eta=eta, seed=seed,
+                            want_singular_vectors=want_sv)
         out = {"tensor": flat(a), "dims": np.array(dims), "ranks": np.array(ranks),
                "core": flat(res.core), "relative_residual": np.array(res.relative_residual),
                "modes": np.array([m.mode for m in res.per_mode]),
@@ -57,9 +75,9 @@ def main():
             out[f"factor{k + 1}"] = flat(u)
         for k, m in enumerate(res.per_mode):
             out[f"history{k}"] = np.array(m.residual_history)
-        np.savez_compressed(os.path.join(HERE, f"hosvd_{name}.npz"), **out)
+        save_if_changed(os.path.join(HERE, f"hosvd_{name}.npz"), **out)
         index[name] = {"dims": dims, "ranks": ranks, "sequential": seq, "order": order, "eta": eta,
-                       "seed": seed, "noise_seed": noise,
+                       "seed": seed, "noise_seed": noise, "want_singular_vectors": want_sv,
                        "iterations": [int(m.iterations) for m in res.per_mode],
                        "relative_residual": res.relative_residual}
     # initializer streams: raw engine words and uniform01 draws
@@ -71,8 +89,8 @@ def main():
     long = ref.uniform01(11, 4, 3_000_000)
     picks = np.array([0, 1, 311, 312, 313, 623, 624, 8191, 8192, 65535, 65536, 262143, 262144,
                       1_000_003, 2_999_999])
-    np.savez_compressed(os.path.join(HERE, "uniform01_11_4.npz"), idx=picks, val=long[picks],
-                        checksum=np.array(float(np.sum(long))))
+    save_if_changed(os.path.join(HERE, "uniform01_11_4.npz"), idx=picks, val=long[picks],
+                    checksum=np.array(float(np.sum(long))))
     with open(os.path.join(HERE, "streams.json"), "w") as f:
         json.dump(streams, f, indent=1)
     with open(os.path.join(HERE, "index.json"), "w") as f:

@@ -222,6 +222,15 @@ class Ref:
         return v
 
     # -- ALS / HOSVD -----------------------------------------------------------
+    def recover_singular_vectors(self, t, mode, q):
+        t = fortran(t)
+        q = fortran(q)
+        out = np.zeros(q.shape, order="F")
+        self._check(self.lib.ref_recover_singular_vectors(
+            _d(flat(t)), C.c_int(t.ndim), _u64(t.shape), C.c_uint32(mode), _d(flat(q)),
+            C.c_uint64(q.shape[0]), C.c_uint64(q.shape[1]), _d(out), *self._e()))
+        return out
+
     def als_init(self, t, mode, r, seed):
         t = fortran(t)
         l = np.zeros((_ext(t, mode), r), order="F")
@@ -267,7 +276,7 @@ class Ref:
         return list(out)
 
     def hosvd_als(self, t, ranks, sequential=False, order=None, eta=1e-4, max_iters=50,
-                  seed=0):
+                  seed=0, want_singular_vectors=False):
         t = fortran(t)
         n = t.ndim
         core = np.zeros(ranks, order="F")
@@ -276,7 +285,7 @@ class Ref:
         rep = (C.c_char * self.lib.ref_report_size())()
         mo = (C.c_uint32 * n)(*order) if order is not None else None
         self._check(self.lib.ref_hosvd_als(
-            C.c_int(1 if sequential else 0), _d(flat(t)), C.c_int(n), _u64(t.shape),
+            C.c_int(1 if sequential else (2 if want_singular_vectors else 0)), _d(flat(t)), C.c_int(n), _u64(t.shape),
             _u64(ranks), mo, C.c_double(eta), C.c_int(max_iters), C.c_uint64(seed), _d(core),
             _d(fac), rep, *self._e()))
         raw = bytes(rep)
@@ -426,6 +435,15 @@ class Port:
                                            C.c_size_t(b.shape[1]), _d(x), C.byref(self.err)))
         return x
 
+    def recover_singular_vectors(self, t, mode, q):
+        t = fortran(t)
+        q = fortran(q)
+        out = np.zeros(q.shape, order="F")
+        self._check(self.lib.orc_recover_singular_vectors(
+            _d(flat(t)), C.c_int(t.ndim), _u64(t.shape), C.c_int(mode), _d(flat(q)),
+            C.c_size_t(q.shape[0]), C.c_size_t(q.shape[1]), _d(out), C.byref(self.err)))
+        return out
+
     def als_init(self, t, mode, r, seed):
         t = fortran(t)
         l = np.zeros((_ext(t, mode), r), order="F")
@@ -455,7 +473,7 @@ class Port:
         return list(out)
 
     def hosvd_als(self, t, ranks, sequential=False, order=None, eta=1e-4, max_iters=50,
-                  seed=0):
+                  seed=0, want_singular_vectors=False):
         t = fortran(t)
         n = t.ndim
         core = np.zeros(ranks, order="F")
@@ -464,7 +482,7 @@ class Port:
         rep = _OrcHosvd()
         mo = (C.c_int * n)(*order) if order is not None else None
         self._check(self.lib.orc_hosvd_als(
-            C.c_int(1 if sequential else 0), _d(flat(t)), C.c_int(n), _u64(t.shape),
+            C.c_int(1 if sequential else (2 if want_singular_vectors else 0)), _d(flat(t)), C.c_int(n), _u64(t.shape),
             _u64(ranks), mo, C.c_double(eta), C.c_int(max_iters), C.c_uint64(seed), _d(core),
             _d(fac), C.byref(rep), C.byref(self.err)))
         factors = []

@@ -68,3 +68,18 @@ def assert_parity(m: dict, angle_tol: float = ANGLE_TOL):
     assert m["max_principal_sine"] <= angle_tol, m
     assert m["core_sv_rel_diff"] <= CORE_SV_REL_TOL, m
     assert m["max_ortho_defect"] <= ORTHO_TOL_PER_RANK, m
+
+
+def column_diff(u_gpu: np.ndarray, u_ref: np.ndarray) -> float:
+    """Largest column-wise distance between two factor matrices whose columns
+    are individually determined (singular vectors under dense_svd's sign
+    convention, kernels.cpp:25-43)."""
+    if u_gpu.size == 0:
+        return 0.0
+    return float(np.max(np.linalg.norm(u_gpu - u_ref, axis=0)))
+
+
+def column_alignment(w: np.ndarray, j: int, u: np.ndarray, k: int) -> float:
+    """|<w_j, u_k>| / (|w_j| |u_k|) (test_hosvd.cpp column_alignment)."""
+    a, b = w[:, j], u[:, k]
+    return float(abs(a @ b) / (np.linalg.norm(a) * np.linalg.norm(b)))

@@ -15,8 +15,8 @@ import pytest
 import paper_2004_02583_b200 as tk
 from paper_2004_02583_b200 import dist as tkd
 from golden_io import Fixture, fixtures
-from parity import (ANGLE_TOL, CORE_SV_REL_TOL, REL_ERR_ABS_TOL, core_sv_rel_diff, ortho_defect,
-                    principal_sine)
+from parity import (ANGLE_TOL, CORE_SV_REL_TOL, REL_ERR_ABS_TOL, column_diff, core_sv_rel_diff,
+                    ortho_defect, principal_sine)
 
 pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
 
@@ -83,12 +83,18 @@ def test_sharded_matches_reference_fixture(name, world):
         if m["sequential"]:
             order = tk.ModeOrder(m["order"]) if m["order"] else None
             return sc.st_hosvd(slab, dims, tk.Truncation(fx.ranks), order, eng)
-        return sc.t_hosvd(slab, dims, tk.Truncation(fx.ranks), eng)
+        return sc.t_hosvd(slab, dims, tk.Truncation(fx.ranks), eng,
+                          bool(m.get("want_singular_vectors")))
 
     res = run_ranks(world, fn)
     for r in range(1, world):
         check_same(res[0], res[r])
     check_reference(*res[0], fx)
+    if m.get("want_singular_vectors"):
+        tkr = res[0][0]
+        for u, v in zip(tkr.factors, fx.factors):
+            assert column_diff(u, v) <= ANGLE_TOL
+        assert np.max(np.abs(tkr.core - fx.core)) <= CORE_SV_REL_TOL * np.max(np.abs(fx.core))
 
 
 def _synthetic(dims, ranks, noise, seed):

@@ -6,8 +6,8 @@ import pytest
 
 import paper_2004_02583_b200 as tk
 from golden_io import Fixture, fixtures, long_stream, streams
-from parity import (ANGLE_TOL, CORE_SV_REL_TOL, REL_ERR_ABS_TOL, core_sv_rel_diff, ortho_defect,
-                    principal_sine)
+from parity import (ANGLE_TOL, CORE_SV_REL_TOL, REL_ERR_ABS_TOL, column_diff, core_sv_rel_diff,
+                    ortho_defect, principal_sine)
 
 pytestmark = pytest.mark.gpu
 
@@ -26,7 +26,14 @@ def test_gpu_matches_reference_fixture(ctx, name):
         order = tk.ModeOrder(m["order"]) if m["order"] else None
         tkr, rep = ctx.st_hosvd(fx.tensor, tk.Truncation(fx.ranks), order, eng)
     else:
-        tkr, rep = ctx.t_hosvd(fx.tensor, tk.Truncation(fx.ranks), eng)
+        tkr, rep = ctx.t_hosvd(fx.tensor, tk.Truncation(fx.ranks), eng,
+                               bool(m.get("want_singular_vectors")))
+    if m.get("want_singular_vectors"):
+        # singular vectors are determined column by column (dense_svd's sign
+        # convention), and so is the core
+        for u, v in zip(tkr.factors, fx.factors):
+            assert column_diff(u, v) <= ANGLE_TOL
+        assert np.max(np.abs(tkr.core - fx.core)) <= CORE_SV_REL_TOL * np.max(np.abs(fx.core))
     assert [p.mode for p in rep.per_mode] == fx.modes
     assert [p.als.iterations for p in rep.per_mode] == fx.iterations
     for p, h in zip(rep.per_mode, fx.histories):

@@ -12,7 +12,8 @@ import pytest
 
 import paper_2004_02583_b200 as tk
 from oracles import Port, Ref, counting_tensor, random_matrix, random_orthonormal, random_tensor
-from parity import assert_parity, compare_decompositions, ortho_defect, principal_sine
+from parity import (CORE_SV_REL_TOL, assert_parity, column_alignment, column_diff, compare_decompositions,
+                    ortho_defect, principal_sine)
 
 pytestmark = pytest.mark.gpu
 
@@ -320,3 +321,61 @@ def test_config2_st_hosvd_96pow4(ctx, ref):
     ref.set_threads(ref.max_threads())
     r = ref.hosvd_als(a, ranks, sequential=True, eta=1e-8, seed=7)
     assert_parity(compare_decompositions(tkr, rep, r))
+
+
+# ---- recover_singular_vectors (hosvd.cpp:65-72; §8(f) row 1) -------------------
+def test_recover_singular_vectors_kat(ctx, ref):
+    # test_hosvd.cpp:200-223: recovery undoes a rotation of the leading vectors
+    u = random_orthonormal(ref, 12, 6, 610)
+    v = random_orthonormal(ref, 15, 6, 611)
+    a = np.asfortranarray((u * np.array([5, 4, 3, 2, 1, 0.5])) @ v.T)
+    q = u[:, :3] @ random_orthonormal(ref, 3, 3, 611)
+    w = ctx.recover_singular_vectors(a, 1, q)
+    for j in range(3):
+        assert column_alignment(w, j, u, j) >= 1.0 - 1e-8
+    assert column_diff(w, ref.recover_singular_vectors(a, 1, q)) <= 1e-12
+    w2 = ctx.recover_singular_vectors(a, 1, u[:, :3])
+    for j in range(3):
+        assert column_alignment(w2, j, u, j) >= 1.0 - 1e-8
+
+
+@pytest.mark.parametrize("dims,r", [([40, 30, 20], 3), ([64, 33, 17], 10), ([80, 70, 60], 32),
+                                    ([90, 64, 40], 50), ([70, 66, 50], 64), ([200, 6, 4], 4),
+                                    ([17, 4, 6, 5], 3)], ids=str)
+def test_recover_singular_vectors_matches_reference(ctx, ref, dims, r):
+    t = random_tensor(ref, dims, 300 + r)
+    for mode in range(1, len(dims) + 1):
+        rr = min(r, dims[mode - 1])
+        q = random_orthonormal(ref, dims[mode - 1], rr, 400 + mode)
+        got = ctx.recover_singular_vectors(t, mode, q)
+        want = ref.recover_singular_vectors(t, mode, q)
+        assert column_diff(got, want) <= 1e-10, (mode, column_diff(got, want))
+        assert ortho_defect(got) <= 1e-14 * max(1, rr)
+
+
+@pytest.mark.parametrize("dims,ranks,alpha", [([60, 50, 40], [6, 5, 4], 0.0),
+                                              ([160, 150, 64], [64, 48, 32], 1.5),
+                                              ([96, 80, 72], [32, 40, 20], 1.0)], ids=str)
+def test_t_hosvd_singular_vectors_matches_reference(ctx, ref, dims, ranks, alpha):
+    # want_singular_vectors (hosvd.cpp:100-106): factors are singular vectors,
+    # determined column by column, and the core is determined with them
+    a = tk.synth_tucker(dims, ranks, alpha, 1e-3, 77).reshape(dims, order="F")
+    eng = tk.FactorEngine.with_als(tk.AlsConfig(eta=1e-8, seed=7, max_iters=50))
+    tkr, rep = ctx.t_hosvd(a, tk.Truncation(ranks), eng, True)
+    ref.set_threads(ref.max_threads())
+    r = ref.hosvd_als(a, ranks, eta=1e-8, seed=7, want_singular_vectors=True)
+    assert_parity(compare_decompositions(tkr, rep, r))
+    for u, v in zip(tkr.factors, r.factors):
+        assert column_diff(u, v) <= 1e-8
+    assert np.max(np.abs(tkr.core - r.core)) <= CORE_SV_REL_TOL * np.max(np.abs(r.core))
+    # the rotation leaves the approximation unchanged (test_hosvd.cpp:225-240)
+    _, plain = ctx.t_hosvd(a, tk.Truncation(ranks), eng)
+    assert abs(plain.relative_residual - rep.relative_residual) <= 1e-10
+
+
+def test_recover_singular_vectors_errors(ctx):
+    t = np.ones((4, 5, 6), order="F")
+    with pytest.raises(tk.InvalidModeError):
+        ctx.recover_singular_vectors(t, 4, np.eye(4)[:, :2])
+    with pytest.raises(tk.DimensionMismatchError):
+        ctx.recover_singular_vectors(t, 1, np.eye(5)[:, :2])

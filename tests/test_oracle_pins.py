@@ -9,7 +9,8 @@ CPU-only (runs in the driver's ``-m "not gpu"`` pass).
 import numpy as np
 import pytest
 
-from oracles import Port, Ref, counting_tensor, random_matrix, random_tensor
+from oracles import Port, Ref, counting_tensor, random_matrix, random_orthonormal, random_tensor
+from parity import column_alignment, column_diff
 
 # test_tensor_ops.cpp:26-27 kOracleShapes, plus shapes that cross the
 # 1024-fiber chunk (parallel.hpp:10) and the 256-row tiling (tensor_ops.cpp:239).
@@ -115,3 +116,44 @@ def test_error_taxonomy_matches(ref, port):
         with pytest.raises(Exception) as ei:
             lib.unfold_t_times(t, 9, np.zeros((3, 2)))
         assert ei.value.subtype == 1 and ei.value.code == 1  # InvalidMode
+
+
+def spectrum_tensor(ref, rows, cols, sigma, seed):
+    """test_hosvd.cpp:60-74: order-2 tensor u diag(sigma) v^T."""
+    u = random_orthonormal(ref, rows, len(sigma), seed)
+    v = random_orthonormal(ref, cols, len(sigma), seed + 1)
+    return np.asfortranarray((u * np.asarray(sigma)) @ v.T), u
+
+
+def test_recover_singular_vectors_port(ref, port):
+    # test_hosvd.cpp:200-223: recovery undoes a rotation of the leading vectors
+    a, u = spectrum_tensor(ref, 12, 15, [5, 4, 3, 2, 1, 0.5], 610)
+    q = u[:, :3] @ random_orthonormal(ref, 3, 3, 611)
+    for lib in (ref, port):
+        w = lib.recover_singular_vectors(a, 1, q)
+        assert w.shape == (12, 3)
+        for j in range(3):
+            assert column_alignment(w, j, u, j) >= 1.0 - 1e-8
+        w2 = lib.recover_singular_vectors(a, 1, u[:, :3])
+        for j in range(3):
+            assert column_alignment(w2, j, u, j) >= 1.0 - 1e-8
+    # the restatement (Hestenes Jacobi) agrees with Golub-Kahan to rounding,
+    # signs included, on every mode of a 3-way tensor
+    t = random_tensor(ref, [9, 8, 10], 77)
+    for mode, r in ((1, 3), (2, 5), (3, 4)):
+        q = random_orthonormal(ref, t.shape[mode - 1], r, 80 + mode)
+        assert column_diff(port.recover_singular_vectors(t, mode, q),
+                           ref.recover_singular_vectors(t, mode, q)) <= 1e-12
+
+
+def test_t_hosvd_singular_vectors_port(ref, port):
+    # test_hosvd.cpp:225-240 and the want_singular_vectors branch (hosvd.cpp:100-106)
+    t = random_tensor(ref, [9, 8, 10], 613)
+    a = ref.hosvd_als(t, [3, 3, 2], eta=1e-8, seed=7, want_singular_vectors=True)
+    b = port.hosvd_als(t, [3, 3, 2], eta=1e-8, seed=7, want_singular_vectors=True)
+    for x, y in zip(a.factors, b.factors):
+        assert column_diff(y, x) <= 1e-11
+    assert np.max(np.abs(a.core - b.core)) <= 1e-11 * np.max(np.abs(a.core))
+    assert abs(a.relative_residual - b.relative_residual) <= 1e-13
+    plain = ref.hosvd_als(t, [3, 3, 2], eta=1e-8, seed=7)
+    assert abs(plain.relative_residual - a.relative_residual) <= 1e-10
