@@ -19,6 +19,10 @@
  *   tkg_uniform01      <- uniform01(seeded_engine(seed, stream)) include/tenkit/rng.hpp:19-21,57-61
  *   tkg_recover_singular_vectors <- tenkit::recover_singular_vectors include/tenkit/hosvd.hpp:78-82,
  *                                   src/hosvd.cpp:65-72
+ *   tkg_t_hosvd_engine / tkg_st_hosvd_engine <- t_hosvd / st_hosvd with any FactorEngine
+ *                                   (kSvd, kEig, kAls; hosvd.hpp:19-27, hosvd.cpp:89-110, 150-182)
+ *   tkg_mode_gram      <- tenkit::mode_gram      include/tenkit/tensor_ops.hpp, src/tensor_ops.cpp:332-389
+ *   tkg_sym_eig        <- tenkit::sym_eig        include/tenkit/kernels.hpp:51, src/kernels.cpp:448-604
  *
  * Conventions (identical to the reference):
  *   - tensors: flat doubles, generalized column-major, first index fastest
@@ -78,7 +82,15 @@ typedef struct tkg_als_config {
   const double* init;
 } tkg_als_config;
 
-/* AlsReport + ModeReport (als.hpp:27-33, hosvd.hpp:33-37). */
+/* FactorEngine (hosvd.hpp:19-27): kind + the ALS configuration (kAls only). */
+enum tkg_engine_kind { TKG_ENGINE_SVD = 0, TKG_ENGINE_EIG = 1, TKG_ENGINE_ALS = 2 };
+typedef struct tkg_factor_engine {
+  int32_t kind; /* enum tkg_engine_kind */
+  tkg_als_config als;
+} tkg_factor_engine;
+
+/* AlsReport + ModeReport (als.hpp:27-33, hosvd.hpp:33-37). status -1: the
+ * mode's factor came from the SVD / EIG engine (ModeReport::als empty). */
 typedef struct tkg_mode_report {
   int32_t mode;        /* 1-based */
   int32_t iterations;
@@ -125,6 +137,17 @@ int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
                  const uint64_t* dims, const uint64_t* ranks, const uint32_t* mode_order,
                  const tkg_als_config* cfg, double* core, double* factors, tkg_report* report,
                  tkg_error* err);
+
+/* t_hosvd / st_hosvd with any factor engine. kSvd / kEig: the factor is the
+ * leading R_n eigenvectors of A_(n) A_(n)^T (mode_gram on the device +
+ * symmetric eigensolver), descending, signed as the reference
+ * (kernels.cpp:25-43, 584-603). want_singular_vectors applies to kAls only. */
+int tkg_t_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                       const uint64_t* ranks, const tkg_factor_engine* engine, int32_t want_singular_vectors,
+                       double* core, double* factors, tkg_report* report, tkg_error* err);
+int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                        const uint64_t* ranks, const uint32_t* mode_order, const tkg_factor_engine* engine,
+                        double* core, double* factors, tkg_report* report, tkg_error* err);
 
 /* ---- Sharded decomposition (one context per GPU, tensor split along its
  * last mode; BASELINE north star). The reference is single-process; these
@@ -189,6 +212,14 @@ int tkg_reduced_qr(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, 
                    double* r, tkg_error* err);
 int tkg_gram(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* out,
              tkg_error* err);
+/* mode_gram: out = A_(mode) A_(mode)^T (extent x extent, column-major). */
+int tkg_mode_gram(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode, double* out,
+                  tkg_error* err);
+/* sym_eig: the k leading eigenpairs of the symmetric n x n matrix g,
+ * descending; vectors n x k column-major, each column's largest-magnitude
+ * entry positive. */
+int tkg_sym_eig(tkg_ctx* ctx, const double* g, uint64_t n, uint64_t k, double* values, double* vectors,
+                tkg_error* err);
 /* recover_singular_vectors: q (rows = I_mode x cols, orthonormal columns)
  * -> out = q V, V the left singular vectors of q^T A_(mode) in descending
  * order, each column's largest-magnitude entry positive (dense_svd's

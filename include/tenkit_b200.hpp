@@ -122,6 +122,7 @@ struct Options {
   double eta = 1e-4;  // AlsConfig defaults (als.hpp:17-23)
   int max_iters = 50;
   uint64_t seed = 0;
+  int kind = TKG_ENGINE_ALS;  // FactorEngine::Kind (hosvd.hpp:19-27)
 };
 
 inline Tucker hosvd_raw(Context& ctx, bool sequential, const double* a, bool a_on_device,
@@ -138,7 +139,7 @@ inline Tucker hosvd_raw(Context& ctx, bool sequential, const double* a, bool a_o
   }
   t.core.assign(core, 0.0);
   std::vector<double> flat(fac ? fac : 1, 0.0);
-  tkg_als_config cfg{opt.eta, opt.max_iters, opt.seed, nullptr};
+  tkg_factor_engine cfg{opt.kind, {opt.eta, opt.max_iters, opt.seed, nullptr}};
   tkg_error e{};
   int rc;
   if (ranks.size() != dims.size()) {
@@ -148,11 +149,11 @@ inline Tucker hosvd_raw(Context& ctx, bool sequential, const double* a, bool a_o
     rethrow(e);
   }
   if (sequential)
-    rc = tkg_st_hosvd(ctx.get(), a, a_on_device, int32_t(dims.size()), dims.data(), ranks.data(),
-                      order ? order->data() : nullptr, &cfg, t.core.data(), flat.data(), rep, &e);
+    rc = tkg_st_hosvd_engine(ctx.get(), a, a_on_device, int32_t(dims.size()), dims.data(), ranks.data(),
+                             order ? order->data() : nullptr, &cfg, t.core.data(), flat.data(), rep, &e);
   else
-    rc = tkg_t_hosvd(ctx.get(), a, a_on_device, int32_t(dims.size()), dims.data(), ranks.data(), &cfg,
-                     want_singular_vectors ? 1 : 0, t.core.data(), flat.data(), rep, &e);
+    rc = tkg_t_hosvd_engine(ctx.get(), a, a_on_device, int32_t(dims.size()), dims.data(), ranks.data(), &cfg,
+                            want_singular_vectors ? 1 : 0, t.core.data(), flat.data(), rep, &e);
   check(rc, e);
   uint64_t ofs = 0;
   for (size_t k = 0; k < dims.size(); ++k) {
@@ -171,6 +172,10 @@ inline tenkit::DecompositionReport to_report(const tkg_report& r) {
     tenkit::ModeReport mr;
     mr.mode = std::size_t(m.mode);
     mr.seconds = m.seconds;
+    if (m.status < 0) {  // SVD / EIG engine: no ALS report
+      out.per_mode.push_back(mr);
+      continue;
+    }
     tenkit::AlsReport ar;
     ar.iterations = m.iterations;
     ar.residual_history.assign(m.residual_history, m.residual_history + m.history_len);
@@ -192,7 +197,7 @@ inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> run(
   std::vector<uint64_t> ranks(trunc.ranks.begin(), trunc.ranks.end());
   std::vector<uint32_t> ord;
   if (order) ord.assign(order->order.begin(), order->order.end());
-  Options opt{engine.als.eta, engine.als.max_iters, engine.als.seed};
+  Options opt{engine.als.eta, engine.als.max_iters, engine.als.seed, static_cast<int>(engine.kind)};
   tkg_report rep{};
   Tucker r = hosvd_raw(Context::default_context(), sequential, t.data(), false, dims, ranks, opt,
                        order ? &ord : nullptr, &rep, want_singular_vectors);

@@ -333,6 +333,52 @@ int ref_hosvd_als(int sequential, const double* a, int order,
   });
 }
 
+// t_hosvd / st_hosvd with the SVD (kind 0) or EIG (kind 1) engine
+// (hosvd.cpp:89-99, 151-171); same buffers as ref_hosvd_als.
+int ref_hosvd_exact(int sequential, int kind, const double* a, int order,
+                    const uint64_t* dims, const uint64_t* ranks,
+                    const uint32_t* mode_order, double* core_out, double* factors_out,
+                    void* report, int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    DenseTensor t = make_tensor(a, order, dims);
+    Truncation tr{std::vector<std::size_t>(ranks, ranks + order)};
+    FactorEngine eng = kind == 0 ? FactorEngine::svd() : FactorEngine::eig();
+    std::pair<TuckerTensor, DecompositionReport> res =
+        sequential
+            ? st_hosvd(t, tr,
+                       mode_order ? std::optional<ModeOrder>(ModeOrder{
+                                        std::vector<std::size_t>(mode_order, mode_order + order)})
+                                  : std::nullopt,
+                       eng)
+            : t_hosvd(t, tr, eng);
+    copy_out(res.first.core, core_out);
+    double* p = factors_out;
+    for (const Matrix& u : res.first.factors) {
+      std::copy(u.values().begin(), u.values().end(), p);
+      p += u.values().size();
+    }
+    fill_report(res.second, static_cast<RefReport*>(report));
+  });
+}
+
+// mode_gram (tensor_ops.cpp:332-389), extent x extent.
+int ref_mode_gram(const double* a, int order, const uint64_t* dims, uint32_t mode,
+                  double* out, int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    copy_out(mode_gram(make_tensor(a, order, dims), mode), out);
+  });
+}
+
+// sym_eig (kernels.cpp:448-604): k leading pairs.
+int ref_sym_eig(const double* g, uint64_t n, uint64_t k, double* values,
+                double* vectors, int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    SpectrumReport sr = sym_eig(make_matrix(g, n, n), k);
+    std::copy(sr.values.begin(), sr.values.end(), values);
+    copy_out(*sr.left_vectors, vectors);
+  });
+}
+
 // reconstruct (tensor_ops.cpp:420-440) from a core and concatenated factors.
 int ref_reconstruct(const double* core, int order, const uint64_t* ranks,
                     const uint64_t* dims, const double* factors, double* out,

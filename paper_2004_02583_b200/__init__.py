@@ -8,7 +8,8 @@ from .tenkit import (AlsConfig, AlsReport, Context, DecompositionReport, Degener
                      FormatError, InvalidModeError, IoError, ModeOrder, ModeReport,
                      NoConvergenceError, RankTooLargeError, SingularGramError, Truncation,
                      TuckerTensor, UnsupportedError, ZeroReferenceError, als_init, als_low_rank,
-                     default_context, frobenius_norm, gram, mode_n_product, recover_singular_vectors, reduced_qr,
+                     default_context, frobenius_norm, gram, mode_gram, mode_n_product, recover_singular_vectors,
+                     reduced_qr, sym_eig,
                      relative_error, select_order, st_hosvd, synth_tucker, synth_tucker_slab, t_hosvd, unfold_t_times,
                      unfold_times)
 

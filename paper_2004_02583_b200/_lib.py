@@ -27,6 +27,13 @@ class TkgAlsConfig(C.Structure):
                 ("init", C.POINTER(C.c_double))]
 
 
+class TkgFactorEngine(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("als", TkgAlsConfig)]
+
+
+ENGINE_KINDS = {"svd": 0, "eig": 1, "als": 2}
+
+
 class TkgModeReport(C.Structure):
     _fields_ = [("mode", C.c_int32), ("iterations", C.c_int32), ("status", C.c_int32),
                 ("history_len", C.c_int32), ("achieved_eta", C.c_double), ("seconds", C.c_double),
@@ -63,6 +70,14 @@ SIGNATURES = [
     ("tkg_st_hosvd", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, _u64p, _u32p,
                                C.POINTER(TkgAlsConfig), _dp, _dp, C.POINTER(TkgReport),
                                C.POINTER(TkgError)]),
+    ("tkg_t_hosvd_engine", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, _u64p,
+                                     C.POINTER(TkgFactorEngine), C.c_int32, _dp, _dp,
+                                     C.POINTER(TkgReport), C.POINTER(TkgError)]),
+    ("tkg_st_hosvd_engine", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, _u64p, _u32p,
+                                      C.POINTER(TkgFactorEngine), _dp, _dp, C.POINTER(TkgReport),
+                                      C.POINTER(TkgError)]),
+    ("tkg_mode_gram", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.POINTER(TkgError)]),
+    ("tkg_sym_eig", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_select_order", C.c_int, [C.c_int32, _u64p, _u64p, _u32p, C.POINTER(TkgError)]),
     ("tkg_nccl_unique_id", C.c_int, [C.c_void_p, C.POINTER(TkgError)]),
     ("tkg_comm_init_nccl", C.c_int, [_ctxp, C.c_int, C.c_int, C.c_void_p, C.POINTER(TkgError)]),

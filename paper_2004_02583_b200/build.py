@@ -25,8 +25,9 @@ SYNTH = os.path.join(PKG, "libtkg_synth.so")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 GXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else (shutil.which("g++") or "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SRCS = ["contract.cu", "contract_tma.cu", "smallla.cu", "mtrng.cu", "recon.cu", "als_step.cu", "coop.cu"]
-CPP_SRCS = ["engine.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp"]
+CU_SRCS = ["contract.cu", "contract_tma.cu", "smallla.cu", "mtrng.cu", "recon.cu", "als_step.cu", "coop.cu",
+           "gram.cu"]
+CPP_SRCS = ["engine.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp", "eig.cpp"]
 
 
 def _newest(paths):

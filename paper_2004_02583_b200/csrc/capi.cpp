@@ -158,6 +158,51 @@ int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, 
   });
 }
 
+int tkg_t_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                       const uint64_t* ranks, const tkg_factor_engine* engine, int32_t want_singular_vectors,
+                       double* core, double* factors, tkg_report* report, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    const int kind = engine ? engine->kind : TKG_ENGINE_ALS;
+    if (kind < TKG_ENGINE_SVD || kind > TKG_ENGINE_ALS) tkg::raise(TKG_E_UNSUPPORTED, "unknown factor engine kind");
+    tkg::DecompRep rep;
+    eng(ctx).t_hosvd(a, a_on_device != 0, sh, rk, make_cfg(engine ? &engine->als : nullptr), core, factors, &rep,
+                     kind == TKG_ENGINE_ALS && want_singular_vectors != 0, kind);
+    fill_report(rep, order, report);
+  });
+}
+
+int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+                        const uint64_t* ranks, const uint32_t* mode_order, const tkg_factor_engine* engine,
+                        double* core, double* factors, tkg_report* report, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    std::vector<int> mo;
+    if (mode_order) mo.assign(mode_order, mode_order + order);
+    const int kind = engine ? engine->kind : TKG_ENGINE_ALS;
+    if (kind < TKG_ENGINE_SVD || kind > TKG_ENGINE_ALS) tkg::raise(TKG_E_UNSUPPORTED, "unknown factor engine kind");
+    tkg::DecompRep rep;
+    eng(ctx).st_hosvd(a, a_on_device != 0, sh, rk, mode_order ? &mo : nullptr,
+                      make_cfg(engine ? &engine->als : nullptr), core, factors, &rep, kind);
+    fill_report(rep, order, report);
+  });
+}
+
+int tkg_mode_gram(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode, double* out,
+                  tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    eng(ctx).mode_gram(a, sh, int(mode), out);
+  });
+}
+
+int tkg_sym_eig(tkg_ctx* ctx, const double* g, uint64_t n, uint64_t k, double* values, double* vectors,
+                tkg_error* err) {
+  return guarded(err, [&] { eng(ctx).sym_eig(g, n, k, values, vectors); });
+}
+
 int tkg_nccl_unique_id(void* out128, tkg_error* err) {
   return guarded(err, [&] {
     if (!tkg::nccl_unique_id(out128)) tkg::raise(TKG_E_CUDA, "NCCL (libnccl.so.2) could not be loaded");

@@ -142,6 +142,7 @@ Engine::~Engine() {
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto e : mode_ev_) cudaEventDestroy(e);
   if (stage_h_) cudaFreeHost(stage_h_);
+  if (norm_h_) cudaFreeHost(norm_h_);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
   cudaStreamSynchronize(st2_);
@@ -839,6 +840,72 @@ void Engine::recover_singular_vectors(const double* a, const Shape& sh, int mode
   sync();
 }
 
+// ---- SVD / EIG factor engines (hosvd.cpp:89-99, 151-171) -----------------------
+// The EIG engine's factor is sym_eig(mode_gram(t, n), R_n) (tensor_ops.cpp:332-389,
+// kernels.cpp:448-604); the SVD engine's is the leading R_n left singular
+// vectors of A_(n) (dense_svd, kernels.cpp:419-446), i.e. the same eigenvectors
+// of A_(n) A_(n)^T, with the same descending order and sign convention. Here:
+// the Gram matrix on DMMA straight from the tensor layout (gram.cu), cuSOLVER's
+// syevd (eig.cpp), and the ordering / sign pass (leading_vectors_kernel).
+void Engine::gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
+  if (I > 32768) raise(12, "mode " + std::to_string(mode) + ": extent " + std::to_string(I) +
+                               " above the 32768 supported by the SVD / EIG engines");
+  FiberView v{A, s, P, uint32_t(I), s, s * I};
+  const GramPlan gp = gram_tensor_plan(v, sms_);
+  double* part = gram_t_part_.d(std::max<size_t>(gp.part_doubles, 1));
+  double* G = gram_t_.d(I * I);
+  double* W = gram_w_.d(I);
+  CK(launch_gram_tensor(v, gp, part, G, st_));
+  count_launch(2);
+  const std::string why = eig_.eig(G, int(I), W, st_);
+  if (!why.empty()) raise(why.rfind("sym_eig", 0) == 0 ? 7 : 11, why);
+  CK(launch_leading_vectors(G, W, uint32_t(I), r, U, nullptr, st_));
+  count_launch();
+}
+
+double* Engine::sumsq_to_host(const double* A, uint64_t n) {
+  if (!norm_h_) CK(cudaHostAlloc(reinterpret_cast<void**>(&norm_h_), 2 * sizeof(double), cudaHostAllocDefault));
+  double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(n))));
+  CK(launch_sumsq(A, n, sq, st_));
+  CK(launch_sum(sq, sumsq_partials_count(n), sumsq_d_.d(2), st_));
+  count_launch(2);
+  if (dist_) dist_->allreduce_sum(sumsq_d_.d(2), 1, st_);
+  CK(cudaMemcpyAsync(norm_h_, sumsq_d_.d(2), sizeof(double), cudaMemcpyDeviceToHost, st_));
+  return norm_h_;
+}
+
+void Engine::mode_gram(const double* a, const Shape& sh, int mode, double* out) {
+  if (mode < 1 || mode > sh.N)
+    raise(1, "mode " + std::to_string(mode) + " out of range 1.." + std::to_string(sh.N));
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
+  const double* A = upload(a, sh.count(), false, tensor_, nullptr);
+  FiberView v{A, s, P, uint32_t(I), s, s * I};
+  const GramPlan gp = gram_tensor_plan(v, sms_);
+  double* part = gram_t_part_.d(std::max<size_t>(gp.part_doubles, 1));
+  double* G = gram_t_.d(I * I);
+  CK(launch_gram_tensor(v, gp, part, G, st_));
+  CK(cudaMemcpyAsync(out, G, I * I * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
+void Engine::sym_eig(const double* g, uint64_t n, uint64_t k, double* values, double* vectors) {
+  if (k > n)
+    raise(2, "sym_eig: requested " + std::to_string(k) + " pairs from a " + std::to_string(n) +
+                 "-dimensional matrix");
+  double* G = gram_t_.d(std::max<uint64_t>(n * n, 1));
+  double* W = gram_w_.d(std::max<uint64_t>(n, 1));
+  double* U = sv_u_.d(std::max<uint64_t>(n * k, 1));
+  double* V = sv_g_.d(std::max<uint64_t>(k, 1));
+  CK(cudaMemcpyAsync(G, g, n * n * sizeof(double), cudaMemcpyHostToDevice, st_));
+  const std::string why = eig_.eig(G, int(n), W, st_);
+  if (!why.empty()) raise(why.rfind("sym_eig", 0) == 0 ? 7 : 11, why);
+  CK(launch_leading_vectors(G, W, uint32_t(n), uint32_t(k), U, V, st_));
+  CK(cudaMemcpyAsync(values, V, k * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(vectors, U, n * k * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+}
+
 void Engine::begin_timed() {
   launches_ = 0;
   passes_ = 0;
@@ -928,13 +995,68 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
   return std::sqrt(diff_sq / ref_sumsq);
 }
 
+// Reports, D2H and the residual of an SVD / EIG decomposition (the modes carry
+// no ALS report: status -1, ModeReport::als empty, hosvd.hpp:33-37).
+void Engine::finish_exact(const Shape& sh, const std::vector<uint64_t>& ranks, const Shape& cs, const double* A,
+                          const double* core_buf, const std::vector<double*>& U, const double* ref_sumsq,
+                          double* core, double* factors, DecompRep* rep, Clock::time_point t0,
+                          const std::vector<int>* order) {
+  sync();
+  for (int k = 0; k < sh.N; ++k) {
+    ModeRep mr;
+    mr.mode = order ? (*order)[k] : k + 1;
+    mr.iterations = 0;
+    mr.status = -1;
+    mr.seconds = mode_seconds(k);
+    rep->per_mode.push_back(mr);
+  }
+  rep->seconds = since(t0);
+  rep->launches = launches_;
+  rep->passes = passes_;
+  rep->bytes = bytes_;
+  const auto td = Clock::now();
+  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  size_t ofs = 0;
+  for (int n = 0; n < sh.N; ++n) {
+    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    ofs += sh.d[n] * ranks[n];
+  }
+  sync();
+  rep->d2h_seconds = since(td);
+  const auto tr = Clock::now();
+  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+  rep->residual_seconds = since(tr);
+}
+
 void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
-                     const AlsCfg& cfg, double* core, double* factors, DecompRep* rep, bool want_sv) {
+                     const AlsCfg& cfg, double* core, double* factors, DecompRep* rep, bool want_sv,
+                     int engine) {
   validate_truncation(sh, ranks);
   *rep = DecompRep();
   const double* A = upload(a, sh.count(), a_dev, tensor_, &rep->h2d_seconds);
   while (factor_bufs_.size() < size_t(sh.N)) factor_bufs_.push_back(new DBuf());
   std::vector<double*> U(sh.N);
+  if (engine != kEngineAls) {
+    // SVD / EIG engines (hosvd.cpp:89-99): per-mode factor, then the full TTM chain
+    stage_reserve(sh.N, 1);
+    begin_timed();
+    const auto t0 = Clock::now();
+    for (int n = 1; n <= sh.N; ++n) {
+      const uint32_t r = uint32_t(ranks[n - 1]);
+      mode_begin(n - 1);
+      U[n - 1] = factor_bufs_[n - 1]->d(sh.d[n - 1] * r);
+      gram_factor(A, sh, n, r, U[n - 1]);
+      mode_end(n - 1);
+    }
+    Shape cs;
+    cs.N = sh.N;
+    for (int k = 0; k < sh.N; ++k) cs.d[k] = ranks[k];
+    double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
+    core_chain(A, sh, ranks, U, core_buf);
+    const double* ref_sumsq = sumsq_to_host(A, sh.count());
+    finish_exact(sh, ranks, cs, A, core_buf, U, ref_sumsq, core, factors, rep, t0, nullptr);
+    return;
+  }
   begin_timed();
   const auto t0 = Clock::now();
   g_trace_t0 = t0;
@@ -1031,7 +1153,7 @@ std::vector<int> checked_order(const Shape& sh, const std::vector<uint64_t>& ran
 
 void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
                       const std::vector<int>* order_in, const AlsCfg& cfg, double* core,
-                      double* factors, DecompRep* rep) {
+                      double* factors, DecompRep* rep, int engine) {
   validate_truncation(sh, ranks);
   const std::vector<int> order = checked_order(sh, ranks, order_in);
   *rep = DecompRep();
@@ -1044,6 +1166,36 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
   const double* work = A;
   DBuf* bufs[2] = {&work_a_, &work_b_};
   int which = 0;
+  if (engine != kEngineAls) {
+    // SVD / EIG engines (hosvd.cpp:151-171): factor, then working <- working x_n U^T
+    stage_reserve(sh.N, 1);
+    const double* ref_sumsq = sumsq_to_host(A, sh.count());
+    for (size_t k = 0; k < order.size(); ++k) {
+      const int mode = order[k];
+      const uint32_t r = uint32_t(ranks[mode - 1]);
+      const uint64_t I = cur.extent(mode), s = cur.stride(mode), F = cur.count() / I, P = F / s;
+      mode_begin(int(k));
+      U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
+      gram_factor(work, cur, mode, r, U[mode - 1]);
+      const uint32_t ncp = pad_nc(r);
+      double* Mt = mt_.d(I * ncp);
+      CK(launch_pack(U[mode - 1], 1, I, uint32_t(I), r, Mt, ncp, st_));
+      count_launch();
+      Shape nxt = cur;
+      nxt.d[mode - 1] = r;
+      double* dst = bufs[which]->d(nxt.count());
+      FiberView v{work, s, P, uint32_t(I), s, s * I};
+      fc(v, Mt, ncp, r, dst, 1, s, s * r, nullptr, nullptr, nullptr, true);
+      mode_end(int(k));
+      work = dst;
+      cur = nxt;
+      which ^= 1;
+    }
+    double* core_buf = static_cast<double*>(q_.ensure(cur.count() * sizeof(double)));
+    CK(cudaMemcpyAsync(core_buf, work, cur.count() * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+    finish_exact(sh, ranks, cur, A, core_buf, U, ref_sumsq, core, factors, rep, t0, &order);
+    return;
+  }
   bool sumsq_known = false;
   {
     std::vector<PreGen> items;

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "comm.hpp"
+#include "eig.hpp"
 #include "kernels.cuh"
 
 namespace tkg {
@@ -51,10 +52,13 @@ struct AlsCfg {
   const double* init = nullptr;  // host I x r col-major
 };
 
+// FactorEngine::Kind (hosvd.hpp:19-27)
+enum EngineKind { kEngineSvd = 0, kEngineEig = 1, kEngineAls = 2 };
+
 struct ModeRep {
   int mode = 0;
   int iterations = 0;
-  int status = 1;
+  int status = 1;  // -1: no ALS report (SVD / EIG engine), ModeReport::als empty
   double achieved_eta = 0.0;
   double seconds = 0.0;
   std::vector<double> history;
@@ -97,11 +101,13 @@ class Engine {
 
   // Decomposition drivers; `a` is host (a_dev false) or device memory.
   // want_sv: rotate each factor onto singular vectors (recover_singular_vectors)
+  // engine: EngineKind (kEngineAls uses cfg)
   void t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
-               const AlsCfg& cfg, double* core, double* factors, DecompRep* rep, bool want_sv = false);
+               const AlsCfg& cfg, double* core, double* factors, DecompRep* rep, bool want_sv = false,
+               int engine = kEngineAls);
   void st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
                 const std::vector<int>* order, const AlsCfg& cfg, double* core, double* factors,
-                DecompRep* rep);
+                DecompRep* rep, int engine = kEngineAls);
   void als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,
                     const AlsCfg& cfg, double* l_out, double* r_out, ModeRep* rep);
   void als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r, uint64_t seed,
@@ -128,6 +134,10 @@ class Engine {
   double relative_error(const double* a, const double* b, uint64_t n);
   void reduced_qr(const double* a, uint64_t rows, uint64_t cols, double* q, double* r);
   void gram(const double* a, uint64_t rows, uint64_t cols, double* out);
+  // mode_gram (tensor_ops.cpp:332-389): out = A_(mode) A_(mode)^T, extent^2 doubles
+  void mode_gram(const double* a, const Shape& sh, int mode, double* out);
+  // sym_eig (kernels.cpp:448-604): g (n x n) -> k leading pairs (values, n x k vectors)
+  void sym_eig(const double* g, uint64_t n, uint64_t k, double* values, double* vectors);
   // recover_singular_vectors (hosvd.cpp:65-72): q (I_mode x cols) -> q V
   void recover_singular_vectors(const double* a, const Shape& sh, int mode, const double* q, uint64_t rows,
                                 uint64_t cols, double* out);
@@ -199,6 +209,13 @@ class Engine {
   // and V^T (r x r, col-major) in vt. Sums the Gram over ranks when dist_.
   void recover_sv(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
+  // SVD / EIG engines: U (device, I x r) <- leading eigenvectors of A_(n) A_(n)^T
+  void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U);
+  double* sumsq_to_host(const double* A, uint64_t n);  // ||A||^2 staged in pinned memory (after sync)
+  void finish_exact(const Shape& sh, const std::vector<uint64_t>& ranks, const Shape& cs, const double* A,
+                    const double* core_buf, const std::vector<double*>& U, const double* ref_sumsq, double* core,
+                    double* factors, DecompRep* rep, std::chrono::steady_clock::time_point t0,
+                    const std::vector<int>* order);
   const double* upload(const double* a, uint64_t n, bool a_dev, DBuf& buf, double* seconds);
   // ref_sumsq_host: pinned ||A||^2, read after the function's own sync
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
@@ -291,6 +308,9 @@ class Engine {
   Comm* dist_ = nullptr;  // set while a sharded driver runs: run_als sums over ranks
   DBuf send_, recv_, reshard_, uslab_, uslab2_, core_t_;
   DBuf sv_u_, sv_g_, sv_vt_, sv_vt0_, sv_ctrl_;
+  DBuf gram_t_, gram_t_part_, gram_w_;
+  SymEig eig_;
+  double* norm_h_ = nullptr;  // pinned
 };
 
 struct ShardRange {

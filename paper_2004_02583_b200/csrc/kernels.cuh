@@ -141,6 +141,26 @@ cudaError_t launch_reduce_partials(const double* part, int nparts, uint32_t rows
 // eigenvalues in that order.
 cudaError_t launch_sym_eig(const double* G, uint32_t r, double* vt, double* evals, cudaStream_t st);
 
+// ---- mode_gram (gram.cu, tensor_ops.cpp:332-389) ------------------------------
+// G = A_(n) A_(n)^T (K x K column-major) from the tensor's natural layout:
+// 64 x 64 upper-triangle blocks x fiber splits on DMMA, partials reduced in a
+// fixed order.
+struct GramPlan {
+  int nb = 0, npairs = 0, nsplit = 0;
+  uint64_t per_split = 0;
+  size_t part_doubles = 0;
+};
+GramPlan gram_tensor_plan(const FiberView& v, int num_sms);
+cudaError_t launch_gram_tensor(const FiberView& v, const GramPlan& p, double* part, double* G, cudaStream_t st);
+
+// sym_eig's output convention (kernels.cpp:584-603) from an ascending
+// eigendecomposition (Z n x n column-major, W ascending): U (n x k) holds the
+// eigenvectors of the k largest eigenvalues in descending order, each column
+// signed so its largest-magnitude entry (first on ties) is positive
+// (fix_column_signs, kernels.cpp:25-43); vals (nullable) the eigenvalues.
+cudaError_t launch_leading_vectors(const double* Z, const double* W, uint32_t n, uint32_t k, double* U,
+                                   double* vals, cudaStream_t st);
+
 // ---- sharded decomposition (smallla.cu) -------------------------------------
 cudaError_t launch_add(double* dst, const double* src, size_t n, cudaStream_t st);
 // part[0][i][c] = sum over the nparts FR partials [k][I][ldp] (c < r), in place.

@@ -111,6 +111,16 @@ class FactorEngine:
     def with_als(cfg: AlsConfig) -> "FactorEngine":
         return FactorEngine("als", cfg)
 
+    @staticmethod
+    def svd() -> "FactorEngine":
+        """hosvd.hpp:24: leading left singular vectors of the unfolding."""
+        return FactorEngine("svd")
+
+    @staticmethod
+    def eig() -> "FactorEngine":
+        """hosvd.hpp:25: leading eigenvectors of the mode Gram matrix."""
+        return FactorEngine("eig")
+
 
 @dataclass
 class Truncation:
@@ -181,6 +191,8 @@ def _flat_ptr(a: np.ndarray):
 
 
 def _mode_report(m: _lib.TkgModeReport) -> ModeReport:
+    if m.status < 0:  # SVD / EIG engine: ModeReport::als is empty (hosvd.hpp:33-37)
+        return ModeReport(m.mode, m.seconds, None)
     hist = [m.residual_history[k] for k in range(m.history_len)]
     als = AlsReport(m.iterations, hist, "converged" if m.status == 0 else "max_iters_reached",
                     m.achieved_eta)
@@ -192,6 +204,12 @@ def _decomp_report(r: _lib.TkgReport) -> DecompositionReport:
                                r.relative_residual, r.seconds, r.h2d_seconds, r.d2h_seconds,
                                r.residual_seconds, int(r.kernel_launches), int(r.tensor_passes),
                                int(r.algorithmic_bytes))
+
+
+def _engine(e: "FactorEngine", keep):
+    if e.kind not in _lib.ENGINE_KINDS:
+        raise UnsupportedError(f"unknown factor engine kind {e.kind!r}")
+    return _lib.TkgFactorEngine(_lib.ENGINE_KINDS[e.kind], _cfg(e.als, keep))
 
 
 def _cfg(c: AlsConfig, keep):
@@ -246,10 +264,10 @@ class Context:
         rep = _lib.TkgReport()
         err = _lib.TkgError()
         hold = []
-        cfg = _cfg(engine.als, hold)
-        rc = self._l.tkg_t_hosvd(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks),
-                                 C.byref(cfg), int(bool(want_singular_vectors)), _flat_ptr(core),
-                                 _flat_ptr(fac), C.byref(rep), C.byref(err))
+        eng = _engine(engine, hold)
+        rc = self._l.tkg_t_hosvd_engine(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks),
+                                        C.byref(eng), int(bool(want_singular_vectors)), _flat_ptr(core),
+                                        _flat_ptr(fac), C.byref(rep), C.byref(err))
         _raise(rc, err)
         return self._tucker(core, fac, dims, ranks), _decomp_report(rep)
 
@@ -264,15 +282,15 @@ class Context:
         rep = _lib.TkgReport()
         err = _lib.TkgError()
         hold = []
-        cfg = _cfg(engine.als, hold)
+        eng = _engine(engine, hold)
         mo = None
         if order is not None:
             if len(order.order) != n:
                 raise InvalidModeError(f"st_hosvd: order has {len(order.order)} entries for an order-{n} tensor")
             mo = _lib.u32([max(0, int(m)) for m in order.order])
-        rc = self._l.tkg_st_hosvd(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks), mo,
-                                  C.byref(cfg), _flat_ptr(core), _flat_ptr(fac), C.byref(rep),
-                                  C.byref(err))
+        rc = self._l.tkg_st_hosvd_engine(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks), mo,
+                                         C.byref(eng), _flat_ptr(core), _flat_ptr(fac), C.byref(rep),
+                                         C.byref(err))
         _raise(rc, err)
         return self._tucker(core, fac, dims, ranks), _decomp_report(rep)
 
@@ -393,6 +411,29 @@ class Context:
                                 C.byref(err)), err)
         return g
 
+    def mode_gram(self, t, mode: int):
+        """tensor_ops.cpp:332-389: A_(mode) A_(mode)^T."""
+        a = _host(t)
+        ext = a.shape[mode - 1] if 1 <= mode <= a.ndim else 1
+        out = np.zeros((ext, ext), order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_mode_gram(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape), int(mode),
+                                     _flat_ptr(out), C.byref(err)), err)
+        return out
+
+    def sym_eig(self, g, k: int):
+        """kernels.cpp:448-604: the k leading eigenpairs, descending (values, n x k vectors)."""
+        g = _host(g)
+        n = g.shape[0]
+        if g.ndim != 2 or g.shape[1] != n:
+            raise DimensionMismatchError(f"sym_eig: matrix is {g.shape[0]}x{g.shape[1] if g.ndim > 1 else 1}")
+        vals = np.zeros(int(k))
+        vecs = np.zeros((n, int(k)), order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_sym_eig(self._ctx, _flat_ptr(g), n, int(k), _flat_ptr(vals), _flat_ptr(vecs),
+                                   C.byref(err)), err)
+        return vals, vecs
+
     def recover_singular_vectors(self, t, mode: int, q):
         """hosvd.cpp:65-72: q (I_mode x r, orthonormal) -> q V, V the left
         singular vectors of q^T A_(mode) (descending, dense_svd's signs)."""
@@ -499,6 +540,14 @@ def reduced_qr(a):
 
 def gram(a):
     return default_context().gram(a)
+
+
+def mode_gram(t, mode):
+    return default_context().mode_gram(t, mode)
+
+
+def sym_eig(g, k):
+    return default_context().sym_eig(g, k)
 
 
 def recover_singular_vectors(t, mode, q):

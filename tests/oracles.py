@@ -309,6 +309,47 @@ class Ref:
                                        list(hist[p, :min(its, 64)]), float(secs[p])))
         return HosvdResult(core, factors, per_mode, float(relres), float(seconds))
 
+    def hosvd_exact(self, t, ranks, kind, sequential=False, order=None):
+        """t_hosvd / st_hosvd with FactorEngine::svd() (kind "svd") or ::eig() ("eig")."""
+        t = fortran(t)
+        n = t.ndim
+        core = np.zeros(ranks, order="F")
+        total = sum(int(t.shape[k]) * int(ranks[k]) for k in range(n))
+        fac = np.zeros(total)
+        rep = (C.c_char * self.lib.ref_report_size())()
+        mo = (C.c_uint32 * n)(*order) if order is not None else None
+        self._check(self.lib.ref_hosvd_exact(
+            C.c_int(1 if sequential else 0), C.c_int(0 if kind == "svd" else 1), _d(flat(t)), C.c_int(n),
+            _u64(t.shape), _u64(ranks), mo, _d(core), _d(fac), rep, *self._e()))
+        raw = bytes(rep)
+        f64 = np.frombuffer(raw, dtype=np.float64, offset=768)
+        i32 = np.frombuffer(raw, dtype=np.int32, count=192)
+        factors = []
+        ofs = 0
+        for k in range(n):
+            sz = int(t.shape[k]) * int(ranks[k])
+            factors.append(fac[ofs:ofs + sz].reshape((t.shape[k], ranks[k]), order="F"))
+            ofs += sz
+        per_mode = [ModeRecord(int(i32[p]), 0, -1, 0.0) for p in range(n)]
+        return HosvdResult(core, factors, per_mode, float(f64[128 + 4097]), float(f64[128 + 4096]))
+
+    def mode_gram(self, t, mode):
+        t = fortran(t)
+        ext = _ext(t, mode)
+        out = np.zeros((ext, ext), order="F")
+        self._check(self.lib.ref_mode_gram(_d(flat(t)), C.c_int(t.ndim), _u64(t.shape), C.c_uint32(mode),
+                                           _d(out), *self._e()))
+        return out
+
+    def sym_eig(self, g, k):
+        g = fortran(g)
+        n = g.shape[0]
+        vals = np.zeros(k)
+        vecs = np.zeros((n, k), order="F")
+        self._check(self.lib.ref_sym_eig(_d(flat(g)), C.c_uint64(n), C.c_uint64(k), _d(vals), _d(vecs),
+                                         *self._e()))
+        return vals, vecs
+
     def reconstruct(self, core, factors, dims):
         core = fortran(core)
         ranks = core.shape
