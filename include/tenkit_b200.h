@@ -21,6 +21,7 @@
  *                                   src/hosvd.cpp:65-72
  *   tkg_t_hosvd_engine / tkg_st_hosvd_engine <- t_hosvd / st_hosvd with any FactorEngine
  *                                   (kSvd, kEig, kAls; hosvd.hpp:19-27, hosvd.cpp:89-110, 150-182)
+ *   tkg_hooi           <- tenkit::hooi           include/tenkit/hooi.hpp:33-37, src/hooi.cpp:53-110
  *   tkg_mode_gram      <- tenkit::mode_gram      include/tenkit/tensor_ops.hpp, src/tensor_ops.cpp:332-389
  *   tkg_sym_eig        <- tenkit::sym_eig        include/tenkit/kernels.hpp:51, src/kernels.cpp:448-604
  *
@@ -148,6 +149,15 @@ int tkg_t_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t o
 int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
                         const uint64_t* ranks, const uint32_t* mode_order, const tkg_factor_engine* engine,
                         double* core, double* factors, tkg_report* report, tkg_error* err);
+
+/* hooi (HooiConfig{tol, max_iters}, hooi.hpp:15-18) from a warm start:
+ * init_core prod R_n doubles, init_factors concatenated I_n x R_n (host).
+ * Results: core, factors, *iterations, *converged, and fit_history[0 ..
+ * iterations] (capacity max(1, max_iters) + 1; [0] = the warm start's fit). */
+int tkg_hooi(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+             const uint64_t* ranks, const double* init_core, const double* init_factors, double tol,
+             int32_t max_iters, double* core, double* factors, int32_t* iterations, int32_t* converged,
+             double* fit_history, tkg_error* err);
 
 /* ---- Sharded decomposition (one context per GPU, tensor split along its
  * last mode; BASELINE north star). The reference is single-process; these

@@ -20,6 +20,7 @@
 
 #include "tenkit/als.hpp"
 #include "tenkit/errors.hpp"
+#include "tenkit/hooi.hpp"
 #include "tenkit/hosvd.hpp"
 #include "tenkit/kernels.hpp"
 #include "tenkit/matrix.hpp"
@@ -358,6 +359,37 @@ int ref_hosvd_exact(int sequential, int kind, const double* a, int order,
       p += u.values().size();
     }
     fill_report(res.second, static_cast<RefReport*>(report));
+  });
+}
+
+// hooi (hooi.cpp:53-110) from a warm start (core prod R_n, factors
+// concatenated I_n x R_n); fit_history capacity max(1, max_iters) + 1.
+int ref_hooi(const double* a, int order, const uint64_t* dims, const uint64_t* ranks,
+             const double* init_core, const double* init_factors, double tol, int max_iters,
+             double* core_out, double* factors_out, int* iterations, int* converged,
+             double* fit_history, int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    DenseTensor t = make_tensor(a, order, dims);
+    Truncation tr{std::vector<std::size_t>(ranks, ranks + order)};
+    TuckerTensor init{make_tensor(init_core, order, ranks), {}, t.shape()};
+    const double* p = init_factors;
+    for (int n = 0; n < order; ++n) {
+      init.factors.push_back(make_matrix(p, dims[n], ranks[n]));
+      p += dims[n] * ranks[n];
+    }
+    HooiConfig cfg;
+    cfg.tol = tol;
+    cfg.max_iters = max_iters;
+    HooiResult res = hooi(t, tr, init, cfg);
+    copy_out(res.tucker.core, core_out);
+    double* q = factors_out;
+    for (const Matrix& u : res.tucker.factors) {
+      std::copy(u.values().begin(), u.values().end(), q);
+      q += u.values().size();
+    }
+    *iterations = res.iterations;
+    *converged = res.converged ? 1 : 0;
+    std::copy(res.fit_history.begin(), res.fit_history.end(), fit_history);
   });
 }
 

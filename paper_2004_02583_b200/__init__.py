@@ -4,11 +4,11 @@ The product is libtenkit_b200.so (CUDA sm_100a kernels + C++ engine behind
 the C-ABI in include/tenkit_b200.h); this package is its Python binding.
 """
 from .tenkit import (AlsConfig, AlsReport, Context, DecompositionReport, DegenerateInitError,
-                     DeviceError, DeviceTensor, DimensionMismatchError, Error, FactorEngine,
+                     DeviceError, DeviceTensor, HooiConfig, HooiResult, DimensionMismatchError, Error, FactorEngine,
                      FormatError, InvalidModeError, IoError, ModeOrder, ModeReport,
                      NoConvergenceError, RankTooLargeError, SingularGramError, Truncation,
                      TuckerTensor, UnsupportedError, ZeroReferenceError, als_init, als_low_rank,
-                     default_context, frobenius_norm, gram, mode_gram, mode_n_product, recover_singular_vectors,
+                     default_context, frobenius_norm, gram, hooi, mode_gram, mode_n_product, recover_singular_vectors,
                      reduced_qr, sym_eig,
                      relative_error, select_order, st_hosvd, synth_tucker, synth_tucker_slab, t_hosvd, unfold_t_times,
                      unfold_times)

@@ -76,6 +76,9 @@ SIGNATURES = [
     ("tkg_st_hosvd_engine", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, _u64p, _u32p,
                                       C.POINTER(TkgFactorEngine), _dp, _dp, C.POINTER(TkgReport),
                                       C.POINTER(TkgError)]),
+    ("tkg_hooi", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, _u64p, _dp, _dp, C.c_double,
+                           C.c_int32, _dp, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _dp,
+                           C.POINTER(TkgError)]),
     ("tkg_mode_gram", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.POINTER(TkgError)]),
     ("tkg_sym_eig", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_select_order", C.c_int, [C.c_int32, _u64p, _u64p, _u32p, C.POINTER(TkgError)]),

@@ -190,6 +190,25 @@ int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t 
   });
 }
 
+int tkg_hooi(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
+             const uint64_t* ranks, const double* init_core, const double* init_factors, double tol,
+             int32_t max_iters, double* core, double* factors, int32_t* iterations, int32_t* converged,
+             double* fit_history, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<uint64_t> rk(ranks, ranks + order);
+    if (!init_core || !init_factors) tkg::raise(TKG_E_DIMENSION_MISMATCH, "hooi: init is not an order-" +
+                                                                                  std::to_string(order) +
+                                                                                  " decomposition");
+    tkg::HooiRep rep;
+    eng(ctx).hooi(a, a_on_device != 0, sh, rk, init_core, init_factors, tol, max_iters, core, factors, &rep);
+    if (iterations) *iterations = rep.iterations;
+    if (converged) *converged = rep.converged ? 1 : 0;
+    if (fit_history)
+      for (size_t k = 0; k < rep.fit_history.size(); ++k) fit_history[k] = rep.fit_history[k];
+  });
+}
+
 int tkg_mode_gram(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode, double* out,
                   tkg_error* err) {
   return guarded(err, [&] {

@@ -906,6 +906,120 @@ void Engine::sym_eig(const double* g, uint64_t n, uint64_t k, double* values, do
   sync();
 }
 
+// ---- HOOI (hooi.cpp:53-110) --------------------------------------------------------
+void Engine::ttm_mode(const double* X, const Shape& sh, int mode, const double* U, uint32_t r, double* out) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
+  const uint32_t ncp = pad_nc(r);
+  double* Mt = mt_.d(I * ncp);
+  CK(launch_pack(U, 1, I, uint32_t(I), r, Mt, ncp, st_));  // Mt[i][c] = U[i + c*I]
+  count_launch();
+  FiberView v{X, s, P, uint32_t(I), s, s * I};
+  fc(v, Mt, ncp, r, out, 1, s, s * r, nullptr, nullptr, nullptr, false);
+}
+
+Shape Engine::ttm_others(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                         const std::vector<double*>& U, int skip, double* dst) {
+  Shape cur = sh;
+  const double* src = A;
+  DBuf* bufs[2] = {&work_a_, &work_b_};
+  int which = 0;
+  int last = sh.N;
+  while (last >= 1 && last == skip) --last;
+  if (last < 1) {  // order 1: nothing to contract
+    CK(cudaMemcpyAsync(dst, A, sh.count() * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+    return cur;
+  }
+  for (int m = 1; m <= sh.N; ++m) {
+    if (m == skip) continue;
+    Shape nxt = cur;
+    nxt.d[m - 1] = ranks[m - 1];
+    double* out = (m == last) ? dst : bufs[which]->d(nxt.count());
+    ttm_mode(src, cur, m, U[m - 1], uint32_t(ranks[m - 1]), out);
+    src = out;
+    cur = nxt;
+    which ^= 1;
+  }
+  return cur;
+}
+
+// Per outer iteration and mode (ascending): contract the tensor with every
+// other factor transposed, replace U_n by the leading R_n left singular
+// vectors of that shrunk tensor's unfolding (dense_svd, hooi.cpp:89-94: here
+// the eigenvectors of its Gram matrix W W^T, the same vectors with the same
+// order and signs, gram_factor), and after the last mode form the core from
+// the last shrunk tensor (:95-98). The fit is the explicit one,
+// 1 - ||t - reconstruct|| / ||t|| (:47-49, the fused expansion-difference
+// pass), and the loop stops at |fit_k - fit_{k-1}| <= tol (:104-108).
+void Engine::hooi(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
+                  const double* init_core, const double* init_factors, double tol, int max_iters, double* core,
+                  double* factors, HooiRep* rep) {
+  validate_truncation(sh, ranks);
+  const int N = sh.N;
+  for (int n = 1; n <= N; ++n) {
+    uint64_t other = 1;
+    for (int m = 1; m <= N; ++m)
+      if (m != n) other *= ranks[m - 1];
+    if (ranks[n - 1] > other)
+      raise(4, "hooi: mode " + std::to_string(n) + " rank " + std::to_string(ranks[n - 1]) +
+                   " exceeds the product of the other ranks (" + std::to_string(other) + ")");
+  }
+  *rep = HooiRep();
+  const double* A = upload(a, sh.count(), a_dev, tensor_, nullptr);
+  while (factor_bufs_.size() < size_t(N)) factor_bufs_.push_back(new DBuf());
+  std::vector<double*> U(N);
+  Shape cs;
+  cs.N = N;
+  for (int k = 0; k < N; ++k) cs.d[k] = ranks[k];
+  begin_timed();
+  const auto t0 = Clock::now();
+  const double* ref_sumsq = sumsq_to_host(A, sh.count());
+  sync();
+  if (*ref_sumsq == 0.0) raise(3, "hooi: input tensor has zero norm");
+  size_t ofs = 0;
+  for (int n = 0; n < N; ++n) {
+    U[n] = factor_bufs_[n]->d(sh.d[n] * ranks[n]);
+    CK(cudaMemcpyAsync(U[n], init_factors + ofs, sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyHostToDevice,
+                       st_));
+    ofs += sh.d[n] * ranks[n];
+  }
+  double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
+  CK(cudaMemcpyAsync(core_buf, init_core, cs.count() * sizeof(double), cudaMemcpyHostToDevice, st_));
+  rep->fit_history.push_back(1.0 - relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq));
+  uint64_t smax = 0;
+  for (int n = 1; n <= N; ++n) {
+    uint64_t c = sh.d[n - 1];
+    for (int m = 1; m <= N; ++m)
+      if (m != n) c *= ranks[m - 1];
+    smax = std::max(smax, c);
+  }
+  double* shr = hooi_s_.d(std::max<uint64_t>(smax, 1));
+  const int iters = std::max(1, max_iters);
+  for (int iter = 1; iter <= iters; ++iter) {
+    for (int n = 1; n <= N; ++n) {
+      const Shape S = ttm_others(A, sh, ranks, U, n, shr);
+      gram_factor(shr, S, n, uint32_t(ranks[n - 1]), U[n - 1]);
+      if (n == N) ttm_mode(shr, S, N, U[N - 1], uint32_t(ranks[N - 1]), core_buf);
+    }
+    rep->iterations = iter;
+    const double fit = 1.0 - relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+    const double prev = rep->fit_history.back();
+    rep->fit_history.push_back(fit);
+    if (std::fabs(fit - prev) <= tol) {
+      rep->converged = true;
+      break;
+    }
+  }
+  rep->seconds = since(t0);
+  rep->launches = launches_;
+  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  ofs = 0;
+  for (int n = 0; n < N; ++n) {
+    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    ofs += sh.d[n] * ranks[n];
+  }
+  sync();
+}
+
 void Engine::begin_timed() {
   launches_ = 0;
   passes_ = 0;

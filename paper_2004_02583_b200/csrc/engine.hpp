@@ -76,6 +76,15 @@ struct DecompRep {
   uint64_t bytes = 0;
 };
 
+// HooiResult (hooi.hpp:23-31) minus the Tucker tensor (returned in buffers)
+struct HooiRep {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> fit_history;  // [0] = the warm start's fit
+  double seconds = 0.0;
+  uint64_t launches = 0;
+};
+
 class DBuf {
  public:
   DBuf() = default;
@@ -134,6 +143,11 @@ class Engine {
   double relative_error(const double* a, const double* b, uint64_t n);
   void reduced_qr(const double* a, uint64_t rows, uint64_t cols, double* q, double* r);
   void gram(const double* a, uint64_t rows, uint64_t cols, double* out);
+  // hooi (hooi.cpp:53-110) from a warm start (init_core prod R_n, init_factors
+  // concatenated I_n x R_n, host); results into core / factors (host).
+  void hooi(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
+            const double* init_core, const double* init_factors, double tol, int max_iters, double* core,
+            double* factors, HooiRep* rep);
   // mode_gram (tensor_ops.cpp:332-389): out = A_(mode) A_(mode)^T, extent^2 doubles
   void mode_gram(const double* a, const Shape& sh, int mode, double* out);
   // sym_eig (kernels.cpp:448-604): g (n x n) -> k leading pairs (values, n x k vectors)
@@ -211,6 +225,12 @@ class Engine {
   void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   // SVD / EIG engines: U (device, I x r) <- leading eigenvectors of A_(n) A_(n)^T
   void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U);
+  // dst <- A x_m U_m^T for every m != skip, ascending (multi_mode_product with
+  // the other factors, hooi.cpp:82-88); returns dst's shape
+  Shape ttm_others(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                   const std::vector<double*>& U, int skip, double* dst);
+  // out <- X x_mode U^T (U: I x r device col-major), tensor layout
+  void ttm_mode(const double* X, const Shape& sh, int mode, const double* U, uint32_t r, double* out);
   double* sumsq_to_host(const double* A, uint64_t n);  // ||A||^2 staged in pinned memory (after sync)
   void finish_exact(const Shape& sh, const std::vector<uint64_t>& ranks, const Shape& cs, const double* A,
                     const double* core_buf, const std::vector<double*>& U, const double* ref_sumsq, double* core,
@@ -308,7 +328,7 @@ class Engine {
   Comm* dist_ = nullptr;  // set while a sharded driver runs: run_als sums over ranks
   DBuf send_, recv_, reshard_, uslab_, uslab2_, core_t_;
   DBuf sv_u_, sv_g_, sv_vt_, sv_vt0_, sv_ctrl_;
-  DBuf gram_t_, gram_t_part_, gram_w_;
+  DBuf gram_t_, gram_t_part_, gram_w_, hooi_s_;
   SymEig eig_;
   double* norm_h_ = nullptr;  // pinned
 };

@@ -162,6 +162,23 @@ class DecompositionReport:
 
 
 @dataclass
+class HooiConfig:
+    """hooi.hpp:15-18."""
+    tol: float = 1e-12
+    max_iters: int = 100
+
+
+@dataclass
+class HooiResult:
+    """hooi.hpp:20-31 (fit_history[0] = the warm start's fit)."""
+    tucker: "TuckerTensor"
+    iterations: int = 0
+    fit_history: List[float] = field(default_factory=list)
+    converged: bool = False
+    seconds: float = 0.0
+
+
+@dataclass
 class TuckerTensor:
     core: np.ndarray
     factors: List[np.ndarray]
@@ -411,6 +428,38 @@ class Context:
                                 C.byref(err)), err)
         return g
 
+    def hooi(self, t, trunc: Truncation, init: "TuckerTensor", cfg: HooiConfig = None) -> HooiResult:
+        """hooi.cpp:53-110: refine a conformal warm start (check_conformal :17-40)."""
+        cfg = cfg or HooiConfig()
+        ptr, on_dev, dims, keep = self._tensor(t)
+        ranks = list(trunc.ranks)
+        n = len(dims)
+        if len(ranks) != n:
+            raise DimensionMismatchError(f"truncation lists {len(ranks)} ranks for an order-{n} tensor")
+        origin = tuple(int(x) for x in (init.origin_shape if init.origin_shape is not None else ()))
+        if origin != tuple(dims):
+            raise DimensionMismatchError(f"hooi: init origin shape {origin} does not match tensor {tuple(dims)}")
+        core0 = np.asarray(init.core)
+        if len(init.factors) != n or core0.ndim != n:
+            raise DimensionMismatchError(f"hooi: init is not an order-{n} decomposition")
+        for mode in range(1, n + 1):
+            u = np.asarray(init.factors[mode - 1])
+            if u.shape != (dims[mode - 1], ranks[mode - 1]) or core0.shape[mode - 1] != ranks[mode - 1]:
+                raise DimensionMismatchError(f"hooi: init factor for mode {mode} does not match the truncation")
+        c_in = np.ascontiguousarray(core0.reshape(-1, order="F"), dtype=np.float64)
+        f_in = np.concatenate([np.asarray(u, dtype=np.float64).reshape(-1, order="F") for u in init.factors])
+        core = np.zeros(int(np.prod(ranks)))
+        fac = np.zeros(sum(int(dims[k]) * int(ranks[k]) for k in range(n)))
+        fits = np.zeros(max(1, int(cfg.max_iters)) + 1)
+        iters, conv = C.c_int32(0), C.c_int32(0)
+        err = _lib.TkgError()
+        _raise(self._l.tkg_hooi(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks), _flat_ptr(c_in),
+                                _flat_ptr(f_in), float(cfg.tol), int(cfg.max_iters), _flat_ptr(core),
+                                _flat_ptr(fac), C.byref(iters), C.byref(conv), _flat_ptr(fits),
+                                C.byref(err)), err)
+        return HooiResult(self._tucker(core, fac, dims, ranks), int(iters.value),
+                          list(fits[: iters.value + 1]), bool(conv.value))
+
     def mode_gram(self, t, mode: int):
         """tensor_ops.cpp:332-389: A_(mode) A_(mode)^T."""
         a = _host(t)
@@ -540,6 +589,10 @@ def reduced_qr(a):
 
 def gram(a):
     return default_context().gram(a)
+
+
+def hooi(t, trunc, init, cfg=None):
+    return default_context().hooi(t, trunc, init, cfg)
 
 
 def mode_gram(t, mode):

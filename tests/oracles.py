@@ -333,6 +333,26 @@ class Ref:
         per_mode = [ModeRecord(int(i32[p]), 0, -1, 0.0) for p in range(n)]
         return HosvdResult(core, factors, per_mode, float(f64[128 + 4097]), float(f64[128 + 4096]))
 
+    def hooi(self, t, ranks, init_core, init_factors, tol=1e-12, max_iters=100):
+        """hooi.cpp:53-110; returns (core, factors, iterations, converged, fit_history)."""
+        t = fortran(t)
+        n = t.ndim
+        core = np.zeros(ranks, order="F")
+        fac = np.zeros(sum(int(t.shape[k]) * int(ranks[k]) for k in range(n)))
+        f_in = np.concatenate([flat(u) for u in init_factors])
+        fits = np.zeros(max(1, max_iters) + 1)
+        it, cv = C.c_int(0), C.c_int(0)
+        self._check(self.lib.ref_hooi(_d(flat(t)), C.c_int(n), _u64(t.shape), _u64(ranks), _d(flat(init_core)),
+                                      _d(f_in), C.c_double(tol), C.c_int(max_iters), _d(core), _d(fac),
+                                      C.byref(it), C.byref(cv), _d(fits), *self._e()))
+        factors = []
+        ofs = 0
+        for k in range(n):
+            sz = int(t.shape[k]) * int(ranks[k])
+            factors.append(fac[ofs:ofs + sz].reshape((t.shape[k], ranks[k]), order="F"))
+            ofs += sz
+        return core, factors, int(it.value), bool(cv.value), list(fits[: it.value + 1])
+
     def mode_gram(self, t, mode):
         t = fortran(t)
         ext = _ext(t, mode)
