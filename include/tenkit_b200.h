@@ -22,6 +22,8 @@
  *   tkg_t_hosvd_engine / tkg_st_hosvd_engine <- t_hosvd / st_hosvd with any FactorEngine
  *                                   (kSvd, kEig, kAls; hosvd.hpp:19-27, hosvd.cpp:89-110, 150-182)
  *   tkg_hooi           <- tenkit::hooi           include/tenkit/hooi.hpp:33-37, src/hooi.cpp:53-110
+ *   tkg_read_tnsr / tkg_write_tnsr / tkg_write_tukr <- read_tnsr / write_tnsr / write_tukr
+ *                                   include/tenkit/io.hpp, src/io.cpp:131-193
  *   tkg_mode_gram      <- tenkit::mode_gram      include/tenkit/tensor_ops.hpp, src/tensor_ops.cpp:332-389
  *   tkg_sym_eig        <- tenkit::sym_eig        include/tenkit/kernels.hpp:51, src/kernels.cpp:448-604
  *
@@ -153,11 +155,20 @@ int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t 
 /* hooi (HooiConfig{tol, max_iters}, hooi.hpp:15-18) from a warm start:
  * init_core prod R_n doubles, init_factors concatenated I_n x R_n (host).
  * Results: core, factors, *iterations, *converged, and fit_history[0 ..
- * iterations] (capacity max(1, max_iters) + 1; [0] = the warm start's fit). */
+ * iterations] (capacity max(1, max_iters) + 1; [0] = the warm start's fit),
+ * *relative_residual (nullable) of the returned decomposition. */
 int tkg_hooi(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
              const uint64_t* ranks, const double* init_core, const double* init_factors, double tol,
              int32_t max_iters, double* core, double* factors, int32_t* iterations, int32_t* converged,
-             double* fit_history, tkg_error* err);
+             double* fit_history, double* relative_residual, tkg_error* err);
+
+/* Device memory on the context's device, for FFI callers without a CUDA
+ * runtime of their own (e.g. a TNSR loaded with tkg_read_tnsr and decomposed
+ * with a_on_device = 1). tkg_device_copy: any direction (cudaMemcpyDefault),
+ * synchronous on the context's stream. */
+int tkg_device_alloc(tkg_ctx* ctx, uint64_t bytes, void** out, tkg_error* err);
+int tkg_device_free(tkg_ctx* ctx, void* p);
+int tkg_device_copy(tkg_ctx* ctx, void* dst, const void* src, uint64_t bytes, tkg_error* err);
 
 /* ---- Sharded decomposition (one context per GPU, tensor split along its
  * last mode; BASELINE north star). The reference is single-process; these
@@ -222,6 +233,18 @@ int tkg_reduced_qr(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, 
                    double* r, tkg_error* err);
 int tkg_gram(tkg_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* out,
              tkg_error* err);
+/* TNSR / TUKR files (io.cpp:131-224; little-endian, version 1). The shape
+ * first (dims: TKG_MAX_ORDER entries), then the payload straight into dst:
+ * a device buffer is filled through double-buffered pinned chunks whose H2D
+ * copies overlap the file reads (dst_on_device = 1), or a host buffer.
+ * Errors: IoError / FormatError with the reference's messages (category io). */
+int tkg_read_tnsr_shape(const char* path, int32_t* order, uint64_t* dims, tkg_error* err);
+int tkg_read_tnsr(tkg_ctx* ctx, const char* path, double* dst, int dst_on_device, tkg_error* err);
+int tkg_write_tnsr(const char* path, int32_t order, const uint64_t* dims, const double* data, tkg_error* err);
+/* core prod ranks doubles, factors concatenated dims[n] x ranks[n] (host). */
+int tkg_write_tukr(const char* path, int32_t order, const uint64_t* dims, const uint64_t* ranks, const double* core,
+                   const double* factors, tkg_error* err);
+
 /* mode_gram: out = A_(mode) A_(mode)^T (extent x extent, column-major). */
 int tkg_mode_gram(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode, double* out,
                   tkg_error* err);

@@ -21,6 +21,7 @@
 #include "tenkit/als.hpp"
 #include "tenkit/errors.hpp"
 #include "tenkit/hooi.hpp"
+#include "tenkit/io.hpp"
 #include "tenkit/hosvd.hpp"
 #include "tenkit/kernels.hpp"
 #include "tenkit/matrix.hpp"
@@ -390,6 +391,45 @@ int ref_hooi(const double* a, int order, const uint64_t* dims, const uint64_t* r
     *iterations = res.iterations;
     *converged = res.converged ? 1 : 0;
     std::copy(res.fit_history.begin(), res.fit_history.end(), fit_history);
+  });
+}
+
+// read_tnsr / write_tnsr / read_tukr (io.cpp:131-224): format pins.
+int ref_write_tnsr(const char* path, const double* a, int order, const uint64_t* dims,
+                   int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] { write_tnsr(std::string(path), make_tensor(a, order, dims)); });
+}
+
+int ref_read_tnsr(const char* path, int* order, uint64_t* dims, double* out, uint64_t cap,
+                  int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    DenseTensor t = read_tnsr(std::string(path));
+    *order = static_cast<int>(t.shape().order());
+    for (std::size_t k = 1; k <= t.shape().order(); ++k) dims[k - 1] = t.shape().extent(k);
+    if (out && t.size() <= cap) copy_out(t, out);
+  });
+}
+
+// core (prod ranks) then factors concatenated; ranks read from the file.
+int ref_read_tukr(const char* path, int* order, uint64_t* dims, uint64_t* ranks, double* core,
+                  double* factors, uint64_t cap, int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    TuckerTensor tk = read_tukr(std::string(path));
+    const std::size_t n = tk.origin_shape.order();
+    *order = static_cast<int>(n);
+    uint64_t need = tk.core.size();
+    for (std::size_t k = 1; k <= n; ++k) {
+      dims[k - 1] = tk.origin_shape.extent(k);
+      ranks[k - 1] = tk.core.shape().extent(k);
+      need += dims[k - 1] * ranks[k - 1];
+    }
+    if (!core || need > cap) return;
+    copy_out(tk.core, core);
+    double* p = factors;
+    for (const Matrix& u : tk.factors) {
+      std::copy(u.values().begin(), u.values().end(), p);
+      p += u.values().size();
+    }
   });
 }
 

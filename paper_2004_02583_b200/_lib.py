@@ -77,8 +77,15 @@ SIGNATURES = [
                                       C.POINTER(TkgFactorEngine), _dp, _dp, C.POINTER(TkgReport),
                                       C.POINTER(TkgError)]),
     ("tkg_hooi", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, _u64p, _dp, _dp, C.c_double,
-                           C.c_int32, _dp, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _dp,
+                           C.c_int32, _dp, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _dp, _dp,
                            C.POINTER(TkgError)]),
+    ("tkg_device_alloc", C.c_int, [_ctxp, C.c_uint64, C.POINTER(C.c_void_p), C.POINTER(TkgError)]),
+    ("tkg_device_free", C.c_int, [_ctxp, C.c_void_p]),
+    ("tkg_device_copy", C.c_int, [_ctxp, C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(TkgError)]),
+    ("tkg_read_tnsr_shape", C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _u64p, C.POINTER(TkgError)]),
+    ("tkg_read_tnsr", C.c_int, [_ctxp, C.c_char_p, C.c_void_p, C.c_int, C.POINTER(TkgError)]),
+    ("tkg_write_tnsr", C.c_int, [C.c_char_p, C.c_int32, _u64p, _dp, C.POINTER(TkgError)]),
+    ("tkg_write_tukr", C.c_int, [C.c_char_p, C.c_int32, _u64p, _u64p, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_mode_gram", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.POINTER(TkgError)]),
     ("tkg_sym_eig", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_select_order", C.c_int, [C.c_int32, _u64p, _u64p, _u32p, C.POINTER(TkgError)]),

@@ -22,12 +22,13 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libtenkit_b200.so")
 SYNTH = os.path.join(PKG, "libtkg_synth.so")
+CLI = os.path.join(PKG, "tenkit_b200")
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 GXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else (shutil.which("g++") or "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["contract.cu", "contract_tma.cu", "smallla.cu", "mtrng.cu", "recon.cu", "als_step.cu", "coop.cu",
            "gram.cu"]
-CPP_SRCS = ["engine.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp", "eig.cpp"]
+CPP_SRCS = ["engine.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp", "eig.cpp", "io.cpp"]  # cli.cpp: the executable
 
 
 def _newest(paths):
@@ -51,6 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     deps = _deps()
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest(deps):
+        if not os.path.exists(CLI) or os.path.getmtime(CLI) < os.path.getmtime(LIB):
+            build_cli()
         build_synth(force=False)
         return LIB
     cmds, objs = [], []
@@ -72,8 +75,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-lpthread", "-ldl"])
     os.replace(tmp, LIB)
+    build_cli()
     build_synth(force=True)
     return LIB
+
+
+def build_cli() -> str:
+    """tenkit_b200 (csrc/cli.cpp): the reference CLI's `compress` over the C-ABI."""
+    tmp = CLI + ".tmp"
+    _run([GXX, "-O2", "-std=c++17", "-Wall", "-o", tmp, os.path.join(CSRC, "cli.cpp"), f"-L{PKG}", "-ltenkit_b200",
+          "-Wl,-rpath,$ORIGIN"])
+    os.replace(tmp, CLI)
+    return CLI
 
 
 def build_synth(force: bool = False) -> str:

@@ -2,6 +2,7 @@
 // Engine call, maps tkg::Error onto (return code, subtype, message) exactly
 // like the reference's exception taxonomy (errors.hpp:10-77), and never
 // lets a C++ exception cross the ABI.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -10,6 +11,7 @@
 
 #include "../../include/tenkit_b200.h"
 #include "engine.hpp"
+#include "io.hpp"
 
 struct tkg_ctx {
   tkg::Engine* eng;
@@ -193,7 +195,7 @@ int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t 
 int tkg_hooi(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
              const uint64_t* ranks, const double* init_core, const double* init_factors, double tol,
              int32_t max_iters, double* core, double* factors, int32_t* iterations, int32_t* converged,
-             double* fit_history, tkg_error* err) {
+             double* fit_history, double* relative_residual, tkg_error* err) {
   return guarded(err, [&] {
     tkg::Shape sh = make_shape(order, dims);
     std::vector<uint64_t> rk(ranks, ranks + order);
@@ -206,6 +208,53 @@ int tkg_hooi(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, cons
     if (converged) *converged = rep.converged ? 1 : 0;
     if (fit_history)
       for (size_t k = 0; k < rep.fit_history.size(); ++k) fit_history[k] = rep.fit_history[k];
+    if (relative_residual) *relative_residual = rep.relative_residual;
+  });
+}
+
+int tkg_device_alloc(tkg_ctx* ctx, uint64_t bytes, void** out, tkg_error* err) {
+  return guarded(err, [&] {
+    eng(ctx);
+    *out = nullptr;
+    CK(cudaMalloc(out, std::max<uint64_t>(bytes, 1)));
+  });
+}
+
+int tkg_device_free(tkg_ctx* ctx, void* p) {
+  (void)ctx;
+  return p && cudaFree(p) != cudaSuccess ? 2 : 0;
+}
+
+int tkg_device_copy(tkg_ctx* ctx, void* dst, const void* src, uint64_t bytes, tkg_error* err) {
+  return guarded(err, [&] {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, eng(ctx).stream()));
+    CK(cudaStreamSynchronize(eng(ctx).stream()));
+  });
+}
+
+int tkg_read_tnsr_shape(const char* path, int32_t* order, uint64_t* dims, tkg_error* err) {
+  return guarded(err, [&] {
+    const tkg::Shape sh = tkg::tnsr_shape(path ? path : "");
+    *order = sh.N;
+    for (int k = 0; k < sh.N; ++k) dims[k] = sh.d[k];
+  });
+}
+
+int tkg_read_tnsr(tkg_ctx* ctx, const char* path, double* dst, int dst_on_device, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::tnsr_load(path ? path : "", dst, dst_on_device != 0, eng(ctx).stream());
+  });
+}
+
+int tkg_write_tnsr(const char* path, int32_t order, const uint64_t* dims, const double* data, tkg_error* err) {
+  return guarded(err, [&] { tkg::tnsr_write(path ? path : "", make_shape(order, dims), data); });
+}
+
+int tkg_write_tukr(const char* path, int32_t order, const uint64_t* dims, const uint64_t* ranks, const double* core,
+                   const double* factors, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::tukr_write(path ? path : "", make_shape(order, dims), std::vector<uint64_t>(ranks, ranks + order), core,
+                    factors);
   });
 }
 

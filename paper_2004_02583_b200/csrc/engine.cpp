@@ -984,7 +984,8 @@ void Engine::hooi(const double* a, bool a_dev, const Shape& sh, const std::vecto
   }
   double* core_buf = static_cast<double*>(q_.ensure(cs.count() * sizeof(double)));
   CK(cudaMemcpyAsync(core_buf, init_core, cs.count() * sizeof(double), cudaMemcpyHostToDevice, st_));
-  rep->fit_history.push_back(1.0 - relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq));
+  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+  rep->fit_history.push_back(1.0 - rep->relative_residual);
   uint64_t smax = 0;
   for (int n = 1; n <= N; ++n) {
     uint64_t c = sh.d[n - 1];
@@ -1001,7 +1002,8 @@ void Engine::hooi(const double* a, bool a_dev, const Shape& sh, const std::vecto
       if (n == N) ttm_mode(shr, S, N, U[N - 1], uint32_t(ranks[N - 1]), core_buf);
     }
     rep->iterations = iter;
-    const double fit = 1.0 - relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+    rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
+    const double fit = 1.0 - rep->relative_residual;
     const double prev = rep->fit_history.back();
     rep->fit_history.push_back(fit);
     if (std::fabs(fit - prev) <= tol) {

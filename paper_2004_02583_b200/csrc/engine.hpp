@@ -81,6 +81,7 @@ struct HooiRep {
   int iterations = 0;
   bool converged = false;
   std::vector<double> fit_history;  // [0] = the warm start's fit
+  double relative_residual = 0.0;   // of the returned decomposition (1 - fit, unrounded)
   double seconds = 0.0;
   uint64_t launches = 0;
 };
@@ -166,6 +167,7 @@ class Engine {
   void flush_l2();
   void kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], double flops[4]);
   const std::string& device_name() const { return name_; }
+  cudaStream_t stream() const { return st_; }
 
  private:
   struct AlsOut {

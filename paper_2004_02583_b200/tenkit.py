@@ -15,6 +15,7 @@ through libtenkit_b200.so; there is no CPU implementation behind it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -175,7 +176,7 @@ class HooiResult:
     iterations: int = 0
     fit_history: List[float] = field(default_factory=list)
     converged: bool = False
-    seconds: float = 0.0
+    relative_residual: float = 0.0
 
 
 @dataclass
@@ -183,6 +184,22 @@ class TuckerTensor:
     core: np.ndarray
     factors: List[np.ndarray]
     origin_shape: tuple
+
+
+class OwnedDeviceTensor:
+    """A DeviceTensor whose HBM buffer belongs to the library (tkg_device_alloc);
+    freed with the object."""
+
+    def __init__(self, ptr: int, dims, ctx):
+        self.ptr, self.dims, self._ctx = ptr, list(dims), ctx
+
+    def __del__(self):
+        try:
+            if self.ptr and self._ctx._ctx:
+                self._ctx._l.tkg_device_free(self._ctx._ctx, C.c_void_p(self.ptr))
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+        self.ptr = 0
 
 
 @dataclass
@@ -261,7 +278,7 @@ class Context:
     # -- input marshalling --------------------------------------------------------
     @staticmethod
     def _tensor(t):
-        if isinstance(t, DeviceTensor):
+        if isinstance(t, (DeviceTensor, OwnedDeviceTensor)):
             return C.c_void_p(t.ptr), 1, tuple(t.dims), None
         a = _host(t)
         if a.ndim == 0:
@@ -451,14 +468,45 @@ class Context:
         core = np.zeros(int(np.prod(ranks)))
         fac = np.zeros(sum(int(dims[k]) * int(ranks[k]) for k in range(n)))
         fits = np.zeros(max(1, int(cfg.max_iters)) + 1)
-        iters, conv = C.c_int32(0), C.c_int32(0)
+        iters, conv, rr = C.c_int32(0), C.c_int32(0), C.c_double(0)
         err = _lib.TkgError()
         _raise(self._l.tkg_hooi(self._ctx, ptr, on_dev, n, _lib.u64(dims), _lib.u64(ranks), _flat_ptr(c_in),
                                 _flat_ptr(f_in), float(cfg.tol), int(cfg.max_iters), _flat_ptr(core),
-                                _flat_ptr(fac), C.byref(iters), C.byref(conv), _flat_ptr(fits),
+                                _flat_ptr(fac), C.byref(iters), C.byref(conv), _flat_ptr(fits), C.byref(rr),
                                 C.byref(err)), err)
         return HooiResult(self._tucker(core, fac, dims, ranks), int(iters.value),
-                          list(fits[: iters.value + 1]), bool(conv.value))
+                          list(fits[: iters.value + 1]), bool(conv.value), relative_residual=rr.value)
+
+    def read_tnsr(self, path: str, device: bool = True):
+        """read_tnsr (io.cpp:150-161). device=True: the payload goes straight
+        into HBM through pinned chunks and a DeviceTensor (owning its buffer)
+        is returned; else a host numpy array."""
+        order, dims = C.c_int32(0), (C.c_uint64 * 16)()
+        err = _lib.TkgError()
+        _raise(self._l.tkg_read_tnsr_shape(os.fsencode(path), C.byref(order), dims, C.byref(err)), err)
+        shape = [int(dims[k]) for k in range(order.value)]
+        n = int(np.prod(shape))
+        if not device:
+            out = np.zeros(shape, order="F")
+            _raise(self._l.tkg_read_tnsr(self._ctx, os.fsencode(path), out.ctypes.data, 0, C.byref(err)), err)
+            return out
+        ptr = C.c_void_p()
+        _raise(self._l.tkg_device_alloc(self._ctx, n * 8, C.byref(ptr), C.byref(err)), err)
+        rc = self._l.tkg_read_tnsr(self._ctx, os.fsencode(path), ptr, 1, C.byref(err))
+        if rc:
+            self._l.tkg_device_free(self._ctx, ptr)
+            _raise(rc, err)
+        return OwnedDeviceTensor(int(ptr.value), shape, self)
+
+    def write_tukr(self, path: str, tucker: "TuckerTensor"):
+        """write_tukr (io.cpp:163-193)."""
+        dims = [int(x) for x in tucker.origin_shape]
+        ranks = list(np.asarray(tucker.core).shape)
+        core = np.ascontiguousarray(np.asarray(tucker.core).reshape(-1, order="F"))
+        fac = np.concatenate([np.asarray(u, dtype=np.float64).reshape(-1, order="F") for u in tucker.factors])
+        err = _lib.TkgError()
+        _raise(self._l.tkg_write_tukr(os.fsencode(path), len(dims), _lib.u64(dims), _lib.u64(ranks),
+                                      _flat_ptr(core), _flat_ptr(fac), C.byref(err)), err)
 
     def mode_gram(self, t, mode: int):
         """tensor_ops.cpp:332-389: A_(mode) A_(mode)^T."""

@@ -353,6 +353,39 @@ class Ref:
             ofs += sz
         return core, factors, int(it.value), bool(cv.value), list(fits[: it.value + 1])
 
+    def write_tnsr(self, path, t):
+        t = fortran(t)
+        self._check(self.lib.ref_write_tnsr(os.fsencode(path), _d(flat(t)), C.c_int(t.ndim), _u64(t.shape),
+                                            *self._e()))
+
+    def read_tnsr(self, path):
+        order, dims = C.c_int(0), (C.c_uint64 * 64)()
+        self._check(self.lib.ref_read_tnsr(os.fsencode(path), C.byref(order), dims, None, C.c_uint64(0),
+                                           *self._e()))
+        shape = [int(dims[k]) for k in range(order.value)]
+        out = np.zeros(int(np.prod(shape)))
+        self._check(self.lib.ref_read_tnsr(os.fsencode(path), C.byref(order), dims, _d(out),
+                                           C.c_uint64(out.size), *self._e()))
+        return out.reshape(shape, order="F")
+
+    def read_tukr(self, path):
+        """(core, factors, origin dims) of a TUKR file read by the reference."""
+        order, dims, ranks = C.c_int(0), (C.c_uint64 * 64)(), (C.c_uint64 * 64)()
+        self._check(self.lib.ref_read_tukr(os.fsencode(path), C.byref(order), dims, ranks, None, None,
+                                           C.c_uint64(0), *self._e()))
+        n = order.value
+        d = [int(dims[k]) for k in range(n)]
+        r = [int(ranks[k]) for k in range(n)]
+        core = np.zeros(int(np.prod(r)))
+        fac = np.zeros(sum(d[k] * r[k] for k in range(n)))
+        self._check(self.lib.ref_read_tukr(os.fsencode(path), C.byref(order), dims, ranks, _d(core), _d(fac),
+                                           C.c_uint64(core.size + fac.size), *self._e()))
+        factors, ofs = [], 0
+        for k in range(n):
+            factors.append(fac[ofs:ofs + d[k] * r[k]].reshape((d[k], r[k]), order="F"))
+            ofs += d[k] * r[k]
+        return core.reshape(r, order="F"), factors, d
+
     def mode_gram(self, t, mode):
         t = fortran(t)
         ext = _ext(t, mode)
