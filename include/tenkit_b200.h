@@ -284,10 +284,12 @@ int tkg_timer_stop(tkg_ctx* ctx, double* ms);
 /* Overwrite a buffer larger than L2 on the context's stream (bench hygiene). */
 int tkg_flush_l2(tkg_ctx* ctx);
 
-/* Diagnostic: time the two contraction kernels of one ALS sweep on a
+/* Diagnostic: time the contraction kernels of one ALS sweep on a
  * device-resident tensor (d_a) along `mode` with r columns, `reps` times each
- * (CUDA events). out_ms[0] = mean FC (A_(n)^T L) launch, out_ms[1] = mean FR
- * (A_(n) R) launch. Used by tools/kernel_bench.py and the ncu captures. */
+ * (CUDA events). out_ms (4 doubles): [0] mean FC (A_(n)^T L) launch, [1] mean
+ * FR (A_(n) R) launch, [2] the init pass A_(n) S (S column-major) with the
+ * fused ||A||^2, [3] the same without it. Used by tools/kernel_bench.py and
+ * the ncu captures. */
 int tkg_bench_contractions(tkg_ctx* ctx, const double* d_a, int32_t order, const uint64_t* dims,
                            uint32_t mode, uint32_t r, int32_t reps, double* out_ms,
                            tkg_error* err);

@@ -207,14 +207,20 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 #pragma unroll
       for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 
+    // warps whose 16 rows are all past the tile's fibers have nothing to add
+    const bool wact = MODE == kFibS   ? uint64_t(warp * 16) < a.pc * a.s
+                      : MODE == kFibJ ? jl0 + uint64_t(warp * 16) < a.s
+                                      : j0 + uint64_t(warp * 16) < F;
     for (int kb = 0; kb < nkb; ++kb, ++it) {
       const int slot = it % C::kStages;
       const uint32_t ph = (it / C::kStages) & 1;
       mbar_wait(&full[slot], ph);
       const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes);
       const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes + bytes_a);
-#pragma unroll
-      for (int t = 0; t < C::kKB / 4; ++t) {
+      // the last block of a contraction extent that is not a multiple of kKB:
+      // k-steps past K only add TMA zero-fill
+      const int kleft = wact ? int(a.K) - kb * C::kKB : 0;
+      auto kstep = [&](int t) {
         const int kk = 4 * t + q;
         double af[2];
 #pragma unroll
@@ -230,6 +236,14 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         for (int n = 0; n < C::kNT; ++n)
 #pragma unroll
           for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+      };
+      if (kleft >= C::kKB) {  // full block: the straight unrolled path
+#pragma unroll
+        for (int t = 0; t < C::kKB / 4; ++t) kstep(t);
+      } else {
+#pragma unroll
+        for (int t = 0; t < C::kKB / 4; ++t)
+          if (4 * t < kleft) kstep(t);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -479,6 +493,7 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
   const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
   const uint64_t f1 = min(F, f0 + a.fibers_per_range);
   const int i0 = int(ig) * C::kIC;
+  const bool wact = i0 + warp * 16 < int(a.K), m1act = i0 + warp * 16 + 8 < int(a.K);
   double acc[2][C::kNT][2];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
@@ -490,11 +505,12 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
     mbar_wait(&full[slot], ph);
     const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes);
     const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * stage_bytes + bytes_a);
-    // fibers past the chunk (next panel / next range) are dropped
+    // fibers past the chunk (next panel / next range) are dropped; warps whose
+    // rows are all past the contraction extent skip the chunk
     const int kvalid = chunk_len(j, f1);
     j += kvalid;
-#pragma unroll
-    for (int t = 0; t < C::kKB / 4; ++t) {
+    const int kuse = wact ? kvalid : 0;
+    auto kstep = [&](int t, bool m1) {
       const int kk = 4 * t + q;
       const bool kok = kk < kvalid;
       double af[2];
@@ -518,9 +534,18 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
         }
       }
 #pragma unroll
-      for (int n = 0; n < C::kNT; ++n)
+      for (int n = 0; n < C::kNT; ++n) {
+        dmma(acc[0][n][0], acc[0][n][1], af[0], bf[n]);
+        if (m1) dmma(acc[1][n][0], acc[1][n][1], af[1], bf[n]);
+      }
+    };
+    if (kuse == C::kKB && m1act) {  // full chunk, both row tiles live: the straight path
 #pragma unroll
-        for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+      for (int t = 0; t < C::kKB / 4; ++t) kstep(t, true);
+    } else {
+#pragma unroll
+      for (int t = 0; t < C::kKB / 4; ++t)
+        if (4 * t < kuse) kstep(t, m1act);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);

@@ -1578,6 +1578,20 @@ void Engine::bench_contractions(const double* A, const Shape& sh, int mode, uint
   CK(cudaEventSynchronize(e1));
   CK(cudaEventElapsedTime(&ms, e0, e1));
   out_ms[1] = ms / reps;
+  // the init pass: S column-major (the reference's storage order), with and
+  // without the fused ||A||^2
+  double* S = s_.d(F * r + 8);
+  CK(cudaMemsetAsync(S, 0, F * r * sizeof(double), st_));
+  double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
+  for (int with_sq = 1; with_sq >= 0; --with_sq) {
+    fr(v, S, 1, F, r, part, with_sq ? sq : nullptr, false, nullptr);
+    CK(cudaEventRecord(e0, st_));
+    for (int k = 0; k < reps; ++k) fr(v, S, 1, F, r, part, with_sq ? sq : nullptr, false, nullptr);
+    CK(cudaEventRecord(e1, st_));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    out_ms[with_sq ? 2 : 3] = ms / reps;
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 }

@@ -46,7 +46,7 @@ def main():
     for name in sel:
         dims, mode, r = CASES[name]
         n = int(np.prod(dims))
-        ms = (C.c_double * 2)()
+        ms = (C.c_double * 4)()
         err = _lib.TkgError()
         rc = l.tkg_bench_contractions(ctx._ctx, C.c_void_p(buf.data_ptr()), len(dims), _lib.u64(dims),
                                       mode, r, args.reps, ms, C.byref(err))
@@ -59,7 +59,7 @@ def main():
         flops = 2 * n * r
         tmin = max(bytes_ / (bw * 1e9), flops / (p64 * 1e12)) * 1e3
         row = {"case": name, "dims": dims, "mode": mode, "r": r}
-        for k, nm in enumerate(["fc", "fr"]):
+        for k, nm in enumerate(["fc", "fr", "init_sq", "init"]):
             t = ms[k]
             row[nm] = {"ms": round(t, 4), "GB/s": round(bytes_ / t / 1e6, 1),
                        "TF/s": round(flops / t / 1e9, 2), "roof_frac": round(tmin / t, 3)}
