@@ -397,7 +397,7 @@ def b200_arm(args, c, world, rank, local):
         achieved = st["bytes"] / (st["ms"] * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["hbm_src"]}
-    roof.update({"kernel": {"fc": "FC fiber contraction (right update A_(n)^T L', TTM)",
+    roof.update({"kernel": {"fc": "FC fiber contraction (ALS right update A_(n)^T L')",
                             "fr": "FR fiber reduction (left update A_(n) R, init A_(n) S)"}[cls],
                  "traffic": (ncu_traffic(args.config) or {}).get("dram_bytes_per_launch"),
                  "traffic_source": ncu_traffic(args.config), "launch_ms": per_launch_ms,

@@ -266,13 +266,15 @@ int tkg_uniform01(tkg_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t n, doub
                   tkg_error* err);
 
 /* Per-kernel-class device time (CUDA events on the launch stream) while
- * profiling is on. classes: 0 FC (right update / TTM), 1 FR (left update /
- * init), 2 small LA, 3 RNG. */
+ * profiling is on. classes: 0 FC (ALS right update), 1 FR (left update /
+ * init), 2 small LA, 3 RNG, 4 TTM outside the ALS loop (core chain, st TTM,
+ * singular vectors), 5 relative-residual expansion, 6-7 unused. */
+#define TKG_KERNEL_CLASSES 8
 typedef struct tkg_kernel_stats {
-  double ms[4];
-  uint64_t launches[4];
-  double bytes[4]; /* algorithmic bytes */
-  double flops[4]; /* algorithmic flops */
+  double ms[TKG_KERNEL_CLASSES];
+  uint64_t launches[TKG_KERNEL_CLASSES];
+  double bytes[TKG_KERNEL_CLASSES]; /* algorithmic bytes */
+  double flops[TKG_KERNEL_CLASSES]; /* algorithmic flops */
 } tkg_kernel_stats;
 int tkg_set_profiling(tkg_ctx* ctx, int on);
 int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out);

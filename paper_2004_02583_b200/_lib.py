@@ -50,8 +50,8 @@ class TkgReport(C.Structure):
 
 
 class TkgKernelStats(C.Structure):
-    _fields_ = [("ms", C.c_double * 4), ("launches", C.c_uint64 * 4), ("bytes", C.c_double * 4),
-                ("flops", C.c_double * 4)]
+    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_uint64 * 8), ("bytes", C.c_double * 8),
+                ("flops", C.c_double * 8)]
 
 
 _dp = C.POINTER(C.c_double)

@@ -213,7 +213,8 @@ void Engine::record(int cls, cudaEvent_t a, cudaEvent_t b, double bytes, double 
   recs_.push_back({cls, a, b, bytes, flops});
 }
 
-void Engine::kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], double flops[4]) {
+void Engine::kernel_stats(double ms[kNumCls], uint64_t launches[kNumCls], double bytes[kNumCls],
+                          double flops[kNumCls]) {
   sync();
   for (auto& r : recs_) {
     float t = 0;
@@ -227,7 +228,7 @@ void Engine::kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], d
     stat_flops_[r.cls] += r.flops;
   }
   recs_.clear();
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < kNumCls; ++k) {
     ms[k] = stat_ms_[k];
     launches[k] = stat_launch_[k];
     bytes[k] = stat_bytes_[k];
@@ -293,7 +294,7 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
   const double bytes = 8.0 * (elems + F * nc + double(v.K) * nc);
   if (profiling_) {
     CK(cudaEventRecord(ev.second, st_));
-    record(kClsFC, ev.first, ev.second, bytes, 2.0 * elems * nc);
+    record(fc_cls_, ev.first, ev.second, bytes, 2.0 * elems * nc);
   }
   if (count_pass) {
     passes_ += 1;
@@ -775,6 +776,7 @@ void Engine::recover_sv(const double* A, const Shape& sh, int mode, uint32_t r, 
 }
 
 void Engine::recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt) {
+  ClsScope cls(fc_cls_, kClsTTM);
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
   if (F < r)
     raise(12, "recover_singular_vectors: mode " + std::to_string(mode) + " has " + std::to_string(F) +
@@ -908,6 +910,7 @@ void Engine::sym_eig(const double* g, uint64_t n, uint64_t k, double* values, do
 
 // ---- HOOI (hooi.cpp:53-110) --------------------------------------------------------
 void Engine::ttm_mode(const double* X, const Shape& sh, int mode, const double* U, uint32_t r, double* out) {
+  ClsScope cls(fc_cls_, kClsTTM);
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
   const uint32_t ncp = pad_nc(r);
   double* Mt = mt_.d(I * ncp);
@@ -1031,6 +1034,7 @@ void Engine::begin_timed() {
 // multi_mode_product(t, {U_n^T}) in ascending mode order (hosvd.cpp:115-121).
 void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                         const std::vector<double*>& d_factors, double* d_core, int last_mode) {
+  ClsScope cls(fc_cls_, kClsTTM);
   Shape cur = sh;
   const double* src = A;
   DBuf* bufs[2] = {&work_a_, &work_b_};
@@ -1088,12 +1092,24 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
     } else {
       ea.out = bufs[which]->d(nxt.count());
     }
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (profiling_) {
+      ev = ev_pair();
+      CK(cudaEventRecord(ev.first, st_));
+    }
     if (last && !force_v1_ && expand_diff_tma_ok(ea)) {
       nsq = expand_diff_tma_grid(F, sms_);
       CK(launch_expand_diff_tma(ea, sms_, st_, nullptr));
     } else {
       if (last) nsq = expand_grid(F, sms_);
       CK(launch_expand(ea, sms_, st_, nullptr));
+    }
+    if (profiling_) {
+      // expansion of mode n: 2 K Iout flops per output element; reads the input
+      // (and the reference tensor on the last mode), writes the output
+      const double outn = double(F) * double(Iout);
+      CK(cudaEventRecord(ev.second, st_));
+      record(kClsResid, ev.first, ev.second, 8.0 * (double(cur.count()) + outn), 2.0 * double(K) * outn);
     }
     count_launch();
     src = ea.out;
@@ -1301,6 +1317,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
       nxt.d[mode - 1] = r;
       double* dst = bufs[which]->d(nxt.count());
       FiberView v{work, s, P, uint32_t(I), s, s * I};
+      ClsScope cls(fc_cls_, kClsTTM);
       fc(v, Mt, ncp, r, dst, 1, s, s * r, nullptr, nullptr, nullptr, true);
       mode_end(int(k));
       work = dst;

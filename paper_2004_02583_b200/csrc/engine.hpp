@@ -102,7 +102,11 @@ class DBuf {
   size_t bytes_ = 0;
 };
 
-enum KernelClass { kClsFC = 0, kClsFR = 1, kClsSmall = 2, kClsRng = 3 };
+// device-time classes of bench.py's per-class breakdown (profiling only):
+// FC right updates, FR left updates + init passes, small LA steps, RNG,
+// TTM contractions outside the ALS loop (core chain, st TTM, singular
+// vectors), the relative-residual expansion passes
+enum KernelClass { kClsFC = 0, kClsFR = 1, kClsSmall = 2, kClsRng = 3, kClsTTM = 4, kClsResid = 5, kNumCls = 8 };
 
 class Engine {
  public:
@@ -165,7 +169,7 @@ class Engine {
   void timer_start();
   double timer_stop();
   void flush_l2();
-  void kernel_stats(double ms[4], uint64_t launches[4], double bytes[4], double flops[4]);
+  void kernel_stats(double ms[kNumCls], uint64_t launches[kNumCls], double bytes[kNumCls], double flops[kNumCls]);
   const std::string& device_name() const { return name_; }
   cudaStream_t stream() const { return st_; }
 
@@ -317,10 +321,17 @@ class Engine {
   };
   std::vector<SpecRec> spec_recs_;
   std::vector<cudaEvent_t> ev_pool_;
-  double stat_ms_[4] = {0, 0, 0, 0};
-  uint64_t stat_launch_[4] = {0, 0, 0, 0};
-  double stat_bytes_[4] = {0, 0, 0, 0};
-  double stat_flops_[4] = {0, 0, 0, 0};
+  double stat_ms_[kNumCls] = {0};
+  uint64_t stat_launch_[kNumCls] = {0};
+  double stat_bytes_[kNumCls] = {0};
+  double stat_flops_[kNumCls] = {0};
+  int fc_cls_ = kClsFC;  // class recorded for fc() launches (kClsTTM outside the ALS loop)
+  struct ClsScope {
+    int& ref;
+    int old;
+    ClsScope(int& r, int c) : ref(r), old(r) { ref = c; }
+    ~ClsScope() { ref = old; }
+  };
 
   uint64_t launches_ = 0;
   uint64_t passes_ = 0;

@@ -567,9 +567,9 @@ class Context:
     def kernel_stats(self):
         st = _lib.TkgKernelStats()
         self._l.tkg_get_kernel_stats(self._ctx, C.byref(st))
-        names = ["fc", "fr", "small", "rng"]
+        names = ["fc", "fr", "small", "rng", "ttm", "residual"]
         return {names[k]: {"ms": st.ms[k], "launches": int(st.launches[k]), "bytes": st.bytes[k],
-                           "flops": st.flops[k]} for k in range(4)}
+                           "flops": st.flops[k]} for k in range(len(names))}
 
 
 def select_order(trunc: Truncation, shape: Sequence[int]) -> ModeOrder:
