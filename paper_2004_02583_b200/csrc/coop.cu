@@ -476,30 +476,20 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
   AlsCtrl* ctrl = a.ctrl;
   if (ctrl->stop) return;
   constexpr int kRows = 64, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2, kStg = 3;
-  constexpr int kPer = (kTri + 7) / 8;
   extern __shared__ __align__(16) double sm[];
   double* tile = sm;  // [kStg][kRows][kLd]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
   const uint32_t r = a.r;
 
   // Phase 1 (R^T R not fused into FC): Gram partial of the CTA's contiguous
-  // row range of R (row-major [F][ld])
+  // row range of R (row-major [F][ld]). Each warp takes 2 of the 16 k-steps
+  // (4 rows each) of every 64-row block and accumulates ALL upper 8x8 tiles
+  // for them, loading each column tile's fragment once per k-step (kNT loads
+  // for kTri DMMAs); the 8 warp partials are summed in a fixed order.
   if (a.gram_nparts == 0 && a.mode != 2) {
-    double acc[kPer][2];
-    int tm[kPer], tn[kPer];
+    double acc[kTri][2];
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      acc[k][0] = acc[k][1] = 0.0;
-      int tt = warp + 8 * k, mt = 0;
-      if (tt < kTri) {
-        int rem = tt;
-        while (rem >= kNT - mt) { rem -= kNT - mt; ++mt; }
-        tm[k] = mt;
-        tn[k] = mt + rem;
-      } else {
-        tm[k] = tn[k] = -1;
-      }
-    }
+    for (int k = 0; k < kTri; ++k) acc[k][0] = acc[k][1] = 0.0;
     const uint64_t nblk = (a.F + kRows - 1) / kRows;
     const uint64_t per = (nblk + gridDim.x - 1) / gridDim.x;
     const uint64_t b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
@@ -530,23 +520,43 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
       cp_async_commit();
       const double* t = tile + size_t(slot) * kRows * kLd;
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        if (tm[k] < 0) continue;
-#pragma unroll 8
-        for (int k0 = 0; k0 < kRows; k0 += 4) {
-          const double* rp = t + (k0 + q) * kLd;
-          dmma(acc[k][0], acc[k][1], rp[tm[k] * 8 + r8], rp[tn[k] * 8 + r8]);
-        }
+      for (int ks = 0; ks < 2; ++ks) {
+        const double* rp = t + ((warp * 2 + ks) * 4 + q) * kLd;
+        double fr[kNT];
+#pragma unroll
+        for (int c = 0; c < kNT; ++c) fr[c] = rp[c * 8 + r8];
+        int idx = 0;
+#pragma unroll
+        for (int tm = 0; tm < kNT; ++tm)
+#pragma unroll
+          for (int tn = tm; tn < kNT; ++tn, ++idx) dmma(acc[idx][0], acc[idx][1], fr[tm], fr[tn]);
       }
     }
     cp_async_wait<0>();
-    double* out = a.gpart + size_t(blockIdx.x) * NC * NC;
+    __syncthreads();  // the ring is free: the warp partials are summed there, warp 0 first
+    double* ws = tile;
+    for (int w = 0; w < int(kThreads / 32); ++w) {
+      if (warp == w) {
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      if (tm[k] < 0) continue;
-      const int c1 = tm[k] * 8 + r8, c2 = tn[k] * 8 + 2 * q;
-      out[c1 * NC + c2] = acc[k][0];
-      out[c1 * NC + c2 + 1] = acc[k][1];
+        for (int k = 0; k < kTri; ++k) {
+          double* p = ws + k * 64 + lane * 2;
+          p[0] = w == 0 ? acc[k][0] : p[0] + acc[k][0];
+          p[1] = w == 0 ? acc[k][1] : p[1] + acc[k][1];
+        }
+      }
+      __syncthreads();
+    }
+    double* out = a.gpart + size_t(blockIdx.x) * NC * NC;
+    for (int e = threadIdx.x; e < kTri * 64; e += blockDim.x) {
+      const double sum = ws[e];
+      const int tt = e / 64, l = (e % 64) / 2, el = e % 2;
+      int tm = 0, rem = tt;
+      while (rem >= kNT - tm) {
+        rem -= kNT - tm;
+        ++tm;
+      }
+      const int tn = tm + rem;
+      out[(tm * 8 + (l >> 2)) * NC + tn * 8 + 2 * (l & 3) + el] = sum;
     }
     if (a.mode == 1) return;
     grid.sync();

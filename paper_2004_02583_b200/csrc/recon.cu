@@ -193,7 +193,7 @@ cudaError_t launch_expand(const ExpandArgs& a, int num_sms, cudaStream_t st, int
     expand_kernel<N><<<grid, 256, smem, st>>>(a);                                               \
     return cudaGetLastError();                                                                  \
   }
-  TKG_E(8) TKG_E(16) TKG_E(32) TKG_E(64)
+  TKG_E(8) TKG_E(16) TKG_E(24) TKG_E(32) TKG_E(40) TKG_E(48) TKG_E(56) TKG_E(64)
 #undef TKG_E
   return cudaErrorInvalidValue;
 }
