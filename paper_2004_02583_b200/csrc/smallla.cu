@@ -358,16 +358,26 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int f = warp * 16 + m * 8 + r8, c = n * 8 + 2 * q + e;
-          Os[c * kLdO + f] = acc[m][n][e];
+          Os[s == 1 ? f * (NC + 1) + c : c * kLdO + f] = acc[m][n][e];
         }
     __syncthreads();
-    for (int e = threadIdx.x; e < int(r) * kShrinkTile; e += blockDim.x) {
-      const int c = e / kShrinkTile, f = e % kShrinkTile;
-      if (f >= nf) continue;
-      const uint64_t j = j0 + f, p = j / s, jl = j - p * s;
-      const double v = Os[c * kLdO + f];
-      out[jl + uint64_t(c) * s + p * s * r] = v;
-      sq = fma(v, v, sq);
+    if (s == 1) {  // mode-1 output: a fiber's r values are one contiguous run
+      for (int e = threadIdx.x; e < int(r) * kShrinkTile; e += blockDim.x) {
+        const int f = e / int(r), c = e - f * int(r);
+        if (f >= nf) continue;
+        const double v = Os[f * (NC + 1) + c];  // fiber-major staging: conflict-free reads
+        out[c + (j0 + f) * r] = v;
+        sq = fma(v, v, sq);
+      }
+    } else {
+      for (int e = threadIdx.x; e < int(r) * kShrinkTile; e += blockDim.x) {
+        const int c = e / kShrinkTile, f = e % kShrinkTile;
+        if (f >= nf) continue;
+        const uint64_t j = j0 + f, p = j / s, jl = j - p * s;
+        const double v = Os[c * kLdO + f];
+        out[jl + uint64_t(c) * s + p * s * r] = v;
+        sq = fma(v, v, sq);
+      }
     }
   }
   sq = block_sum(sq, red);
