@@ -48,10 +48,11 @@ def main():
         rb = d.get("dram__bytes_read.sum", 0)
         wb = d.get("dram__bytes_write.sum", 0)
         ub = d.get("dram__bytes_read.sum.unit")
-        print(f"{d['kernel']:60s} t={t} {tu}  dram_rd={rb} {ub} dram_wr={wb}  "
+        print(f"{d['kernel']:60s} t={t} {tu}  dram_rd={rb} {ub} dram_wr={wb} {d.get('dram__bytes_write.sum.unit')}  "
               f"dram%={d.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')}  "
               f"sm%={d.get('sm__throughput.avg.pct_of_peak_sustained_elapsed')}  "
-              f"fp64pipe%={d.get('sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active')}  "
+              f"dmma_inst%={d.get('sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active')}  "
+              f"tensor_active%={d.get('TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed')}  "
               f"regs={d.get('launch__registers_per_thread')}")
 
 
