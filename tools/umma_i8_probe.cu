@@ -234,6 +234,10 @@ int main() {
     for (int as = 0; as < 2; ++as)
       for (int bs = 0; bs < 2; ++bs) fails += run<128, 32>(as, bs, mode, 1);
   fails += run<128, 64>(1, 0, 0, 1);
+  // M = 64 (rank on M, fibers on N): issue rate only (mode 1, A from smem)
+  run<64, 128>(1, 1, 1, 4096, 0);
+  run<64, 192>(1, 1, 1, 4096, 0);
+  run<128, 192>(1, 1, 1, 4096, 0);
   // issue rate vs N: unrolled issue (ndst 0), one accumulator chain, round-robin
   for (int mode = 0; mode < 2; ++mode) {
     run<128, 32>(1, 1, mode, 4096, 0);
