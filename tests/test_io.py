@@ -74,3 +74,25 @@ def test_io_errors_match_reference(lib, tmp_path):
     bad.write_bytes(b"TNSR" + (1).to_bytes(4, "little") + (2).to_bytes(4, "little") + (3).to_bytes(8, "little"))
     assert lib.tkg_read_tnsr_shape(os.fsencode(str(bad)), C.byref(order), dims, C.byref(err)) == 2
     assert err.message.decode().startswith("truncated file")
+
+
+def test_cli_usage_errors_on_cpu(tmp_path):
+    # tenkit_main.cpp:644-664: parse errors exit 1, io errors 2 (no device needed
+    # for either: both fail before a context is created)
+    import subprocess
+    cli = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2004_02583_b200",
+                       "tenkit_b200")
+    if not os.path.exists(cli):
+        pytest.skip("CLI not built")
+    def run(*a):
+        p = subprocess.run([cli, *a], capture_output=True, text=True, timeout=60)
+        return p.returncode, p.stderr
+    assert run()[0] == 1
+    code, err = run("compress", "--in", "a.tnsr")
+    assert code == 1 and "--out is required" in err
+    code, err = run("compress", "--in", "a", "--out", "b", "--ranks", "2,x")
+    assert code == 1 and "--ranks" in err
+    code, err = run("compress", "--in", "a", "--out", "b", "--ranks", "2,2", "--method", "t-pca")
+    assert code == 1 and "--method" in err
+    code, err = run("compress", "--in", str(tmp_path / "none.tnsr"), "--out", "b", "--ranks", "2,2")
+    assert code == 2 and "cannot open for reading" in err
