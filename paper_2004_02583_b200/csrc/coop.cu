@@ -396,11 +396,13 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
   double* W = M + r * r;          // r*r (CTA 0 scratch)
   const uint32_t nblk = (I + kRB - 1) / kRB;
 
+  PHASE(20);
   // Phase A: sum of the FR partials into slot 0
   if (a.from_partials && a.nparts > 1) {
     reduce_partials_grid(a.part, a.nparts, I, a.ldp, r);
     grid.sync();
   }
+  PHASE(21);
   // Phase B: L rows (from partials: Y G_R^{-1}, kept row-major in slot 0 and
   // written to Lc), and their Gram partial
   if (a.from_partials) load_mat_rm(a.GRinv, M, r);
@@ -427,8 +429,10 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
   }
   g.store(a.gpart + size_t(blockIdx.x) * r * r, r);
   grid.sync();
+  PHASE(22);
   reduce_gram_grid(a.gpart, gridDim.x, uint64_t(r) * r, r, r, a.gs);
   grid.sync();
+  PHASE(23);
 
   // Phase C (CTA 0): G_L, its inverse with the spd_solve pivot floor
   if (blockIdx.x == 0) {
@@ -448,7 +452,9 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
       }
     }
   }
+  PHASE(24);
   grid.sync();
+  PHASE(25);
   if (ctrl->stop) return;
 
   // Phase D: Mt rows = L rows G_L^{-1}, padded to ncp
@@ -467,6 +473,7 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
     }
     __syncthreads();
   }
+  PHASE(26);
 }
 
 // ---- finish_step -----------------------------------------------------------------

@@ -82,11 +82,14 @@ int main() {
       }
       printf("{\"kernel\":\"%s\",\"I\":%u,\"r\":%u,\"nparts\":%d,\"us\":%.2f}\n", kind ? "prep" : "cholqr", c.I, c.r,
              c.nparts, tot / reps * 1000);
-      if (kind == 0) {
+      {
         unsigned long long ph[64];
         phase_read(ph);
         printf("   phases(us):");
-        for (int k = 1; k < 12; ++k) printf(" %d:%.1f", k, (ph[k] - ph[k - 1]) * 1e-3);
+        if (kind == 0)
+          for (int k = 1; k < 12; ++k) printf(" %d:%.1f", k, (ph[k] - ph[k - 1]) * 1e-3);
+        else
+          for (int k = 21; k < 27; ++k) printf(" %d:%.1f", k, (ph[k] - ph[k - 1]) * 1e-3);
         printf("\n");
       }
     }
