@@ -105,7 +105,9 @@ class AlsConfig:
 
 @dataclass
 class FactorEngine:
-    kind: str = "als"
+    """FactorEngine (hosvd.hpp:19-27): kind "svd" (the reference's default),
+    "eig" or "als"; `als` is used by the ALS engine only."""
+    kind: str = "svd"
     als: AlsConfig = field(default_factory=AlsConfig)
 
     @staticmethod
