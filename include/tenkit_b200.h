@@ -24,6 +24,9 @@
  *   tkg_hooi           <- tenkit::hooi           include/tenkit/hooi.hpp:33-37, src/hooi.cpp:53-110
  *   tkg_read_tnsr / tkg_write_tnsr / tkg_write_tukr <- read_tnsr / write_tnsr / write_tukr
  *                                   include/tenkit/io.hpp, src/io.cpp:131-193
+ *   tkg_multi_mode_product <- tenkit::multi_mode_product include/tenkit/tensor_ops.hpp:33-34,
+ *                                   src/tensor_ops.cpp:171-191
+ *   tkg_reconstruct    <- tenkit::reconstruct    src/tensor_ops.cpp:420-440
  *   tkg_mode_gram      <- tenkit::mode_gram      include/tenkit/tensor_ops.hpp, src/tensor_ops.cpp:332-389
  *   tkg_sym_eig        <- tenkit::sym_eig        include/tenkit/kernels.hpp:51, src/kernels.cpp:448-604
  *
@@ -245,6 +248,17 @@ int tkg_write_tnsr(const char* path, int32_t order, const uint64_t* dims, const 
 int tkg_write_tukr(const char* path, int32_t order, const uint64_t* dims, const uint64_t* ranks, const double* core,
                    const double* factors, tkg_error* err);
 
+/* multi_mode_product: factor k is rows[k] x cols[k] (cols[k] = extent of
+ * modes[k]), column-major host memory; applied in ascending mode order,
+ * duplicate modes rejected (InvalidMode). out: the result, dims with
+ * dims[modes[k]-1] replaced by rows[k]. */
+int tkg_multi_mode_product(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, int32_t nfactors,
+                           const uint32_t* modes, const double* const* factors, const uint64_t* rows,
+                           const uint64_t* cols, double* out, tkg_error* err);
+/* reconstruct: core (ranks) x_n U_n, factors concatenated dims[n] x ranks[n];
+ * out has dims. */
+int tkg_reconstruct(tkg_ctx* ctx, const double* core, int32_t order, const uint64_t* ranks, const uint64_t* dims,
+                    const double* factors, double* out, tkg_error* err);
 /* mode_gram: out = A_(mode) A_(mode)^T (extent x extent, column-major). */
 int tkg_mode_gram(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode, double* out,
                   tkg_error* err);

@@ -8,7 +8,8 @@ from .tenkit import (AlsConfig, AlsReport, Context, DecompositionReport, Degener
                      FormatError, InvalidModeError, IoError, ModeOrder, ModeReport,
                      NoConvergenceError, RankTooLargeError, SingularGramError, Truncation,
                      TuckerTensor, UnsupportedError, ZeroReferenceError, als_init, als_low_rank,
-                     default_context, frobenius_norm, gram, hooi, mode_gram, mode_n_product, recover_singular_vectors,
+                     default_context, frobenius_norm, gram, hooi, mode_gram, mode_n_product, multi_mode_product,
+                     reconstruct, recover_singular_vectors,
                      reduced_qr, sym_eig,
                      relative_error, select_order, st_hosvd, synth_tucker, synth_tucker_slab, t_hosvd, unfold_t_times,
                      unfold_times)

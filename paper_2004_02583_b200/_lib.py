@@ -86,6 +86,9 @@ SIGNATURES = [
     ("tkg_read_tnsr", C.c_int, [_ctxp, C.c_char_p, C.c_void_p, C.c_int, C.POINTER(TkgError)]),
     ("tkg_write_tnsr", C.c_int, [C.c_char_p, C.c_int32, _u64p, _dp, C.POINTER(TkgError)]),
     ("tkg_write_tukr", C.c_int, [C.c_char_p, C.c_int32, _u64p, _u64p, _dp, _dp, C.POINTER(TkgError)]),
+    ("tkg_multi_mode_product", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_int32, _u32p, C.POINTER(_dp), _u64p,
+                                         _u64p, _dp, C.POINTER(TkgError)]),
+    ("tkg_reconstruct", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, _u64p, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_mode_gram", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.POINTER(TkgError)]),
     ("tkg_sym_eig", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_select_order", C.c_int, [C.c_int32, _u64p, _u64p, _u32p, C.POINTER(TkgError)]),

@@ -258,6 +258,38 @@ int tkg_write_tukr(const char* path, int32_t order, const uint64_t* dims, const 
   });
 }
 
+int tkg_multi_mode_product(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, int32_t nfactors,
+                           const uint32_t* modes, const double* const* factors, const uint64_t* rows,
+                           const uint64_t* cols, double* out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    std::vector<int> m(modes, modes + nfactors);
+    std::vector<const double*> f(factors, factors + nfactors);
+    std::vector<uint64_t> rw(rows, rows + nfactors), cl(cols, cols + nfactors);
+    eng(ctx).multi_mode_product(a, sh, m, f, rw, cl, out);
+  });
+}
+
+int tkg_reconstruct(tkg_ctx* ctx, const double* core, int32_t order, const uint64_t* ranks, const uint64_t* dims,
+                    const double* factors, double* out, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape cs = make_shape(order, ranks);
+    (void)make_shape(order, dims);
+    std::vector<int> m(order);
+    std::vector<const double*> f(order);
+    std::vector<uint64_t> rw(order), cl(order);
+    const double* p = factors;
+    for (int n = 0; n < order; ++n) {  // reconstruct (tensor_ops.cpp:420-440): U_n is dims[n] x ranks[n]
+      m[n] = n + 1;
+      f[n] = p;
+      rw[n] = dims[n];
+      cl[n] = ranks[n];
+      p += dims[n] * ranks[n];
+    }
+    eng(ctx).multi_mode_product(core, cs, m, f, rw, cl, out);
+  });
+}
+
 int tkg_mode_gram(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode, double* out,
                   tkg_error* err) {
   return guarded(err, [&] {

@@ -1480,9 +1480,26 @@ void Engine::unfold_t_times(const double* a, const Shape& sh, int mode, const do
   sync();
 }
 
+// dst <- X x_mode U, U (rows x I_mode, device, column-major), tensor layout,
+// in chunks of 64 output rows (mode_n_product, tensor_ops.cpp:129-169)
+void Engine::mode_product_dev(const double* X, const Shape& sh, int mode, const double* U, uint64_t rows,
+                              double* dst) {
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
+  FiberView v{X, s, F / s, uint32_t(I), s, s * I};
+  for (uint64_t c0 = 0; c0 < rows; c0 += 64) {
+    const uint32_t nc = uint32_t(std::min<uint64_t>(64, rows - c0));
+    const uint32_t ncp = pad_nc(nc);
+    double* Mt = mt_.d(I * ncp);
+    // Mt[i][c] = U[(c0 + c) + i*rows]
+    CK(launch_pack(U + c0, rows, 1, uint32_t(I), nc, Mt, ncp, st_));
+    count_launch();
+    fc(v, Mt, ncp, nc, dst + c0 * s, 1, s, s * rows, nullptr, nullptr, nullptr, false);
+  }
+}
+
 void Engine::mode_n_product(const double* a, const Shape& sh, const double* u, uint64_t rows,
                             uint64_t cols, int mode, double* out) {
-  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
+  const uint64_t I = sh.extent(mode);
   if (cols != I)
     raise(2, "mode_n_product: factor has " + std::to_string(cols) + " columns, mode " +
                  std::to_string(mode) + " has extent " + std::to_string(I));
@@ -1492,17 +1509,52 @@ void Engine::mode_n_product(const double* a, const Shape& sh, const double* u, u
   Shape nxt = sh;
   nxt.d[mode - 1] = rows;
   double* dst = work_a_.d(nxt.count());
-  FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  for (uint64_t c0 = 0; c0 < rows; c0 += 64) {
-    const uint32_t nc = uint32_t(std::min<uint64_t>(64, rows - c0));
-    const uint32_t ncp = pad_nc(nc);
-    double* Mt = mt_.d(I * ncp);
-    // Mt[i][c] = u[(c0 + c) + i*rows]  (u is rows x cols column-major)
-    CK(launch_pack(U + c0, rows, 1, uint32_t(I), nc, Mt, ncp, st_));
-    fc(v, Mt, ncp, nc, dst + c0 * s, 1, s, s * rows, nullptr, nullptr, nullptr, false);
-  }
+  mode_product_dev(A, sh, mode, U, rows, dst);
   CK(cudaMemcpyAsync(out, dst, nxt.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
+}
+
+// multi_mode_product (tensor_ops.cpp:171-191): the factors sorted by mode
+// (duplicates rejected), applied ascending on the device. Returns the shape.
+Shape Engine::multi_mode_product(const double* a, const Shape& sh, const std::vector<int>& modes,
+                                 const std::vector<const double*>& factors, const std::vector<uint64_t>& rows,
+                                 const std::vector<uint64_t>& cols, double* out) {
+  std::vector<size_t> idx(modes.size());
+  for (size_t k = 0; k < idx.size(); ++k) idx[k] = k;
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return modes[x] < modes[y]; });
+  for (size_t k = 0; k + 1 < idx.size(); ++k)
+    if (modes[idx[k]] == modes[idx[k + 1]])
+      raise(1, "multi_mode_product: duplicate mode " + std::to_string(modes[idx[k]]));
+  Shape cur = sh;
+  for (size_t k : idx) {
+    const int m = modes[k];
+    if (m < 1 || m > sh.N)
+      raise(1, "mode " + std::to_string(m) + " out of range 1.." + std::to_string(sh.N));
+    if (cols[k] != sh.extent(m))
+      raise(2, "mode_n_product: factor has " + std::to_string(cols[k]) + " columns, mode " + std::to_string(m) +
+                   " has extent " + std::to_string(sh.extent(m)));
+  }
+  const double* src = upload(a, sh.count(), false, tensor_, nullptr);
+  DBuf* bufs[2] = {&work_a_, &work_b_};
+  int which = 0;
+  for (size_t k : idx) {
+    const int m = modes[k];
+    const uint64_t I = cur.extent(m);
+    const uint64_t nr = rows[k];
+    // the factor is rows x I column-major on the host
+    double* U = misc_.d(nr * I);
+    CK(cudaMemcpyAsync(U, factors[k], nr * I * sizeof(double), cudaMemcpyHostToDevice, st_));
+    Shape nxt = cur;
+    nxt.d[m - 1] = nr;
+    double* dst = bufs[which]->d(std::max<uint64_t>(nxt.count(), 1));
+    mode_product_dev(src, cur, m, U, nr, dst);
+    src = dst;
+    cur = nxt;
+    which ^= 1;
+  }
+  CK(cudaMemcpyAsync(out, src, cur.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  return cur;
 }
 
 double Engine::frobenius_norm(const double* a, uint64_t n) {

@@ -144,6 +144,11 @@ class Engine {
   void unfold_t_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r, double* out);
   void mode_n_product(const double* a, const Shape& sh, const double* u, uint64_t rows, uint64_t cols,
                       int mode, double* out);
+  // multi_mode_product (tensor_ops.cpp:171-191): factor k is rows[k] x I_{modes[k]}
+  // (host, column-major); returns the result's shape
+  Shape multi_mode_product(const double* a, const Shape& sh, const std::vector<int>& modes,
+                           const std::vector<const double*>& factors, const std::vector<uint64_t>& rows,
+                           const std::vector<uint64_t>& cols, double* out);
   double frobenius_norm(const double* a, uint64_t n);
   double relative_error(const double* a, const double* b, uint64_t n);
   void reduced_qr(const double* a, uint64_t rows, uint64_t cols, double* q, double* r);
@@ -228,6 +233,7 @@ class Engine {
   // col-major) <- U V; leaves R = A_(n)^T U_old in r_ (row-major [F][ncp])
   // and V^T (r x r, col-major) in vt. Sums the Gram over ranks when dist_.
   void recover_sv(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
+  void mode_product_dev(const double* X, const Shape& sh, int mode, const double* U, uint64_t rows, double* dst);
   void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   // SVD / EIG engines: U (device, I x r) <- leading eigenvectors of A_(n) A_(n)^T
   void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U);

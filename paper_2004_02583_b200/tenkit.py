@@ -510,6 +510,43 @@ class Context:
         _raise(self._l.tkg_write_tukr(os.fsencode(path), len(dims), _lib.u64(dims), _lib.u64(ranks),
                                       _flat_ptr(core), _flat_ptr(fac), C.byref(err)), err)
 
+    def multi_mode_product(self, t, factors):
+        """tensor_ops.cpp:171-191: factors is a list of (matrix rows x I_mode, mode)."""
+        a = _host(t)
+        mats = [np.asfortranarray(np.asarray(u, dtype=np.float64)) for u, _ in factors]
+        modes = [int(m) for _, m in factors]
+        dims = list(a.shape)
+        for u, m in zip(mats, modes):
+            if 1 <= m <= a.ndim:
+                dims[m - 1] = u.shape[0]
+        out = np.zeros(dims, order="F")
+        n = len(mats)
+        ptrs = (_lib._dp * max(1, n))(*[_flat_ptr(u) for u in mats])
+        err = _lib.TkgError()
+        _raise(self._l.tkg_multi_mode_product(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape), n,
+                                              _lib.u32(modes), ptrs, _lib.u64([u.shape[0] for u in mats]),
+                                              _lib.u64([u.shape[1] for u in mats]), _flat_ptr(out),
+                                              C.byref(err)), err)
+        return out
+
+    def reconstruct(self, tucker: "TuckerTensor"):
+        """tensor_ops.cpp:420-440."""
+        core = np.asfortranarray(np.asarray(tucker.core, dtype=np.float64))
+        ranks = list(core.shape)
+        dims = [int(x) for x in tucker.origin_shape]
+        if len(tucker.factors) != core.ndim:
+            raise DimensionMismatchError(f"reconstruct: {len(tucker.factors)} factors for an order-{core.ndim} core")
+        for n, u in enumerate(tucker.factors):
+            if np.asarray(u).shape != (dims[n], ranks[n]):
+                raise DimensionMismatchError(f"reconstruct: factor {n + 1} is {np.asarray(u).shape}, "
+                                             f"expected {(dims[n], ranks[n])}")
+        fac = np.concatenate([np.asarray(u, dtype=np.float64).reshape(-1, order="F") for u in tucker.factors])
+        out = np.zeros(dims, order="F")
+        err = _lib.TkgError()
+        _raise(self._l.tkg_reconstruct(self._ctx, _flat_ptr(core), core.ndim, _lib.u64(ranks), _lib.u64(dims),
+                                       _flat_ptr(fac), _flat_ptr(out), C.byref(err)), err)
+        return out
+
     def mode_gram(self, t, mode: int):
         """tensor_ops.cpp:332-389: A_(mode) A_(mode)^T."""
         a = _host(t)
@@ -643,6 +680,14 @@ def gram(a):
 
 def hooi(t, trunc, init, cfg=None):
     return default_context().hooi(t, trunc, init, cfg)
+
+
+def multi_mode_product(t, factors):
+    return default_context().multi_mode_product(t, factors)
+
+
+def reconstruct(tucker):
+    return default_context().reconstruct(tucker)
 
 
 def mode_gram(t, mode):

@@ -431,3 +431,25 @@ def test_rank_above_64_is_an_explicit_error(ctx, ref):
     eng = tk.FactorEngine.with_als(tk.AlsConfig(eta=1e-8, seed=3))
     with pytest.raises(tk.UnsupportedError):
         ctx.t_hosvd(t, tk.Truncation([70, 3, 3]), eng)
+
+
+# ---- multi_mode_product / reconstruct (tensor_ops.cpp:171-191, 420-440) -------
+def test_multi_mode_product_and_reconstruct(ctx, ref):
+    t = random_tensor(ref, [9, 8, 7, 6], 41)
+    us = [(random_matrix(ref, 5, 8, 42), 2), (random_matrix(ref, 70, 6, 43), 4), (random_matrix(ref, 3, 9, 44), 1)]
+    got = ctx.multi_mode_product(t, us)
+    want = t
+    for u, m in sorted(us, key=lambda x: x[1]):  # ascending modes, as the reference applies them
+        want = ref.mode_n_product(want, u, m)
+    assert got.shape == (3, 5, 7, 70)
+    assert rel(got, want) <= 1e-13
+    assert np.array_equal(ctx.multi_mode_product(t, []), t)
+    with pytest.raises(tk.InvalidModeError):
+        ctx.multi_mode_product(t, [(us[0][0], 2), (us[0][0], 2)])
+    with pytest.raises(tk.DimensionMismatchError):
+        ctx.multi_mode_product(t, [(random_matrix(ref, 2, 5, 45), 1)])
+    # reconstruct: core x_n U_n against the reference
+    core = random_tensor(ref, [3, 4, 2], 46)
+    factors = [random_orthonormal(ref, d, r, 47 + d) for d, r in zip([20, 15, 10], [3, 4, 2])]
+    tkr = tk.TuckerTensor(core, factors, (20, 15, 10))
+    assert rel(ctx.reconstruct(tkr), ref.reconstruct(core, factors, [20, 15, 10])) <= 1e-13
