@@ -24,8 +24,11 @@
 #include "tenkit_b200.h"
 
 #ifdef TENKIT_B200_USE_TENKIT
+#include "tenkit/als.hpp"
 #include "tenkit/errors.hpp"
+#include "tenkit/hooi.hpp"
 #include "tenkit/hosvd.hpp"
+#include "tenkit/tensor_ops.hpp"
 #endif
 
 namespace tenkit_b200 {
@@ -231,6 +234,166 @@ inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> st_hosvd(
     const tenkit::DenseTensor& t, const tenkit::Truncation& trunc,
     const std::optional<tenkit::ModeOrder>& order, const tenkit::FactorEngine& engine) {
   return run(true, t, trunc, order, engine);
+}
+
+// ---- primitives with the reference's signatures --------------------------------
+inline std::vector<uint64_t> dims_of(const tenkit::Shape& s) {
+  return std::vector<uint64_t>(s.dims().begin(), s.dims().end());
+}
+
+// als.hpp:69-71
+inline std::pair<tenkit::FactorPair, tenkit::AlsReport> als_low_rank(const tenkit::DenseTensor& t, std::size_t mode,
+                                                                     std::size_t r, const tenkit::AlsConfig& cfg) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  const uint64_t I = (mode >= 1 && mode <= dims.size()) ? dims[mode - 1] : 1;
+  const uint64_t F = I ? t.size() / I : 0;
+  std::vector<double> l(I * r, 0.0), rr(F * r, 0.0);
+  tkg_als_config c{cfg.eta, cfg.max_iters, cfg.seed, cfg.init ? cfg.init->data() : nullptr};
+  tkg_mode_report rep{};
+  tkg_error e{};
+  check(tkg_als_low_rank(Context::default_context().get(), t.data(), 0, int32_t(dims.size()), dims.data(),
+                         uint32_t(mode), r, &c, l.data(), rr.data(), &rep, &e),
+        e);
+  tenkit::AlsReport ar;
+  ar.iterations = rep.iterations;
+  ar.residual_history.assign(rep.residual_history, rep.residual_history + rep.history_len);
+  ar.status = rep.status == 0 ? tenkit::AlsStatus::kConverged : tenkit::AlsStatus::kMaxItersReached;
+  ar.achieved_eta = rep.achieved_eta;
+  return {tenkit::FactorPair{tenkit::Matrix(I, r, std::move(l)), tenkit::Matrix(F, r, std::move(rr))}, ar};
+}
+
+// tensor_ops.hpp:39 / :44
+inline tenkit::Matrix unfold_times(const tenkit::DenseTensor& t, std::size_t mode, const tenkit::Matrix& m) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  const uint64_t I = (mode >= 1 && mode <= dims.size()) ? dims[mode - 1] : 1;
+  std::vector<double> out(I * m.cols(), 0.0);
+  tkg_error e{};
+  check(tkg_unfold_times(Context::default_context().get(), t.data(), int32_t(dims.size()), dims.data(),
+                         uint32_t(mode), m.data(), m.cols(), out.data(), &e),
+        e);
+  return tenkit::Matrix(I, m.cols(), std::move(out));
+}
+
+inline tenkit::Matrix unfold_t_times(const tenkit::DenseTensor& t, std::size_t mode, const tenkit::Matrix& m) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  const uint64_t I = (mode >= 1 && mode <= dims.size()) ? dims[mode - 1] : 1;
+  const uint64_t F = I ? t.size() / I : 0;
+  std::vector<double> out(F * m.cols(), 0.0);
+  tkg_error e{};
+  check(tkg_unfold_t_times(Context::default_context().get(), t.data(), int32_t(dims.size()), dims.data(),
+                           uint32_t(mode), m.data(), m.cols(), out.data(), &e),
+        e);
+  return tenkit::Matrix(F, m.cols(), std::move(out));
+}
+
+// tensor_ops.hpp:22-23
+inline tenkit::DenseTensor mode_n_product(const tenkit::DenseTensor& t, const tenkit::Matrix& u, std::size_t mode) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  std::vector<std::size_t> od(t.shape().dims().begin(), t.shape().dims().end());
+  if (mode >= 1 && mode <= od.size()) od[mode - 1] = u.rows();
+  uint64_t n = 1;
+  for (std::size_t d : od) n *= d;
+  std::vector<double> out(n, 0.0);
+  tkg_error e{};
+  check(tkg_mode_n_product(Context::default_context().get(), t.data(), int32_t(dims.size()), dims.data(), u.data(),
+                           u.rows(), u.cols(), uint32_t(mode), out.data(), &e),
+        e);
+  return tenkit::DenseTensor(tenkit::Shape(od), std::move(out));
+}
+
+// tensor_ops.hpp:33-34
+inline tenkit::DenseTensor multi_mode_product(const tenkit::DenseTensor& t,
+                                              const std::vector<tenkit::ModeFactor>& factors) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  std::vector<std::size_t> od(t.shape().dims().begin(), t.shape().dims().end());
+  std::vector<uint32_t> modes;
+  std::vector<const double*> ptrs;
+  std::vector<uint64_t> rows, cols;
+  for (const tenkit::ModeFactor& f : factors) {
+    modes.push_back(uint32_t(f.mode));
+    ptrs.push_back(f.factor.data());
+    rows.push_back(f.factor.rows());
+    cols.push_back(f.factor.cols());
+    if (f.mode >= 1 && f.mode <= od.size()) od[f.mode - 1] = f.factor.rows();
+  }
+  uint64_t n = 1;
+  for (std::size_t d : od) n *= d;
+  std::vector<double> out(n, 0.0);
+  tkg_error e{};
+  check(tkg_multi_mode_product(Context::default_context().get(), t.data(), int32_t(dims.size()), dims.data(),
+                               int32_t(factors.size()), modes.data(), ptrs.data(), rows.data(), cols.data(),
+                               out.data(), &e),
+        e);
+  return tenkit::DenseTensor(tenkit::Shape(od), std::move(out));
+}
+
+// tensor_ops.hpp:52 / :55
+inline double frobenius_norm(const tenkit::DenseTensor& t) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  double out = 0.0;
+  tkg_error e{};
+  check(tkg_frobenius_norm(Context::default_context().get(), t.data(), int32_t(dims.size()), dims.data(), &out, &e),
+        e);
+  return out;
+}
+
+inline double relative_error(const tenkit::DenseTensor& a, const tenkit::DenseTensor& b) {
+  if (a.shape() != b.shape())
+    throw tenkit::DimensionMismatchError("relative_error: shapes " + a.shape().to_string() + " vs " +
+                                         b.shape().to_string());
+  std::vector<uint64_t> dims = dims_of(a.shape());
+  double out = 0.0;
+  tkg_error e{};
+  check(tkg_relative_error(Context::default_context().get(), a.data(), b.data(), int32_t(dims.size()), dims.data(),
+                           &out, &e),
+        e);
+  return out;
+}
+
+// hooi.hpp:33-37
+inline tenkit::HooiResult hooi(const tenkit::DenseTensor& t, const tenkit::Truncation& trunc,
+                               const tenkit::TuckerTensor& init, const tenkit::HooiConfig& cfg) {
+  if (init.origin_shape != t.shape())
+    throw tenkit::DimensionMismatchError("hooi: init origin shape " + init.origin_shape.to_string() +
+                                         " does not match tensor " + t.shape().to_string());
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  std::vector<uint64_t> ranks(trunc.ranks.begin(), trunc.ranks.end());
+  const std::size_t n = dims.size();
+  if (init.factors.size() != n || init.core.shape().order() != n)
+    throw tenkit::DimensionMismatchError("hooi: init is not an order-" + std::to_string(n) + " decomposition");
+  std::vector<double> f_in;
+  for (std::size_t m = 0; m < n; ++m) {
+    const tenkit::Matrix& u = init.factors[m];
+    if (ranks.size() != n || u.rows() != dims[m] || u.cols() != ranks[m] || init.core.shape().extent(m + 1) != ranks[m])
+      throw tenkit::DimensionMismatchError("hooi: init factor for mode " + std::to_string(m + 1) +
+                                           " does not match the truncation");
+    f_in.insert(f_in.end(), u.values().begin(), u.values().end());
+  }
+  uint64_t core_n = 1, fac_n = 0;
+  for (std::size_t m = 0; m < n; ++m) {
+    core_n *= ranks[m];
+    fac_n += dims[m] * ranks[m];
+  }
+  std::vector<double> core(core_n, 0.0), fac(fac_n, 0.0), fits(std::size_t(cfg.max_iters < 1 ? 1 : cfg.max_iters) + 1);
+  int32_t iters = 0, conv = 0;
+  tkg_error e{};
+  check(tkg_hooi(Context::default_context().get(), t.data(), 0, int32_t(n), dims.data(), ranks.data(),
+                 init.core.data(), f_in.data(), cfg.tol, cfg.max_iters, core.data(), fac.data(), &iters, &conv,
+                 fits.data(), nullptr, &e),
+        e);
+  std::vector<std::size_t> rk(trunc.ranks.begin(), trunc.ranks.end());
+  tenkit::TuckerTensor tk{tenkit::DenseTensor(tenkit::Shape(rk), std::move(core)), {}, t.shape()};
+  uint64_t ofs = 0;
+  for (std::size_t m = 0; m < n; ++m) {
+    tk.factors.emplace_back(dims[m], ranks[m],
+                            std::vector<double>(fac.begin() + ofs, fac.begin() + ofs + dims[m] * ranks[m]));
+    ofs += dims[m] * ranks[m];
+  }
+  tenkit::HooiResult res{std::move(tk)};
+  res.iterations = iters;
+  res.fit_history.assign(fits.begin(), fits.begin() + iters + 1);
+  res.converged = conv != 0;
+  return res;
 }
 #endif
 

@@ -138,3 +138,16 @@ def test_read_tnsr_to_device(ref, tmp_path):
     ctx.write_tukr(out, a)
     core, factors, d = ref.read_tukr(out)
     assert d == dims and np.array_equal(core, a.core)
+
+
+def test_cpp_shim_with_reference_types_runs_on_device():
+    # tools/shim_example.cpp built by build() against the reference's headers:
+    # tenkit::DenseTensor in, tenkit::TuckerTensor / DecompositionReport /
+    # HooiResult / FactorPair out, through the B200 library
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "shim_tenkit")
+    if not os.path.exists(exe):
+        pytest.skip("shim example not built (needs the reference headers at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "rel err" in p.stdout

@@ -18,6 +18,16 @@ int main() {
     auto [tk, rep] = tenkit_b200::st_hosvd(t, tenkit::Truncation{{2, 2, 2}}, std::nullopt,
                                            tenkit::FactorEngine::with_als(cfg));
     std::printf("rel err %.6e, modes %zu\n", rep.relative_residual, rep.per_mode.size());
+    // the primitives with the reference's signatures
+    tenkit::Matrix u(3, 5);
+    tenkit::DenseTensor p = tenkit_b200::mode_n_product(t, u, 2);
+    tenkit::DenseTensor q = tenkit_b200::multi_mode_product(t, {{u, 2}});
+    tenkit::HooiResult h = tenkit_b200::hooi(t, tenkit::Truncation{{2, 2, 2}}, tk, tenkit::HooiConfig{});
+    auto [pair, ar] = tenkit_b200::als_low_rank(t, 1, 2, cfg);
+    std::printf("%zu %zu %d %d %.3e %.3e\n", p.size(), q.size(), h.iterations, ar.iterations,
+                tenkit_b200::frobenius_norm(t), tenkit_b200::relative_error(t, p.size() == t.size() ? t : t));
+    (void)tenkit_b200::unfold_times(t, 1, pair.r);
+    (void)tenkit_b200::unfold_t_times(t, 1, pair.l);
   } catch (const tenkit::Error& e) {
     std::printf("tenkit error (category %d): %s\n", int(e.category()), e.what());
     return 2;
