@@ -115,6 +115,9 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     fc_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FcTmaArgs a) {
   using C = FcT<NC, MODE>;
+  // launched with programmatic stream serialization: this grid's launch
+  // overlaps the tail of the previous kernel; wait for its results here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -401,6 +404,7 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
     fr_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FrTmaArgs a) {
   using C = FrT<NC, MODE, MCOL>;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see fc_tma_kernel
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -755,6 +759,24 @@ cudaError_t set_smem(K k, size_t bytes) {
   return raise_smem_limit(k, bytes);
 }
 
+// Launch with programmatic stream serialization (PDL): the grid may begin
+// launching while the previous kernel on the stream drains; the kernel's
+// griddepcontrol.wait orders its reads after that kernel's writes.
+template <class K, class... Args>
+cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kThreadsTma);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int NC, int MODE>
 cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTmaArgs& a, int grid,
                           cudaStream_t st) {
@@ -762,8 +784,7 @@ cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTm
   auto k = fc_tma_kernel<NC, MODE>;
   cudaError_t e = set_smem(k, C::kSmem);
   if (e != cudaSuccess) return e;
-  k<<<grid, kThreadsTma, C::kSmem, st>>>(A, M, a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, C::kSmem, st, A, M, a);
 }
 
 template <int NC, int MODE, bool MCOL>
@@ -773,8 +794,7 @@ cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTm
   auto k = fr_tma_kernel<NC, MODE, MCOL>;
   cudaError_t e = set_smem(k, C::kSmem);
   if (e != cudaSuccess) return e;
-  k<<<grid, kThreadsTma, C::kSmem, st>>>(A, M, a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, C::kSmem, st, A, M, a);
 }
 
 #define TKG_NC_SWITCH(ncp, CALL)            \

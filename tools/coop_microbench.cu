@@ -93,6 +93,28 @@ int main() {
       printf("{\"bench\":\"flag_sync\",\"grid\":%d,\"n\":%d,\"us\":%.2f}\n", grid, n, ms * 1000);
     }
   }
+  // launch overhead: back-to-back empty kernels, cooperative vs regular launch
+  for (int grid : {148}) {
+    int n = 0;
+    void* args[] = {&n, &sink};
+    for (int kind = 0; kind < 2; ++kind) {
+      for (int w = 0; w < 3; ++w) {
+        if (kind == 0) cudaLaunchCooperativeKernel((void*)syncs, grid, 256, args, 0, 0);
+        else syncs<<<grid, 256>>>(n, sink);
+      }
+      cudaEventRecord(a);
+      for (int it = 0; it < 100; ++it) {
+        if (kind == 0) cudaLaunchCooperativeKernel((void*)syncs, grid, 256, args, 0, 0);
+        else syncs2<<<grid, 256>>>(n, sink);
+      }
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("{\"bench\":\"%s_launch\",\"grid\":%d,\"us_per_kernel\":%.2f}\n", kind ? "regular" : "cooperative",
+             grid, ms * 1000 / 100);
+    }
+  }
   for (int r : {10, 32, 64}) {
     for (int reps : {1, 11}) {
       gj<<<1, 256, 2 * r * r * 8>>>(r, reps, out);
