@@ -9,6 +9,7 @@
  *   tkg_select_order   <- tenkit::select_order   include/tenkit/hosvd.hpp:76,    src/hosvd.cpp:54-63
  *   tkg_als_low_rank   <- tenkit::als_low_rank   include/tenkit/als.hpp:69-71,   src/als.cpp:98-161
  *   tkg_als_init       <- tenkit::als_init       include/tenkit/als.hpp:46-47,   src/als.cpp:59-87
+ *   tkg_als_sweep      <- tenkit::als_sweep      include/tenkit/als.hpp:56-57,   src/als.cpp:89-96
  *   tkg_unfold_times   <- tenkit::unfold_times   include/tenkit/tensor_ops.hpp:39, src/tensor_ops.cpp:193-261
  *   tkg_unfold_t_times <- tenkit::unfold_t_times include/tenkit/tensor_ops.hpp:44, src/tensor_ops.cpp:263-330
  *   tkg_mode_n_product <- tenkit::mode_n_product include/tenkit/tensor_ops.hpp:22-23, src/tensor_ops.cpp:129-169
@@ -218,6 +219,13 @@ int tkg_als_low_rank(tkg_ctx* ctx, const double* a, int a_on_device, int32_t ord
 int tkg_als_init(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order,
                  const uint64_t* dims, uint32_t mode, uint64_t r, uint64_t seed, double* l_out,
                  tkg_error* err);
+
+/* als_sweep: one ALS sweep from l (I_mode x r): l_out = the updated left
+ * factor, r_out (nullable, fibers x r) = this sweep's right factor,
+ * *residual = the closed-form residual after the right update. A singular
+ * normal equation raises SingularGramError with spd_solve's message. */
+int tkg_als_sweep(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode,
+                  const double* l, uint64_t r, double* l_out, double* r_out, double* residual, tkg_error* err);
 
 /* Contraction primitives (host buffers). m is fibers x r (unfold_times) or
  * I_mode x r (unfold_t_times); u is rows x I_mode (mode_n_product). */

@@ -262,6 +262,23 @@ inline std::pair<tenkit::FactorPair, tenkit::AlsReport> als_low_rank(const tenki
   return {tenkit::FactorPair{tenkit::Matrix(I, r, std::move(l)), tenkit::Matrix(F, r, std::move(rr))}, ar};
 }
 
+// als.hpp:56-57
+inline std::pair<tenkit::FactorPair, double> als_sweep(const tenkit::DenseTensor& t, std::size_t mode,
+                                                       const tenkit::Matrix& l) {
+  std::vector<uint64_t> dims = dims_of(t.shape());
+  const uint64_t I = (mode >= 1 && mode <= dims.size()) ? dims[mode - 1] : 1;
+  const uint64_t F = I ? t.size() / I : 0;
+  std::vector<double> ln(l.rows() * l.cols(), 0.0), rr(F * l.cols(), 0.0);
+  double res = 0.0;
+  tkg_error e{};
+  check(tkg_als_sweep(Context::default_context().get(), t.data(), int32_t(dims.size()), dims.data(), uint32_t(mode),
+                      l.data(), l.cols(), ln.data(), rr.data(), &res, &e),
+        e);
+  return {tenkit::FactorPair{tenkit::Matrix(l.rows(), l.cols(), std::move(ln)),
+                             tenkit::Matrix(F, l.cols(), std::move(rr))},
+          res};
+}
+
 // tensor_ops.hpp:39 / :44
 inline tenkit::Matrix unfold_times(const tenkit::DenseTensor& t, std::size_t mode, const tenkit::Matrix& m) {
   std::vector<uint64_t> dims = dims_of(t.shape());

@@ -7,7 +7,7 @@ from .tenkit import (AlsConfig, AlsReport, Context, DecompositionReport, Degener
                      DeviceError, DeviceTensor, HooiConfig, HooiResult, DimensionMismatchError, Error, FactorEngine,
                      FormatError, InvalidModeError, IoError, ModeOrder, ModeReport,
                      NoConvergenceError, RankTooLargeError, SingularGramError, Truncation,
-                     TuckerTensor, UnsupportedError, ZeroReferenceError, als_init, als_low_rank,
+                     TuckerTensor, UnsupportedError, ZeroReferenceError, als_init, als_low_rank, als_sweep,
                      default_context, frobenius_norm, gram, hooi, mode_gram, mode_n_product, multi_mode_product,
                      reconstruct, recover_singular_vectors,
                      reduced_qr, sym_eig,

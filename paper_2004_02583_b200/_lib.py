@@ -109,6 +109,8 @@ SIGNATURES = [
                                    C.POINTER(TkgModeReport), C.POINTER(TkgError)]),
     ("tkg_als_init", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint32,
                                C.c_uint64, C.c_uint64, _dp, C.POINTER(TkgError)]),
+    ("tkg_als_sweep", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.c_uint64, _dp, _dp, _dp,
+                                C.POINTER(TkgError)]),
     ("tkg_unfold_times", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.c_uint64,
                                    _dp, C.POINTER(TkgError)]),
     ("tkg_unfold_t_times", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.c_uint64,

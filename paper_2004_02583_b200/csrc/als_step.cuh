@@ -27,7 +27,7 @@ struct AlsCtrl {
   int32_t max_iters;
   int32_t history_cap;
   int32_t degenerate_col;  // CholQR: als_init collapse column (1-based), 0 if none
-  int32_t pad;
+  int32_t pad;             // failing Gram column (1-based) of a singular solve
   double norm, norm_sq, prev, eta, residual, achieved, pivot;
 };
 

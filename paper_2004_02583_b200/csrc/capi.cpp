@@ -399,6 +399,15 @@ int tkg_als_low_rank(tkg_ctx* ctx, const double* a, int a_on_device, int32_t ord
   });
 }
 
+int tkg_als_sweep(tkg_ctx* ctx, const double* a, int32_t order, const uint64_t* dims, uint32_t mode,
+                  const double* l, uint64_t r, double* l_out, double* r_out, double* residual, tkg_error* err) {
+  return guarded(err, [&] {
+    tkg::Shape sh = make_shape(order, dims);
+    if (r > 0xffffffffu) tkg::raise(TKG_E_UNSUPPORTED, "als_sweep: rank too large");
+    eng(ctx).als_sweep(a, sh, int(mode), l, uint32_t(r), l_out, r_out, residual);
+  });
+}
+
 int tkg_als_init(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, const uint64_t* dims,
                  uint32_t mode, uint64_t r, uint64_t seed, double* l_out, tkg_error* err) {
   return guarded(err, [&] {

@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
       if (threadIdx.x == 0) {
         ctrl->error = kAlsErrRightSingular;
         ctrl->pivot = piv;
+        ctrl->pad = fail;  // failing column (1-based)
         ctrl->stop = 1;
       }
     } else {
@@ -633,6 +634,7 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
     if (threadIdx.x == 0) {
       ctrl->error = kAlsErrLeftSingular;
       ctrl->pivot = piv;
+      ctrl->pad = fail;  // failing column (1-based)
       ctrl->stop = 1;
     }
     return;

@@ -1419,6 +1419,98 @@ void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode
   collect(o, *rep);
 }
 
+// als_sweep (als.cpp:89-96): one right update from l, the closed-form
+// residual right after it, one left update; the sweep kernels of run_als on
+// a private control block (eta < 0: the stop rule never fires).
+void Engine::als_sweep(const double* a, const Shape& sh, int mode, const double* l, uint32_t r, double* l_out,
+                       double* r_out, double* residual) {
+  if (mode < 1 || mode > sh.N)
+    raise(1, "mode " + std::to_string(mode) + " out of range 1.." + std::to_string(sh.N));
+  if (r < 1 || r > kMaxRank) raise(12, "als_sweep: r must be in 1..64");
+  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
+  const uint32_t ncp = pad_nc(r);
+  const double* A = upload(a, sh.count(), false, tensor_, nullptr);
+  FiberView v{A, s, P, uint32_t(I), s, s * I};
+  double* Lc = l_.d(I * r);
+  CK(cudaMemcpyAsync(Lc, l, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
+  double* Mt = mt_.d(I * ncp);
+  double* R = r_.d(F * ncp + 8);
+  double* GL = gl_.d(kMaxRank * kMaxRank);
+  double* GLinv = cholL_.d(kMaxRank * kMaxRank);
+  double* GRinv = cholR_.d(kMaxRank * kMaxRank);
+  double* gpl = gram_part_.d(size_t(coop_partials_cap(sms_)) * r * r);
+  double* gs = gs_.d(size_t(r) * r);
+  const uint32_t nranges = fr_ranges(v, r);
+  double* part = fr_part_.d(size_t(nranges) * I * ncp);
+  double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
+  double* sumsq = sumsq_d_.d(2);
+  CK(launch_sumsq(A, sh.count(), sq, st_));
+  CK(launch_sum(sq, sumsq_partials_count(sh.count()), sumsq, st_));
+  AlsCtrl* ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
+  double* hist = hist_d_.d(2);
+  CK(launch_ctrl_init(ctrl, sumsq, -1.0, 2, 2, 0, st_));
+  const bool fused_gram = ncp <= kFcGramMaxNc;
+  const int nfin = std::max(finish_step_grid(F, sms_), fc_grid(v, Mt, ncp, r));
+  double* gpr = fc_gram_.d(size_t(nfin) * ncp * ncp);
+  PrepArgs pa;
+  pa.from_partials = 0;
+  pa.I = uint32_t(I);
+  pa.r = r;
+  pa.ncp = ncp;
+  pa.Lc = Lc;
+  pa.GL = GL;
+  pa.GLinv = GLinv;
+  pa.Mt = Mt;
+  pa.gpart = gpl;
+  pa.gs = gs;
+  pa.ctrl = ctrl;
+  coop_launch([&] { CK(launch_prep_step(pa, sms_, st_)); });
+  int fc_used = 0;
+  fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, false, &ctrl->stop,
+     fused_gram ? gpr : nullptr);
+  FinishArgs fa;
+  fa.R = R;
+  fa.F = F;
+  fa.ld = ncp;
+  fa.r = r;
+  fa.GL = GL;
+  fa.GRinv = GRinv;
+  fa.gpart = gpr;
+  fa.gs = gs;
+  fa.ctrl = ctrl;
+  fa.history = hist;
+  fa.gram_nparts = fused_gram ? fc_used : 0;
+  coop_launch([&] { CK(launch_finish_step(fa, sms_, st_)); });
+  if (r_out) {  // R of this sweep, column-major F x r, before the left update
+    double* rc = work_b_.d(F * r);
+    CK(launch_pack(R, 1, ncp, r, uint32_t(F), rc, uint32_t(F), st_));
+    CK(cudaMemcpyAsync(r_out, rc, F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  }
+  AlsCtrl h1;
+  CK(cudaMemcpyAsync(&h1, ctrl, sizeof(AlsCtrl), cudaMemcpyDeviceToHost, st_));
+  const uint32_t ranges = fr(v, R, ncp, 1, r, part, nullptr, false, nullptr, &ctrl->stop);
+  // left update L = Y G_R^{-1} (the prep step's phase B writes Lc; a singular
+  // Gram of the new L, which the reference never factors here, is ignored)
+  pa.from_partials = 1;
+  pa.part = part;
+  pa.nparts = int(ranges);
+  pa.ldp = ncp;
+  pa.GRinv = GRinv;
+  coop_launch([&] { CK(launch_prep_step(pa, sms_, st_)); });
+  double res = 0.0;
+  CK(cudaMemcpyAsync(&res, hist, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(l_out, Lc, I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  count_launch(8);
+  auto singular = [&](double piv, int col) {
+    raise(5, "spd_solve: pivot " + std::to_string(piv) + " at column " + std::to_string(col) +
+                 " is singular to working precision");
+  };
+  if (h1.error == kAlsErrZeroNorm) singular(0.0, 1);  // R = 0: R^T R has a zero pivot
+  if (h1.error == kAlsErrRightSingular || h1.error == kAlsErrLeftSingular) singular(h1.pivot, h1.pad);
+  if (residual) *residual = res;
+}
+
 void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,
                       uint64_t seed, double* l_out) {
   const uint64_t I = sh.extent(mode);

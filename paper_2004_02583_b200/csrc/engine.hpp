@@ -126,6 +126,10 @@ class Engine {
                     const AlsCfg& cfg, double* l_out, double* r_out, ModeRep* rep);
   void als_init(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r, uint64_t seed,
                 double* l_out);
+  // als_sweep (als.cpp:89-96): l (I x r, host) -> updated L, this sweep's R
+  // (F x r, nullable) and the closed-form residual after the right update
+  void als_sweep(const double* a, const Shape& sh, int mode, const double* l, uint32_t r, double* l_out,
+                 double* r_out, double* residual);
 
   // Sharded drivers (engine_dist.cpp): `a` is this rank's slab [begin,
   // begin + len) of the last mode of the global shape G (shard_range split);

@@ -547,6 +547,20 @@ class Context:
                                        _flat_ptr(fac), _flat_ptr(out), C.byref(err)), err)
         return out
 
+    def als_sweep(self, t, mode: int, l):
+        """als.cpp:89-96: (FactorPair(l_next, r), residual after the right update)."""
+        a = _host(t)
+        l = _host(l)
+        ext = a.shape[mode - 1] if 1 <= mode <= a.ndim else 1
+        r = l.shape[1]
+        ln = np.zeros(l.shape, order="F")
+        rr = np.zeros((a.size // max(1, ext), r), order="F")
+        res = C.c_double(0)
+        err = _lib.TkgError()
+        _raise(self._l.tkg_als_sweep(self._ctx, _flat_ptr(a), a.ndim, _lib.u64(a.shape), int(mode), _flat_ptr(l),
+                                     r, _flat_ptr(ln), _flat_ptr(rr), C.byref(res), C.byref(err)), err)
+        return (ln, rr), res.value
+
     def mode_gram(self, t, mode: int):
         """tensor_ops.cpp:332-389: A_(mode) A_(mode)^T."""
         a = _host(t)
@@ -688,6 +702,10 @@ def multi_mode_product(t, factors):
 
 def reconstruct(tucker):
     return default_context().reconstruct(tucker)
+
+
+def als_sweep(t, mode, l):
+    return default_context().als_sweep(t, mode, l)
 
 
 def mode_gram(t, mode):

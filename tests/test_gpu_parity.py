@@ -453,3 +453,27 @@ def test_multi_mode_product_and_reconstruct(ctx, ref):
     factors = [random_orthonormal(ref, d, r, 47 + d) for d, r in zip([20, 15, 10], [3, 4, 2])]
     tkr = tk.TuckerTensor(core, factors, (20, 15, 10))
     assert rel(ctx.reconstruct(tkr), ref.reconstruct(core, factors, [20, 15, 10])) <= 1e-13
+
+
+# ---- als_sweep (als.cpp:89-96) -----------------------------------------------------
+@pytest.mark.parametrize("dims,mode,r", [([7, 8, 6], 1, 2), ([40, 30, 20], 2, 10), ([64, 17, 40], 3, 32),
+                                         ([90, 64, 40], 1, 50), ([17, 4, 6, 5], 4, 3)], ids=str)
+def test_als_sweep_matches_reference(ctx, ref, dims, mode, r):
+    t = random_tensor(ref, dims, 600 + r)
+    l = random_matrix(ref, dims[mode - 1], r, 601 + r)
+    (ln, rr), res = ctx.als_sweep(t, mode, l)
+    ln_ref, rr_ref, res_ref = ref.als_sweep(t, mode, l)
+    assert rel(rr, rr_ref) <= 1e-12 and rel(ln, ln_ref) <= 1e-12
+    assert abs(res - res_ref) <= 1e-12 * max(1.0, res_ref)
+
+
+def test_als_sweep_singular_gram(ctx, ref):
+    # a rank-deficient L: spd_solve rejects L^T L (kernels.cpp:385-391)
+    t = random_tensor(ref, [9, 8, 7], 5)
+    l = np.asfortranarray(np.repeat(random_matrix(ref, 9, 1, 6), 2, axis=1))
+    with pytest.raises(tk.SingularGramError) as ei:
+        ctx.als_sweep(t, 1, l)
+    assert str(ei.value).startswith("spd_solve: pivot ") and "at column 2" in str(ei.value)
+    with pytest.raises(Exception) as er:
+        ref.als_sweep(t, 1, l)
+    assert "at column 2" in str(er.value)
