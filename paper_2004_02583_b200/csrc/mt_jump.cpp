@@ -290,10 +290,11 @@ std::vector<uint64_t> mt_jump_table(uint64_t J, int count) {
 MtPlan mt_plan(uint64_t total, bool side) {
   MtPlan p;
   p.total = total;
-  // A chunk costs one jump (19937 x 312 bit-word XORs, ~0.35 us of the whole
-  // GPU) and J/312 twists of one warp (~0.4 us each, latency-bound): the sum
-  // T/(312 C) * 0.4 + 0.35 C is smallest near C = sqrt(T / 256).
-  uint64_t C = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(total) / 256.0)));
+  // A chunk costs one jump (19937 x 312 bit-word XORs, ~1.3 us of the whole
+  // GPU) and J draws of one CTA (~1.6 ns each: a 312-draw block is three
+  // barriers, mt_gen_cta_kernel): 1.3 us C + 1.6 ns T / C is smallest near
+  // C = sqrt(T / 800).
+  uint64_t C = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(total) / 800.0)));
   C = std::max<uint64_t>(1, std::min<uint64_t>(C, 1184));
   // streams generated on the side stream, behind the sweeps of earlier modes,
   // are not latency-critical: a quarter of the chunks (a quarter of the jump

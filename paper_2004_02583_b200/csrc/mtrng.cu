@@ -1,5 +1,5 @@
 // Device side of the MT19937-64 jump-ahead (see mt_jump.hpp): chunk states
-// by GF(2) XOR-sums over the raw sequence, then one warp per chunk generates
+// by GF(2) XOR-sums over the raw sequence, then one CTA per chunk generates
 // its J draws with the standard twist (in-place semantics of
 // std::mersenne_twister_engine) and writes uniform01 values
 // ((y >> 11) * 2^-53, rng.hpp:19-21) straight into S (storage order, or the
@@ -88,18 +88,6 @@ __global__ void __launch_bounds__(32) mt_jump_kernel(const uint64_t* __restrict_
   }
 }
 
-// One warp per chunk with the 312-word state in registers: word j = 32*s + L
-// lives in slot s of lane L (slot 9 only for L < 24). A twist (in-place
-// std::mersenne_twister_engine semantics) is
-//   new[j] = twist(old[j], old[j+1], old[j+156])   j < 156
-//   new[j] = twist(old[j], old[j+1], new[j-156])   156 <= j < 311
-//   new[311] = twist(old[311], new[0], new[155])
-// with the neighbours fetched by warp shuffles: j+1 is lane L+1 (lane 0's
-// next slot for L = 31), j+156 = 32(s+4) + L+28 and j-156 = 32(s-5) + L+4, so
-// each source lane sends the slot its reader needs. No shared memory, no
-// barriers; the ten words of a slot are written as one coalesced row.
-constexpr int kGenWarps = 4;
-
 // n / d for n < 2^51 from a double reciprocal plus one correction step.
 __device__ __forceinline__ uint64_t fast_div(uint64_t n, uint64_t d, double inv) {
   uint64_t q = static_cast<uint64_t>(static_cast<double>(n) * inv);
@@ -109,94 +97,64 @@ __device__ __forceinline__ uint64_t fast_div(uint64_t n, uint64_t d, double inv)
   return q;
 }
 
-__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
-  return static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(v), src));
+// One CTA per chunk, one state word per thread (312 of 320 threads): the
+// twist's three dependency phases (j < 156 reads old words only; 156 <= j <
+// 311 reads new[j-156]; j = 311 reads new[0] and new[155]) are separated by
+// CTA barriers on a shared-memory state, so a 312-draw block costs a few
+// barriers instead of the warp version's chain of dependent shuffles; each
+// thread tempers and stores its own draw (consecutive positions, coalesced).
+constexpr int kGenThreads = 320;
+
+__device__ __forceinline__ void store_draw(double* __restrict__ out, const MtWindow& win, uint64_t p, double v) {
+  if (win.nloc == 0) {
+    out[p] = v;
+    return;
+  }
+  // S window (see MtWindow): position c*Fg + j -> column c, fiber j
+  const uint64_t col = fast_div(p, win.Fg, win.inv_fg);
+  const uint64_t j = p - col * win.Fg;
+  const uint64_t Fl = win.Fg / win.Gsm * win.nloc;
+  uint64_t loc = j;
+  if (win.Gsm > 1) {  // a shard: keep its own fibers, in its local order
+    const uint64_t t = fast_div(j, win.Plo, win.inv_plo);
+    const uint64_t jhi = fast_div(t, win.Gsm, win.inv_gsm);
+    const uint64_t ism = t - jhi * win.Gsm;
+    if (ism < win.o0 || ism >= win.o0 + win.nloc) return;
+    loc = (j - t * win.Plo) + win.Plo * ((ism - win.o0) + win.nloc * jhi);
+  }
+  out[win.ld ? loc * win.ld + col : loc + col * Fl] = v;
 }
 
-__global__ void __launch_bounds__(32 * kGenWarps) mt_gen_kernel(const uint64_t* __restrict__ states,
-                                                               int C, uint64_t J, uint64_t total,
-                                                               double* __restrict__ out, MtWindow win,
-                                                               const int* __restrict__ chunk_ids) {
-  const int warp = threadIdx.x >> 5, L = threadIdx.x & 31;
-  const int slot = blockIdx.x * kGenWarps + warp;
-  if (slot >= C) return;
+__global__ void __launch_bounds__(kGenThreads) mt_gen_cta_kernel(const uint64_t* __restrict__ states, uint64_t J,
+                                                                 uint64_t total, double* __restrict__ out,
+                                                                 MtWindow win, const int* __restrict__ chunk_ids) {
+  __shared__ uint64_t mt[kMtN];
+  const int slot = blockIdx.x;
   const int c = chunk_ids ? chunk_ids[slot] : slot;
+  const int j = threadIdx.x;
+  const bool own = j < kMtN;
   const uint64_t start = uint64_t(c) * J;
   const uint64_t end = min(start + J, total);
-  uint64_t w[10];
-#pragma unroll
-  for (int s = 0; s < 10; ++s) {
-    const int j = 32 * s + L;
-    w[s] = j < kMtN ? states[size_t(slot) * kMtN + j] : 0ull;
-  }
-  const int nxt = (L + 1) & 31, far = (L + 28) & 31, back = (L + 4) & 31;
-  uint64_t pos = start;
-  while (true) {
-    if (win.nloc == 0) {
-      if (pos + kMtN <= end) {
-#pragma unroll
-        for (int s = 0; s < 10; ++s)
-          if (s < 9 || L < 24) out[pos + 32 * s + L] = to_uniform01(w[s]);
-      } else {
-#pragma unroll
-        for (int s = 0; s < 10; ++s) {
-          const uint64_t j = 32 * s + L;
-          if ((s < 9 || L < 24) && pos + j < end) out[pos + j] = to_uniform01(w[s]);
-        }
-      }
-    } else {
-      // S window (see MtWindow): position c*Fg + j -> column c, fiber j
-      const uint64_t c0 = fast_div(pos, win.Fg, win.inv_fg);
-      const uint64_t j0 = pos - c0 * win.Fg;
-      const uint64_t Fl = win.Fg / win.Gsm * win.nloc;
-#pragma unroll
-      for (int s = 0; s < 10; ++s) {
-        const uint64_t k = 32 * s + L;
-        if (!(s < 9 || L < 24) || pos + k >= end) continue;
-        uint64_t j = j0 + k, col = c0;
-        while (j >= win.Fg) {
-          j -= win.Fg;
-          ++col;
-        }
-        uint64_t loc = j;
-        if (win.Gsm > 1) {  // a shard: keep its own fibers, in its local order
-          const uint64_t t = fast_div(j, win.Plo, win.inv_plo);
-          const uint64_t jhi = fast_div(t, win.Gsm, win.inv_gsm);
-          const uint64_t ism = t - jhi * win.Gsm;
-          if (ism < win.o0 || ism >= win.o0 + win.nloc) continue;
-          loc = (j - t * win.Plo) + win.Plo * ((ism - win.o0) + win.nloc * jhi);
-        }
-        out[win.ld ? loc * win.ld + col : loc + col * Fl] = to_uniform01(w[s]);
-      }
+  if (own) mt[j] = states[size_t(slot) * kMtN + j];
+  __syncthreads();
+  for (uint64_t pos = start;;) {
+    uint64_t cur = 0, nxt = 0, far = 0;
+    if (own) {
+      cur = mt[j];
+      if (pos + j < end) store_draw(out, win, pos + j, to_uniform01(cur));
+      nxt = mt[j + 1 < kMtN ? j + 1 : 0];
+      far = mt[j < 156 ? j + 156 : j - 156];
     }
     pos += kMtN;
     if (pos >= end) break;
-    // phase A: j = 32s + L < 156 (s <= 4; s = 4 for L < 28)
-    uint64_t na[5];
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-      const uint64_t v1 = shfl64(L == 0 ? w[s + 1] : w[s], nxt);
-      const uint64_t v2 = shfl64(L >= 28 ? w[s + 4] : w[s + 5], far);
-      na[s] = twist(w[s], v1, v2);
+    __syncthreads();                    // every old word is in registers
+    if (j < 156) mt[j] = twist(cur, nxt, far);
+    __syncthreads();                    // new[0 .. 155]
+    if (own && j >= 156) {
+      // j < 311: twist(old[j], old[j+1], new[j-156]); j = 311: twist(old[311], new[0], new[155])
+      mt[j] = j < kMtN - 1 ? twist(cur, nxt, mt[j - 156]) : twist(cur, mt[0], mt[155]);
     }
-    // phase B: 156 <= j < 311 (s = 4 for L >= 28, s = 5..9)
-    uint64_t nb[10];
-#pragma unroll
-    for (int s = 4; s < 10; ++s) {
-      const uint64_t v1 = shfl64(L == 0 ? w[s < 9 ? s + 1 : 9] : w[s], nxt);
-      const int ia = s - 4 < 4 ? s - 4 : 4, ib = s - 5 > 0 ? s - 5 : 0;
-      const uint64_t v3 = shfl64(s == 4 ? na[0] : (L < 4 ? na[ia] : na[ib]), back);
-      nb[s] = twist(w[s], v1, v3);
-    }
-    // j = 311 (lane 23, slot 9)
-    const uint64_t n0 = shfl64(na[0], 0), n155 = shfl64(na[4], 27);
-    const uint64_t n311 = twist(w[9], n0, n155);
-#pragma unroll
-    for (int s = 0; s < 4; ++s) w[s] = na[s];
-    w[4] = L < 28 ? na[4] : nb[4];
-#pragma unroll
-    for (int s = 5; s < 9; ++s) w[s] = nb[s];
-    w[9] = L < 23 ? nb[9] : (L == 23 ? n311 : 0ull);
+    __syncthreads();
   }
 }
 
@@ -217,8 +175,8 @@ cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C
 
 cudaError_t launch_mt_generate(const uint64_t* d_states, int C, const int* d_chunk_ids, uint64_t J,
                                uint64_t total, double* d_out, MtWindow win, cudaStream_t st) {
-  mt_gen_kernel<<<(C + kGenWarps - 1) / kGenWarps, 32 * kGenWarps, 0, st>>>(d_states, C, J, total, d_out,
-                                                                           win, d_chunk_ids);
+  if (C <= 0) return cudaSuccess;
+  mt_gen_cta_kernel<<<C, kGenThreads, 0, st>>>(d_states, J, total, d_out, win, d_chunk_ids);
   return cudaGetLastError();
 }
 
