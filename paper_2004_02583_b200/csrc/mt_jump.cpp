@@ -295,7 +295,9 @@ MtPlan mt_plan(uint64_t total, bool side) {
   // barriers, mt_gen_cta_kernel): 1.3 us C + 1.6 ns T / C is smallest near
   // C = sqrt(T / 800).
   uint64_t C = static_cast<uint64_t>(std::ceil(std::sqrt(static_cast<double>(total) / 800.0)));
-  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 1184));
+  // beyond two chunks per SM the generation runs at the machine's draw rate
+  // whatever C is, and only the jump work keeps growing
+  C = std::max<uint64_t>(1, std::min<uint64_t>(C, 296));
   // streams generated on the side stream, behind the sweeps of earlier modes,
   // are not latency-critical: a quarter of the chunks (a quarter of the jump
   // work competing with the sweeps for the SMs) and 4x longer chunks

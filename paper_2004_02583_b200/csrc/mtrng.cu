@@ -164,8 +164,9 @@ cudaError_t launch_mt_states(const uint64_t* d_y, const uint64_t* d_polys, int C
                              uint64_t* d_states, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_states, 0, sizeof(uint64_t) * size_t(C) * kMtN, st);
   if (e != cudaSuccess) return e;
-  // enough warps to fill the machine (~16 per SM), at least 5 words per warp
-  const int parts = std::max(4, std::min(64, (2368 + C - 1) / C));
+  // enough one-warp blocks to fill the machine (~48 per SM: small shared
+  // windows, so the XOR chains have other warps to hide behind)
+  const int parts = std::max(4, std::min(64, (7104 + C - 1) / C));
   const int wpp = (kPolyWords + parts - 1) / parts;
   const int nparts = (kPolyWords + wpp - 1) / wpp;
   const size_t smem = sizeof(uint64_t) * (size_t(wpp) * 64 + 32 * kJW + kJW);
