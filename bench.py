@@ -283,7 +283,7 @@ def reference_arm(args, c, world, rank):
         "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -438,11 +438,26 @@ def b200_arm(args, c, world, rank, local):
         "clocks": clocks.summary(),
         "device": torch.cuda.get_device_name(local),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line goes to the real stdout; everything native code
+    prints (NCCL's banner, for instance) was moved to stderr in main()."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
