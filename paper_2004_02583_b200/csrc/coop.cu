@@ -478,40 +478,61 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
 }
 
 // ---- finish_step -----------------------------------------------------------------
+constexpr int kFinRows = 128;   // rows of R per block of the row pass
+constexpr int kFinStages = 3;   // ring depth of the row pass
+
 template <int NC>
 __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
   cg::grid_group grid = cg::this_grid();
   AlsCtrl* ctrl = a.ctrl;
   if (ctrl->stop) return;
-  constexpr int kRows = 64, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2, kStg = 3;
+  constexpr int kRows = kFinRows, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2, kStg = kFinStages;
   extern __shared__ __align__(16) double sm[];
   double* tile = sm;  // [kStg][kRows][kLd]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
   const uint32_t r = a.r;
 
   // Phase 1 (R^T R not fused into FC): Gram partial of the CTA's contiguous
-  // row range of R (row-major [F][ld]). Each warp takes 2 of the 16 k-steps
-  // (4 rows each) of every 64-row block and accumulates ALL upper 8x8 tiles
-  // for them, loading each column tile's fragment once per k-step (kNT loads
-  // for kTri DMMAs); the 8 warp partials are summed in a fixed order.
+  // row range of R (row-major [F][ld]), streamed in kFinRows-row blocks through a
+  // kStg-deep cp.async ring into padded rows (kLd = NC + 4: conflict-free
+  // fragment loads); each thread copies one 16-byte column chunk of every
+  // kRpp-th row. Each warp takes kKs consecutive k-steps (4 rows each) of
+  // every block and accumulates ALL upper 8x8 tiles for them,
+  // loading each column tile's fragment once per k-step (kNT loads for kTri
+  // DMMAs); the 8 warp partials are summed in a fixed order.
   if (a.gram_nparts == 0 && a.mode != 2) {
+    // copy map: kRpp rows of kCpr 16-byte chunks per pass of the CTA
+    constexpr int kCpr = NC / 2, kRpp = kThreads / kCpr, kPasses = (kRows + kRpp - 1) / kRpp;
+    constexpr int kKs = kRows / 32;  // k-steps of 4 rows per warp per block
     double acc[kTri][2];
 #pragma unroll
     for (int k = 0; k < kTri; ++k) acc[k][0] = acc[k][1] = 0.0;
     const uint64_t nblk = (a.F + kRows - 1) / kRows;
     const uint64_t per = (nblk + gridDim.x - 1) / gridDim.x;
     const uint64_t b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
-    // kStg-deep cp.async ring of 64-row blocks of R
+    const int crow = threadIdx.x < kRpp * kCpr ? int(threadIdx.x) / kCpr : kRows;
+    const int ccol = (int(threadIdx.x) % kCpr) * 2;
+    const uint32_t goff = uint32_t(crow) * uint32_t(a.ld) + ccol, gstep = uint32_t(kRpp) * uint32_t(a.ld);
+    const int soff = crow * kLd + ccol;
     auto issue = [&](uint64_t b, int slot) {
-      double* t = tile + size_t(slot) * kRows * kLd;
-      for (int e = threadIdx.x; e < kRows * (NC / 2); e += blockDim.x) {
-        const int row = e / (NC / 2), c = (e % (NC / 2)) * 2;
-        const uint64_t gr = b * kRows + row;
-        if (gr < a.F) {
-          cp_async16(t + row * kLd + c, a.R + gr * a.ld + c);
-        } else {
-          t[row * kLd + c] = 0.0;
-          t[row * kLd + c + 1] = 0.0;
+      double* t = tile + size_t(slot) * kRows * kLd + soff;
+      const double* g = a.R + b * kRows * a.ld + goff;
+      const uint64_t left = a.F - b * kRows;
+      if (left >= uint64_t(kRows)) {
+#pragma unroll
+        for (int j = 0; j < kPasses; ++j)
+          if (crow + j * kRpp < kRows) cp_async16(t + j * kRpp * kLd, g + j * gstep);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kPasses; ++j) {
+          const int row = crow + j * kRpp;
+          if (row >= kRows) continue;
+          if (uint64_t(row) < left) {
+            cp_async16(t + j * kRpp * kLd, g + j * gstep);
+          } else {
+            t[j * kRpp * kLd] = 0.0;
+            t[j * kRpp * kLd + 1] = 0.0;
+          }
         }
       }
     };
@@ -528,8 +549,8 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
       cp_async_commit();
       const double* t = tile + size_t(slot) * kRows * kLd;
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const double* rp = t + ((warp * 2 + ks) * 4 + q) * kLd;
+      for (int ks = 0; ks < kKs; ++ks) {
+        const double* rp = t + ((warp * kKs + ks) * 4 + q) * kLd;
         double fr[kNT];
 #pragma unroll
         for (int c = 0; c < kNT; ++c) fr[c] = rp[c * 8 + r8];
@@ -801,7 +822,7 @@ size_t rows_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1
 int coop_partials_cap(int num_sms) { return num_sms * (2048 / kThreads); }
 
 int finish_step_grid(uint64_t F, int num_sms) {
-  return int(std::max<uint64_t>(1, std::min<uint64_t>((F + 63) / 64, uint64_t(num_sms))));
+  return int(std::max<uint64_t>(1, std::min<uint64_t>((F + kFinRows - 1) / kFinRows, uint64_t(num_sms))));
 }
 
 #define TKG_KE_SWITCH(r, CALL) \
@@ -822,7 +843,7 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
                    : a.gram_nparts ? int(std::min<uint32_t>(uint32_t(num_sms), (ntri + 7) / 8))
                                    : finish_step_grid(a.F, num_sms);
   const uint32_t ncp = a.r <= 8 ? 8 : (a.r + 7) / 8 * 8;
-  const size_t smem = sizeof(double) * std::max<size_t>(3 * 64 * (ncp + 4), 2 * size_t(a.r) * a.r);
+  const size_t smem = sizeof(double) * std::max<size_t>(size_t(kFinStages) * kFinRows * (ncp + 4), 2 * size_t(a.r) * a.r);
   switch (ncp) {
 #define TKG_F(N) \
   case N: return coop_launch(finish_step_kernel<N>, want, num_sms, smem, &a, st);
