@@ -124,6 +124,8 @@ Engine::Engine(int device) : device_(device) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&st2_, cudaStreamNonBlocking, lo));  // lowest priority
     CK(cudaEventCreateWithFlags(&pre_gate_, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&cp_st_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&out_ready_, cudaEventDisableTiming));
   }
   CK(cudaHostAlloc(reinterpret_cast<void**>(&status_h_), sizeof(DevStatus), cudaHostAllocMapped));
   std::memset(status_h_, 0, sizeof(DevStatus));
@@ -153,6 +155,9 @@ Engine::~Engine() {
   for (auto ev : pre_ev_) cudaEventDestroy(ev);
   cudaEventDestroy(pre_gate_);
   if (status_h_) cudaFreeHost(status_h_);
+  cudaStreamSynchronize(cp_st_);
+  cudaEventDestroy(out_ready_);
+  cudaStreamDestroy(cp_st_);
   cudaStreamDestroy(st2_);
   cudaStreamDestroy(st_);
 }
@@ -1064,6 +1069,11 @@ void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint
 double Engine::relative_residual_dev(const double* A, const Shape& sh,
                                      const std::vector<uint64_t>& ranks, const double* d_core,
                                      const std::vector<double*>& d_factors, const double* ref_sumsq_host) {
+  return residual_read(residual_enqueue(A, sh, ranks, d_core, d_factors), ref_sumsq_host);
+}
+
+double* Engine::residual_enqueue(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                                 const double* d_core, const std::vector<double*>& d_factors) {
   Shape cur;
   cur.N = sh.N;
   for (int k = 0; k < sh.N; ++k) cur.d[k] = ranks[k];
@@ -1119,12 +1129,41 @@ double Engine::relative_residual_dev(const double* A, const Shape& sh,
   double* out = misc2_.d(1);
   CK(launch_sum(sq, nsq, out, st_));
   if (dist_) dist_->allreduce_sum(out, 1, st_);
+  return out;
+}
+
+double Engine::residual_read(const double* out, const double* ref_sumsq_host) {
   double diff_sq = 0.0;
   CK(cudaMemcpyAsync(&diff_sq, out, sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
   const double ref_sumsq = *ref_sumsq_host;
   if (ref_sumsq == 0.0) raise(3, "relative_error: reference tensor has zero norm");
   return std::sqrt(diff_sq / ref_sumsq);
+}
+
+// Results to the caller and the relative residual (hosvd.cpp:123,189). The
+// core and factors go out on the copy stream while the residual expansion
+// runs on the main stream: a copy to pageable host memory blocks the host
+// until it completes, so the residual kernels are enqueued first and the
+// transfer overlaps them. Destinations may be host or device pointers (UVA).
+void Engine::outputs_and_residual(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                                  const Shape& cs, const double* core_buf, const std::vector<double*>& U,
+                                  const double* ref_sumsq, double* core, double* factors, DecompRep* rep) {
+  const auto tr = Clock::now();
+  CK(cudaEventRecord(out_ready_, st_));
+  const double* out = residual_enqueue(A, sh, ranks, core_buf, U);
+  const auto td = Clock::now();
+  CK(cudaStreamWaitEvent(cp_st_, out_ready_, 0));
+  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDefault, cp_st_));
+  size_t ofs = 0;
+  for (int n = 0; n < sh.N; ++n) {
+    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDefault, cp_st_));
+    ofs += sh.d[n] * ranks[n];
+  }
+  CK(cudaStreamSynchronize(cp_st_));
+  rep->d2h_seconds = since(td);
+  rep->relative_residual = residual_read(out, ref_sumsq);
+  rep->residual_seconds = since(tr);
 }
 
 // Reports, D2H and the residual of an SVD / EIG decomposition (the modes carry
@@ -1146,18 +1185,7 @@ void Engine::finish_exact(const Shape& sh, const std::vector<uint64_t>& ranks, c
   rep->launches = launches_;
   rep->passes = passes_;
   rep->bytes = bytes_;
-  const auto td = Clock::now();
-  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  size_t ofs = 0;
-  for (int n = 0; n < sh.N; ++n) {
-    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    ofs += sh.d[n] * ranks[n];
-  }
-  sync();
-  rep->d2h_seconds = since(td);
-  const auto tr = Clock::now();
-  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
-  rep->residual_seconds = since(tr);
+  outputs_and_residual(A, sh, ranks, cs, core_buf, U, ref_sumsq, core, factors, rep);
 }
 
 void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::vector<uint64_t>& ranks,
@@ -1254,18 +1282,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   rep->launches = launches_;
   rep->passes = passes_;
   rep->bytes = bytes_;
-  const auto td = Clock::now();
-  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  size_t ofs = 0;
-  for (int n = 0; n < sh.N; ++n) {
-    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    ofs += sh.d[n] * ranks[n];
-  }
-  sync();
-  rep->d2h_seconds = since(td);
-  const auto tr = Clock::now();
-  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
-  rep->residual_seconds = since(tr);
+  outputs_and_residual(A, sh, ranks, cs, core_buf, U, ref_sumsq, core, factors, rep);
   trace("residual synced");
 }
 
@@ -1383,18 +1400,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
   rep->launches = launches_;
   rep->passes = passes_;
   rep->bytes = bytes_;
-  const auto td = Clock::now();
-  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  size_t ofs = 0;
-  for (int n = 0; n < sh.N; ++n) {
-    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    ofs += sh.d[n] * ranks[n];
-  }
-  sync();
-  rep->d2h_seconds = since(td);
-  const auto tr = Clock::now();
-  rep->relative_residual = relative_residual_dev(A, sh, ranks, core_buf, U, ref_sumsq);
-  rep->residual_seconds = since(tr);
+  outputs_and_residual(A, sh, ranks, cs, core_buf, U, ref_sumsq, core, factors, rep);
 }
 
 void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,

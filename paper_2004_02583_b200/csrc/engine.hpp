@@ -257,6 +257,14 @@ class Engine {
   double relative_residual_dev(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                                const double* d_core, const std::vector<double*>& d_factors,
                                const double* ref_sumsq_host);
+  // the same split: expansion kernels + difference norm on st_ (returns the
+  // device scalar), then the synchronising read
+  double* residual_enqueue(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
+                           const double* d_core, const std::vector<double*>& d_factors);
+  double residual_read(const double* d_diff_sq, const double* ref_sumsq_host);
+  void outputs_and_residual(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks, const Shape& cs,
+                            const double* core_buf, const std::vector<double*>& U, const double* ref_sumsq,
+                            double* core, double* factors, DecompRep* rep);
   // TTMs of modes 1..last_mode (0 = all) with U_n^T, ascending (hosvd.cpp:115-121)
   void core_chain(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                   const std::vector<double*>& d_factors, double* d_core, int last_mode = 0);
@@ -293,6 +301,8 @@ class Engine {
   cudaStream_t st_;
   cudaStream_t st2_;  // low-priority side stream for the initializer streams
   cudaEvent_t pre_gate_;
+  cudaStream_t cp_st_;      // result copies (overlap the residual expansion)
+  cudaEvent_t out_ready_;
   struct PreS {
     double* ptr;
     cudaEvent_t ready;
