@@ -1152,6 +1152,7 @@ void Engine::outputs_and_residual(const double* A, const Shape& sh, const std::v
   const auto tr = Clock::now();
   CK(cudaEventRecord(out_ready_, st_));
   const double* out = residual_enqueue(A, sh, ranks, core_buf, U);
+  trace("residual enqueued");
   const auto td = Clock::now();
   CK(cudaStreamWaitEvent(cp_st_, out_ready_, 0));
   CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDefault, cp_st_));
@@ -1161,6 +1162,7 @@ void Engine::outputs_and_residual(const double* A, const Shape& sh, const std::v
     ofs += sh.d[n] * ranks[n];
   }
   CK(cudaStreamSynchronize(cp_st_));
+  trace("results copied");
   rep->d2h_seconds = since(td);
   rep->relative_residual = residual_read(out, ref_sumsq);
   rep->residual_seconds = since(tr);
@@ -1376,7 +1378,17 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     double* dst = bufs[which]->d(nxt.count());
     const int nsh = shrink_count(F);
     double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (profiling_) {
+      ev = ev_pair();
+      CK(cudaEventRecord(ev.first, st_));
+    }
     CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_));
+    if (profiling_) {
+      // shrink: reads R (F x r), writes the r x F working tensor, 2 r^2 F flops
+      CK(cudaEventRecord(ev.second, st_));
+      record(kClsTTM, ev.first, ev.second, 16.0 * double(F) * r, 2.0 * double(F) * r * r);
+    }
     CK(launch_sum(sq, nsh, sumsq_d_.d(2), st_));
     count_launch(2);
     (void)RhT;
