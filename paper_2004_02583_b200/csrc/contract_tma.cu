@@ -602,12 +602,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // ---------------------------------------------------------------------------
-// Expansion along the last mode fused with the difference norm:
-//   sq += sum_{j, i} (ref[j + i*F] - sum_c X[j + c*F] U[i + c*Iout])^2
-// (relative_error(t, reconstruct(tk)) without the reconstruction,
-// tensor_ops.cpp:395-440). A CTA keeps the A fragments of a 128-fiber tile
-// of X in registers for all Iout columns; the producer warp streams 32-column
-// blocks of U and of the reference through the TMA ring.
+// Mode expansion out(jl, i, p) = sum_c X(jl, c, p) U[i + c*Iout], X read as
+// the 3-D view X[jl + c*s + p*s*K] (reconstruct, tensor_ops.cpp:395-440).
+// A CTA keeps the A fragments of a 128-fiber tile of X (inside one panel) in
+// registers for all Iout columns; the producer warp streams 32-column blocks
+// of U through the TMA ring. Two epilogues:
+//   DIFF  (last mode, s = F, P = 1): fused with the difference norm,
+//         sq += sum (ref[j + i*F] - out(j, i))^2 with 32-column blocks of the
+//         reference streamed beside U (relative_error(t, reconstruct(tk))
+//         without the reconstruction);
+//   STORE (intermediate modes): out[jl + i*s + p*s*Iout] written directly.
 // ---------------------------------------------------------------------------
 template <int KC>
 struct ExT {
@@ -621,11 +625,11 @@ struct ExT {
   static constexpr size_t kSmem = 1024 + size_t(kBytesX) + size_t(kStages) * kStageBytes;
 };
 
-template <int KC>
+template <int KC, bool DIFF>
 __global__ void __launch_bounds__(kThreadsTma, 1)
-    expand_diff_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmU,
-                           const __grid_constant__ CUtensorMap tmR, uint64_t F, uint32_t Iout,
-                           double* sumsq_part) {
+    expand_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmU,
+                      const __grid_constant__ CUtensorMap tmR, uint64_t s, uint64_t P, uint32_t Iout,
+                      double* sumsq_part, double* out) {
   using C = ExT<KC>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -635,7 +639,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   double* Xs = reinterpret_cast<double*>(smem_raw + 1024);
   unsigned char* ring = smem_raw + 1024 + C::kBytesX;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t ntiles = (F + C::kTF - 1) / C::kTF;
+  const uint64_t tpp = (s + C::kTF - 1) / C::kTF;  // tiles per panel
+  const uint64_t ntiles = tpp * P;
   const int nblk = int((Iout + C::kCB - 1) / C::kCB);
 
   if (threadIdx.x == 0) {
@@ -656,18 +661,18 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       prefetch_map(&tmR);
       uint32_t it = 0, xt = 0;
       for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++xt) {
-        const int j0 = int(tile * C::kTF);
+        const int p = int(tile / tpp), j0 = int((tile % tpp) * C::kTF);
         mbar_wait(xempty, (xt & 1) ^ 1);
         mbar_arrive_expect_tx(xfull, KC * C::kLdX * 8);
-        tma_2d(Xs, &tmX, xfull, j0, 0);
+        tma_3d(Xs, &tmX, xfull, j0, 0, p);
         for (int b = 0; b < nblk; ++b, ++it) {
           const int slot = it % C::kStages;
           const uint32_t ph = (it / C::kStages) & 1;
           mbar_wait(&empty[slot], ph ^ 1);
           unsigned char* st = ring + size_t(slot) * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[slot], C::kBytesU + C::kBytesR);
+          mbar_arrive_expect_tx(&full[slot], DIFF ? C::kBytesU + C::kBytesR : C::kBytesU);
           tma_2d(st, &tmU, &full[slot], b * C::kCB, 0);
-          tma_2d(st + C::kBytesU, &tmR, &full[slot], j0, b * C::kCB);
+          if (DIFF) tma_2d(st + C::kBytesU, &tmR, &full[slot], j0, b * C::kCB);
         }
       }
     }
@@ -678,6 +683,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   double sqv[4] = {0.0, 0.0, 0.0, 0.0};  // independent chains (see the FR init pass)
   uint32_t it = 0, xt = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++xt) {
+    const uint64_t p = tile / tpp, j0 = (tile % tpp) * C::kTF;
     mbar_wait(xfull, xt & 1);
     double af[KC / 4][2];
 #pragma unroll
@@ -707,20 +713,35 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 #pragma unroll
           for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[t][m], bf[n]);
       }
-      // rows past F / columns past Iout: TMA zero-fill on both sides
+      if (DIFF) {
+        // rows past F / columns past Iout: TMA zero-fill on both sides
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+        for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int n = 0; n < 4; ++n)
+          for (int n = 0; n < 4; ++n)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double d = Rs[(n * 8 + 2 * q + e) * C::kLdR + warp * 16 + m * 8 + r8] - acc[m][n][e];
-            sqv[(n & 1) * 2 + e] = fma(d, d, sqv[(n & 1) * 2 + e]);
-          }
+            for (int e = 0; e < 2; ++e) {
+              const double d = Rs[(n * 8 + 2 * q + e) * C::kLdR + warp * 16 + m * 8 + r8] - acc[m][n][e];
+              sqv[(n & 1) * 2 + e] = fma(d, d, sqv[(n & 1) * 2 + e]);
+            }
+      } else {
+        const uint32_t i0 = b * C::kCB + 2 * q;  // column of acc[.][0][0]
+        double* ob = out + (p * Iout + i0) * s + j0 + warp * 16 + r8;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          if (j0 + warp * 16 + m * 8 + r8 >= s) continue;
+#pragma unroll
+          for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (i0 + n * 8 + e < Iout) ob[m * 8 + (n * 8 + e) * s] = acc[m][n][e];
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
   }
+  if (!DIFF) return;
   __shared__ double red[kCons];
   double sq = (sqv[0] + sqv[1]) + (sqv[2] + sqv[3]);
 #pragma unroll
@@ -811,13 +832,13 @@ cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTm
   }
 
 template <int KC>
-cudaError_t expand_diff_launch(const CUtensorMap& X, const CUtensorMap& U, const CUtensorMap& R,
-                               const ExpandArgs& a, int grid, cudaStream_t st) {
+cudaError_t expand_tma_launch(const CUtensorMap& X, const CUtensorMap& U, const CUtensorMap& R,
+                              const ExpandArgs& a, int grid, cudaStream_t st) {
   using C = ExT<KC>;
-  auto k = expand_diff_tma_kernel<KC>;
+  auto k = a.ref ? expand_tma_kernel<KC, true> : expand_tma_kernel<KC, false>;
   cudaError_t e = set_smem(k, C::kSmem);
   if (e != cudaSuccess) return e;
-  k<<<grid, kThreadsTma, C::kSmem, st>>>(X, U, R, a.s * a.P, a.Iout, a.sumsq_part);
+  k<<<grid, kThreadsTma, C::kSmem, st>>>(X, U, R, a.s, a.P, a.Iout, a.sumsq_part, a.out);
   return cudaGetLastError();
 }
 
@@ -1012,20 +1033,30 @@ bool expand_diff_tma_ok(const ExpandArgs& a) {
          F < (1ull << 31) && aligned16(a.in) && aligned16(a.U) && aligned16(a.ref) && a.sumsq_part;
 }
 
-int expand_diff_tma_grid(uint64_t F, int num_sms) {
-  const uint64_t tiles = (F + 127) / 128;
+bool expand_tma_ok(const ExpandArgs& a) {
+  return encode_fn() && !a.ref && a.out && a.K >= 1 && a.K <= 64 && a.s % 2 == 0 && a.Iout % 2 == 0 &&
+         a.s < (1ull << 31) && a.P < (1ull << 31) && aligned16(a.in) && aligned16(a.U);
+}
+
+int expand_diff_tma_grid(uint64_t F, int num_sms) { return expand_tma_grid(F, 1, num_sms); }
+
+int expand_tma_grid(uint64_t s, uint64_t P, int num_sms) {
+  const uint64_t tiles = (s + 127) / 128 * P;
   return int(std::max<uint64_t>(1, std::min<uint64_t>(tiles, uint64_t(num_sms))));
 }
 
 cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used) {
-  const uint64_t F = a.s * a.P;
+  return launch_expand_tma(a, num_sms, st, grid_used);
+}
+
+cudaError_t launch_expand_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used) {
   const uint32_t kc = (a.K + 7) / 8 * 8;  // K padded to the DMMA k granularity used here
   CUtensorMap X, U, R;
   {
-    const uint64_t dims[2] = {F, a.K};
-    const uint64_t strides[1] = {F * 8};
-    const uint32_t box[2] = {132, kc};
-    if (!encode(&X, a.in, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    const uint64_t dims[3] = {a.s, a.K, a.P};
+    const uint64_t strides[2] = {a.s * 8, a.s * a.K * 8};
+    const uint32_t box[3] = {132, kc, 1};
+    if (!encode(&X, a.in, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[2] = {a.Iout, a.K};
@@ -1033,23 +1064,26 @@ cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_
     const uint32_t box[2] = {36, kc};
     if (!encode(&U, a.U, 2, dims, strides, box)) return cudaErrorInvalidValue;
   }
-  {
+  if (a.ref) {
+    const uint64_t F = a.s * a.P;
     const uint64_t dims[2] = {F, a.Iout};
     const uint64_t strides[1] = {F * 8};
     const uint32_t box[2] = {132, 32};
     if (!encode(&R, a.ref, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
+    R = U;  // unused by the STORE epilogue
   }
-  const int grid = expand_diff_tma_grid(F, num_sms);
+  const int grid = expand_tma_grid(a.s, a.P, num_sms);
   if (grid_used) *grid_used = grid;
   switch (kc) {
-    case 8: return expand_diff_launch<8>(X, U, R, a, grid, st);
-    case 16: return expand_diff_launch<16>(X, U, R, a, grid, st);
-    case 24: return expand_diff_launch<24>(X, U, R, a, grid, st);
-    case 32: return expand_diff_launch<32>(X, U, R, a, grid, st);
-    case 40: return expand_diff_launch<40>(X, U, R, a, grid, st);
-    case 48: return expand_diff_launch<48>(X, U, R, a, grid, st);
-    case 56: return expand_diff_launch<56>(X, U, R, a, grid, st);
-    default: return expand_diff_launch<64>(X, U, R, a, grid, st);
+    case 8: return expand_tma_launch<8>(X, U, R, a, grid, st);
+    case 16: return expand_tma_launch<16>(X, U, R, a, grid, st);
+    case 24: return expand_tma_launch<24>(X, U, R, a, grid, st);
+    case 32: return expand_tma_launch<32>(X, U, R, a, grid, st);
+    case 40: return expand_tma_launch<40>(X, U, R, a, grid, st);
+    case 48: return expand_tma_launch<48>(X, U, R, a, grid, st);
+    case 56: return expand_tma_launch<56>(X, U, R, a, grid, st);
+    default: return expand_tma_launch<64>(X, U, R, a, grid, st);
   }
 }
 

@@ -66,5 +66,9 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
 bool expand_diff_tma_ok(const ExpandArgs& a);
 int expand_diff_tma_grid(uint64_t F, int num_sms);
 cudaError_t launch_expand_diff_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used);
+// intermediate-mode expansion (a.ref null, a.out set), s even
+bool expand_tma_ok(const ExpandArgs& a);
+int expand_tma_grid(uint64_t s, uint64_t P, int num_sms);
+cudaError_t launch_expand_tma(const ExpandArgs& a, int num_sms, cudaStream_t st, int* grid_used);
 
 }  // namespace tkg

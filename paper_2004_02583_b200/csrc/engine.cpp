@@ -1110,6 +1110,8 @@ double* Engine::residual_enqueue(const double* A, const Shape& sh, const std::ve
     if (last && !force_v1_ && expand_diff_tma_ok(ea)) {
       nsq = expand_diff_tma_grid(F, sms_);
       CK(launch_expand_diff_tma(ea, sms_, st_, nullptr));
+    } else if (!last && !force_v1_ && expand_tma_ok(ea)) {
+      CK(launch_expand_tma(ea, sms_, st_, nullptr));
     } else {
       if (last) nsq = expand_grid(F, sms_);
       CK(launch_expand(ea, sms_, st_, nullptr));
