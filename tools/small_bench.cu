@@ -26,7 +26,7 @@ int main() {
   cudaEventCreate(&b);
   struct Case { uint32_t I, r; int nparts; };
   for (Case c : {Case{256, 10, 0}, Case{256, 10, 78}, Case{1024, 32, 0}, Case{1024, 32, 37}, Case{2048, 64, 0},
-                 Case{200, 50, 0}, Case{200, 50, 40}}) {
+                 Case{200, 50, 0}, Case{200, 50, 40}, Case{200, 50, 148}, Case{200, 50, 296}}) {
     const uint32_t ncp = (c.r + 7) / 8 * 8;
     const int np = std::max(c.nparts, 1);
     std::vector<double> h(size_t(np) * c.I * ncp);
