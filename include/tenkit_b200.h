@@ -116,8 +116,9 @@ typedef struct tkg_report {
   double relative_residual; /* outside the timed region, as the reference */
   double seconds;           /* factor + core computation (hosvd.cpp:82,122) */
   double h2d_seconds;       /* host->device copy of a (0 when a_on_device) */
-  double d2h_seconds;       /* core + factors device->host */
-  double residual_seconds;  /* relative_residual evaluation */
+  double d2h_seconds;       /* core + factors device->host (t/st drivers: overlaps
+                               the residual evaluation, on a copy stream) */
+  double residual_seconds;  /* relative_residual evaluation (incl. the copies) */
   uint64_t kernel_launches; /* our kernels launched for the timed region */
   uint64_t tensor_passes;   /* full passes over the working tensor */
   uint64_t algorithmic_bytes; /* sum of 8*(|A| + F r + I r) per contraction pass */
