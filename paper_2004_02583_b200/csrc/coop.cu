@@ -57,28 +57,33 @@ constexpr int kThreads = 256;
 constexpr int kMaxR = 64;
 constexpr int kGE = (kMaxR * kMaxR + kThreads - 1) / kThreads;  // Gram entries per thread
 
-// entries of an r x r matrix per thread
-__host__ __device__ constexpr int ke_for(int r) { return (r * r + kThreads - 1) / kThreads; }
+// entries of an r x r matrix per thread: a kB x kB block, kB = ceil(r / 16)
+__host__ __device__ constexpr int kb_for(int r) { return (r + 15) / 16; }
+__host__ __device__ constexpr int ke_for(int r) { return kb_for(r) * kb_for(r); }
 
 // ---- one-CTA dense kernels (CTA 0), register-resident -------------------------------
-// Thread t owns the column-major entries e = t + k*kThreads (k < KE); entries
-// past r*r get the dummy index (r, r), which every step treats as a no-op
-// owner of slot r of the shared vectors (sized kMaxR + 1).
+// The r x r matrix is tiled 16 x 16 over the threads: thread t owns the
+// kB x kB block of rows i0 + a, columns j0 + b (i0 = (t % 16) kB,
+// j0 = (t / 16) kB), entry t' = a + b kB. A step needs kB entries of the
+// published row / column per thread instead of one per owned entry (the
+// steps are shared-memory bound). Entries past r are dummies: they read the
+// spare slots of the shared vectors (sized kMaxR + 1 >= 16 kB), never
+// publish into a live slot and are never stored.
 template <int KE>
 struct Owned {
+  static constexpr int kB = KE == 1 ? 1 : KE == 4 ? 2 : KE == 9 ? 3 : 4;
+  static_assert(kB * kB == KE, "KE must be a square");
   double v[KE];
-  int i[KE], j[KE];
-  __device__ explicit Owned(uint32_t r) {
+  int i0, j0;
+  __device__ explicit Owned(uint32_t) {
+    i0 = int(threadIdx.x % 16) * kB;
+    j0 = int(threadIdx.x / 16) * kB;
 #pragma unroll
-    for (int t = 0; t < KE; ++t) {
-      const uint32_t e = threadIdx.x + t * kThreads;
-      const bool ok = e < r * r;
-      i[t] = ok ? int(e % r) : int(r);
-      j[t] = ok ? int(e / r) : int(r);
-      v[t] = 0.0;
-    }
+    for (int t = 0; t < KE; ++t) v[t] = 0.0;
   }
-  __device__ bool valid(int t, uint32_t r) const { return i[t] < int(r); }
+  __device__ int i(int t) const { return i0 + t % kB; }
+  __device__ int j(int t) const { return j0 + t / kB; }
+  __device__ bool valid(int t, uint32_t r) const { return i(t) < int(r) && j(t) < int(r); }
 };
 
 // Lower Cholesky factor of G (column-major, smem) into L (smem): right-looking
@@ -87,13 +92,15 @@ struct Owned {
 // Returns the failing column + 1 or 0.
 template <int KE>
 __device__ int chol_reg(const double* G, double* L, uint32_t r) {
+  constexpr int B = Owned<KE>::kB;
   __shared__ double cb[2][kMaxR + 1];
   __shared__ double dg[kMaxR + 1];
   Owned<KE> o(r);
 #pragma unroll
   for (int t = 0; t < KE; ++t) {
-    if (o.valid(t, r) && o.i[t] >= o.j[t]) o.v[t] = G[o.i[t] + o.j[t] * r];
-    if (o.j[t] == 0) cb[0][o.i[t]] = o.v[t];
+    const int i = o.i(t), j = o.j(t);
+    if (o.valid(t, r) && i >= j) o.v[t] = G[i + j * r];
+    if (j == 0 && i < int(r)) cb[0][i] = o.v[t];
   }
   __syncthreads();
   int fail = 0;
@@ -107,17 +114,17 @@ __device__ int chol_reg(const double* G, double* L, uint32_t r) {
     }
     if (threadIdx.x == 0) dg[k] = p;
     const double inv = __drcp_rn(p);
-    double ci[KE], cj[KE];
+    double ci[B], cj[B];
 #pragma unroll
-    for (int t = 0; t < KE; ++t) {
-      ci[t] = c[o.i[t]];
-      cj[t] = c[o.j[t]];
+    for (int a = 0; a < B; ++a) {
+      ci[a] = c[o.i0 + a];
+      cj[a] = c[o.j0 + a];
     }
 #pragma unroll
     for (int t = 0; t < KE; ++t) {
-      const int i = o.i[t], j = o.j[t];
-      if (j > int(k) && i >= j) o.v[t] = fma(-ci[t] * inv, cj[t], o.v[t]);
-      if (j == int(k) + 1) cn[i] = o.v[t];
+      const int i = o.i(t), j = o.j(t);
+      if (j > int(k) && i >= j) o.v[t] = fma(-ci[t % B] * inv, cj[t / B], o.v[t]);
+      if (j == int(k) + 1 && i < int(r)) cn[i] = o.v[t];
     }
     __syncthreads();
   }
@@ -128,7 +135,7 @@ __device__ int chol_reg(const double* G, double* L, uint32_t r) {
 #pragma unroll
   for (int t = 0; t < KE; ++t) {
     if (!o.valid(t, r)) continue;
-    const int i = o.i[t], j = o.j[t];
+    const int i = o.i(t), j = o.j(t);
     const double d = sqrt(dg[j]);
     L[i + j * r] = i > j ? o.v[t] / d : (i == j ? d : 0.0);
   }
@@ -140,36 +147,38 @@ __device__ int chol_reg(const double* G, double* L, uint32_t r) {
 // row k, final up to its 1/L_kk scale after step k-1, updates the rows below.
 template <int KE>
 __device__ void tri_inv_reg(const double* L, double* X, uint32_t r) {
+  constexpr int B = Owned<KE>::kB;
   __shared__ double rb[2][kMaxR + 1];
   Owned<KE> o(r);
 #pragma unroll
   for (int t = 0; t < KE; ++t) {
-    o.v[t] = o.i[t] == o.j[t] ? 1.0 : 0.0;
-    if (o.i[t] == 0) rb[0][o.j[t]] = o.v[t];
+    const int i = o.i(t), j = o.j(t);
+    o.v[t] = i == j ? 1.0 : 0.0;
+    if (i == 0 && j < int(r)) rb[0][j] = o.v[t];
   }
   __syncthreads();
   for (uint32_t k = 0; k + 1 < r; ++k) {
     const double* u = rb[k & 1];
     double* un = rb[(k + 1) & 1];
     const double rk = __drcp_rn(L[k + k * r]);
-    double lik[KE], ukc[KE];
+    double lik[B], ukc[B];
 #pragma unroll
-    for (int t = 0; t < KE; ++t) {
-      lik[t] = L[min(o.i[t], int(r) - 1) + k * r];
-      ukc[t] = u[o.j[t]];
+    for (int a = 0; a < B; ++a) {
+      lik[a] = L[min(o.i0 + a, int(r) - 1) + k * r];
+      ukc[a] = u[o.j0 + a];
     }
 #pragma unroll
     for (int t = 0; t < KE; ++t) {
-      const int i = o.i[t], c = o.j[t];
-      if (i > int(k) && c <= int(k) && i < int(r)) o.v[t] = fma(-lik[t] * rk, ukc[t], o.v[t]);
-      if (i == int(k) + 1) un[c] = o.v[t];
+      const int i = o.i(t), c = o.j(t);
+      if (i > int(k) && c <= int(k) && i < int(r)) o.v[t] = fma(-lik[t % B] * rk, ukc[t / B], o.v[t]);
+      if (i == int(k) + 1 && c < int(r)) un[c] = o.v[t];
     }
     __syncthreads();
   }
 #pragma unroll
   for (int t = 0; t < KE; ++t) {
     if (!o.valid(t, r)) continue;
-    const int i = o.i[t], c = o.j[t];
+    const int i = o.i(t), c = o.j(t);
     X[i + c * r] = i >= c ? o.v[t] / L[i + i * r] : 0.0;
   }
   __syncthreads();
@@ -183,6 +192,7 @@ __device__ void tri_inv_reg(const double* L, double* X, uint32_t r) {
 // failing column + 1 (pivot in *piv_out) or 0.
 template <int KE>
 __device__ int gj_inv_reg(const double* G, double* out, uint32_t r, double floor_rel, double* piv_out) {
+  constexpr int B = Owned<KE>::kB;
   __shared__ double rowb[2][kMaxR + 1], colb[2][kMaxR + 1];
   Owned<KE> o(r);
   double md = 0.0;
@@ -190,9 +200,10 @@ __device__ int gj_inv_reg(const double* G, double* out, uint32_t r, double floor
   const double floor_v = floor_rel * md;
 #pragma unroll
   for (int t = 0; t < KE; ++t) {
-    if (o.valid(t, r)) o.v[t] = G[o.i[t] + o.j[t] * r];
-    if (o.i[t] == 0) rowb[0][o.j[t]] = o.v[t];
-    if (o.j[t] == 0) colb[0][o.i[t]] = o.v[t];
+    const int i = o.i(t), j = o.j(t);
+    if (o.valid(t, r)) o.v[t] = G[i + j * r];
+    if (i == 0 && j < int(r)) rowb[0][j] = o.v[t];
+    if (j == 0 && i < int(r)) colb[0][i] = o.v[t];
   }
   __syncthreads();
   for (uint32_t k = 0; k < r; ++k) {
@@ -207,29 +218,29 @@ __device__ int gj_inv_reg(const double* G, double* out, uint32_t r, double floor
       return int(k) + 1;
     }
     const double ip = __drcp_rn(p);
-    double aik[KE], akj[KE];
+    double aik[B], akj[B];
 #pragma unroll
-    for (int t = 0; t < KE; ++t) {
-      aik[t] = cl[o.i[t]];
-      akj[t] = rw[o.j[t]];
+    for (int a = 0; a < B; ++a) {
+      aik[a] = cl[o.i0 + a];
+      akj[a] = rw[o.j0 + a];
     }
 #pragma unroll
     for (int t = 0; t < KE; ++t) {
-      const int i = o.i[t], j = o.j[t];
+      const int i = o.i(t), j = o.j(t);
       const double old = o.v[t];
       double v;
       if (i == int(k)) v = j == int(k) ? ip : old * ip;
       else if (j == int(k)) v = -old * ip;
-      else v = fma(-aik[t] * ip, akj[t], old);
+      else v = fma(-aik[t % B] * ip, akj[t / B], old);
       o.v[t] = v;
-      if (i == int(k) + 1) rwn[j] = v;
-      if (j == int(k) + 1) cln[i] = v;
+      if (i == int(k) + 1 && j < int(r)) rwn[j] = v;
+      if (j == int(k) + 1 && i < int(r)) cln[i] = v;
     }
     __syncthreads();
   }
 #pragma unroll
   for (int t = 0; t < KE; ++t)
-    if (o.valid(t, r)) out[o.i[t] + o.j[t] * r] = o.v[t];
+    if (o.valid(t, r)) out[o.i(t) + o.j(t) * r] = o.v[t];
   __syncthreads();
   return 0;
 }
