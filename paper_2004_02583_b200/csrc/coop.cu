@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "als_step.cuh"
 #include "coop.cuh"
@@ -489,11 +490,12 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
 }
 
 // ---- finish_step -----------------------------------------------------------------
-constexpr int kFinRows = 128;   // rows of R per block of the row pass
+constexpr int kFinRows = 64;    // rows of R per block of the row pass
 constexpr int kFinStages = 3;   // ring depth of the row pass
+constexpr int kFinPerSm = 2;    // resident CTAs per SM (grid of the row pass)
 
 template <int NC>
-__global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
+__global__ void __launch_bounds__(kThreads, kFinPerSm) finish_step_kernel(FinishArgs a) {
   cg::grid_group grid = cg::this_grid();
   AlsCtrl* ctrl = a.ctrl;
   if (ctrl->stop) return;
@@ -514,10 +516,14 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
   if (a.gram_nparts == 0 && a.mode != 2) {
     // copy map: kRpp rows of kCpr 16-byte chunks per pass of the CTA
     constexpr int kCpr = NC / 2, kRpp = kThreads / kCpr, kPasses = (kRows + kRpp - 1) / kRpp;
-    constexpr int kKs = kRows / 32;  // k-steps of 4 rows per warp per block
-    double acc[kTri][2];
+    // the upper 8x8 tiles are dealt to kSets warp sets (tile idx mod kSets):
+    // warp w accumulates set w % kSets over the k-steps of warp group w / kSets
+    constexpr int kSets = kTri >= 2 ? 2 : 1, kTriS = (kTri + kSets - 1) / kSets;
+    constexpr int kGroups = kThreads / 32 / kSets, kKs = kRows / 4 / kGroups;
+    const int set = warp % kSets, group = warp / kSets;
+    double acc[kTriS][2];
 #pragma unroll
-    for (int k = 0; k < kTri; ++k) acc[k][0] = acc[k][1] = 0.0;
+    for (int k = 0; k < kTriS; ++k) acc[k][0] = acc[k][1] = 0.0;
     const uint64_t nblk = (a.F + kRows - 1) / kRows;
     const uint64_t per = (nblk + gridDim.x - 1) / gridDim.x;
     const uint64_t b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
@@ -559,18 +565,24 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
       if (b + kStg - 1 < b1) issue(b + kStg - 1, int((b - b0 + kStg - 1) % kStg));
       cp_async_commit();
       const double* t = tile + size_t(slot) * kRows * kLd;
+      auto steps = [&](auto S) {
+        constexpr int sset = decltype(S)::value;
 #pragma unroll
-      for (int ks = 0; ks < kKs; ++ks) {
-        const double* rp = t + ((warp * kKs + ks) * 4 + q) * kLd;
-        double fr[kNT];
+        for (int ks = 0; ks < kKs; ++ks) {
+          const double* rp = t + ((group * kKs + ks) * 4 + q) * kLd;
+          double fr[kNT];
 #pragma unroll
-        for (int c = 0; c < kNT; ++c) fr[c] = rp[c * 8 + r8];
-        int idx = 0;
+          for (int c = 0; c < kNT; ++c) fr[c] = rp[c * 8 + r8];
+          int idx = 0;
 #pragma unroll
-        for (int tm = 0; tm < kNT; ++tm)
+          for (int tm = 0; tm < kNT; ++tm)
 #pragma unroll
-          for (int tn = tm; tn < kNT; ++tn, ++idx) dmma(acc[idx][0], acc[idx][1], fr[tm], fr[tn]);
-      }
+            for (int tn = tm; tn < kNT; ++tn, ++idx)
+              if (idx % kSets == sset) dmma(acc[idx / kSets][0], acc[idx / kSets][1], fr[tm], fr[tn]);
+        }
+      };
+      if (kSets == 2 && set == 1) steps(std::integral_constant<int, 1>{});
+      else steps(std::integral_constant<int, 0>{});
     }
     cp_async_wait<0>();
     __syncthreads();  // the ring is free: the warp partials are summed there, warp 0 first
@@ -578,10 +590,12 @@ __global__ void __launch_bounds__(kThreads) finish_step_kernel(FinishArgs a) {
     for (int w = 0; w < int(kThreads / 32); ++w) {
       if (warp == w) {
 #pragma unroll
-        for (int k = 0; k < kTri; ++k) {
-          double* p = ws + k * 64 + lane * 2;
-          p[0] = w == 0 ? acc[k][0] : p[0] + acc[k][0];
-          p[1] = w == 0 ? acc[k][1] : p[1] + acc[k][1];
+        for (int k = 0; k < kTriS; ++k) {
+          const int idx = k * kSets + set;
+          if (idx >= kTri) continue;
+          double* p = ws + idx * 64 + lane * 2;
+          p[0] = w < kSets ? acc[k][0] : p[0] + acc[k][0];
+          p[1] = w < kSets ? acc[k][1] : p[1] + acc[k][1];
         }
       }
       __syncthreads();
@@ -809,12 +823,15 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
 }
 
 template <class K>
-cudaError_t coop_launch(K kernel, int want, int num_sms, size_t smem, void* args, cudaStream_t st) {
+// exact: the caller sized per-CTA partials for `want` CTAs (fail rather than
+// launch fewer).
+cudaError_t coop_launch(K kernel, int want, int num_sms, size_t smem, void* args, cudaStream_t st,
+                        bool exact = false) {
   cudaError_t e = raise_smem_limit(kernel, smem);
   if (e != cudaSuccess) return e;
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
-  if (e != cudaSuccess || occ < 1) {
+  if (e != cudaSuccess || occ < 1 || (exact && occ * num_sms < want)) {
     cudaGetLastError();
     return e != cudaSuccess ? e : cudaErrorCooperativeLaunchTooLarge;
   }
@@ -833,7 +850,7 @@ size_t rows_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1
 int coop_partials_cap(int num_sms) { return num_sms * (2048 / kThreads); }
 
 int finish_step_grid(uint64_t F, int num_sms) {
-  return int(std::max<uint64_t>(1, std::min<uint64_t>((F + kFinRows - 1) / kFinRows, uint64_t(num_sms))));
+  return int(std::max<uint64_t>(1, std::min<uint64_t>((F + kFinRows - 1) / kFinRows, uint64_t(kFinPerSm) * num_sms)));
 }
 
 #define TKG_KE_SWITCH(r, CALL) \
@@ -857,7 +874,7 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
   const size_t smem = sizeof(double) * std::max<size_t>(size_t(kFinStages) * kFinRows * (ncp + 4), 2 * size_t(a.r) * a.r);
   switch (ncp) {
 #define TKG_F(N) \
-  case N: return coop_launch(finish_step_kernel<N>, want, num_sms, smem, &a, st);
+  case N: return coop_launch(finish_step_kernel<N>, want, num_sms, smem, &a, st, a.mode == 1);
     TKG_F(8) TKG_F(16) TKG_F(24) TKG_F(32) TKG_F(40) TKG_F(48) TKG_F(56) TKG_F(64)
 #undef TKG_F
     default: return cudaErrorInvalidValue;
