@@ -12,7 +12,7 @@ for c in 3 1 2 4 5; do
   timeout 900 python bench.py --config $c > gpurun_out/prof/bench_c$c.json 2> gpurun_out/prof/bench_c$c.err || exit 1
 done
 for c in 3 1 5; do
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
     --log-file gpurun_out/prof/launches_c$c.csv \
     python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_launch_c$c.log 2>&1
 done
