@@ -1393,7 +1393,6 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     }
     CK(launch_sum(sq, nsh, sumsq_d_.d(2), st_));
     count_launch(2);
-    (void)RhT;
     sumsq_known = true;
     mode_end(k);
     work = dst;
