@@ -335,6 +335,49 @@ int ref_hosvd_als(int sequential, const double* a, int order,
   });
 }
 
+// The same decomposition on a tensor read from a TNSR file by the
+// reference's own read_tnsr (io.cpp:150-161), so the calling process never
+// synthesises or copies the tensor itself (tools/parity_full.py, bench.py's
+// reference arm). dims_out receives the file's extents (order <= 64);
+// call_seconds the wall time of the t_hosvd / st_hosvd call alone (reading
+// excluded; the relative residual, which the API computes, included).
+int ref_hosvd_als_tnsr(int sequential, const char* path, const uint64_t* ranks,
+                       const uint32_t* mode_order, double eta, int max_iters,
+                       uint64_t seed, double* core_out, double* factors_out,
+                       void* report, uint64_t* dims_out, double* call_seconds,
+                       int* subtype, char* msg, int len) {
+  return guarded({subtype, msg, len}, [&] {
+    DenseTensor t = read_tnsr(std::string(path));
+    const std::size_t order = t.shape().order();
+    for (std::size_t k = 1; k <= order; ++k) dims_out[k - 1] = t.shape().extent(k);
+    Truncation tr{std::vector<std::size_t>(ranks, ranks + order)};
+    AlsConfig cfg;
+    cfg.eta = eta;
+    cfg.max_iters = max_iters;
+    cfg.seed = seed;
+    FactorEngine eng = FactorEngine::with_als(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::pair<TuckerTensor, DecompositionReport> res =
+        sequential == 1
+            ? st_hosvd(t, tr,
+                       mode_order ? std::optional<ModeOrder>(ModeOrder{
+                                        std::vector<std::size_t>(mode_order, mode_order + order)})
+                                  : std::nullopt,
+                       eng)
+            : t_hosvd(t, tr, eng, sequential == 2);
+    *call_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    copy_out(res.first.core, core_out);
+    if (factors_out) {
+      double* p = factors_out;
+      for (const Matrix& u : res.first.factors) {
+        std::copy(u.values().begin(), u.values().end(), p);
+        p += u.values().size();
+      }
+    }
+    fill_report(res.second, static_cast<RefReport*>(report));
+  });
+}
+
 // t_hosvd / st_hosvd with the SVD (kind 0) or EIG (kind 1) engine
 // (hosvd.cpp:89-99, 151-171); same buffers as ref_hosvd_als.
 int ref_hosvd_exact(int sequential, int kind, const double* a, int order,

@@ -309,6 +309,45 @@ class Ref:
                                        list(hist[p, :min(its, 64)]), float(secs[p])))
         return HosvdResult(core, factors, per_mode, float(relres), float(seconds))
 
+    def hosvd_als_tnsr(self, path, dims, ranks, sequential=False, order=None, eta=1e-4,
+                       max_iters=50, seed=0):
+        """ref_hosvd_als_tnsr: the reference reads the TNSR itself (read_tnsr)
+        and decomposes it; returns (HosvdResult, call_seconds)."""
+        n = len(dims)
+        core = np.zeros(ranks, order="F")
+        total = sum(int(dims[k]) * int(ranks[k]) for k in range(n))
+        fac = np.zeros(total)
+        rep = (C.c_char * self.lib.ref_report_size())()
+        mo = (C.c_uint32 * n)(*order) if order is not None else None
+        dims_out = (C.c_uint64 * 64)()
+        secs = C.c_double(0.0)
+        self._check(self.lib.ref_hosvd_als_tnsr(
+            C.c_int(1 if sequential else 0), os.fsencode(path), _u64(ranks), mo, C.c_double(eta),
+            C.c_int(max_iters), C.c_uint64(seed), _d(core), _d(fac), rep, dims_out, C.byref(secs),
+            *self._e()))
+        if list(dims_out[:n]) != [int(d) for d in dims]:
+            raise ValueError(f"TNSR extents {list(dims_out[:n])} != {list(dims)}")
+        return self._unpack_report(bytes(rep), core, fac, dims, ranks), float(secs.value)
+
+    @staticmethod
+    def _unpack_report(raw, core, fac, dims, ranks):
+        n = len(dims)
+        i32 = np.frombuffer(raw, dtype=np.int32, count=192)
+        f64 = np.frombuffer(raw, dtype=np.float64, offset=768)
+        ach, secs = f64[0:64], f64[64:128]
+        hist = f64[128:128 + 64 * 64].reshape(64, 64)
+        factors, ofs = [], 0
+        for k in range(n):
+            sz = int(dims[k]) * int(ranks[k])
+            factors.append(fac[ofs:ofs + sz].reshape((int(dims[k]), int(ranks[k])), order="F"))
+            ofs += sz
+        per_mode = []
+        for p in range(n):
+            its = int(i32[64 + p])
+            per_mode.append(ModeRecord(int(i32[p]), its, int(i32[128 + p]), float(ach[p]),
+                                       list(hist[p, :min(its, 64)]), float(secs[p])))
+        return HosvdResult(core, factors, per_mode, float(f64[128 + 4097]), float(f64[128 + 4096]))
+
     def hosvd_exact(self, t, ranks, kind, sequential=False, order=None):
         """t_hosvd / st_hosvd with FactorEngine::svd() (kind "svd") or ::eig() ("eig")."""
         t = fortran(t)
