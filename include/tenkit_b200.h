@@ -54,8 +54,8 @@
 extern "C" {
 #endif
 
-#define TKG_MAX_ORDER 16
-#define TKG_MAX_HISTORY 64
+#define TKG_MAX_ORDER 64   /* the reference's TNSR limit (io.cpp:24) */
+#define TKG_MAX_HISTORY 64 /* inline entries; tkg_residual_history returns all */
 
 /* err->subtype: which tenkit exception the call maps to (errors.hpp:24-77). */
 enum tkg_subtype {
@@ -79,14 +79,17 @@ typedef struct tkg_error {
   char message[512];
 } tkg_error;
 
-/* AlsConfig (als.hpp:17-23). init: nullable host I_mode x r column-major
- * warm start (used by tkg_als_low_rank only, like the reference's drivers
- * which never set it). */
+/* AlsConfig (als.hpp:17-23). init: nullable host column-major warm start
+ * of init_rows x init_cols (used by tkg_als_low_rank only, like the
+ * reference's drivers which never set it); a shape other than I_mode x r is
+ * rejected with DimensionMismatchError as als.cpp:106-113 does. */
 typedef struct tkg_als_config {
   double eta;
   int32_t max_iters;
   uint64_t seed;
   const double* init;
+  uint64_t init_rows;
+  uint64_t init_cols;
 } tkg_als_config;
 
 /* FactorEngine (hosvd.hpp:19-27): kind + the ALS configuration (kAls only). */
@@ -102,7 +105,9 @@ typedef struct tkg_mode_report {
   int32_t mode;        /* 1-based */
   int32_t iterations;
   int32_t status;      /* 0 kConverged, 1 kMaxItersReached (als.hpp:25) */
-  int32_t history_len; /* min(iterations, TKG_MAX_HISTORY) */
+  int32_t history_len; /* min(iterations, TKG_MAX_HISTORY) entries inline below;
+                          the full history (one entry per sweep, als.cpp:137-138)
+                          via tkg_residual_history */
   double achieved_eta;
   double seconds;      /* factor engine + working-tensor shrink */
   double residual_history[TKG_MAX_HISTORY];
@@ -206,6 +211,14 @@ int tkg_st_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t
                          uint64_t slab_begin, uint64_t slab_len, const uint64_t* ranks,
                          const uint32_t* mode_order, const tkg_als_config* cfg, double* core, double* factors,
                          tkg_report* report, tkg_error* err);
+
+/* Full residual history of the mode at processing position `position`
+ * (0-based) of the context's last tkg_t_hosvd* / tkg_st_hosvd* /
+ * tkg_*_sharded / tkg_als_low_rank call: *len = its entry count (= that
+ * mode's iterations, als.cpp:137-138); min(*len, cap) entries go to out
+ * (nullable, to query the length). */
+int tkg_residual_history(tkg_ctx* ctx, int32_t position, double* out, uint64_t cap, uint64_t* len,
+                         tkg_error* err);
 
 /* Stable ascending-rank order (Proposition 1). out: order entries. */
 int tkg_select_order(int32_t order, const uint64_t* dims, const uint64_t* ranks, uint32_t* out,

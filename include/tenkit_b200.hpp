@@ -168,7 +168,21 @@ inline Tucker hosvd_raw(Context& ctx, bool sequential, const double* a, bool a_o
 
 #ifdef TENKIT_B200_USE_TENKIT
 // Drop-in signatures of hosvd.hpp:55-70 for FactorEngine::Kind::kAls.
-inline tenkit::DecompositionReport to_report(const tkg_report& r) {
+// One entry per sweep (als.cpp:137-138): the report carries the first
+// TKG_MAX_HISTORY inline, the rest comes from tkg_residual_history.
+inline std::vector<double> full_history(tkg_ctx* ctx, int position, const tkg_mode_report& m) {
+  std::vector<double> h(m.residual_history, m.residual_history + m.history_len);
+  if (m.iterations > m.history_len) {
+    h.assign(std::size_t(m.iterations), 0.0);
+    uint64_t len = 0;
+    tkg_error e{};
+    check(tkg_residual_history(ctx, position, h.data(), h.size(), &len, &e), e);
+    h.resize(std::size_t(len));
+  }
+  return h;
+}
+
+inline tenkit::DecompositionReport to_report(tkg_ctx* ctx, const tkg_report& r) {
   tenkit::DecompositionReport out;
   for (int k = 0; k < r.n_modes; ++k) {
     const tkg_mode_report& m = r.per_mode[k];
@@ -181,7 +195,7 @@ inline tenkit::DecompositionReport to_report(const tkg_report& r) {
     }
     tenkit::AlsReport ar;
     ar.iterations = m.iterations;
-    ar.residual_history.assign(m.residual_history, m.residual_history + m.history_len);
+    ar.residual_history = full_history(ctx, k, m);
     ar.status = m.status == 0 ? tenkit::AlsStatus::kConverged : tenkit::AlsStatus::kMaxItersReached;
     ar.achieved_eta = m.achieved_eta;
     mr.als = ar;
@@ -208,7 +222,7 @@ inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> run(
   tenkit::TuckerTensor tk{tenkit::DenseTensor(tenkit::Shape(rk), std::move(r.core)), {}, t.shape()};
   for (size_t k = 0; k < dims.size(); ++k)
     tk.factors.emplace_back(dims[k], ranks[k], std::move(r.factors[k]));
-  return {std::move(tk), to_report(rep)};
+  return {std::move(tk), to_report(Context::default_context().get(), rep)};
 }
 
 inline std::pair<tenkit::TuckerTensor, tenkit::DecompositionReport> t_hosvd(
@@ -248,7 +262,8 @@ inline std::pair<tenkit::FactorPair, tenkit::AlsReport> als_low_rank(const tenki
   const uint64_t I = (mode >= 1 && mode <= dims.size()) ? dims[mode - 1] : 1;
   const uint64_t F = I ? t.size() / I : 0;
   std::vector<double> l(I * r, 0.0), rr(F * r, 0.0);
-  tkg_als_config c{cfg.eta, cfg.max_iters, cfg.seed, cfg.init ? cfg.init->data() : nullptr};
+  tkg_als_config c{cfg.eta, cfg.max_iters, cfg.seed, cfg.init ? cfg.init->data() : nullptr,
+                   cfg.init ? cfg.init->rows() : 0, cfg.init ? cfg.init->cols() : 0};
   tkg_mode_report rep{};
   tkg_error e{};
   check(tkg_als_low_rank(Context::default_context().get(), t.data(), 0, int32_t(dims.size()), dims.data(),
@@ -256,7 +271,7 @@ inline std::pair<tenkit::FactorPair, tenkit::AlsReport> als_low_rank(const tenki
         e);
   tenkit::AlsReport ar;
   ar.iterations = rep.iterations;
-  ar.residual_history.assign(rep.residual_history, rep.residual_history + rep.history_len);
+  ar.residual_history = full_history(Context::default_context().get(), 0, rep);
   ar.status = rep.status == 0 ? tenkit::AlsStatus::kConverged : tenkit::AlsStatus::kMaxItersReached;
   ar.achieved_eta = rep.achieved_eta;
   return {tenkit::FactorPair{tenkit::Matrix(I, r, std::move(l)), tenkit::Matrix(F, r, std::move(rr))}, ar};

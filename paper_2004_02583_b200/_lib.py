@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libtenkit_b200.so")
 SYNTH_PATH = os.path.join(PKG, "libtkg_synth.so")
 
-MAX_ORDER = 16
+MAX_ORDER = 64
 MAX_HISTORY = 64
 
 
@@ -24,7 +24,7 @@ class TkgError(C.Structure):
 
 class TkgAlsConfig(C.Structure):
     _fields_ = [("eta", C.c_double), ("max_iters", C.c_int32), ("seed", C.c_uint64),
-                ("init", C.POINTER(C.c_double))]
+                ("init", C.POINTER(C.c_double)), ("init_rows", C.c_uint64), ("init_cols", C.c_uint64)]
 
 
 class TkgFactorEngine(C.Structure):
@@ -91,6 +91,7 @@ SIGNATURES = [
     ("tkg_reconstruct", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, _u64p, _dp, _dp, C.POINTER(TkgError)]),
     ("tkg_mode_gram", C.c_int, [_ctxp, _dp, C.c_int32, _u64p, C.c_uint32, _dp, C.POINTER(TkgError)]),
     ("tkg_sym_eig", C.c_int, [_ctxp, _dp, C.c_uint64, C.c_uint64, _dp, _dp, C.POINTER(TkgError)]),
+    ("tkg_residual_history", C.c_int, [_ctxp, C.c_int32, _dp, C.c_uint64, _u64p, C.POINTER(TkgError)]),
     ("tkg_select_order", C.c_int, [C.c_int32, _u64p, _u64p, _u32p, C.POINTER(TkgError)]),
     ("tkg_nccl_unique_id", C.c_int, [C.c_void_p, C.POINTER(TkgError)]),
     ("tkg_comm_init_nccl", C.c_int, [_ctxp, C.c_int, C.c_int, C.c_void_p, C.POINTER(TkgError)]),

@@ -15,6 +15,9 @@
 
 struct tkg_ctx {
   tkg::Engine* eng;
+  // residual histories of the last decomposition / als_low_rank call, per
+  // processing position (tkg_residual_history)
+  std::vector<std::vector<double>> last_hist;
 };
 
 struct tkg_local_group {
@@ -51,7 +54,7 @@ int guarded(tkg_error* err, F&& f) {
 
 tkg::Shape make_shape(int32_t order, const uint64_t* dims) {
   if (order < 1) tkg::raise(TKG_E_DIMENSION_MISMATCH, "Shape: at least one extent required");
-  if (order > TKG_MAX_ORDER) tkg::raise(TKG_E_UNSUPPORTED, "order above 16 is not supported");
+  if (order > TKG_MAX_ORDER) tkg::raise(TKG_E_UNSUPPORTED, "order above 64 is not supported");
   tkg::Shape s;
   s.N = order;
   for (int k = 0; k < order; ++k) {
@@ -68,6 +71,8 @@ tkg::AlsCfg make_cfg(const tkg_als_config* c) {
     a.max_iters = c->max_iters;
     a.seed = c->seed;
     a.init = c->init;
+    a.init_rows = c->init_rows;
+    a.init_cols = c->init_cols;
   }
   return a;
 }
@@ -84,7 +89,9 @@ void fill_mode(const tkg::ModeRep& m, tkg_mode_report* out) {
   for (size_t k = 0; k < n; ++k) out->residual_history[k] = m.history[k];
 }
 
-void fill_report(const tkg::DecompRep& r, int order, tkg_report* out) {
+void fill_report(tkg_ctx* ctx, const tkg::DecompRep& r, int order, tkg_report* out) {
+  ctx->last_hist.clear();
+  for (const tkg::ModeRep& m : r.per_mode) ctx->last_hist.push_back(m.history);
   if (!out) return;
   std::memset(out, 0, sizeof(*out));
   out->order = order;
@@ -141,7 +148,7 @@ int tkg_t_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, c
     std::vector<uint64_t> rk(ranks, ranks + order);
     tkg::DecompRep rep;
     eng(ctx).t_hosvd(a, a_on_device != 0, sh, rk, make_cfg(cfg), core, factors, &rep, want_singular_vectors != 0);
-    fill_report(rep, order, report);
+    fill_report(ctx, rep, order, report);
   });
 }
 
@@ -156,7 +163,7 @@ int tkg_st_hosvd(tkg_ctx* ctx, const double* a, int a_on_device, int32_t order, 
     tkg::DecompRep rep;
     eng(ctx).st_hosvd(a, a_on_device != 0, sh, rk, mode_order ? &mo : nullptr, make_cfg(cfg), core,
                       factors, &rep);
-    fill_report(rep, order, report);
+    fill_report(ctx, rep, order, report);
   });
 }
 
@@ -171,7 +178,7 @@ int tkg_t_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t o
     tkg::DecompRep rep;
     eng(ctx).t_hosvd(a, a_on_device != 0, sh, rk, make_cfg(engine ? &engine->als : nullptr), core, factors, &rep,
                      kind == TKG_ENGINE_ALS && want_singular_vectors != 0, kind);
-    fill_report(rep, order, report);
+    fill_report(ctx, rep, order, report);
   });
 }
 
@@ -188,7 +195,7 @@ int tkg_st_hosvd_engine(tkg_ctx* ctx, const double* a, int a_on_device, int32_t 
     tkg::DecompRep rep;
     eng(ctx).st_hosvd(a, a_on_device != 0, sh, rk, mode_order ? &mo : nullptr,
                       make_cfg(engine ? &engine->als : nullptr), core, factors, &rep, kind);
-    fill_report(rep, order, report);
+    fill_report(ctx, rep, order, report);
   });
 }
 
@@ -350,7 +357,7 @@ int tkg_t_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t 
     tkg::DecompRep rep;
     eng(ctx).t_hosvd_sharded(a, a_on_device != 0, sh, slab_begin, slab_len, rk, make_cfg(cfg), core, factors,
                              &rep, want_singular_vectors != 0);
-    fill_report(rep, order, report);
+    fill_report(ctx, rep, order, report);
   });
 }
 
@@ -366,7 +373,7 @@ int tkg_st_hosvd_sharded(tkg_ctx* ctx, const double* a, int a_on_device, int32_t
     tkg::DecompRep rep;
     eng(ctx).st_hosvd_sharded(a, a_on_device != 0, sh, slab_begin, slab_len, rk, mode_order ? &mo : nullptr,
                               make_cfg(cfg), core, factors, &rep);
-    fill_report(rep, order, report);
+    fill_report(ctx, rep, order, report);
   });
 }
 
@@ -386,16 +393,29 @@ int tkg_als_low_rank(tkg_ctx* ctx, const double* a, int a_on_device, int32_t ord
                      double* l_out, double* r_out, tkg_mode_report* report, tkg_error* err) {
   return guarded(err, [&] {
     tkg::Shape sh = make_shape(order, dims);
-    const uint64_t I = sh.extent(int(mode));
-    if (cfg && cfg->init == nullptr && (r < 1 || r > I)) {
-      // ZeroReference is checked before the initializer's guard (als.cpp:102-105 vs 62-66);
-      // the engine reproduces that order, so only reject ranks that do not fit a uint32.
-    }
+    sh.extent(int(mode));  // InvalidMode first
+    // the zero-norm / rank / init-shape guards run in the engine, in the
+    // reference's order (als.cpp:101-113, 62-66)
     if (r > 0xffffffffu) tkg::raise(TKG_E_RANK_TOO_LARGE, "rank too large");
     tkg::ModeRep rep;
     eng(ctx).als_low_rank(a, a_on_device != 0, sh, int(mode), uint32_t(r), make_cfg(cfg), l_out,
                           r_out, &rep);
+    ctx->last_hist.assign(1, rep.history);
     if (report) fill_mode(rep, report);
+  });
+}
+
+int tkg_residual_history(tkg_ctx* ctx, int32_t position, double* out, uint64_t cap, uint64_t* len,
+                         tkg_error* err) {
+  return guarded(err, [&] {
+    eng(ctx);
+    if (position < 0 || size_t(position) >= ctx->last_hist.size())
+      tkg::raise(TKG_E_INVALID_MODE, "residual_history: no mode at position " + std::to_string(position) +
+                                         " in the last decomposition");
+    const std::vector<double>& h = ctx->last_hist[size_t(position)];
+    if (len) *len = h.size();
+    if (out)
+      for (size_t k = 0; k < h.size() && k < cap; ++k) out[k] = h[k];
   });
 }
 

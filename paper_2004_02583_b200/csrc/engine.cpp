@@ -481,6 +481,11 @@ void Engine::pregenerate(const std::vector<PreGen>& items, uint64_t seed) {
 // for the well-conditioned factors ALS produces.
 void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32_t r, double* Q,
                     double* rmat, double* rt, uint32_t ldrt, bool check) {
+  if (r > kMaxRank) {  // column-major Y only (the wide ALS reduces its own partials)
+    if (nparts != 0 || rt) raise(12, "qr_dev: wide ranks take a column-major Y");
+    qr_wide(Y, I, r, Q, rmat, check);
+    return;
+  }
   CholQrArgs q;
   q.Y = const_cast<double*>(Y);  // written only when nparts > 1 (partials summed in place)
   q.nparts = nparts;
@@ -557,11 +562,31 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   const uint64_t P = F / s;
   const uint32_t ncp = pad_nc(r);
   const std::string mname = "mode " + std::to_string(mode);
+  // als.cpp:101-104 (zero norm) precedes als_init's rank guard (:62-66) and
+  // the init shape check (:106-113)
+  if ((cfg.init == nullptr && (r < 1 || r > I)) ||
+      (cfg.init && (cfg.init_rows != I || cfg.init_cols != r))) {
+    if (!sumsq_known) {
+      double* sq0 = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
+      CK(launch_sumsq(A, sh.count(), sq0, st_));
+      CK(launch_sum(sq0, sumsq_partials_count(sh.count()), sumsq_d_.d(2), st_));
+      count_launch(2);
+      if (dist_) dist_->allreduce_sum(sumsq_d_.d(2), 1, st_);
+    }
+    double ss = 0.0;
+    CK(cudaMemcpyAsync(&ss, sumsq_d_.d(2), sizeof(double), cudaMemcpyDeviceToHost, st_));
+    sync();
+    if (ss == 0.0) raise(3, "als_low_rank: input tensor has zero norm");
+    if (cfg.init)
+      raise(2, "als_low_rank: init is " + std::to_string(cfg.init_rows) + "x" + std::to_string(cfg.init_cols) +
+                   ", mode " + std::to_string(mode) + " needs " + std::to_string(I) + "x" + std::to_string(r));
+    raise(4, mname + ": rank " + std::to_string(r) + " outside 1.." + std::to_string(I));
+  }
+  if (r > kMaxRank) return run_als_wide(A, sh, mode, r, cfg, sumsq_known, slot);
   FiberView v{A, s, P, uint32_t(I), s, s * I};
   AlsOut out;
   out.rep.mode = mode;
 
-  if (r > kMaxRank) raise(12, mname + ": rank " + std::to_string(r) + " above the supported 64");
   double* Lc = l_.d(I * r);
   double* Mt = mt_.d(I * ncp);
   double* R = r_.d(F * ncp + 8);  // row-major [F][ncp]
@@ -588,8 +613,6 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     }
     CK(cudaMemcpyAsync(Lc, cfg.init, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
   } else {
-    if (r < 1 || r > I)
-      raise(4, mname + ": rank " + std::to_string(r) + " outside 1.." + std::to_string(I));
     const double* S = nullptr;
     auto pit = pre_.find(mode);
     if (pit != pre_.end() && pit->second.F == F && pit->second.r == r) {
@@ -914,17 +937,6 @@ void Engine::sym_eig(const double* g, uint64_t n, uint64_t k, double* values, do
 }
 
 // ---- HOOI (hooi.cpp:53-110) --------------------------------------------------------
-void Engine::ttm_mode(const double* X, const Shape& sh, int mode, const double* U, uint32_t r, double* out) {
-  ClsScope cls(fc_cls_, kClsTTM);
-  const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
-  const uint32_t ncp = pad_nc(r);
-  double* Mt = mt_.d(I * ncp);
-  CK(launch_pack(U, 1, I, uint32_t(I), r, Mt, ncp, st_));  // Mt[i][c] = U[i + c*I]
-  count_launch();
-  FiberView v{X, s, P, uint32_t(I), s, s * I};
-  fc(v, Mt, ncp, r, out, 1, s, s * r, nullptr, nullptr, nullptr, false);
-}
-
 Shape Engine::ttm_others(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                          const std::vector<double*>& U, int skip, double* dst) {
   Shape cur = sh;
@@ -1046,17 +1058,11 @@ void Engine::core_chain(const double* A, const Shape& sh, const std::vector<uint
   int which = 0;
   const int nlast = last_mode > 0 ? last_mode : sh.N;
   for (int n = 1; n <= nlast; ++n) {
-    const uint64_t I = cur.extent(n), s = cur.stride(n), F = cur.count() / I, P = F / s;
     const uint32_t r = uint32_t(ranks[n - 1]);
-    const uint32_t ncp = pad_nc(r);
-    double* Mt = mt_.d(I * ncp);
-    CK(launch_pack(d_factors[n - 1], 1, I, uint32_t(I), r, Mt, ncp, st_));  // Mt[i][c] = U[i + c*I]
-    count_launch();
     Shape nxt = cur;
     nxt.d[n - 1] = r;
     double* dst = (n == nlast) ? d_core : bufs[which]->d(nxt.count());
-    FiberView v{src, s, P, uint32_t(I), s, s * I};
-    fc(v, Mt, ncp, r, dst, 1, s, s * r, nullptr, nullptr, nullptr, n == 1 && last_mode == 0);
+    ttm_mode(src, cur, n, d_factors[n - 1], r, dst, n == 1 && last_mode == 0);
     src = dst;
     cur = nxt;
     which ^= 1;
@@ -1088,6 +1094,26 @@ double* Engine::residual_enqueue(const double* A, const Shape& sh, const std::ve
     Shape nxt = cur;
     nxt.d[n - 1] = Iout;
     const bool last = (n == sh.N);
+    if (K > kMaxRank) {
+      // the expansion kernels hold at most 64 core indices: an FC TTM (the
+      // contraction extent K is free there) in 64-row output blocks, and for
+      // the last mode the materialised expansion against A
+      double* dst = bufs[which]->d(nxt.count());
+      {
+        ClsScope cls(fc_cls_, kClsResid);
+        mode_product_dev(src, cur, n, d_factors[n - 1], Iout, dst);
+      }
+      if (last) {
+        nsq = sumsq_partials_count(nxt.count());
+        sq = sq_part_.d(size_t(std::max(4096, nsq)));
+        CK(launch_sumsq_diff(A, dst, nxt.count(), sq, st_));
+        count_launch();
+      }
+      src = dst;
+      cur = nxt;
+      which ^= 1;
+      continue;
+    }
     ExpandArgs ea;
     ea.in = src;
     ea.s = s;
@@ -1236,6 +1262,8 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   for (int n = 1; n <= sh.N; ++n) {
     const uint32_t r = uint32_t(ranks[n - 1]);
     const uint64_t I = sh.d[n - 1];
+    if (want_sv && r > kMaxRank)
+      raise(12, "recover_singular_vectors: ranks above 64 are not supported (mode " + std::to_string(n) + ")");
     mode_begin(n - 1);
     outs.push_back(run_als(A, sh, n, r, cfg, sumsq_known, MtWindow(), n - 1));
     sumsq_known = true;
@@ -1261,7 +1289,9 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   // (L^T L)^{-1}), so A_(N)^T U_N = R R_hat^T exactly: the first contraction
   // of the chain is the st-HOSVD shrink of R (hosvd.cpp:176-178) instead of
   // another pass over A, and the remaining TTMs run on the r_N-extent tensor.
-  {
+  if (ranks[sh.N - 1] > kMaxRank) {
+    core_chain(A, sh, ranks, U, core_buf);  // wide last rank: the plain TTM chain
+  } else {
     const int N = sh.N;
     const uint32_t rN = uint32_t(ranks[N - 1]), ncpN = pad_nc(rN);
     const uint64_t IN = sh.d[N - 1], sN = sh.stride(N), FN = sh.count() / IN;
@@ -1371,6 +1401,25 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
     outs.push_back(run_als(work, cur, mode, r, cfg, sumsq_known, MtWindow(), k));
     const uint32_t ncp = pad_nc(r);
     U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
+    if (r > kMaxRank) {
+      // wide rank: working <- working x_mode U^T (the TTM form of the shrink,
+      // equal to R_hat R^T for the returned consistent pair)
+      qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[mode - 1], nullptr, nullptr, 0, false);
+      Shape nxt = cur;
+      nxt.d[mode - 1] = r;
+      double* dst = bufs[which]->d(nxt.count());
+      ttm_mode(work, cur, mode, U[mode - 1], r, dst, true);
+      double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(nxt.count()))));
+      CK(launch_sumsq(dst, nxt.count(), sq, st_));
+      CK(launch_sum(sq, sumsq_partials_count(nxt.count()), sumsq_d_.d(2), st_));
+      count_launch(2);
+      sumsq_known = true;
+      mode_end(k);
+      work = dst;
+      cur = nxt;
+      which ^= 1;
+      continue;
+    }
     double* RhT = rhatT_.d(size_t(r) * ncp);
     qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[mode - 1], rhat_.d(r * r), RhT, ncp, false);
     // working <- tensorize(R_hat R^T, mode, shrunk) (hosvd.cpp:176-178): an FC
@@ -1419,13 +1468,8 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
 void Engine::als_low_rank(const double* a, bool a_dev, const Shape& sh, int mode, uint32_t r,
                           const AlsCfg& cfg, double* l_out, double* r_out, ModeRep* rep) {
   const uint64_t I = sh.extent(mode);
-  if (cfg.init == nullptr && (r < 1 || r > I)) {
-    // als_low_rank computes the norm first; a zero tensor reports ZeroReference
-    // before the initializer's rank guard. Keep that order.
-  }
   const double* A = upload(a, sh.count(), a_dev, tensor_, nullptr);
-  if (cfg.init && r > kMaxRank) raise(12, "rank above the supported 64");
-  AlsOut o = run_als(A, sh, mode, r, cfg, false);
+  AlsOut o = run_als(A, sh, mode, r, cfg, false);  // zero norm, then the rank / init guards
   const uint64_t F = sh.count() / I;
   CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   if (r_out) {  // R is row-major [F][ncp] on the device; the API returns column-major F x r
@@ -1535,9 +1579,28 @@ void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, ui
   const uint64_t I = sh.extent(mode);
   if (r < 1 || r > I)
     raise(4, "mode " + std::to_string(mode) + ": rank " + std::to_string(r) + " outside 1.." + std::to_string(I));
-  if (r > kMaxRank) raise(12, "rank above the supported 64");
   const double* A = upload(a, sh.count(), a_dev, tensor_, nullptr);
   const uint64_t s = sh.stride(mode), F = sh.count() / I;
+  if (r > kMaxRank) {  // 64-column FR blocks + CholQR2 (engine_wide.cpp)
+    FiberView v{A, s, F / s, uint32_t(I), s, s * I};
+    double* S = s_.d(F * r + 8);
+    gen_uniform(seed, uint32_t(mode), F * r, S);
+    double* Y = qy_.d(I * r);
+    double* part = fr_part_.d(size_t(fr_ranges(v, 64)) * I * 64);
+    for (uint32_t c0 = 0; c0 < r; c0 += 64) {
+      const uint32_t nc = std::min<uint32_t>(64, r - c0);
+      const uint32_t ranges = fr(v, S + uint64_t(c0) * F, 1, F, nc, part, nullptr, false, nullptr);
+      CK(launch_reduce_partials(part, int(ranges), uint32_t(I), pad_nc(nc), nc, Y + uint64_t(c0) * I, st_));
+    }
+    qr_wide(Y, uint32_t(I), r, l_.d(I * r), nullptr, true);
+    const int bad = qr_degenerate_col();
+    if (bad != 0)
+      raise(6, "als_init: randomized range collapsed at column " + std::to_string(bad) + " for mode " +
+                   std::to_string(mode));
+    CK(cudaMemcpyAsync(l_out, l_.d(I * r), I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    sync();
+    return;
+  }
   const uint32_t ncp = pad_nc(r);
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
   double* S = s_.d(F * r + 8);
@@ -1559,17 +1622,18 @@ void Engine::als_init(const double* a, bool a_dev, const Shape& sh, int mode, ui
 void Engine::unfold_times(const double* a, const Shape& sh, int mode, const double* m, uint32_t r,
                           double* out) {
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
-  if (r > kMaxRank) raise(12, "unfold_times: more than 64 columns");
   const double* A = upload(a, sh.count(), false, tensor_, nullptr);
   double* M = s_.d(F * r + 8);  // column-major F x r, as given
   CK(cudaMemcpyAsync(M, m, F * r * sizeof(double), cudaMemcpyHostToDevice, st_));
-  const uint32_t ncp = pad_nc(r);
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  const uint32_t nranges = fr_ranges(v, r);
-  double* part = fr_part_.d(size_t(nranges) * I * ncp);
-  const uint32_t ranges = fr(v, M, 1, F, r, part, nullptr, false, nullptr);
+  const uint32_t nranges = fr_ranges(v, std::min<uint32_t>(r, kMaxRank));
+  double* part = fr_part_.d(size_t(nranges) * I * pad_nc(std::min<uint32_t>(r, kMaxRank)));
   double* y = misc_.d(I * r);
-  CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, y, st_));
+  for (uint32_t c0 = 0; c0 < r; c0 += kMaxRank) {  // 64-column blocks
+    const uint32_t nc = std::min(kMaxRank, r - c0);
+    const uint32_t ranges = fr(v, M + uint64_t(c0) * F, 1, F, nc, part, nullptr, false, nullptr);
+    CK(launch_reduce_partials(part, int(ranges), uint32_t(I), pad_nc(nc), nc, y + uint64_t(c0) * I, st_));
+  }
   CK(cudaMemcpyAsync(out, y, I * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
 }
@@ -1577,16 +1641,17 @@ void Engine::unfold_times(const double* a, const Shape& sh, int mode, const doub
 void Engine::unfold_t_times(const double* a, const Shape& sh, int mode, const double* m,
                             uint32_t r, double* out) {
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I;
-  if (r > kMaxRank) raise(12, "unfold_t_times: more than 64 columns");
   const double* A = upload(a, sh.count(), false, tensor_, nullptr);
-  const uint32_t ncp = pad_nc(r);
   double* Mc = misc_.d(I * r);
   CK(cudaMemcpyAsync(Mc, m, I * r * sizeof(double), cudaMemcpyHostToDevice, st_));
-  double* Mt = mt_.d(I * ncp);
-  CK(launch_pack(Mc, 1, I, uint32_t(I), r, Mt, ncp, st_));
   double* R = r_.d(F * r);
   FiberView v{A, s, F / s, uint32_t(I), s, s * I};
-  fc(v, Mt, ncp, r, R, 1, F, s, nullptr, nullptr, nullptr, false);  // column-major F x r
+  for (uint32_t c0 = 0; c0 < r; c0 += kMaxRank) {  // 64-column blocks, column-major F x r
+    const uint32_t nc = std::min(kMaxRank, r - c0), ncp = pad_nc(nc);
+    double* Mt = mt_.d(I * ncp);
+    CK(launch_pack(Mc + uint64_t(c0) * I, 1, I, uint32_t(I), nc, Mt, ncp, st_));
+    fc(v, Mt, ncp, nc, R + uint64_t(c0) * F, 1, F, s, nullptr, nullptr, nullptr, false);
+  }
   CK(cudaMemcpyAsync(out, R, F * r * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
 }

@@ -38,7 +38,7 @@ void check_cuda(cudaError_t e, const char* what);
 
 struct Shape {
   int N = 0;
-  uint64_t d[16] = {0};
+  uint64_t d[64] = {0};  // TKG_MAX_ORDER
   uint64_t count() const;
   uint64_t extent(int mode) const;  // validates, 1-based
   uint64_t stride(int mode) const;
@@ -50,6 +50,7 @@ struct AlsCfg {
   int max_iters = 50;
   uint64_t seed = 0;
   const double* init = nullptr;  // host I x r col-major
+  uint64_t init_rows = 0, init_cols = 0;  // init's shape (checked against I x r, als.cpp:106-113)
 };
 
 // FactorEngine::Kind (hosvd.hpp:19-27)
@@ -203,6 +204,14 @@ class Engine {
   // ||A||^2 of this tensor.
   AlsOut run_als(const double* A, const Shape& sh, int mode, uint32_t r, const AlsCfg& cfg,
                  bool sumsq_known, const MtWindow& win = MtWindow(), int slot = 0);
+  // ranks above 64 (engine_wide.cpp): 64-column contraction blocks, Cholesky
+  // + row substitutions for the r x r solves, one host read per sweep
+  AlsOut run_als_wide(const double* A, const Shape& sh, int mode, uint32_t r, const AlsCfg& cfg,
+                      bool sumsq_known, int slot);
+  // CholQR2 of a column-major I x r matrix for r > 64 (Q may alias Y)
+  void qr_wide(const double* Y, uint32_t I, uint32_t r, double* Q, double* rmat, bool check);
+  // G (r x r) = X^T X of a row-major [rows][ld] or column-major (ld) matrix
+  void gram_cols(const double* X, uint64_t rows, uint32_t r, uint64_t ld, bool row_major, double* G);
   uint32_t reduce_left_partials(double* part, uint32_t nparts, uint32_t I, uint32_t ncp, uint32_t r);
   // draws 0..n-1 in storage order, or a shard's window of them (MtWindow)
   void gen_uniform(uint64_t seed, uint32_t stream, uint64_t n, double* d_out, const MtWindow& win = MtWindow());
@@ -245,8 +254,9 @@ class Engine {
   // the other factors, hooi.cpp:82-88); returns dst's shape
   Shape ttm_others(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                    const std::vector<double*>& U, int skip, double* dst);
-  // out <- X x_mode U^T (U: I x r device col-major), tensor layout
-  void ttm_mode(const double* X, const Shape& sh, int mode, const double* U, uint32_t r, double* out);
+  // out <- X x_mode U^T (U: I x r device col-major), tensor layout, any r
+  void ttm_mode(const double* X, const Shape& sh, int mode, const double* U, uint32_t r, double* out,
+                bool count_pass = false);
   double* sumsq_to_host(const double* A, uint64_t n);  // ||A||^2 staged in pinned memory (after sync)
   void finish_exact(const Shape& sh, const std::vector<uint64_t>& ranks, const Shape& cs, const double* A,
                     const double* core_buf, const std::vector<double*>& U, const double* ref_sumsq, double* core,
@@ -362,6 +372,7 @@ class Engine {
   DBuf send_, recv_, reshard_, uslab_, uslab2_, core_t_;
   DBuf sv_u_, sv_g_, sv_vt_, sv_vt0_, sv_ctrl_;
   DBuf gram_t_, gram_t_part_, gram_w_, hooi_s_;
+  DBuf wide_gpart_, wide_g_, wide_c1_, wide_c2_, wide_fail_, wide_lp_;
   SymEig eig_;
   double* norm_h_ = nullptr;  // pinned
 };

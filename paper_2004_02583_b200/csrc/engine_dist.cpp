@@ -73,7 +73,7 @@ void Engine::reshard(const double* src, const Shape& G, int from, int to, double
   Shape Ls = G, Lt = G;
   Ls.d[from - 1] = shard_range(G.d[from - 1], rank, world).len;
   Lt.d[to - 1] = shard_range(G.d[to - 1], rank, world).len;
-  uint64_t ss[16], ts[16];
+  uint64_t ss[64], ts[64];
   strides_of(Ls, ss);
   strides_of(Lt, ts);
   std::vector<size_t> scount(world), soff(world), rcount(world), roff(world);
@@ -98,7 +98,7 @@ void Engine::reshard(const double* src, const Shape& G, int from, int to, double
     Shape bs = Ls;
     const ShardRange tr = shard_range(G.d[to - 1], q, world);
     bs.d[to - 1] = tr.len;
-    uint64_t bstr[16];
+    uint64_t bstr[64];
     strides_of(bs, bstr);
     for (int k = 0; k < G.N; ++k) {
       b.box[k] = bs.d[k];
@@ -117,7 +117,7 @@ void Engine::reshard(const double* src, const Shape& G, int from, int to, double
     Shape br = Lt;
     const ShardRange fr_ = shard_range(G.d[from - 1], q, world);
     br.d[from - 1] = fr_.len;
-    uint64_t bstr[16];
+    uint64_t bstr[64];
     strides_of(br, bstr);
     for (int k = 0; k < G.N; ++k) {
       b.box[k] = br.d[k];
@@ -403,7 +403,7 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
   CK(cudaMemsetAsync(core_buf, 0, cs.count() * sizeof(double), st_));
   {
     const Shape Lw = local_shape(Gw, sm);
-    uint64_t ls[16], gs[16];
+    uint64_t ls[64], gs[64];
     strides_of(Lw, ls);
     strides_of(cs, gs);
     BoxCopy b;

@@ -73,7 +73,6 @@ Shape read_header(FILE* f, const char* magic, const std::string& what, uint32_t*
   if (version != kVersion) raise(9, what + ": unsupported version " + std::to_string(version));
   const uint32_t order = read_u32(f);
   if (order == 0 || order > kMaxOrder) raise(9, what + ": implausible order " + std::to_string(order));
-  if (order > 16) raise(12, what + ": order " + std::to_string(order) + " above this build's 16");
   Shape sh;
   sh.N = int(order);
   for (uint32_t i = 0; i < order; ++i) {

@@ -170,8 +170,8 @@ cudaError_t launch_gram_reduce(const double* part, int nparts, uint64_t pld, uin
                                cudaStream_t st);
 struct BoxCopy {
   int N = 0;
-  uint64_t box[16] = {0};
-  uint64_t src_stride[16] = {0}, dst_stride[16] = {0};
+  uint64_t box[64] = {0};
+  uint64_t src_stride[64] = {0}, dst_stride[64] = {0};
   uint64_t src_base = 0, dst_base = 0;
 };
 cudaError_t launch_copy_box(const double* src, double* dst, const BoxCopy& b, cudaStream_t st);

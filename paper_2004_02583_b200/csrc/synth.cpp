@@ -98,7 +98,7 @@ extern "C" {
 // per-slice numbers). Returns 0 on success.
 int tkg_synth_tucker_slab(int order, const uint64_t* dims, const uint64_t* ranks, double alpha, uint64_t seed,
                           uint64_t k0, uint64_t nloc, double* out, double* slice_sq) {
-  if (order < 1 || order > 16) return 1;
+  if (order < 1 || order > 64) return 1;
   uint64_t core = 1;
   for (int n = 0; n < order; ++n) {
     if (ranks[n] < 1 || ranks[n] > dims[n]) return 1;
@@ -176,7 +176,7 @@ int tkg_synth_tucker_slab(int order, const uint64_t* dims, const uint64_t* ranks
 // from the sums of all slices of the tensor (tkg_synth_noise_scale).
 int tkg_synth_add_noise(int order, const uint64_t* dims, uint64_t seed, uint64_t k0, uint64_t nloc, double scale,
                         double* out) {
-  if (order < 1 || order > 16) return 1;
+  if (order < 1 || order > 64) return 1;
   uint64_t slice = 1;
   for (int n = 0; n + 1 < order; ++n) slice *= dims[n];
   const uint64_t key = stream_key(seed, 1000);
@@ -199,7 +199,7 @@ double tkg_synth_noise_scale(uint64_t nslices, const double* slice_sq, double nu
 // The whole tensor (prod(dims) doubles, column-major). Returns 0 on success.
 int tkg_synth_tucker(int order, const uint64_t* dims, const uint64_t* ranks, double alpha, double nu,
                      uint64_t seed, double* out) {
-  if (order < 1 || order > 16) return 1;
+  if (order < 1 || order > 64) return 1;
   const uint64_t IN = dims[order - 1];
   std::vector<double> sq(2 * IN);
   int rc = tkg_synth_tucker_slab(order, dims, ranks, alpha, seed, 0, IN, out, sq.data());

@@ -157,7 +157,7 @@ class ShardedContext:
                                        C.byref(cfg), int(bool(want_singular_vectors)), _flat_ptr(core),
                                        _flat_ptr(fac), C.byref(rep), C.byref(err))
         _raise(rc, err)
-        return Context._tucker(core, fac, dims, ranks), _decomp_report(rep)
+        return Context._tucker(core, fac, dims, ranks), _decomp_report(rep, self.ctx)
 
     def t_hosvd(self, slab, dims: Sequence[int], trunc: Truncation, engine: FactorEngine,
                 want_singular_vectors: bool = False):

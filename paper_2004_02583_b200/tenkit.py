@@ -226,17 +226,30 @@ def _flat_ptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
-def _mode_report(m: _lib.TkgModeReport) -> ModeReport:
+def _full_history(m: _lib.TkgModeReport, ctx, position: int) -> List[float]:
+    """One entry per sweep (als.cpp:137-138): the first TKG_MAX_HISTORY come
+    inline in the report, the rest from tkg_residual_history."""
+    hist = [m.residual_history[k] for k in range(m.history_len)]
+    if ctx is not None and m.iterations > m.history_len:
+        buf = np.zeros(int(m.iterations))
+        n = C.c_uint64(0)
+        err = _lib.TkgError()
+        _raise(ctx._l.tkg_residual_history(ctx._ctx, int(position), _flat_ptr(buf), buf.size, C.byref(n),
+                                           C.byref(err)), err)
+        hist = list(buf[: int(n.value)])
+    return hist
+
+
+def _mode_report(m: _lib.TkgModeReport, ctx=None, position: int = 0) -> ModeReport:
     if m.status < 0:  # SVD / EIG engine: ModeReport::als is empty (hosvd.hpp:33-37)
         return ModeReport(m.mode, m.seconds, None)
-    hist = [m.residual_history[k] for k in range(m.history_len)]
-    als = AlsReport(m.iterations, hist, "converged" if m.status == 0 else "max_iters_reached",
-                    m.achieved_eta)
+    als = AlsReport(m.iterations, _full_history(m, ctx, position),
+                    "converged" if m.status == 0 else "max_iters_reached", m.achieved_eta)
     return ModeReport(m.mode, m.seconds, als)
 
 
-def _decomp_report(r: _lib.TkgReport) -> DecompositionReport:
-    return DecompositionReport([_mode_report(r.per_mode[k]) for k in range(r.n_modes)],
+def _decomp_report(r: _lib.TkgReport, ctx=None) -> DecompositionReport:
+    return DecompositionReport([_mode_report(r.per_mode[k], ctx, k) for k in range(r.n_modes)],
                                r.relative_residual, r.seconds, r.h2d_seconds, r.d2h_seconds,
                                r.residual_seconds, int(r.kernel_launches), int(r.tensor_passes),
                                int(r.algorithmic_bytes))
@@ -249,12 +262,14 @@ def _engine(e: "FactorEngine", keep):
 
 
 def _cfg(c: AlsConfig, keep):
-    init = None
+    init, rows, cols = None, 0, 0
     if c.init is not None:
         arr = _host(c.init)
         keep.append(arr)
         init = _flat_ptr(arr)
-    return _lib.TkgAlsConfig(float(c.eta), int(c.max_iters), int(c.seed) & (2**64 - 1), init)
+        rows = arr.shape[0] if arr.ndim >= 1 else 1
+        cols = (arr.shape[1] if arr.ndim >= 2 else 1) * int(np.prod(arr.shape[2:]) if arr.ndim > 2 else 1)
+    return _lib.TkgAlsConfig(float(c.eta), int(c.max_iters), int(c.seed) & (2**64 - 1), init, rows, cols)
 
 
 class Context:
@@ -305,7 +320,7 @@ class Context:
                                         C.byref(eng), int(bool(want_singular_vectors)), _flat_ptr(core),
                                         _flat_ptr(fac), C.byref(rep), C.byref(err))
         _raise(rc, err)
-        return self._tucker(core, fac, dims, ranks), _decomp_report(rep)
+        return self._tucker(core, fac, dims, ranks), _decomp_report(rep, self)
 
     def st_hosvd(self, t, trunc: Truncation, order: Optional[ModeOrder], engine: FactorEngine):
         ptr, on_dev, dims, keep = self._tensor(t)
@@ -328,7 +343,7 @@ class Context:
                                          C.byref(eng), _flat_ptr(core), _flat_ptr(fac), C.byref(rep),
                                          C.byref(err))
         _raise(rc, err)
-        return self._tucker(core, fac, dims, ranks), _decomp_report(rep)
+        return self._tucker(core, fac, dims, ranks), _decomp_report(rep, self)
 
     @staticmethod
     def _tucker(core, fac, dims, ranks):
@@ -350,18 +365,12 @@ class Context:
         rep = _lib.TkgModeReport()
         err = _lib.TkgError()
         hold = []
-        c = _cfg(cfg, hold)
-        if cfg.init is not None:
-            ini = _host(cfg.init)
-            if ini.shape != (ext, r):
-                raise DimensionMismatchError(
-                    f"als_low_rank: init is {ini.shape[0]}x{ini.shape[1] if ini.ndim > 1 else 1}, "
-                    f"mode {mode} needs {ext}x{r}")
+        c = _cfg(cfg, hold)  # init's shape travels with it; the library checks it (als.cpp:106-113)
         rc = self._l.tkg_als_low_rank(self._ctx, ptr, on_dev, n, _lib.u64(dims), int(mode), int(r),
                                       C.byref(c), _flat_ptr(l), _flat_ptr(rr), C.byref(rep),
                                       C.byref(err))
         _raise(rc, err)
-        m = _mode_report(rep)
+        m = _mode_report(rep, self, 0)
         return (l, rr), m.als
 
     def als_init(self, t, mode: int, r: int, seed: int):
@@ -483,7 +492,7 @@ class Context:
         """read_tnsr (io.cpp:150-161). device=True: the payload goes straight
         into HBM through pinned chunks and a DeviceTensor (owning its buffer)
         is returned; else a host numpy array."""
-        order, dims = C.c_int32(0), (C.c_uint64 * 16)()
+        order, dims = C.c_int32(0), (C.c_uint64 * _lib.MAX_ORDER)()
         err = _lib.TkgError()
         _raise(self._l.tkg_read_tnsr_shape(os.fsencode(path), C.byref(order), dims, C.byref(err)), err)
         shape = [int(dims[k]) for k in range(order.value)]

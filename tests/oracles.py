@@ -260,13 +260,14 @@ class Ref:
         it = C.c_int(0)
         st = C.c_int(0)
         ae = C.c_double(0)
-        hist = np.zeros(64)
+        cap = max(64, int(max_iters))
+        hist = np.zeros(cap)
         self._check(self.lib.ref_als_low_rank(
             _d(flat(t)), C.c_int(t.ndim), _u64(t.shape), C.c_uint32(mode), C.c_uint64(r),
             C.c_double(eta), C.c_int(max_iters), C.c_uint64(seed),
             _d(flat(init)) if init is not None else None, _d(l), _d(rr), C.byref(it),
-            C.byref(st), C.byref(ae), _d(hist), C.c_int(64), *self._e()))
-        rec = ModeRecord(mode, it.value, st.value, ae.value, list(hist[: min(it.value, 64)]))
+            C.byref(st), C.byref(ae), _d(hist), C.c_int(cap), *self._e()))
+        rec = ModeRecord(mode, it.value, st.value, ae.value, list(hist[: min(it.value, cap)]))
         return l, rr, rec
 
     def select_order(self, dims, ranks):

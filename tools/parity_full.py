@@ -63,14 +63,6 @@ def decisions(history, norm, eta):
     return out
 
 
-def infer_norm(history, achieved_eta):
-    """||A_work|| from the final decision: achieved_eta = |res_{K-1}-res_K|/||A||
-    (the st working tensor's norm is not reported)."""
-    if len(history) >= 2:
-        return abs(history[-2] - history[-1]) / achieved_eta
-    return history[0] / (1.0 - achieved_eta)
-
-
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -117,6 +109,16 @@ def run(cfg_id, scale, tmpdir, threads):
     rec["core_vs_explicit_ttm_rel"] = float(np.max(np.abs(explicit - g_tk.core)) /
                                             np.max(np.abs(explicit)))
     del explicit
+    # ||working tensor|| at each st position: A x_m U_m^T over the modes
+    # processed before it (the stop rule's denominator, als.cpp:102)
+    work_norms = [norm_a]
+    if st:
+        done = []
+        for m in [pm.mode for pm in g_rep.per_mode][:-1]:
+            done.append((g_tk.factors[m - 1].T, m))
+            w = ctx.multi_mode_product(a, sorted(done, key=lambda x: x[1]))
+            work_norms.append(float(np.linalg.norm(w)))
+            del w
     ctx.close()
     del ctx
 
@@ -138,9 +140,9 @@ def run(cfg_id, scale, tmpdir, threads):
 
     # ---- compare ---------------------------------------------------------------
     modes = []
-    for gm, rm in zip(g_rep.per_mode, r_res.per_mode):
+    for pos, (gm, rm) in enumerate(zip(g_rep.per_mode, r_res.per_mode)):
         g_hist, r_hist = gm.als.residual_history, rm.residual_history
-        nrm = norm_a if not st or rm is r_res.per_mode[0] else infer_norm(r_hist, rm.achieved_eta)
+        nrm = work_norms[pos] if st else norm_a
         r_ratio = decisions(r_hist, nrm, c["eta"])
         g_ratio = decisions(g_hist, nrm, c["eta"])
         closest = min(r_ratio, key=lambda x: abs(np.log(max(x, 1e-300))))
