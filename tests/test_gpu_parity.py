@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2004_02583_b200 as tk
-from oracles import SUBTYPES, Port, Ref, counting_tensor, random_matrix, random_orthonormal, random_tensor
+from oracles import SUBTYPES, OracleError, Port, Ref, counting_tensor, random_matrix, random_orthonormal, random_tensor
 from parity import (CORE_SV_REL_TOL, assert_parity, column_alignment, column_diff, compare_decompositions,
                     ortho_defect, principal_sine)
 
@@ -426,11 +426,15 @@ def test_st_all_orders_of_a_4way_tensor(ctx, ref):
         assert_parity(compare_decompositions(tkr, rep, r))
 
 
-def test_rank_above_64_is_an_explicit_error(ctx, ref):
+def test_rank_above_fiber_count_collapses_like_reference(ctx, ref):
+    # r = 70 > 30 fibers: the randomized range has rank 30 (als.cpp:74-86)
     t = random_tensor(ref, [80, 6, 5], 9)
     eng = tk.FactorEngine.with_als(tk.AlsConfig(eta=1e-8, seed=3))
-    with pytest.raises(tk.UnsupportedError):
+    with pytest.raises(OracleError) as want:
+        ref.hosvd_als(t, [70, 3, 3], eta=1e-8, seed=3)
+    with pytest.raises(tk.DegenerateInitError) as got:
         ctx.t_hosvd(t, tk.Truncation([70, 3, 3]), eng)
+    assert str(got.value) == str(want.value)
 
 
 # ---- multi_mode_product / reconstruct (tensor_ops.cpp:171-191, 420-440) -------

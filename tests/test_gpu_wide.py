@@ -66,7 +66,11 @@ def test_als_low_rank_wide(ctx, ref, dims, mode, r):
     lr, rr, rrep = ref.als_low_rank(t, mode, r, eta=1e-8, seed=5)
     assert rep.iterations == rrep.iterations
     assert rep.status == ("converged" if rrep.status == 0 else "max_iters_reached")
-    assert np.allclose(rep.residual_history, rrep.residual_history, rtol=1e-10, atol=0)
+    # residuals as fractions of ||A||, BASELINE's 1e-10 absolute bar on the
+    # relative error (the closed form cancels ||A||^2 - tr(G_L G_R), so the
+    # raw residual carries ~1e-14 ||A||^2 / res^2 of rounding either way)
+    nrm = np.linalg.norm(t)
+    assert np.max(np.abs(np.subtract(rep.residual_history, rrep.residual_history))) / nrm <= 1e-10
     q = np.linalg.qr(lg)[0]
     qr_ = np.linalg.qr(lr)[0]
     assert principal_sine(q, qr_) <= 1e-8
