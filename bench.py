@@ -212,11 +212,13 @@ def load_peaks():
     return peaks
 
 
-def ncu_traffic(config_id):
+def ncu_traffic(config_id, cls):
+    """DRAM bytes per launch of the kernel class `cls` ("fc" / "fr") on this
+    config, from one ncu --set full capture (profiles/ncu_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        return d.get(str(config_id))
+        return d.get(str(config_id), {}).get(cls)
     except Exception:
         return None
 
@@ -236,7 +238,57 @@ def make_tensor(c, dims, pinned):
 
 
 # ---- reference arm (the compiled reference on the host cores) -----------------
+def write_config_tnsr(config_id, dims, path):
+    """Synthesise the config's tensor (dims may be a slab shape) and write it
+    as TNSR v1 (io.cpp:19-24,131-139). Runs in a CHILD process of the
+    reference arm, so the arm's own process maps only oracle/_ref."""
+    c = CONFIGS[config_id]
+    a, _ = make_tensor(c, dims, pinned=False)
+    flat = a.reshape(-1, order="F")
+    with open(path, "wb") as f:
+        f.write(b"TNSR")
+        f.write(np.array([1, len(dims)], dtype="<u4").tobytes())
+        f.write(np.array(dims, dtype="<u8").tobytes())
+        step = 1 << 26
+        for s in range(0, flat.size, step):
+            f.write(flat[s:s + step].astype("<f8", copy=False).tobytes())
+
+
+def tnsr_outside(config_id, dims, tmpdir):
+    path = os.path.join(tmpdir, f"bench_ref_c{config_id}_{'x'.join(map(str, dims))}_{os.getpid()}.tnsr")
+    subprocess.check_call([sys.executable, os.path.abspath(__file__), "--config", str(config_id),
+                           "--write-tnsr", path, "--tnsr-dims", ",".join(map(str, dims))],
+                          stdout=subprocess.DEVNULL)
+    return path
+
+
+def run_reference_tnsr(c, path, dims, steps, threads):
+    """K decompositions of the tensor in `path` by the compiled, unmodified
+    reference (oracle/_ref: its own read_tnsr, then tenkit::t_hosvd /
+    st_hosvd, hosvd.cpp:74-191) with `threads` OpenMP threads. The timed
+    quantity is the decomposition call (the relative residual included, as
+    the API computes it; reading the file excluded: the tensor is resident in
+    host RAM, as the B200 arm's is in HBM)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracles import Ref
+    ref = Ref()
+    ref.set_threads(threads)
+    times, res = [], None
+    for _ in range(steps):
+        res, call_s = ref.hosvd_als_tnsr(path, dims, c["ranks"], sequential=(c["kind"] == "st"),
+                                         eta=c["eta"], max_iters=MAX_ITERS, seed=ALS_SEED)
+        times.append(call_s)
+    per_mode = [(m.mode, m.iterations) for m in res.per_mode]
+    nbytes = step_bytes(c["kind"], dims, c["ranks"], per_mode)
+    t = sum(times) / len(times)
+    return {"value": nbytes / t / 1e9, "seconds": t, "tts_s": res.seconds, "threads": threads,
+            "iterations": per_mode, "dims": list(dims), "rel_err": res.relative_residual,
+            "bytes": nbytes}
+
+
 def run_reference_sample(c, steps=1, warmup=0):
+    """The bounded CPU sample of the B200 arm's cpu_baseline: the same
+    decomposition on the config's slab (`sample_dims`), in-process."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracles import Ref
     ref = Ref()
@@ -260,31 +312,75 @@ def run_reference_sample(c, steps=1, warmup=0):
             "bytes": nbytes}
 
 
+def full_size_cpu(config_id):
+    """Full-size CPU time to solution of the compiled reference on this pool's
+    GPU box, from tools/parity_full.py (profiles/parity_full_r02.jsonl)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "parity_full_r02.jsonl")) as f:
+            for line in f:
+                d = json.loads(line)
+                if d.get("config") == config_id and d.get("scale", 1.0) == 1.0:
+                    return {"time_to_solution_s": d["cpu"]["report_seconds"],
+                            "call_s": d["cpu"]["call_s"], "threads": d["cpu"]["threads"],
+                            "cpu_model": d["cpu"]["cpu_model"],
+                            "source": "profiles/parity_full_r02.jsonl (tools/parity_full.py: the "
+                                      "compiled reference on the full config tensor, same bytes as "
+                                      "the GPU run, on this pool's GPU box)"}
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
+
+
 def reference_arm(args, c, world, rank):
     if rank != 0:
         return 0
-    r = run_reference_sample(c, steps=args.steps, warmup=args.warmup)
-    sample = (f"full {workload_name(c, r['dims'])} via tenkit::{c['kind']}_hosvd "
-              f"(oracle/_ref, unmodified reference sources), {r['threads']} threads"
-              if r["dims"] == c["dims"] else
-              f"bounded sample: the same decomposition on a {'x'.join(map(str, r['dims']))} slab "
-              f"of the config's generator, tenkit::{c['kind']}_hosvd (oracle/_ref), {r['threads']} threads")
+    threads = os.cpu_count() or 1
+    tmpdir = os.environ.get("TKG_BENCH_TMP", "/tmp")
+    dims = c["dims"]
+    # warm-up steps on the slab sample (thread pool, page faults of the code);
+    # the K timed steps decompose the FULL config tensor
+    paths = []
+    try:
+        if args.warmup > 0:
+            paths.append(tnsr_outside(args.config, c["sample_dims"], tmpdir))
+            run_reference_tnsr(c, paths[-1], c["sample_dims"], args.warmup, threads)
+        paths.append(tnsr_outside(args.config, dims, tmpdir))
+        r = run_reference_tnsr(c, paths[-1], dims, args.steps, threads)
+    finally:
+        for p in paths:
+            try:
+                os.unlink(p)
+            except OSError:
+                pass
+    sample = (f"full {workload_name(c)} via the reference's read_tnsr + tenkit::{c['kind']}_hosvd "
+              f"(oracle/_ref, unmodified reference sources), {threads} threads; the TNSR was written "
+              f"by a child process, so this process maps only oracle/_ref; warm-up steps on a "
+              f"{'x'.join(map(str, c['sample_dims']))} slab")
     line = {
         "metric": f"ALS-sweep effective HBM GB/s ({workload_name(c)})",
         "value": r["value"], "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Tucker model, SURVEY §8(d))",
-        "config": {"workload": workload_name(c), "sample_dims": r["dims"],
+        "config": {"workload": workload_name(c), "config_id": args.config,
                    "iterations": r["iterations"]},
+        "value_basis": VALUE_BASIS,
         "time_to_solution_s": r["tts_s"],
-        "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["threads"],
+        "relative_residual": r["rel_err"],
+        "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": threads,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     emit(line)
     return 0
+
+
+VALUE_BASIS = ("effective: algorithmic bytes of the REFERENCE algorithm's tensor passes for the run's "
+               "iteration counts (init + k right + (k-1) left per mode, t: core TTM chain over A, "
+               "st: shrink; 8(|A| + F r + I r) per contraction, SURVEY §8(d)) / step time; the same "
+               "byte count for both arms. The B200 t-HOSVD path skips the first core TTM pass over A "
+               "(DESIGN §3) and runs a fused residual pass the count does not credit")
 
 
 # ---- B200 arm ------------------------------------------------------------------------
@@ -406,8 +502,8 @@ def b200_arm(args, c, world, rank, local):
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["hbm_src"]}
     roof.update({"kernel": {"fc": "FC fiber contraction (ALS right update A_(n)^T L')",
                             "fr": "FR fiber reduction (left update A_(n) R, init A_(n) S)"}[cls],
-                 "traffic": (ncu_traffic(args.config) or {}).get("dram_bytes_per_launch"),
-                 "traffic_source": ncu_traffic(args.config), "launch_ms": per_launch_ms,
+                 "traffic": (ncu_traffic(args.config, cls) or {}).get("dram_bytes_per_launch"),
+                 "traffic_source": ncu_traffic(args.config, cls), "launch_ms": per_launch_ms,
                  "arith_intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge,
                  "share_of_step": st["ms"] / (ms_step * args.steps),
                  "hbm_frac_of_dominant": (st["bytes"] / (st["ms"] * 1e-3) / 1e9) / peaks["hbm_gbs"],
@@ -417,10 +513,10 @@ def b200_arm(args, c, world, rank, local):
     if world == 1 and not args.no_cpu_baseline:
         r = run_reference_sample(c, steps=1, warmup=0)
         cpu = {"value": r["value"], "unit": "GB/s", "cores": r["threads"], "kind": "reference",
-               "sample": (f"tenkit::{c['kind']}_hosvd (oracle/_ref, unmodified reference sources) "
+               "sample": (f"bounded sample: tenkit::{c['kind']}_hosvd (oracle/_ref, unmodified reference sources) "
                           f"on a {'x'.join(map(str, r['dims']))} tensor from the same generator, "
                           f"{r['threads']} host threads, 1 run of {r['seconds']:.1f} s"),
-               "time_to_solution_s": r["tts_s"]}
+               "time_to_solution_s": r["tts_s"], "full_size": full_size_cpu(args.config)}
 
     line = {
         "metric": f"ALS-sweep effective HBM GB/s ({workload_name(c)})",
@@ -434,6 +530,7 @@ def b200_arm(args, c, world, rank, local):
                                    if sharded else "single GPU"),
                    "l2": "flushed between steps" if flush else "tensor larger than L2 (%.1f GiB)" % (n * 8 / 2**30),
                    "iterations": per_mode},
+        "value_basis": VALUE_BASIS,
         "time_to_solution_s": rep.seconds,
         "tflops": nflops / (ms_step * 1e-3) / 1e12,
         "relative_residual": rep.relative_residual,
@@ -474,7 +571,13 @@ def main():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--shard", action="store_true",
                    help="use the sharded (NCCL) path even on one GPU")
+    p.add_argument("--write-tnsr", default=None, help=argparse.SUPPRESS)
+    p.add_argument("--tnsr-dims", default=None, help=argparse.SUPPRESS)
     args = p.parse_args()
+    if args.write_tnsr:  # child of the reference arm: synthesise + write, nothing else
+        dims = [int(x) for x in args.tnsr_dims.split(",")] if args.tnsr_dims else CONFIGS[args.config]["dims"]
+        write_config_tnsr(args.config, dims, args.write_tnsr)
+        return 0
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     c = CONFIGS[args.config]
     world, rank, local = dist_setup()
