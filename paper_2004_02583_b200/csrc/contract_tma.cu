@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -584,6 +585,187 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
 }
 
 // ---------------------------------------------------------------------------
+// FR for 128 < K <= 248 with s == 1 (mode 1 of e.g. a 200^4 tensor): ONE CTA
+// covers all K contraction rows, so R (or S) is streamed once per pass
+// instead of once per 128-row group, and the 8 consumer warps share the
+// MT = ceil(K/8) row tiles evenly: warp w owns the full row tiles
+// w, w+8, ... (all NC/8 column tiles, base = MT/8 of them) plus every 8th
+// (row tile, column tile) pair of the MT % 8 remainder tiles. For K = 200
+// that is 3 x 7 + 1 DMMA tiles per warp (22 each, 175 in all), where two
+// 128-row groups left the second group's SM sub-partitions a third idle.
+// A stage holds two 132-row boxes of the same 16 fibers (rows 0..131 and
+// 128..259; TMA zero-fills rows past K).
+// ---------------------------------------------------------------------------
+template <int NC, bool MCOL>
+struct FrW {
+  static constexpr int kKB = 16;    // fibers per stage
+  static constexpr int kStages = 4;
+  static constexpr int kLdA = 132;
+  static constexpr int kBoxBytes = kKB * kLdA * 8;
+  static constexpr int kBytesA = 2 * kBoxBytes;
+  static constexpr int kLdM = MCOL ? kKB + 4 : NC + 4;
+  static constexpr int kRowsM = MCOL ? NC : kKB;
+  static constexpr int kBytesM = kRowsM * kLdM * 8;
+  static constexpr int kStageBytes = ((kBytesA + kBytesM) + 127) / 128 * 128;
+  static constexpr int kNT = NC / 8;
+  static constexpr int kRemP = 2;   // remainder pairs per warp (register budget)
+  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes;
+};
+
+template <int NC, bool MCOL>
+__global__ void __launch_bounds__(kThreadsTma, 1)
+    fr_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
+                   FrTmaArgs a) {
+  using C = FrW<NC, MCOL>;
+  constexpr int kNT = C::kNT;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see fc_tma_kernel
+  if (a.skip && *a.skip) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + C::kStages;
+  unsigned char* ring = smem_raw + 1024;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t F = a.s * a.P;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCons);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kCons) {
+    if (lane == 0) {
+      prefetch_map(&tmA);
+      prefetch_map(&tmM);
+      int kb = 0;
+      for (uint32_t range = blockIdx.x; range < a.ranges; range += gridDim.x) {
+        const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
+        const uint64_t f1 = min(F, f0 + a.fibers_per_range);
+        for (uint64_t j = f0; j < f1; j += C::kKB, ++kb) {
+          const int slot = kb % C::kStages;
+          const uint32_t ph = (kb / C::kStages) & 1;
+          mbar_wait(&empty[slot], ph ^ 1);
+          unsigned char* st = ring + size_t(slot) * C::kStageBytes;
+          mbar_arrive_expect_tx(&full[slot], C::kBytesA + C::kBytesM);
+          tma_2d(st, &tmA, &full[slot], 0, int(j));
+          tma_2d(st + C::kBoxBytes, &tmA, &full[slot], 128, int(j));
+          if (MCOL) tma_2d(st + C::kBytesA, &tmM, &full[slot], int(j), 0);
+          else tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, int(j));
+        }
+      }
+    }
+    return;
+  }
+
+  const int q = lane & 3;
+  const int r8 = lane >> 2;
+  const int MT = int((a.K + 7) / 8);
+  const int base = MT / 8;              // 2 or 3 full row tiles per warp
+  const int nrem = (MT % 8) * kNT;      // remainder (row tile, column tile) pairs
+  double sq_acc[4] = {0.0, 0.0, 0.0, 0.0};
+  // ||A||^2 is fused only into the init pass (column-major S)
+  const bool want_sq = MCOL && a.sumsq_part != nullptr;
+
+  int kb = 0;
+  for (uint32_t range = blockIdx.x; range < a.ranges; range += gridDim.x) {
+    const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
+    const uint64_t f1 = min(F, f0 + a.fibers_per_range);
+    double acc[3][kNT][2];
+    double accr[C::kRemP][2];
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+#pragma unroll
+      for (int n = 0; n < kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < C::kRemP; ++t) accr[t][0] = accr[t][1] = 0.0;
+    for (uint64_t j = f0; j < f1; j += C::kKB, ++kb) {
+      const int slot = kb % C::kStages;
+      const uint32_t ph = (kb / C::kStages) & 1;
+      mbar_wait(&full[slot], ph);
+      const double* A0 = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes);
+      const double* A1 = A0 + C::kKB * C::kLdA;  // rows 128..259
+      const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes + C::kBytesA);
+      const int kvalid = int(min(uint64_t(C::kKB), f1 - j));
+#pragma unroll
+      for (int t = 0; t < C::kKB / 4; ++t) {
+        const int kk = 4 * t + q;
+        const bool kok = kk < kvalid;
+        // 9 warps: at most 3 per SM sub-partition, so 168 registers per
+        // thread; the column-tile fragments are loaded one at a time
+        double af[3];
+#pragma unroll
+        for (int mi = 0; mi < 3; ++mi) {
+          const int row = (warp + 8 * mi) * 8 + r8;  // mi < 2: box 0, mi == 2: box 1
+          const double v = mi < 2 ? A0[kk * C::kLdA + row] : A1[kk * C::kLdA + row - 128];
+          af[mi] = (kok && mi < base) ? v : 0.0;
+          if (want_sq) sq_acc[(t & 1) * 2 + (mi & 1)] = fma(af[mi], af[mi], sq_acc[(t & 1) * 2 + (mi & 1)]);
+        }
+#pragma unroll
+        for (int n = 0; n < kNT; ++n) {
+          const double b = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
+          dmma(acc[0][n][0], acc[0][n][1], af[0], b);
+          dmma(acc[1][n][0], acc[1][n][1], af[1], b);
+          if (base > 2) dmma(acc[2][n][0], acc[2][n][1], af[2], b);
+        }
+#pragma unroll
+        for (int u = 0; u < C::kRemP; ++u) {
+          const int p = warp + 8 * u;
+          if (p < nrem) {
+            const int m = 8 * base + p / kNT, n = p % kNT;
+            const double v = A1[kk * C::kLdA + m * 8 + r8 - 128];
+            const double af = kok ? v : 0.0;
+            // each A element of a remainder tile is squared once (column tile 0)
+            if (want_sq && n == 0) sq_acc[(t & 1) * 2 + 1] = fma(af, af, sq_acc[(t & 1) * 2 + 1]);
+            const double b = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
+            dmma(accr[u][0], accr[u][1], af, b);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    // this range's partial rows
+    double* dst0 = a.partial + size_t(range) * a.K * a.ncp;
+#pragma unroll
+    for (int mi = 0; mi < 3; ++mi) {
+      if (mi >= base) continue;
+      const int i = (warp + 8 * mi) * 8 + r8;
+      if (i >= int(a.K)) continue;
+#pragma unroll
+      for (int n = 0; n < kNT; ++n)
+        *reinterpret_cast<double2*>(dst0 + size_t(i) * a.ncp + n * 8 + 2 * q) =
+            make_double2(acc[mi][n][0], acc[mi][n][1]);
+    }
+#pragma unroll
+    for (int u = 0; u < C::kRemP; ++u) {
+      const int p = warp + 8 * u;
+      if (p >= nrem) continue;
+      const int i = (8 * base + p / kNT) * 8 + r8, n = p % kNT;
+      if (i < int(a.K))
+        *reinterpret_cast<double2*>(dst0 + size_t(i) * a.ncp + n * 8 + 2 * q) =
+            make_double2(accr[u][0], accr[u][1]);
+    }
+  }
+  if (want_sq) {
+    __shared__ double red[kCons];
+    double sq = (sq_acc[0] + sq_acc[1]) + (sq_acc[2] + sq_acc[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[warp] = sq;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kCons * 32));
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kCons; ++w) s += red[w];
+      a.sumsq_part[blockIdx.x] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -808,6 +990,16 @@ cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTm
   return launch_pdl(k, grid, C::kSmem, st, A, M, a);
 }
 
+template <int NC, bool MCOL>
+cudaError_t fr_wide_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, int grid,
+                           cudaStream_t st) {
+  using C = FrW<NC, MCOL>;
+  auto k = fr_wide_kernel<NC, MCOL>;
+  cudaError_t e = set_smem(k, C::kSmem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k, grid, C::kSmem, st, A, M, a);
+}
+
 template <int NC, int MODE, bool MCOL>
 cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, int grid,
                           cudaStream_t st) {
@@ -940,6 +1132,45 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
   const uint32_t ncp = pad_nc(a.nc);
   CUtensorMap A, M;
   const uint64_t F = v.s * v.P;
+  if (mode == kFibI && fr_wide_ok(v, ncp)) {
+    constexpr uint32_t kKB = 16;
+    {
+      const uint64_t dims[2] = {v.K, F};
+      const uint64_t strides[1] = {v.is_p * 8};
+      const uint32_t box[2] = {132, kKB};
+      if (!encode(&A, v.base, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    if (!mcol) {
+      const uint64_t dims[2] = {ncp, F};
+      const uint64_t strides[1] = {mj * 8};
+      const uint32_t box[2] = {ncp + 4, kKB};
+      if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    } else {
+      const uint64_t dims[2] = {F, a.nc};
+      const uint64_t strides[1] = {mc * 8};
+      const uint32_t box[2] = {kKB + 4, ncp};
+      if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
+    }
+    a.s = v.s;
+    a.P = v.P;
+    a.K = v.K;
+    a.ncp = ncp;
+    a.igroups = 1;
+    const uint64_t steps = (F + kKB - 1) / kKB;
+    const uint64_t ranges = std::min<uint64_t>(uint64_t(num_sms), std::max<uint64_t>(1, steps / 4));
+    a.fibers_per_range = (steps + ranges - 1) / ranges * kKB;
+    a.ranges = uint32_t((F + a.fibers_per_range - 1) / a.fibers_per_range);
+    if (ranges_used) *ranges_used = a.ranges;
+    const int grid = int(std::min<uint64_t>(a.ranges, uint64_t(num_sms)));
+    if (grid_used) *grid_used = grid;
+    switch (ncp) {
+      case 40: return mcol ? fr_wide_launch<40, true>(A, M, a, grid, st) : fr_wide_launch<40, false>(A, M, a, grid, st);
+      case 48: return mcol ? fr_wide_launch<48, true>(A, M, a, grid, st) : fr_wide_launch<48, false>(A, M, a, grid, st);
+      case 56: return mcol ? fr_wide_launch<56, true>(A, M, a, grid, st) : fr_wide_launch<56, false>(A, M, a, grid, st);
+      case 64: return mcol ? fr_wide_launch<64, true>(A, M, a, grid, st) : fr_wide_launch<64, false>(A, M, a, grid, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (mode == kFibI) {
     const uint64_t dims[2] = {v.K, F};
     const uint64_t strides[1] = {v.is_p * 8};
@@ -1009,6 +1240,18 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
                            : fr_tma_launch<N, kFibS, false>(A, M, a, grid, st)))
   TKG_NC_SWITCH(ncp, TKG_FR_CALL)
 #undef TKG_FR_CALL
+}
+
+// one CTA over all K rows (fr_wide_kernel): mode 1 with 128 < K <= 248 at
+// the 1-CTA-per-SM column counts, when the remainder row tiles give each
+// warp at most FrW::kRemP extra pairs (TKG_FR_WIDE=0 disables it)
+bool fr_wide_ok(const FiberView& v, uint32_t ncp) {
+  static const bool on = [] {
+    const char* e = std::getenv("TKG_FR_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  const uint32_t mt = (v.K + 7) / 8, nrem = (mt % 8) * (ncp / 8);
+  return on && v.s == 1 && v.K > 128 && v.K <= 248 && ncp >= 40 && ncp <= 64 && nrem <= 8 * 2;
 }
 
 uint32_t fr_tma_ranges(const FiberView& v, int num_sms) {

@@ -25,6 +25,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <type_traits>
 
@@ -494,6 +497,73 @@ constexpr int kFinRows = 64;    // rows of R per block of the row pass
 constexpr int kFinStages = 3;   // ring depth of the row pass
 constexpr int kFinPerSm = 2;    // resident CTAs per SM (grid of the row pass)
 
+// Residual, stop rule and G_R^{-1} from the reduced Gram G (shared memory,
+// column-major r x r), on one CTA; Gi: r*r shared scratch.
+template <int NC>
+__device__ void finish_tail(const FinishArgs& a, double* G, double* Gi) {
+  AlsCtrl* ctrl = a.ctrl;
+  const uint32_t r = a.r;
+  __shared__ double hi_s[32], lo_s[32];
+  if (threadIdx.x < 32) {
+    // compensated trace(G_L G_R) (als.cpp:136-141)
+    double s = 0.0, c = 0.0;
+    for (uint32_t e = threadIdx.x; e < r * r; e += 32) {
+      const double p = a.GL[e] * G[e];
+      const double pe = fma(a.GL[e], G[e], -p);
+      double t, err;
+      two_sum(s, p, t, err);
+      s = t;
+      c += err + pe;
+    }
+    hi_s[threadIdx.x] = s;
+    lo_s[threadIdx.x] = c;
+  }
+  __syncthreads();
+  __shared__ int cont_s;
+  if (threadIdx.x == 0) {
+    double s = 0.0, c = 0.0;
+    for (int k = 0; k < 32; ++k) {
+      double t, err;
+      two_sum(s, hi_s[k], t, err);
+      s = t;
+      c += err + lo_s[k];
+    }
+    const double tr = s + c;
+    const double residual = sqrt(fmax(0.0, ctrl->norm_sq - tr));
+    const int it = ctrl->iter + 1;
+    ctrl->iter = it;
+    if (it <= ctrl->history_cap) a.history[it - 1] = residual;
+    ctrl->residual = residual;
+    const double achieved = fabs(ctrl->prev - residual) / ctrl->norm;
+    ctrl->achieved = achieved;
+    int cont = 1;
+    if (achieved <= ctrl->eta) {
+      ctrl->status = 0;
+      cont = 0;
+    } else if (it >= ctrl->max_iters) {
+      ctrl->status = 1;
+      cont = 0;
+    }
+    ctrl->prev = residual;
+    cont_s = cont;
+    if (!cont) ctrl->stop = 1;
+  }
+  __syncthreads();
+  if (!cont_s) return;
+  double piv = 0.0;
+  const int fail = gj_inv_reg<ke_for(NC)>(G, Gi, r, 1e-13, &piv);
+  if (fail) {
+    if (threadIdx.x == 0) {
+      ctrl->error = kAlsErrLeftSingular;
+      ctrl->pivot = piv;
+      ctrl->pad = fail;  // failing column (1-based)
+      ctrl->stop = 1;
+    }
+    return;
+  }
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.GRinv[e] = Gi[e];
+}
+
 template <int NC>
 __global__ void __launch_bounds__(kThreads, kFinPerSm) finish_step_kernel(FinishArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -627,65 +697,7 @@ __global__ void __launch_bounds__(kThreads, kFinPerSm) finish_step_kernel(Finish
   double* Gi = G + r * r;
   __syncthreads();
   load_mat(a.gs, G, r * r);
-  __shared__ double hi_s[32], lo_s[32];
-  if (threadIdx.x < 32) {
-    // compensated trace(G_L G_R) (als.cpp:136-141)
-    double s = 0.0, c = 0.0;
-    for (uint32_t e = threadIdx.x; e < r * r; e += 32) {
-      const double p = a.GL[e] * G[e];
-      const double pe = fma(a.GL[e], G[e], -p);
-      double t, err;
-      two_sum(s, p, t, err);
-      s = t;
-      c += err + pe;
-    }
-    hi_s[threadIdx.x] = s;
-    lo_s[threadIdx.x] = c;
-  }
-  __syncthreads();
-  __shared__ int cont_s;
-  if (threadIdx.x == 0) {
-    double s = 0.0, c = 0.0;
-    for (int k = 0; k < 32; ++k) {
-      double t, err;
-      two_sum(s, hi_s[k], t, err);
-      s = t;
-      c += err + lo_s[k];
-    }
-    const double tr = s + c;
-    const double residual = sqrt(fmax(0.0, ctrl->norm_sq - tr));
-    const int it = ctrl->iter + 1;
-    ctrl->iter = it;
-    if (it <= ctrl->history_cap) a.history[it - 1] = residual;
-    ctrl->residual = residual;
-    const double achieved = fabs(ctrl->prev - residual) / ctrl->norm;
-    ctrl->achieved = achieved;
-    int cont = 1;
-    if (achieved <= ctrl->eta) {
-      ctrl->status = 0;
-      cont = 0;
-    } else if (it >= ctrl->max_iters) {
-      ctrl->status = 1;
-      cont = 0;
-    }
-    ctrl->prev = residual;
-    cont_s = cont;
-    if (!cont) ctrl->stop = 1;
-  }
-  __syncthreads();
-  if (!cont_s) return;
-  double piv = 0.0;
-  const int fail = gj_inv_reg<ke_for(NC)>(G, Gi, r, 1e-13, &piv);
-  if (fail) {
-    if (threadIdx.x == 0) {
-      ctrl->error = kAlsErrLeftSingular;
-      ctrl->pivot = piv;
-      ctrl->pad = fail;  // failing column (1-based)
-      ctrl->stop = 1;
-    }
-    return;
-  }
-  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.GRinv[e] = Gi[e];
+  finish_tail<NC>(a, G, Gi);
 }
 
 // ---- cholqr_step -------------------------------------------------------------------
@@ -822,6 +834,312 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
   PHASE(12);
 }
 
+// ---- cluster steps ---------------------------------------------------------------------
+// The same three steps as ONE thread-block cluster (up to 16 CTAs, one per
+// SM) instead of a grid-synchronised launch over every SM. CTA q of the
+// cluster owns the contiguous factor rows [q*rb, (q+1)*rb), rb = ceil(I/cs),
+// and keeps them through every phase; the per-CTA Gram partials live in
+// shared memory and every CTA sums all cs of them over DSMEM in the same
+// fixed order, so each CTA holds bit-identical r x r Gram matrices and runs
+// the r x r factorization itself: no broadcast phase and no grid-wide
+// barrier, a step costs 1-4 cluster barriers. The split-K FR partials are
+// summed row-block by row-block straight into shared memory (fixed k
+// order). Launched with programmatic stream serialization: griddepcontrol.wait
+// orders the first dependent read after the preceding kernel's writes while
+// the launch itself overlaps that kernel's tail.
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// X[row][c] (pitch ld) = sum_{k < nparts} part[k*stride + (i0+row)*ldp + c],
+// k ascending; up to 16 loads per thread in flight.
+__device__ void sum_rows(const double* part, int nparts, uint64_t stride, uint32_t ldp, uint32_t i0,
+                         uint32_t nrow, uint32_t r, double* X, uint32_t ld) {
+  for (uint32_t e = threadIdx.x; e < nrow * r; e += blockDim.x) {
+    const uint32_t row = e / r, c = e % r;
+    const double* p = part + uint64_t(i0 + row) * ldp + c;
+    double s = 0.0;
+    int k = 0;
+    for (; k + 16 <= nparts; k += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldcg(p + uint64_t(k + u) * stride);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+    for (; k < nparts; ++k) s += __ldcg(p + uint64_t(k) * stride);
+    X[row * ld + c] = s;
+  }
+}
+
+// G (column-major, symmetric) = sum over the cluster's CTAs q = 0..cs-1 of
+// their Gram partials gp (GramAcc layout: entry a*r + b, a <= b), read over
+// DSMEM in ascending q.
+__device__ void cluster_gram_sum(cg::cluster_group& cl, double* gp, uint32_t r, double* G) {
+  const uint32_t cs = cl.num_blocks();
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const uint32_t a = e / r, b = e % r;
+    if (a > b) continue;
+    double s = 0.0;
+    for (uint32_t q = 0; q < cs; ++q) s += cl.map_shared_rank(gp, q)[e];
+    G[a + b * r] = s;
+    G[b + a * r] = s;
+  }
+}
+
+__device__ __forceinline__ void cta_rows(uint32_t I, uint32_t q, uint32_t cs, uint32_t& lo, uint32_t& hi) {
+  const uint32_t rb = (I + cs - 1) / cs;
+  lo = min(I, q * rb);
+  hi = min(I, lo + rb);
+}
+
+template <int KE>
+__global__ void __launch_bounds__(kThreads) prep_cluster_kernel(PrepArgs a) {
+  pdl_wait();
+  PHASE(30);
+  cg::cluster_group cl = cg::this_cluster();
+  AlsCtrl* ctrl = a.ctrl;
+  if (ctrl->stop) return;  // uniform over the cluster (written by earlier kernels only)
+  extern __shared__ double sm[];
+  const uint32_t r = a.r, ld = r + 1, I = a.I;
+  double* X = sm;               // [kRB][ld]
+  double* X2 = X + kRB * ld;    // [kRB][ld]
+  double* M = X2 + kRB * ld;    // r*r
+  double* G = M + r * r;        // r*r
+  double* W = G + r * r;        // r*r
+  double* gp = W + r * r;       // r*r (read by the whole cluster)
+  uint32_t lo, hi;
+  cta_rows(I, cl.block_rank(), cl.num_blocks(), lo, hi);
+
+  // L rows (from partials: Y G_R^{-1}) and their Gram partial
+  if (a.from_partials) load_mat_rm(a.GRinv, M, r);
+  GramAcc g;
+  g.zero();
+  for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+    const uint32_t nrow = min(uint32_t(kRB), hi - i0);
+    if (a.from_partials) {
+      sum_rows(a.part, a.nparts, uint64_t(I) * a.ldp, a.ldp, i0, nrow, r, X, ld);
+      __syncthreads();
+      rows_mul(X, nrow, r, ld, M, X2, ld);
+      __syncthreads();
+      store_rows_cm(X2, ld, i0, nrow, r, a.Lc, I);
+    } else {
+      load_rows(a.Lc, false, I, i0, nrow, r, X2, ld);
+      __syncthreads();
+    }
+    g.add(X2, nrow, r, ld);
+    __syncthreads();
+  }
+  PHASE(31);
+  g.store(gp, r);
+  cl.sync();
+  cluster_gram_sum(cl, gp, r, G);
+  cl.sync();  // every remote read of gp is done (CTAs may exit from here on)
+  PHASE(32);
+
+  // G_L^{-1} with the spd_solve pivot floor, in every CTA (identical bits)
+  double piv = 0.0;
+  const int fail = gj_inv_reg<KE>(G, W, r, 1e-13, &piv);
+  PHASE(33);
+  if (fail) {
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+      ctrl->error = kAlsErrRightSingular;
+      ctrl->pivot = piv;
+      ctrl->pad = fail;  // failing column (1-based)
+      ctrl->stop = 1;
+    }
+    return;
+  }
+  if (cl.block_rank() == 0)
+    for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+      a.GL[e] = G[e];
+      a.GLinv[e] = W[e];
+    }
+  // Mt rows = L rows G_L^{-1} (row-major operand of the column-major inverse)
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) M[e] = W[(e / r) + (e % r) * r];
+  __syncthreads();
+  for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+    const uint32_t nrow = min(uint32_t(kRB), hi - i0);
+    load_rows(a.Lc, false, I, i0, nrow, r, X, ld);  // this CTA's own rows (written above)
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < nrow * a.ncp; e += blockDim.x) {
+      const uint32_t row = e / a.ncp, c = e % a.ncp;
+      double s = 0.0;
+      if (c < r)
+        for (uint32_t k = 0; k < r; ++k) s = fma(X[row * ld + k], M[k * r + c], s);
+      a.Mt[uint64_t(i0 + row) * a.ncp + c] = s;
+    }
+    __syncthreads();
+  }
+  PHASE(34);
+}
+
+// finish: G_R = sum of the Gram partials (RᵀR per FC CTA, or per row-pass
+// CTA) split over the cluster's warps, each entry written into CTA 0's
+// shared memory; CTA 0 then runs the residual / stop rule / G_R^{-1} of
+// finish_step_kernel. mode 2 (sharded): G_R already reduced in gs, one CTA.
+template <int NC>
+__global__ void __launch_bounds__(kThreads) finish_cluster_kernel(FinishArgs a) {
+  pdl_wait();
+  cg::cluster_group cl = cg::this_cluster();
+  if (a.ctrl->stop) return;
+  extern __shared__ __align__(16) double sm[];
+  const uint32_t r = a.r;
+  double* G = sm;
+  double* Gi = G + r * r;
+  if (a.mode == 2) {
+    load_mat(a.gs, G, r * r);
+  } else {
+    const uint32_t wpb = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nw = cl.num_blocks() * wpb;
+    const uint32_t ntri = r * (r + 1) / 2;
+    double* G0 = cl.map_shared_rank(G, 0);
+    for (uint32_t t = cl.block_rank() * wpb + (threadIdx.x >> 5); t < ntri; t += nw) {
+      uint32_t aa = 0, rem = t;
+      while (rem >= r - aa) {
+        rem -= r - aa;
+        ++aa;
+      }
+      const uint32_t b = aa + rem;
+      const double* p = a.gpart + size_t(aa) * NC + b;
+      double s = 0.0;
+      for (int k = int(lane); k < a.gram_nparts; k += 32) s += __ldcg(p + size_t(k) * NC * NC);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) {
+        G0[aa + b * r] = s;
+        G0[b + aa * r] = s;
+      }
+    }
+    cl.sync();
+    if (cl.block_rank() != 0) return;
+    if (a.gs)
+      for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.gs[e] = G[e];
+  }
+  finish_tail<NC>(a, G, Gi);
+}
+
+template <int KE>
+__global__ void __launch_bounds__(kThreads) cholqr_cluster_kernel(CholQrArgs a) {
+  pdl_wait();
+  PHASE(40);
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  const uint32_t r = a.r, ld = r + 1, I = a.I;
+  double* X = sm;               // [kRB][ld]
+  double* X2 = X + kRB * ld;    // [kRB][ld]
+  double* G = X2 + kRB * ld;    // r*r
+  double* W = G + r * r;        // r*r  (L1, then L2)
+  double* W2 = W + r * r;       // r*r  (L1^{-1}, then L2^{-1})
+  double* L1 = W2 + r * r;      // r*r
+  double* gp = L1 + r * r;      // r*r (read by the whole cluster)
+  const bool rm = a.nparts > 0;  // Y as row-major partials, else column-major
+  const bool lead = cl.block_rank() == 0;
+  uint32_t lo, hi;
+  cta_rows(I, cl.block_rank(), cl.num_blocks(), lo, hi);
+
+  // Y rows (partials summed) -> Q as scratch, Gram partial
+  GramAcc g;
+  g.zero();
+  for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+    const uint32_t nrow = min(uint32_t(kRB), hi - i0);
+    if (rm) sum_rows(a.Y, a.nparts, uint64_t(I) * a.ldp, uint32_t(a.ldp), i0, nrow, r, X, ld);
+    else load_rows(a.Y, false, a.ldp, i0, nrow, r, X, ld);
+    __syncthreads();
+    store_rows_cm(X, ld, i0, nrow, r, a.Q, I);
+    g.add(X, nrow, r, ld);
+    __syncthreads();
+  }
+  PHASE(41);
+  g.store(gp, r);
+  cl.sync();
+  cluster_gram_sum(cl, gp, r, G);
+  PHASE(42);
+  cl.sync();  // gp is free again
+  const int fail1 = chol_reg<KE>(G, W, r);
+  if (fail1) {
+    if (lead && threadIdx.x == 0) {
+      a.work[0] = fail1;
+      a.work[1] = fail1;
+      a.ctrl->degenerate_col = fail1;
+    }
+    return;
+  }
+  for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) L1[e] = W[e];
+  tri_inv_reg<KE>(W, W2, r);  // L1^{-1}; R1^{-1}(k, c) = L1^{-1}(c, k): row-major operand = W2
+
+  PHASE(43);
+  // Q1 rows = Y rows R1^{-1} (in place in Q), Gram partial of Q1
+  g.zero();
+  for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+    const uint32_t nrow = min(uint32_t(kRB), hi - i0);
+    load_rows(a.Q, false, I, i0, nrow, r, X, ld);
+    __syncthreads();
+    rows_mul(X, nrow, r, ld, W2, X2, ld);
+    __syncthreads();
+    store_rows_cm(X2, ld, i0, nrow, r, a.Q, I);
+    g.add(X2, nrow, r, ld);
+    __syncthreads();
+  }
+  PHASE(44);
+  g.store(gp, r);
+  cl.sync();
+  cluster_gram_sum(cl, gp, r, G);
+  PHASE(45);
+  cl.sync();
+  const int fail = chol_reg<KE>(G, W, r);
+  if (!fail) tri_inv_reg<KE>(W, W2, r);  // L2^{-1}
+  PHASE(46);
+  if (lead) {
+    // R = R2 R1 = L2^T L1^T, the degeneracy test on its diagonal (als.cpp:74-86)
+    double* Rm = G;  // G is no longer needed
+    __syncthreads();
+    if (!fail) {
+      for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+        const uint32_t i = e % r, j = e / r;
+        double acc = 0.0;
+        if (i <= j)
+          for (uint32_t k = i; k <= j; ++k) acc += W[k + i * r] * L1[j + k * r];
+        Rm[e] = acc;
+        if (a.rmat) a.rmat[e] = acc;
+      }
+      __syncthreads();
+      if (a.rt)
+        for (uint32_t e = threadIdx.x; e < r * a.ldrt; e += blockDim.x) {
+          const uint32_t row = e / a.ldrt, c = e % a.ldrt;
+          a.rt[e] = c < r ? Rm[c + row * r] : 0.0;
+        }
+    }
+    if (threadIdx.x == 0) {
+      int bad = fail;
+      if (!fail && a.check) {
+        double md = 0.0;
+        for (uint32_t i = 0; i < r; ++i) md = fmax(md, fabs(Rm[i + i * r]));
+        for (uint32_t i = 0; i < r; ++i)
+          if (fabs(Rm[i + i * r]) <= 1e-13 * md || md == 0.0) {
+            bad = int(i) + 1;
+            break;
+          }
+      }
+      a.ctrl->degenerate_col = bad;
+      a.work[0] = 0;
+      a.work[1] = fail;
+    }
+  }
+  PHASE(47);
+  if (fail) return;
+  // Q rows = Q1 rows R2^{-1}
+  for (uint32_t i0 = lo; i0 < hi; i0 += kRB) {
+    const uint32_t nrow = min(uint32_t(kRB), hi - i0);
+    load_rows(a.Q, false, I, i0, nrow, r, X, ld);
+    __syncthreads();
+    rows_mul(X, nrow, r, ld, W2, X2, ld);
+    __syncthreads();
+    store_rows_cm(X2, ld, i0, nrow, r, a.Q, I);
+    __syncthreads();
+  }
+  PHASE(48);
+}
+
 template <class K>
 // exact: the caller sized per-CTA partials for `want` CTAs (fail rather than
 // launch fewer).
@@ -845,6 +1163,90 @@ cudaError_t coop_launch(K kernel, int want, int num_sms, size_t smem, void* args
 
 size_t rows_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 3 * size_t(r) * r); }
 
+// Cluster steps (TKG_COOP_STEPS=1 selects the grid-synchronised kernels).
+bool use_grid_steps() {
+  static const bool v = [] {
+    const char* e = std::getenv("TKG_COOP_STEPS");
+    return e != nullptr && e[0] == '1';
+  }();
+  return v;
+}
+
+bool use_cluster_prep() {
+  static const bool v = [] {
+    const char* e = std::getenv("TKG_CLUSTER_PREP");
+    return e != nullptr && e[0] == '1';
+  }();
+  return v;
+}
+
+// Largest cluster (16 non-portable, else 8, 4, 2, 1) that the kernel can
+// place with `smem` bytes per CTA; cached per kernel and size.
+template <class K>
+int cluster_size(K kernel, size_t smem) {
+  static std::mutex m;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> g(m);
+  auto it = cache.find({reinterpret_cast<const void*>(kernel), smem});
+  if (it != cache.end()) return it->second;
+  int want = 16;
+  if (const char* e = std::getenv("TKG_CLUSTER")) want = std::max(1, std::min(16, std::atoi(e)));
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    want = std::min(want, 8);
+  }
+  int cs = want;
+  for (; cs > 1; cs /= 2) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) == cudaSuccess && n >= 1) break;
+    cudaGetLastError();
+  }
+  cache[{reinterpret_cast<const void*>(kernel), smem}] = cs;
+  return cs;
+}
+
+template <class K, class A>
+cudaError_t cluster_launch(K kernel, int cs, size_t smem, const A& args, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args);
+  if (e != cudaSuccess) cudaGetLastError();
+  return e;
+}
+
+template <class K, class A>
+cudaError_t cluster_step(K kernel, size_t smem, const A& args, cudaStream_t st, int cs_max = 16) {
+  cudaError_t e = raise_smem_limit(kernel, smem);
+  if (e != cudaSuccess) return e;
+  return cluster_launch(kernel, std::min(cs_max, cluster_size(kernel, smem)), smem, args, st);
+}
+
+size_t prep_cluster_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 4 * size_t(r) * r); }
+size_t cholqr_cluster_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 5 * size_t(r) * r); }
+
 }  // namespace
 
 int coop_partials_cap(int num_sms) { return num_sms * (2048 / kThreads); }
@@ -860,6 +1262,13 @@ int finish_step_grid(uint64_t F, int num_sms) {
   return CALL(16);
 
 cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st) {
+  // the cluster prep loses to the grid one: summing the split-K partials on
+  // 16 SMs is latency-bound (tools/small_bench.cu; TKG_CLUSTER_PREP=1 selects it)
+  if (!use_grid_steps() && use_cluster_prep()) {
+#define TKG_PC(KE) cluster_step(prep_cluster_kernel<KE>, prep_cluster_smem(a.r), a, st)
+    TKG_KE_SWITCH(a.r, TKG_PC)
+#undef TKG_PC
+  }
 #define TKG_P(KE) coop_launch(prep_step_kernel<KE>, num_sms, num_sms, rows_smem(a.r), &a, st)
   TKG_KE_SWITCH(a.r, TKG_P)
 #undef TKG_P
@@ -872,6 +1281,26 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
                                    : finish_step_grid(a.F, num_sms);
   const uint32_t ncp = a.r <= 8 ? 8 : (a.r + 7) / 8 * 8;
   const size_t smem = sizeof(double) * std::max<size_t>(size_t(kFinStages) * kFinRows * (ncp + 4), 2 * size_t(a.r) * a.r);
+  if (!use_grid_steps() && a.mode != 1) {
+    // the R^T R row pass (r > 32) stays a full-grid launch writing per-CTA
+    // partials; the reduction and the CTA-0 tail run as one cluster
+    FinishArgs c = a;
+    if (a.mode == 0 && a.gram_nparts == 0) {
+      c.mode = 1;
+      const cudaError_t e = launch_finish_step(c, num_sms, st);
+      if (e != cudaSuccess) return e;
+      c.mode = 0;
+      c.gram_nparts = want;
+    }
+    const size_t csm = sizeof(double) * 2 * size_t(a.r) * a.r;
+    switch (ncp) {
+#define TKG_FC(N) \
+  case N: return cluster_step(finish_cluster_kernel<N>, csm, c, st, c.mode == 2 ? 1 : 16);
+      TKG_FC(8) TKG_FC(16) TKG_FC(24) TKG_FC(32) TKG_FC(40) TKG_FC(48) TKG_FC(56) TKG_FC(64)
+#undef TKG_FC
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (ncp) {
 #define TKG_F(N) \
   case N: return coop_launch(finish_step_kernel<N>, want, num_sms, smem, &a, st, a.mode == 1);
@@ -882,6 +1311,13 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
 }
 
 cudaError_t launch_cholqr_step(CholQrArgs a, int num_sms, cudaStream_t st) {
+  // cluster CholQR2 while a CTA's rows fit one 32-row block (I <= 512);
+  // taller factors stream more rows per SM than 16 SMs sustain
+  if (!use_grid_steps() && a.I <= 512) {
+#define TKG_QC(KE) cluster_step(cholqr_cluster_kernel<KE>, cholqr_cluster_smem(a.r), a, st)
+    TKG_KE_SWITCH(a.r, TKG_QC)
+#undef TKG_QC
+  }
 #define TKG_Q(KE) coop_launch(cholqr_step_kernel<KE>, num_sms, num_sms, rows_smem(a.r), &a, st)
   TKG_KE_SWITCH(a.r, TKG_Q)
 #undef TKG_Q

@@ -67,6 +67,29 @@ def test_unfold_products(ctx, ref, port, dims, r):
         assert rel(port.unfold_t_times(t, mode, l), ctx.unfold_t_times(t, mode, l)) <= 1e-13
 
 
+# mode 1 with 128 < I_1 <= 248 and 40..64 columns: fr_wide_kernel (one CTA over
+# all contraction rows, row tiles split by (row tile, column tile) pairs)
+@pytest.mark.parametrize("dims", [[200, 64, 9], [129, 31, 20], [208, 17, 10], [248, 17, 10], [136, 5, 3]],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("r", [33, 40, 50, 56, 64])
+def test_unfold_times_wide_rows(ctx, ref, port, dims, r):
+    t = random_tensor(ref, dims, 307 + dims[0])
+    fibers = t.size // dims[0]
+    m = random_matrix(ref, fibers, r, 311 + r)
+    assert rel(port.unfold_times(t, 1, m), ctx.unfold_times(t, 1, m)) <= 1e-13
+
+
+# the init pass (column-major S, fused ||A||^2) and the sweeps through the wide FR
+@pytest.mark.parametrize("dims,r", [([200, 40, 30], 50), ([208, 30, 25], 64), ([144, 40, 20], 40), ([248, 20, 20], 40)])
+def test_als_low_rank_wide_rows(ctx, ref, port, dims, r):
+    t = random_tensor(ref, dims, 577 + r)
+    (lg, rg), rep = ctx.als_low_rank(t, 1, r, tk.AlsConfig(eta=1e-6, seed=13, max_iters=8))
+    lp, rp, prep = port.als_low_rank(t, 1, r, eta=1e-6, seed=13, max_iters=8)
+    assert rep.iterations == prep.iterations
+    assert np.allclose(rep.residual_history, prep.residual_history, rtol=1e-11, atol=0)
+    assert rel(lp, lg) <= 1e-9 and rel(rp, rg) <= 1e-9
+
+
 @pytest.mark.parametrize("dims", SHAPES[:9], ids=lambda d: "x".join(map(str, d)))
 def test_mode_n_product(ctx, port, ref, dims):
     t = random_tensor(ref, dims, 53 + len(dims))

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <vector>
 #include <random>
+#include <cstdlib>
 
 #include "als_step.cuh"
 #include "coop.cuh"
@@ -86,10 +87,10 @@ int main() {
         unsigned long long ph[64];
         phase_read(ph);
         printf("   phases(us):");
-        if (kind == 0)
-          for (int k = 1; k < 12; ++k) printf(" %d:%.1f", k, (ph[k] - ph[k - 1]) * 1e-3);
-        else
-          for (int k = 21; k < 27; ++k) printf(" %d:%.1f", k, (ph[k] - ph[k - 1]) * 1e-3);
+        const bool grid_steps = getenv("TKG_COOP_STEPS") && getenv("TKG_COOP_STEPS")[0] == '1';
+        const int k0 = grid_steps ? (kind == 0 ? 1 : 21) : (kind == 0 ? 41 : 31);
+        const int k1 = grid_steps ? (kind == 0 ? 12 : 27) : (kind == 0 ? 49 : 35);
+        for (int k = k0; k < k1; ++k) printf(" %d:%.1f", k, (ph[k] - ph[k - 1]) * 1e-3);
         printf("\n");
       }
     }
