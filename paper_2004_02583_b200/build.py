@@ -27,8 +27,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 GXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else (shutil.which("g++") or "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["contract.cu", "contract_tma.cu", "smallla.cu", "mtrng.cu", "recon.cu", "als_step.cu", "coop.cu",
-           "gram.cu", "wide.cu"]
-CPP_SRCS = ["engine.cpp", "engine_wide.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp", "eig.cpp", "io.cpp"]  # cli.cpp: the executable
+           "gram.cu", "wide.cu", "eig.cu"]
+CPP_SRCS = ["engine.cpp", "engine_wide.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp", "io.cpp"]  # cli.cpp: the executable
 
 
 def _newest(paths):

@@ -875,12 +875,14 @@ void Engine::recover_singular_vectors(const double* a, const Shape& sh, int mode
 // kernels.cpp:448-604); the SVD engine's is the leading R_n left singular
 // vectors of A_(n) (dense_svd, kernels.cpp:419-446), i.e. the same eigenvectors
 // of A_(n) A_(n)^T, with the same descending order and sign convention. Here:
-// the Gram matrix on DMMA straight from the tensor layout (gram.cu), cuSOLVER's
-// syevd (eig.cpp), and the ordering / sign pass (leading_vectors_kernel).
-void Engine::gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U) {
+// the Gram matrix on DMMA straight from the tensor layout (gram.cu) and the
+// device eigensolver (eig.cu: tridiagonalization, multisection, inverse
+// iteration, blocked back-transform, the sign convention).
+void Engine::gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U, bool refine) {
   const uint64_t I = sh.extent(mode), s = sh.stride(mode), F = sh.count() / I, P = F / s;
-  if (I > 32768) raise(12, "mode " + std::to_string(mode) + ": extent " + std::to_string(I) +
-                               " above the 32768 supported by the SVD / EIG engines");
+  if (I > uint64_t(kSymEigMaxN))
+    raise(12, "mode " + std::to_string(mode) + ": extent " + std::to_string(I) + " above the " +
+                  std::to_string(kSymEigMaxN) + " supported by the SVD / EIG engines");
   FiberView v{A, s, P, uint32_t(I), s, s * I};
   const GramPlan gp = gram_tensor_plan(v, sms_);
   double* part = gram_t_part_.d(std::max<size_t>(gp.part_doubles, 1));
@@ -888,10 +890,39 @@ void Engine::gram_factor(const double* A, const Shape& sh, int mode, uint32_t r,
   double* W = gram_w_.d(I);
   CK(launch_gram_tensor(v, gp, part, G, st_));
   count_launch(2);
-  const std::string why = eig_.eig(G, int(I), W, st_);
-  if (!why.empty()) raise(why.rfind("sym_eig", 0) == 0 ? 7 : 11, why);
-  CK(launch_leading_vectors(G, W, uint32_t(I), r, U, nullptr, st_));
-  count_launch();
+  const std::string why = eig_.leading(G, int(I), int(r), U, W, st_);
+  if (!why.empty()) raise(11, why);
+  count_launch(5);
+  // SVD engine / HOOI (dense_svd of the unfolding, hosvd.cpp:89-92, hooi.cpp:90):
+  // eigenvectors of the Gram matrix carry errors ~eps s1^2 / (si^2 - sj^2)
+  // (and ~eps s1^2 / s_r^2 outside the leading subspace), the singular vectors
+  // of A_(n) ~eps s1 / (si - sj). Refinement: one power step Y = A_(n) A_(n)^T U
+  // (an FC and an FR pass; column i carries errors ~eps s1 si, i.e. relative
+  // eps s1 / si), its columns scaled to unit norm and orthonormalised
+  // (CholQR2 of a near-orthonormal matrix), then one recover_sv round (the
+  // columns of A_(n)^T Q come straight from A, their Gram is diagonal to
+  // eps si sj, its Jacobi rotation fixes the basis inside the subspace). The
+  // EIG engine keeps sym_eig(mode_gram) as the reference computes it.
+  if (refine && r <= kMaxRank && F >= r) {
+    const uint32_t ncp = pad_nc(r);
+    FiberView v{A, s, P, uint32_t(I), s, s * I};
+    double* Mt = mt_.d(I * ncp);
+    CK(launch_pack(U, 1, I, uint32_t(I), r, Mt, ncp, st_));  // Mt[i][c] = U[i + c*I]
+    double* R = r_.d(F * ncp + 8);
+    {
+      ClsScope cls(fc_cls_, kClsTTM);
+      fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, nullptr, true);
+    }
+    double* part = fr_part_.d(size_t(fr_ranges(v, r)) * I * ncp);
+    uint32_t ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr);
+    if (dist_) ranges = reduce_left_partials(part, ranges, uint32_t(I), ncp, r);
+    double* Y = l_.d(I * r);
+    CK(launch_reduce_partials(part, int(ranges), uint32_t(I), ncp, r, Y, st_));
+    CK(launch_normalize_columns(Y, uint32_t(I), r, st_));
+    count_launch(3);
+    qr_dev(Y, 0, I, uint32_t(I), r, U, nullptr, nullptr, 0, false);
+    recover_sv_round(A, sh, mode, r, U, sv_vt0_.d(size_t(r) * r));
+  }
 }
 
 double* Engine::sumsq_to_host(const double* A, uint64_t n) {
@@ -927,10 +958,13 @@ void Engine::sym_eig(const double* g, uint64_t n, uint64_t k, double* values, do
   double* W = gram_w_.d(std::max<uint64_t>(n, 1));
   double* U = sv_u_.d(std::max<uint64_t>(n * k, 1));
   double* V = sv_g_.d(std::max<uint64_t>(k, 1));
+  if (n > uint64_t(kSymEigMaxN))
+    raise(12, "sym_eig: dimension " + std::to_string(n) + " above the " + std::to_string(kSymEigMaxN) +
+                  " supported on the device");
+  (void)W;
   CK(cudaMemcpyAsync(G, g, n * n * sizeof(double), cudaMemcpyHostToDevice, st_));
-  const std::string why = eig_.eig(G, int(n), W, st_);
-  if (!why.empty()) raise(why.rfind("sym_eig", 0) == 0 ? 7 : 11, why);
-  CK(launch_leading_vectors(G, W, uint32_t(n), uint32_t(k), U, V, st_));
+  const std::string why = eig_.leading(G, int(n), int(k), U, V, st_);
+  if (!why.empty()) raise(11, why);
   CK(cudaMemcpyAsync(values, V, k * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CK(cudaMemcpyAsync(vectors, U, n * k * sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
@@ -1018,7 +1052,7 @@ void Engine::hooi(const double* a, bool a_dev, const Shape& sh, const std::vecto
   for (int iter = 1; iter <= iters; ++iter) {
     for (int n = 1; n <= N; ++n) {
       const Shape S = ttm_others(A, sh, ranks, U, n, shr);
-      gram_factor(shr, S, n, uint32_t(ranks[n - 1]), U[n - 1]);
+      gram_factor(shr, S, n, uint32_t(ranks[n - 1]), U[n - 1], true);
       if (n == N) ttm_mode(shr, S, N, U[N - 1], uint32_t(ranks[N - 1]), core_buf);
     }
     rep->iterations = iter;
@@ -1235,7 +1269,7 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
       const uint32_t r = uint32_t(ranks[n - 1]);
       mode_begin(n - 1);
       U[n - 1] = factor_bufs_[n - 1]->d(sh.d[n - 1] * r);
-      gram_factor(A, sh, n, r, U[n - 1]);
+      gram_factor(A, sh, n, r, U[n - 1], engine == kEngineSvd);
       mode_end(n - 1);
     }
     Shape cs;
@@ -1359,7 +1393,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
       const uint64_t I = cur.extent(mode), s = cur.stride(mode), F = cur.count() / I, P = F / s;
       mode_begin(int(k));
       U[mode - 1] = factor_bufs_[mode - 1]->d(I * r);
-      gram_factor(work, cur, mode, r, U[mode - 1]);
+      gram_factor(work, cur, mode, r, U[mode - 1], engine == kEngineSvd);
       const uint32_t ncp = pad_nc(r);
       double* Mt = mt_.d(I * ncp);
       CK(launch_pack(U[mode - 1], 1, I, uint32_t(I), r, Mt, ncp, st_));

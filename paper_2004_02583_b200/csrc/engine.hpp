@@ -249,7 +249,7 @@ class Engine {
   void mode_product_dev(const double* X, const Shape& sh, int mode, const double* U, uint64_t rows, double* dst);
   void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   // SVD / EIG engines: U (device, I x r) <- leading eigenvectors of A_(n) A_(n)^T
-  void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U);
+  void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U, bool refine);
   // dst <- A x_m U_m^T for every m != skip, ascending (multi_mode_product with
   // the other factors, hooi.cpp:82-88); returns dst's shape
   Shape ttm_others(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,

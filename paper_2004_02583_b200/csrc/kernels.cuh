@@ -133,6 +133,9 @@ cudaError_t launch_expand(const ExpandArgs& a, int num_sms, cudaStream_t st, int
 // Y = sum of FR partials, written column-major (rows x r).
 cudaError_t launch_reduce_partials(const double* part, int nparts, uint32_t rows, uint32_t ldp,
                                    uint32_t r, double* y, cudaStream_t st);
+// X (rows x cols, column-major) <- X with every column scaled to unit norm
+// (zero columns are left as they are); one CTA per column, fixed-order sums.
+cudaError_t launch_normalize_columns(double* X, uint32_t rows, uint32_t cols, cudaStream_t st);
 
 // recover_singular_vectors (hosvd.cpp:65-72): eigenvectors of the symmetric
 // r x r matrix G (column-major, r <= 64) by parallel cyclic Jacobi, ordered by
@@ -152,14 +155,6 @@ struct GramPlan {
 };
 GramPlan gram_tensor_plan(const FiberView& v, int num_sms);
 cudaError_t launch_gram_tensor(const FiberView& v, const GramPlan& p, double* part, double* G, cudaStream_t st);
-
-// sym_eig's output convention (kernels.cpp:584-603) from an ascending
-// eigendecomposition (Z n x n column-major, W ascending): U (n x k) holds the
-// eigenvectors of the k largest eigenvalues in descending order, each column
-// signed so its largest-magnitude entry (first on ties) is positive
-// (fix_column_signs, kernels.cpp:25-43); vals (nullable) the eigenvalues.
-cudaError_t launch_leading_vectors(const double* Z, const double* W, uint32_t n, uint32_t k, double* U,
-                                   double* vals, cudaStream_t st);
 
 // ---- sharded decomposition (smallla.cu) -------------------------------------
 cudaError_t launch_add(double* dst, const double* src, size_t n, cudaStream_t st);

@@ -525,41 +525,6 @@ __global__ void __launch_bounds__(kEigThreads) sym_eig_kernel(const double* __re
   }
 }
 
-// Leading eigenvectors in sym_eig's order and sign convention (see kernels.cuh).
-__global__ void __launch_bounds__(256) leading_vectors_kernel(const double* __restrict__ Z,
-                                                              const double* __restrict__ W, uint32_t n,
-                                                              double* __restrict__ U, double* vals) {
-  __shared__ double bmag[256];
-  __shared__ uint32_t bidx[256];
-  const uint32_t c = blockIdx.x, col = n - 1 - c;
-  const double* z = Z + size_t(col) * n;
-  double best = -1.0;
-  uint32_t arg = 0;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const double m = fabs(z[i]);
-    if (m > best) {  // ascending i per thread: keeps the first index on ties
-      best = m;
-      arg = i;
-    }
-  }
-  bmag[threadIdx.x] = best;
-  bidx[threadIdx.x] = arg;
-  __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (int(threadIdx.x) < off) {
-      const double m2 = bmag[threadIdx.x + off];
-      const uint32_t i2 = bidx[threadIdx.x + off];
-      if (m2 > bmag[threadIdx.x] || (m2 == bmag[threadIdx.x] && i2 < bidx[threadIdx.x])) {
-        bmag[threadIdx.x] = m2;
-        bidx[threadIdx.x] = i2;
-      }
-    }
-    __syncthreads();
-  }
-  const double sg = z[bidx[0]] >= 0.0 ? 1.0 : -1.0;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) U[i + size_t(c) * n] = sg * z[i];
-  if (vals && threadIdx.x == 0) vals[c] = W[col];
-}
 
 // ---- sharded-decomposition helpers -------------------------------------------------
 __global__ void add_kernel(double* __restrict__ dst, const double* __restrict__ src, size_t n) {
@@ -751,13 +716,40 @@ cudaError_t launch_sym_eig(const double* G, uint32_t r, double* vt, double* eval
 }
 
 
-cudaError_t launch_leading_vectors(const double* Z, const double* W, uint32_t n, uint32_t k, double* U,
-                                   double* vals, cudaStream_t st) {
-  if (k == 0) return cudaSuccess;
-  if (k > n) return cudaErrorInvalidValue;
-  leading_vectors_kernel<<<k, 256, 0, st>>>(Z, W, n, U, vals);
+
+
+namespace {
+__global__ void __launch_bounds__(256) normalize_columns_kernel(double* X, uint32_t rows) {
+  __shared__ double red[8];
+  double* x = X + size_t(blockIdx.x) * rows;
+  double mx = 0.0;
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) mx = fmax(mx, fabs(x[i]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < 8; ++w) mx = fmax(mx, red[w]);
+  __syncthreads();
+  if (mx == 0.0) return;
+  const double inv = 1.0 / mx;  // scaled first: no overflow in the sum of squares
+  double s = 0.0;
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) s += (x[i] * inv) * (x[i] * inv);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  s = 0.0;
+  for (int w = 0; w < 8; ++w) s += red[w];
+  const double f = inv / sqrt(s);
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) x[i] *= f;
+}
+}  // namespace
+
+cudaError_t launch_normalize_columns(double* X, uint32_t rows, uint32_t cols, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  normalize_columns_kernel<<<cols, 256, 0, st>>>(X, rows);
   return cudaGetLastError();
 }
-
 
 }  // namespace tkg

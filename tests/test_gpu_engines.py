@@ -86,6 +86,24 @@ def test_exact_engines_match_reference(ctx, ref, kind, sequential, order, dims, 
     assert np.max(np.abs(tkr.core - r.core)) <= CORE_SV_REL_TOL * np.max(np.abs(r.core))
 
 
+@pytest.mark.parametrize("sequential", [False, True])
+def test_svd_engine_steep_spectrum(ctx, ref, sequential):
+    # core spectra sigma_k ~ k^-2.5 (sigma_16 / sigma_1 = 1e-3), no noise: the
+    # Gram route alone squares the condition number (errors ~eps s1^2 / (si^2 -
+    # sj^2)); the SVD engine's refinement round keeps dense_svd's accuracy
+    # (hosvd.cpp:89-92)
+    dims, ranks = [96, 80, 72], [16, 12, 10]
+    a = tk.synth_tucker(dims, ranks, 2.5, 0.0, 2025).reshape(dims, order="F")
+    if sequential:
+        tkr, rep = ctx.st_hosvd(a, tk.Truncation(ranks), None, tk.FactorEngine.svd())
+    else:
+        tkr, rep = ctx.t_hosvd(a, tk.Truncation(ranks), tk.FactorEngine.svd())
+    r = ref.hosvd_exact(a, ranks, "svd", sequential=sequential)
+    for u, v in zip(tkr.factors, r.factors):
+        assert column_diff(u, v) <= 1e-10
+    assert np.max(np.abs(tkr.core - r.core)) <= CORE_SV_REL_TOL * np.max(np.abs(r.core))
+
+
 def test_engines_agree_and_als_lands_nearby(ctx):
     # test_hosvd.cpp "exact engines agree; ALS lands nearby"
     dims, ranks = [60, 50, 40], [6, 5, 4]
@@ -98,3 +116,65 @@ def test_engines_agree_and_als_lands_nearby(ctx):
         assert principal_sine(w, u) <= 1e-6
     assert abs(rs.relative_residual - re_.relative_residual) <= 1e-14
     assert abs(ra.relative_residual - rs.relative_residual) <= 1e-8
+
+
+_NO_CUSOLVER = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2004_02583_b200 as tk
+ctx = tk.Context(0)
+rng = np.random.default_rng(5)
+g = rng.standard_normal((300, 300)); g = np.asfortranarray(g @ g.T)
+vals, vecs = ctx.sym_eig(g, 12)
+t = np.asfortranarray(rng.standard_normal((30, 20, 10)))
+for eng in (tk.FactorEngine.svd(), tk.FactorEngine.eig()):
+    ctx.t_hosvd(t, tk.Truncation([4, 3, 2]), eng)
+maps = open("/proc/self/maps").read()
+assert "libcusolver" not in maps, "cuSOLVER mapped"
+w = np.linalg.eigvalsh(g)[::-1][:12]
+assert np.max(np.abs(vals - w)) <= 1e-11 * w[0], (vals, w)
+print("ok")
+"""
+
+
+def test_engines_map_no_cusolver(tmp_path):
+    # the eigensolver is the repo's own (eig.cu): the process that runs the
+    # EIG / SVD engines and sym_eig never maps a cuSOLVER library
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _NO_CUSOLVER, root], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,k,kind", [(64, 64, "cluster"), (200, 50, "decay"), (513, 40, "cluster"),
+                                      (2048, 64, "decay"), (1, 1, "decay"), (2, 2, "decay"), (3, 1, "decay")])
+def test_sym_eig_spectra(ctx, ref, n, k, kind):
+    # clustered (pairs 1e-9 apart) and power-law spectra: values against the
+    # reference, vectors through the invariant subspace of the k leading pairs
+    q = np.linalg.qr(random_matrix(ref, n, n, 900 + n))[0]
+    if kind == "cluster":
+        d = np.repeat(np.linspace(10.0, 1.0, (n + 1) // 2), 2)[:n] + 1e-9 * (np.arange(n) % 2)
+    else:
+        d = (1.0 + np.arange(n)) ** -1.5
+    g = np.asfortranarray((q * d) @ q.T)
+    g = 0.5 * (g + g.T)
+    vals, vecs = ctx.sym_eig(g, k)
+    if n <= 600:
+        rv, ru = ref.sym_eig(g, k)
+    else:  # LAPACK dsyevd (numpy) in the reference's order / sign convention
+        w, z = np.linalg.eigh(g)
+        rv, ru = w[::-1][:k], z[:, ::-1][:, :k].copy()
+        for c in range(k):
+            if ru[np.argmax(np.abs(ru[:, c])), c] < 0:
+                ru[:, c] = -ru[:, c]
+    assert np.max(np.abs(vals - rv)) <= 1e-13 * max(n, 16) * np.max(np.abs(rv))
+    assert ortho_defect(vecs) <= 1e-13 * max(n, 16)
+    resid = g @ vecs - vecs * vals
+    assert np.max(np.abs(resid)) <= 1e-13 * max(n, 16) * np.max(np.abs(rv))
+    # subspace of the leading k (cut where the spectrum has a gap)
+    if k < n and d[k - 1] - d[k] > 1e-6:
+        assert principal_sine(vecs, ru) <= 1e-9
+    if kind == "decay":
+        assert column_diff(vecs, ru) <= 1e-8
