@@ -193,6 +193,12 @@ int tkg_nccl_unique_id(void* out128, tkg_error* err);
 /* Attach an NCCL communicator (rank of world) to ctx; collectives run on
  * the context's stream. */
 int tkg_comm_init_nccl(tkg_ctx* ctx, int rank, int world, const void* unique_id128, tkg_error* err);
+/* Host-staged multi-process group: every rank (a separate process with its
+ * own context, on one GPU or several) passes the same POSIX shm `name`
+ * ("/..."); collectives stage through slot_bytes per rank (0: 64 MiB) in
+ * shared memory behind a process-shared barrier. Replaces NCCL where the
+ * ranks have no NVLink peers (one-GPU pools, tests). */
+int tkg_comm_init_shm(tkg_ctx* ctx, const char* name, int rank, int world, uint64_t slot_bytes, tkg_error* err);
 /* In-process group: `world` contexts driven by `world` host threads of one
  * process (host-synchronous collectives; tests on a single device). */
 int tkg_local_group_create(int world, tkg_local_group** out, tkg_error* err);

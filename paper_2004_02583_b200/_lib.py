@@ -98,6 +98,7 @@ SIGNATURES = [
     ("tkg_local_group_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(TkgError)]),
     ("tkg_local_group_destroy", None, [C.c_void_p]),
     ("tkg_comm_init_local", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.POINTER(TkgError)]),
+    ("tkg_comm_init_shm", C.c_int, [_ctxp, C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.POINTER(TkgError)]),
     ("tkg_shard_range", C.c_int, [C.c_uint64, C.c_int, C.c_int, _u64p, _u64p]),
     ("tkg_t_hosvd_sharded", C.c_int, [_ctxp, C.c_void_p, C.c_int, C.c_int32, _u64p, C.c_uint64, C.c_uint64,
                                       _u64p, C.POINTER(TkgAlsConfig), C.c_int32, _dp, _dp,

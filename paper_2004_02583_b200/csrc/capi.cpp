@@ -323,6 +323,14 @@ int tkg_comm_init_nccl(tkg_ctx* ctx, int rank, int world, const void* unique_id1
   });
 }
 
+int tkg_comm_init_shm(tkg_ctx* ctx, const char* name, int rank, int world, uint64_t slot_bytes, tkg_error* err) {
+  return guarded(err, [&] {
+    if (world < 1 || rank < 0 || rank >= world || !name || name[0] != '/')
+      tkg::raise(TKG_E_DIMENSION_MISMATCH, "comm: bad rank / world / shm name");
+    eng(ctx).set_comm(tkg::make_shm_comm(name, rank, world, slot_bytes ? size_t(slot_bytes) : size_t(64) << 20));
+  });
+}
+
 int tkg_local_group_create(int world, tkg_local_group** out, tkg_error* err) {
   return guarded(err, [&] {
     if (world < 1) tkg::raise(TKG_E_DIMENSION_MISMATCH, "local group: world must be >= 1");

@@ -2,9 +2,15 @@
 #include "comm.hpp"
 
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>  // types only: the library is loaded with dlopen
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -208,6 +214,156 @@ int local_group_world(const LocalGroup& g) { return g.world; }
 
 std::unique_ptr<Comm> make_local_comm(const std::shared_ptr<LocalGroup>& g, int rank) {
   return std::unique_ptr<Comm>(new LocalComm(g, rank));
+}
+
+// ---- host-staged multi-process group (one process per rank, any devices) -------------
+// Ranks are separate processes (their own CUDA contexts; on one GPU or on
+// several) sharing a POSIX shared-memory segment: a process-shared barrier
+// (atomics in the segment) and one staging slot per rank. Every collective
+// synchronises the rank's stream, stages its device data through the slot
+// in chunks and reads its peers' slots after the barrier: no kernel of one
+// rank ever waits on another rank's kernels. allreduce sums the slots in
+// rank order on every rank (identical bits everywhere, like NCCL's ring with
+// one fixed order). Used to run the real per-process sharded path where NCCL
+// has no second GPU (tests, one-GPU pools).
+namespace {
+
+struct ShmHeader {
+  std::atomic<uint32_t> arrived;
+  std::atomic<uint32_t> gen;
+  std::atomic<uint32_t> failed;
+  std::atomic<uint32_t> attached;
+  uint32_t world;
+  uint32_t pad;
+  uint64_t slot_bytes;
+  std::atomic<uint64_t> need[64];  // per-rank chunk counts (alltoallv agreement)
+};
+
+class ShmComm final : public Comm {
+ public:
+  ShmComm(const std::string& name, int rank, int world, size_t slot_bytes) : name_(name) {
+    rank_ = rank;
+    world_ = world;
+    if (world > 64) raise(2, "ShmComm: world above 64");
+    slot_ = (slot_bytes / 64) * 64;
+    bytes_ = 4096 + size_t(world) * slot_;
+    const int fd = shm_open(name.c_str(), O_CREAT | O_RDWR, 0600);
+    if (fd < 0) raise(11, "ShmComm: shm_open(" + name + ") failed");
+    if (ftruncate(fd, off_t(bytes_)) != 0) {
+      close(fd);
+      raise(11, "ShmComm: ftruncate failed");
+    }
+    void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) raise(11, "ShmComm: mmap failed");
+    base_ = static_cast<char*>(p);
+    hdr_ = reinterpret_cast<ShmHeader*>(base_);  // zero-filled by ftruncate on creation
+    hdr_->attached.fetch_add(1);
+    check_cuda(cudaHostRegister(base_, bytes_, cudaHostRegisterDefault), "ShmComm cudaHostRegister");
+    registered_ = true;
+    barrier();  // every rank attached (the first barrier also validates the group)
+    if (rank_ == 0) shm_unlink(name_.c_str());  // the mapping stays; the name is not needed
+  }
+  ~ShmComm() override {
+    if (registered_) cudaHostUnregister(base_);
+    if (base_) munmap(base_, bytes_);
+  }
+  void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
+    const size_t chunk = slot_ / sizeof(double);
+    check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+    if (acc_.size() < std::min(n, chunk)) acc_.resize(std::min(n, chunk));
+    for (size_t o = 0; o < n; o += chunk) {
+      const size_t m = std::min(chunk, n - o);
+      check_cuda(cudaMemcpyAsync(slot(rank_), buf + o, m * sizeof(double), cudaMemcpyDeviceToHost, st),
+                 "ShmComm D2H");
+      check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+      barrier();
+      const double* s0 = slot(0);
+      for (size_t i = 0; i < m; ++i) acc_[i] = s0[i];
+      for (int q = 1; q < world_; ++q) {
+        const double* sq = slot(q);
+        for (size_t i = 0; i < m; ++i) acc_[i] += sq[i];
+      }
+      check_cuda(cudaMemcpyAsync(buf + o, acc_.data(), m * sizeof(double), cudaMemcpyHostToDevice, st),
+                 "ShmComm H2D");
+      check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+      barrier();  // the slots may be overwritten from here on
+    }
+  }
+  void alltoallv(const double* sendbuf, const size_t* scount, const size_t* soff, double* recvbuf,
+                 const size_t* rcount, const size_t* roff, cudaStream_t st) override {
+    check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+    if (rcount[rank_])
+      check_cuda(cudaMemcpyAsync(recvbuf + roff[rank_], sendbuf + soff[rank_], rcount[rank_] * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, st),
+                 "ShmComm copy");
+    const size_t chunk = slot_ / sizeof(double);
+    for (int step = 1; step < world_; ++step) {
+      const int dst = (rank_ + step) % world_, src = (rank_ - step + world_) % world_;
+      // the ranks agree on the number of chunks of this step (the largest need)
+      const uint64_t mine = std::max((scount[dst] + chunk - 1) / chunk, (rcount[src] + chunk - 1) / chunk);
+      hdr_->need[rank_].store(mine);
+      barrier();
+      uint64_t rounds = 0;
+      for (int q = 0; q < world_; ++q) rounds = std::max<uint64_t>(rounds, hdr_->need[q].load());
+      barrier();
+      for (uint64_t c = 0; c < rounds; ++c) {
+        const size_t so = size_t(c) * chunk;
+        if (so < scount[dst]) {
+          const size_t m = std::min(chunk, scount[dst] - so);
+          check_cuda(cudaMemcpyAsync(slot(rank_), sendbuf + soff[dst] + so, m * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st),
+                     "ShmComm D2H");
+          check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+        }
+        barrier();
+        if (so < rcount[src]) {
+          const size_t m = std::min(chunk, rcount[src] - so);
+          check_cuda(cudaMemcpyAsync(recvbuf + roff[src] + so, slot(src), m * sizeof(double),
+                                     cudaMemcpyHostToDevice, st),
+                     "ShmComm H2D");
+          check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+        }
+        barrier();
+      }
+    }
+    check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
+  }
+
+ private:
+  double* slot(int q) const { return reinterpret_cast<double*>(base_ + 4096 + size_t(q) * slot_); }
+  // sense-counting barrier over the shared header; a rank that stops
+  // arriving (crash, divergence) makes the others fail after 120 s
+  void barrier() {
+    if (hdr_->failed.load()) raise(11, "ShmComm: a peer rank failed");
+    const uint32_t g = hdr_->gen.load();
+    if (hdr_->arrived.fetch_add(1) + 1 == uint32_t(world_)) {
+      hdr_->arrived.store(0);
+      hdr_->gen.fetch_add(1);
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t spin = 0; hdr_->gen.load() == g; ++spin) {
+      if (hdr_->failed.load()) raise(11, "ShmComm: a peer rank failed");
+      if (spin > 1000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+        hdr_->failed.store(1);
+        raise(11, "ShmComm: barrier timed out (a peer rank failed or diverged)");
+      }
+    }
+  }
+  std::string name_;
+  char* base_ = nullptr;
+  ShmHeader* hdr_ = nullptr;
+  size_t slot_ = 0, bytes_ = 0;
+  bool registered_ = false;
+  std::vector<double> acc_;
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_shm_comm(const char* name, int rank, int world, size_t slot_bytes) {
+  return std::unique_ptr<Comm>(new ShmComm(name, rank, world, slot_bytes));
 }
 
 }  // namespace tkg

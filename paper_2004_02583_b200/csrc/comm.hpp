@@ -13,6 +13,10 @@
 //                sweep batches without host synchronisation.
 //  * LocalComm : ranks that are host threads of one process (tests on one
 //                GPU): host barriers + device copies; synchronous.
+//  * ShmComm   : ranks that are separate processes (one CUDA context each, on
+//                one GPU or several) staging their data through a POSIX
+//                shared-memory segment with a process-shared barrier; host-
+//                synchronous, no kernel waits on another rank's kernels.
 #pragma once
 
 #include <cstddef>
@@ -50,5 +54,9 @@ struct LocalGroup;
 std::shared_ptr<LocalGroup> make_local_group(int world);
 int local_group_world(const LocalGroup& g);
 std::unique_ptr<Comm> make_local_comm(const std::shared_ptr<LocalGroup>& g, int rank);
+
+// name: a POSIX shm name ("/tkg_..."), the same on every rank of the group;
+// slot_bytes: staging bytes per rank (collectives run in chunks of it).
+std::unique_ptr<Comm> make_shm_comm(const char* name, int rank, int world, size_t slot_bytes);
 
 }  // namespace tkg

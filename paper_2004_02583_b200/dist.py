@@ -116,6 +116,19 @@ class ShardedContext:
         return cls(ctx, rank, world)
 
     @classmethod
+    def shm(cls, device: int, name: str, rank: int, world: int, slot_bytes: int = 0) -> "ShardedContext":
+        """One process per rank, collectives staged through the POSIX shared
+        memory segment `name` ("/..."; the same on every rank) behind a
+        process-shared barrier (csrc/comm.cpp ShmComm): the real per-process
+        sharded path where the ranks have no NVLink peers (one-GPU pools,
+        tests). Every rank must call this (the constructor is a barrier)."""
+        ctx = Context(device)
+        err = _lib.TkgError()
+        _raise(ctx._l.tkg_comm_init_shm(ctx._ctx, name.encode(), int(rank), int(world), int(slot_bytes),
+                                        C.byref(err)), err)
+        return cls(ctx, rank, world)
+
+    @classmethod
     def local(cls, device: int, group: LocalGroup, rank: int) -> "ShardedContext":
         ctx = Context(device)
         err = _lib.TkgError()
