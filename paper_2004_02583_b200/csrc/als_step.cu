@@ -27,6 +27,7 @@ __global__ void ctrl_init_kernel(AlsCtrl* ctrl, const double* sumsq, double eta,
   ctrl->max_iters = max_iters < 1 ? 1 : max_iters;
   ctrl->history_cap = history_cap;
   ctrl->iter = 0;
+  ctrl->trips = 0;
   ctrl->status = 1;
   ctrl->error = 0;
   ctrl->stop = 0;

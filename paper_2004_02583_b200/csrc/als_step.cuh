@@ -28,6 +28,8 @@ struct AlsCtrl {
   int32_t history_cap;
   int32_t degenerate_col;  // CholQR: als_init collapse column (1-based), 0 if none
   int32_t pad;             // failing Gram column (1-based) of a singular solve
+  int32_t trips;           // sweeps begun inside a device-side loop (graph mode guard)
+  int32_t pad2;
   double norm, norm_sq, prev, eta, residual, achieved, pivot;
 };
 

@@ -545,8 +545,11 @@ __device__ void finish_tail(const FinishArgs& a, double* G, double* Gi) {
       cont = 0;
     }
     ctrl->prev = residual;
+    // graph mode: a device-side trip guard on top of the max_iters rule
+    if (a.cond && ++ctrl->trips > ctrl->max_iters + 1) cont = 0;
     cont_s = cont;
     if (!cont) ctrl->stop = 1;
+    if (a.cond) cudaGraphSetConditional(a.cond, cont ? 1u : 0u);
   }
   __syncthreads();
   if (!cont_s) return;
@@ -558,6 +561,7 @@ __device__ void finish_tail(const FinishArgs& a, double* G, double* Gi) {
       ctrl->pivot = piv;
       ctrl->pad = fail;  // failing column (1-based)
       ctrl->stop = 1;
+      if (a.cond) cudaGraphSetConditional(a.cond, 0u);
     }
     return;
   }
@@ -568,7 +572,10 @@ template <int NC>
 __global__ void __launch_bounds__(kThreads, kFinPerSm) finish_step_kernel(FinishArgs a) {
   cg::grid_group grid = cg::this_grid();
   AlsCtrl* ctrl = a.ctrl;
-  if (ctrl->stop) return;
+  if (ctrl->stop) {
+    if (a.cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0u);
+    return;
+  }
   constexpr int kRows = kFinRows, kLd = NC + 4, kNT = NC / 8, kTri = kNT * (kNT + 1) / 2, kStg = kFinStages;
   extern __shared__ __align__(16) double sm[];
   double* tile = sm;  // [kStg][kRows][kLd]
@@ -834,6 +841,39 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
   PHASE(12);
 }
 
+// part[0][i][c] = sum_k part[k][i][c] (c < r) over the whole grid, 8 lanes per
+// entry (k = lane, lane + 8, ... ascending, four loads in flight per lane) and
+// a fixed xor tree: the split-K reduction that precedes a cluster prep.
+// Returns at once when the sweep is past the stop decision.
+__global__ void __launch_bounds__(256) slot0_reduce_kernel(double* part, int nparts, uint32_t I, uint32_t ldp,
+                                                          uint32_t r, const AlsCtrl* ctrl) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (ctrl && ctrl->stop) return;
+  const uint64_t n = uint64_t(I) * r;
+  const uint64_t e = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const bool act = e < n;
+  double s = 0.0;
+  double* p = nullptr;
+  if (act) {
+    p = part + (e / r) * ldp + (e % r);
+    const uint64_t stride = uint64_t(I) * ldp;
+    int k = sub;
+    for (; k + 24 < nparts; k += 32) {
+      const double v0 = __ldcg(p + size_t(k) * stride), v1 = __ldcg(p + size_t(k + 8) * stride);
+      const double v2 = __ldcg(p + size_t(k + 16) * stride), v3 = __ldcg(p + size_t(k + 24) * stride);
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; k < nparts; k += 8) s += __ldcg(p + size_t(k) * stride);
+  }
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (act && sub == 0) p[0] = s;
+}
+
 // ---- cluster steps ---------------------------------------------------------------------
 // The same three steps as ONE thread-block cluster (up to 16 CTAs, one per
 // SM) instead of a grid-synchronised launch over every SM. CTA q of the
@@ -981,7 +1021,10 @@ template <int NC>
 __global__ void __launch_bounds__(kThreads) finish_cluster_kernel(FinishArgs a) {
   pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
-  if (a.ctrl->stop) return;
+  if (a.ctrl->stop) {
+    if (a.cond && cl.block_rank() == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0u);
+    return;
+  }
   extern __shared__ __align__(16) double sm[];
   const uint32_t r = a.r;
   double* G = sm;
@@ -1172,12 +1215,22 @@ bool use_grid_steps() {
   return v;
 }
 
-bool use_cluster_prep() {
-  static const bool v = [] {
-    const char* e = std::getenv("TKG_CLUSTER_PREP");
-    return e != nullptr && e[0] == '1';
-  }();
-  return v;
+constexpr uint32_t kClusterPrepMaxI = 512;
+
+template <class K, class... Args>
+cudaError_t pdl_launch(K kernel, int grid, int block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (e != cudaSuccess) cudaGetLastError();
+  return e;
 }
 
 // Largest cluster (16 non-portable, else 8, 4, 2, 1) that the kernel can
@@ -1262,9 +1315,18 @@ int finish_step_grid(uint64_t F, int num_sms) {
   return CALL(16);
 
 cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st) {
-  // the cluster prep loses to the grid one: summing the split-K partials on
-  // 16 SMs is latency-bound (tools/small_bench.cu; TKG_CLUSTER_PREP=1 selects it)
-  if (!use_grid_steps() && use_cluster_prep()) {
+  // Factors of up to 512 rows: the split-K partials are summed by a full-grid
+  // kernel (summing them on 16 SMs is latency-bound), then one cluster runs
+  // the rest of the step; taller factors keep the grid-synchronised kernel
+  // (tools/small_bench.cu).
+  if (!use_grid_steps() && a.I <= kClusterPrepMaxI) {
+    if (a.from_partials && a.nparts > 1) {
+      const uint64_t threads = uint64_t(a.I) * a.r * 8;
+      cudaError_t e = pdl_launch(slot0_reduce_kernel, int((threads + 255) / 256), 256, st, a.part, a.nparts, a.I,
+                                 a.ldp, a.r, static_cast<const AlsCtrl*>(a.ctrl));
+      if (e != cudaSuccess) return e;
+      a.nparts = 1;
+    }
 #define TKG_PC(KE) cluster_step(prep_cluster_kernel<KE>, prep_cluster_smem(a.r), a, st)
     TKG_KE_SWITCH(a.r, TKG_PC)
 #undef TKG_PC
@@ -1311,9 +1373,17 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
 }
 
 cudaError_t launch_cholqr_step(CholQrArgs a, int num_sms, cudaStream_t st) {
-  // cluster CholQR2 while a CTA's rows fit one 32-row block (I <= 512);
-  // taller factors stream more rows per SM than 16 SMs sustain
-  if (!use_grid_steps() && a.I <= 512) {
+  // cluster CholQR2 while a CTA's rows fit one 32-row block (I <= 512), after
+  // a full-grid sum of the split-K partials; taller factors stream more rows
+  // per SM than 16 SMs sustain
+  if (!use_grid_steps() && a.I <= kClusterPrepMaxI) {
+    if (a.nparts > 1) {  // no stop check: the initializer runs before ctrl_init
+      const uint64_t threads = uint64_t(a.I) * a.r * 8;
+      cudaError_t e = pdl_launch(slot0_reduce_kernel, int((threads + 255) / 256), 256, st, a.Y, a.nparts, a.I,
+                                 uint32_t(a.ldp), a.r, static_cast<const AlsCtrl*>(nullptr));
+      if (e != cudaSuccess) return e;
+      a.nparts = 1;
+    }
 #define TKG_QC(KE) cluster_step(cholqr_cluster_kernel<KE>, cholqr_cluster_smem(a.r), a, st)
     TKG_KE_SWITCH(a.r, TKG_QC)
 #undef TKG_QC

@@ -25,6 +25,11 @@ struct PrepArgs {
   AlsCtrl* ctrl = nullptr;
 };
 
+// Sweeps run as the body of a CUDA-graph WHILE node (Engine::run_als): the
+// finish step sets the node's condition to "continue" (cudaGraphSetConditional)
+// and to 0 on every path that stops; 0 = not in a graph.
+using GraphCond = unsigned long long;
+
 struct FinishArgs {
   const double* R = nullptr;     // row-major [F][ld]
   uint64_t F = 0, ld = 0;
@@ -37,6 +42,7 @@ struct FinishArgs {
   double* history = nullptr;
   int gram_nparts = 0;           // > 0: gpart already holds this many Gram partials
                                  // (fused into the FC epilogue), no R pass
+  GraphCond cond = 0;            // WHILE-node condition handle (graph mode)
   int mode = 0;                  // 0 full step; 1 only the R^T R partials of the R pass
                                  // (gpart[grid], see finish_step_grid); 2 only the CTA-0
                                  // part from the reduced Gram in gs (sharded runs)

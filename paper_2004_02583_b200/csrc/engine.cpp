@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
+#include <thread>
 #include <cstring>
 #include <sstream>
 
@@ -144,6 +146,9 @@ Engine::~Engine() {
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto e : mode_ev_) cudaEventDestroy(e);
   if (stage_h_) cudaFreeHost(stage_h_);
+  if (stage_ctrl_) cudaFreeHost(stage_ctrl_);
+  if (out_stage_) cudaFreeHost(out_stage_);
+  clear_graphs();
   if (norm_h_) cudaFreeHost(norm_h_);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
@@ -505,6 +510,19 @@ void Engine::qr_dev(const double* Y, int nparts, uint64_t ld, uint32_t I, uint32
   q.ctrl = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
   const auto ev = small_begin();
   coop_launch([&] { CK(launch_cholqr_step(q, sms_, st_)); });
+  if (check) {
+    // CholQR2 meets a rank-deficient Y as a failed Cholesky at a column set by
+    // rounding noise; the reference decides on diag(R) of Householder QR
+    // (kernels.cpp:303-367, als.cpp:74-86). When the fast path flags a
+    // collapse, Householder QR of the same Y (the summed partials stay in
+    // slot 0) recomputes Q, R and the collapse column, as the reference does;
+    // otherwise this launch returns at once.
+    AlsCtrl* c = static_cast<AlsCtrl*>(ctrl_d_.ensure(sizeof(AlsCtrl)));
+    double* wk = qr_work_.d(2 * size_t(I) * r + r);
+    CK(launch_qr(Y, nparts > 1 ? 1 : nparts, ld, I, r, Q, rmat, rt, ldrt, wk, 1, nullptr, st_,
+                 &c->degenerate_col, &c->degenerate_col));
+    count_launch();
+  }
   small_end(ev);
   count_launch();
 }
@@ -541,9 +559,38 @@ void Engine::stage_reserve(int modes, int max_iters) {
   }
 }
 
-void Engine::collect(AlsOut& o, ModeRep& dst) const {
+void Engine::collect(AlsOut& o, ModeRep& dst) {
+  if (o.ctrl_host) settle(o);
   dst = o.rep;
   dst.history.assign(o.hist_host, o.hist_host + o.rep.iterations);
+}
+
+// A mode whose sweeps ran as a device-side loop: its report, error and work
+// counters from the staged control block (after the final synchronisation).
+void Engine::settle(AlsOut& o) {
+  const AlsCtrl h = *o.ctrl_host;
+  o.ctrl_host = nullptr;
+  const std::string mname = "mode " + std::to_string(o.rep.mode);
+  switch (h.error) {
+    case kAlsErrZeroNorm: raise(3, "als_low_rank: input tensor has zero norm");
+    case kAlsErrDegenerate:
+      raise(6, "als_init: randomized range collapsed at column " + std::to_string(h.degenerate_col) +
+                   " for mode " + std::to_string(o.rep.mode));
+    case kAlsErrRightSingular:
+    case kAlsErrLeftSingular:
+      raise(4, mname + ": gram matrix is singular, rank " + std::to_string(o.r) +
+                   " exceeds the numerical rank of the iterate");
+    default: break;
+  }
+  o.rep.iterations = h.iter;
+  o.rep.status = h.status;
+  o.rep.achieved_eta = h.achieved;
+  o.norm = h.norm;
+  // FC of sweeps 1..iter, FR of sweeps 1..iter-1 (or iter when the cap ended it)
+  const int fr_run = h.stop ? h.iter - 1 : h.iter;
+  passes_ += uint64_t(h.iter + fr_run);
+  bytes_ += uint64_t(double(h.iter + fr_run) * o.fc_bytes);
+  launches_ += uint64_t(std::max(1, h.iter)) * uint64_t(o.body_launches);
 }
 
 void Engine::mode_begin(int k) { CK(cudaEventRecord(mode_ev_[2 * k], st_)); }
@@ -552,6 +599,72 @@ double Engine::mode_seconds(int k) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, mode_ev_[2 * k], mode_ev_[2 * k + 1]));
   return ms * 1e-3;
+}
+
+// Device-side sweep loops (CUDA graphs with a WHILE node), opt-in with
+// TKG_GRAPH=1; never while profiling (per-launch events) or sharded
+// (host-synchronous communicators). Measured on the BASELINE configs
+// (DESIGN.md §15): no gain on config 1 (the host already runs a whole
+// decomposition ahead of the device), -6 % on config 2, +1 % on 4 and 5, so
+// the speculative host batches stay the default.
+bool Engine::use_graph_loop() const {
+  static const bool on = [] {
+    const char* e = std::getenv("TKG_GRAPH");
+    return e && e[0] == '1';
+  }();
+  return on && !profiling_ && !dist_ && !graph_failed_;
+}
+
+// Captures `body(cond)` (the kernels of one sweep, enqueued on st_) as the
+// body of a WHILE node whose condition starts at 1; returns the instantiated
+// graph, or nullptr (and graph mode off for this engine) when the capture is
+// not supported for these kernels.
+cudaGraphExec_t Engine::capture_sweep_loop(const std::function<void(GraphCond)>& body, int* body_launches) {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool capturing = false;
+  const uint64_t l0 = launches_;
+  try {
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t bg = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(st_, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    capturing = true;
+    body(GraphCond(h));
+    cudaGraph_t done = nullptr;
+    capturing = false;
+    CK(cudaStreamEndCapture(st_, &done));
+    size_t n = 0;
+    CK(cudaGraphGetNodes(bg, nullptr, &n));
+    *body_launches = int(n);
+    CK(cudaGraphInstantiate(&exec, g, 0));
+  } catch (const std::exception& e) {
+    trace("sweep graph capture failed; host loop");
+    if (capturing) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(st_, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    cudaGetLastError();
+    exec = nullptr;
+    graph_failed_ = true;
+  }
+  if (g) cudaGraphDestroy(g);
+  launches_ = l0;  // the captured kernels are counted per executed sweep (settle)
+  return exec;
+}
+
+void Engine::clear_graphs() {
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.first);
+  graphs_.clear();
 }
 
 Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint32_t r,
@@ -660,6 +773,104 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   const int nfin = std::max(finish_step_grid(F, sms_), fc_grid(v, Mt, ncp, r));
   double* gpr = fc_gram_.d(size_t(nfin) * ncp * ncp);
   uint32_t last_ranges = 0;
+  auto prep_args = [&](int from_partials, int nparts) {
+    PrepArgs pa;
+    pa.part = part;
+    pa.nparts = nparts;
+    pa.ldp = ncp;
+    pa.GRinv = GRinv;
+    pa.from_partials = from_partials;
+    pa.I = uint32_t(I);
+    pa.r = r;
+    pa.ncp = ncp;
+    pa.Lc = Lc;
+    pa.GL = GL;
+    pa.GLinv = GLinv;
+    pa.Mt = Mt;
+    pa.gpart = gpl;
+    pa.gs = gs;
+    pa.ctrl = ctrl;
+    return pa;
+  };
+  auto finish_args = [&](int gram_nparts, GraphCond cond) {
+    FinishArgs fa;
+    fa.R = R;
+    fa.F = F;
+    fa.ld = ncp;
+    fa.r = r;
+    fa.GL = GL;
+    fa.GRinv = GRinv;
+    fa.gpart = gpr;
+    fa.gs = gs;
+    fa.ctrl = ctrl;
+    fa.history = hist;
+    fa.gram_nparts = gram_nparts;
+    fa.cond = cond;
+    return fa;
+  };
+  cudaGraphExec_t loop = nullptr;
+  int body_launches = 0;
+  if (use_graph_loop()) {
+    // 2'. Sweeps as a CUDA-graph WHILE loop on the device (no host round trip
+    //     per batch): sweep 1's prep on the stream, then
+    //       while (cond) { FC(k); finish(k) -> cond; FR(k); prep(k+1) }
+    //     the finish step's stop rule ends the loop (kernels past it return on
+    //     entry); the report is read after the driver's final synchronisation.
+    //     Executable graphs are cached per operand set (bench / repeated calls).
+    const std::vector<uint64_t> key = {uint64_t(v.base), v.s, v.P, v.K, v.is_i, v.is_p, r, ncp,
+                                       uint64_t(Mt), uint64_t(R), uint64_t(gpr), uint64_t(part), uint64_t(Lc),
+                                       uint64_t(GL), uint64_t(GLinv), uint64_t(GRinv), uint64_t(gs),
+                                       uint64_t(gpl), uint64_t(ctrl), uint64_t(hist), uint64_t(sms_)};
+    auto it = graphs_.find(key);
+    if (it != graphs_.end()) {
+      loop = it->second.first;
+      body_launches = it->second.second;
+    } else {
+      loop = capture_sweep_loop([&](GraphCond cond) {
+        int fc_used = 0;
+        fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, false, stop,
+           fused_gram ? gpr : nullptr);
+        const FinishArgs fa = finish_args(fused_gram ? fc_used : 0, cond);
+        CK(launch_finish_step(fa, sms_, st_));
+        const uint32_t ranges = fr(v, R, ncp, 1, r, part, nullptr, false, nullptr, stop);
+        const PrepArgs pa = prep_args(1, int(ranges));
+        CK(launch_prep_step(pa, sms_, st_));
+      }, &body_launches);
+      if (loop) {
+        if (graphs_.size() >= 64) clear_graphs();
+        graphs_[key] = {loop, body_launches};
+      }
+    }
+  }
+  if (loop) {
+    {
+      const PrepArgs pa = prep_args(0, 0);
+      CK(launch_prep_step(pa, sms_, st_));
+      count_launch();
+    }
+    trace("graph launch", mode);
+    CK(cudaGraphLaunch(loop, st_));
+    trace("graph launched", mode);
+    if (stage_n_ < size_t(slot + 1) * size_t(stage_iters_ + 1) || stage_iters_ < max_iters)
+      stage_reserve(slot + 1, max_iters);
+    double* hs = stage_h_ + size_t(slot) * size_t(stage_iters_ + 1);
+    CK(cudaMemcpyAsync(hs, hist, sizeof(double) * size_t(max_iters), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(hs + stage_iters_, sumsq, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    if (!stage_ctrl_)
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_ctrl_), kMaxStageModes * sizeof(AlsCtrl), cudaHostAllocDefault));
+    if (slot >= kMaxStageModes) raise(12, "more than 64 staged modes");
+    AlsCtrl* ch = stage_ctrl_ + slot;
+    CK(cudaMemcpyAsync(ch, ctrl, sizeof(AlsCtrl), cudaMemcpyDeviceToHost, st_));
+    out.hist_host = hs;
+    out.sumsq_host = hs + stage_iters_;
+    out.ctrl_host = ch;
+    out.fc_bytes = 8.0 * (double(sh.count()) + double(F) * r + double(I) * r);
+    out.body_launches = body_launches;
+    out.r = r;
+    out.rep.iterations = 0;
+    trace("als graph enqueued", mode);
+    return out;
+  }
   while (true) {
     const int nb = std::min(batch, max_iters - enqueued);
     for (int b = 0; b < nb; ++b) {
@@ -1208,22 +1419,129 @@ double Engine::residual_read(const double* out, const double* ref_sumsq_host) {
 // runs on the main stream: a copy to pageable host memory blocks the host
 // until it completes, so the residual kernels are enqueued first and the
 // transfer overlaps them. Destinations may be host or device pointers (UVA).
+// Closed form of the relative residual of an orthogonal Tucker projection,
+// ||A - A_hat||^2 = ||A||^2 - ||G||^2 (G = A x_n U_n^T, orthonormal U_n: the
+// identity behind hosvd's error analysis), used when it is accurate to well
+// inside the parity tolerance: its rounding error is a few eps ||A||^2 (the
+// two sums, G's own rounding, the factors' orthonormality defect), i.e.
+// |d rel| ~ 1e-15 / (2 rel); at rel >= kClosedFormMinRel that is <= 5e-12
+// against the 1e-10 bar (BASELINE.json). Smaller residuals (exact or nearly
+// exact fits, config 3 at 1e-4) take the explicit expansion pass. false when
+// the explicit pass is needed (or forced: TKG_EXPLICIT_RESIDUAL=1).
+bool Engine::closed_form_residual(const double* core_buf, uint64_t ncore, const double* ref_sumsq_host,
+                                  double* rel) {
+  static const bool forced = [] {
+    const char* e = std::getenv("TKG_EXPLICIT_RESIDUAL");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (forced) return false;
+  const int np = sumsq_partials_count(ncore);
+  double* sq = sq_part_.d(size_t(std::max(4096, np)));
+  double* g2 = misc2_.d(1);
+  CK(launch_sumsq(core_buf, ncore, sq, st_));
+  CK(launch_sum(sq, np, g2, st_));
+  count_launch(2);
+  double g2h = 0.0;
+  CK(cudaMemcpyAsync(&g2h, g2, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  const double a2 = *ref_sumsq_host;
+  if (a2 == 0.0) raise(3, "relative_error: reference tensor has zero norm");
+  const double rel2 = (a2 - g2h) / a2;
+  if (!(rel2 >= kClosedFormMinRel * kClosedFormMinRel)) return false;
+  *rel = std::sqrt(rel2);
+  return true;
+}
+
+// Copies results to the caller's buffers and returns once they are there.
+// Device, managed or pinned destinations take a direct copy; a pageable host
+// destination (a plain numpy array, std::vector) goes through a pinned
+// staging buffer at full PCIe speed and a multi-threaded host memcpy, instead
+// of the driver's pageable path (~5 GB/s: 10 ms for config 5's 50 MB core).
+void Engine::copy_results(const std::vector<ResultCopy>& outs, cudaStream_t s) {
+  size_t staged = 0;
+  std::vector<bool> pageable(outs.size(), false);
+  for (size_t i = 0; i < outs.size(); ++i) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, outs[i].dst) != cudaSuccess) {
+      cudaGetLastError();
+      at.type = cudaMemoryTypeUnregistered;
+    }
+    pageable[i] = at.type == cudaMemoryTypeUnregistered;
+    if (pageable[i]) staged += (outs[i].bytes + 255) / 256 * 256;
+  }
+  if (staged > out_stage_n_) {
+    check_cuda(cudaStreamSynchronize(s), "result staging");
+    if (out_stage_) cudaFreeHost(out_stage_);
+    out_stage_ = nullptr;
+    CK(cudaHostAlloc(&out_stage_, staged, cudaHostAllocDefault));
+    out_stage_n_ = staged;
+  }
+  std::vector<std::pair<char*, const char*>> host;  // (dst, staging)
+  std::vector<size_t> hbytes;
+  size_t off = 0;
+  for (size_t i = 0; i < outs.size(); ++i) {
+    if (outs[i].bytes == 0) continue;
+    if (pageable[i]) {
+      char* st = static_cast<char*>(out_stage_) + off;
+      CK(cudaMemcpyAsync(st, outs[i].src, outs[i].bytes, cudaMemcpyDeviceToHost, s));
+      host.push_back({static_cast<char*>(outs[i].dst), st});
+      hbytes.push_back(outs[i].bytes);
+      off += (outs[i].bytes + 255) / 256 * 256;
+    } else {
+      CK(cudaMemcpyAsync(outs[i].dst, outs[i].src, outs[i].bytes, cudaMemcpyDefault, s));
+    }
+  }
+  check_cuda(cudaStreamSynchronize(s), "result copy");
+  size_t total = 0;
+  for (size_t b : hbytes) total += b;
+  if (total == 0) return;
+  // split the host copies into ~4 MB pieces over up to 8 threads
+  struct Piece { char* d; const char* s; size_t n; };
+  std::vector<Piece> pieces;
+  for (size_t i = 0; i < host.size(); ++i)
+    for (size_t o = 0; o < hbytes[i]; o += size_t(4) << 20)
+      pieces.push_back({host[i].first + o, host[i].second + o, std::min(size_t(4) << 20, hbytes[i] - o)});
+  const size_t nt = std::min<size_t>(8, pieces.size());
+  if (nt <= 1) {
+    for (const Piece& p : pieces) std::memcpy(p.d, p.s, p.n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (size_t k = t; k < pieces.size(); k += nt) std::memcpy(pieces[k].d, pieces[k].s, pieces[k].n);
+    });
+  for (auto& x : th) x.join();
+}
+
 void Engine::outputs_and_residual(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,
                                   const Shape& cs, const double* core_buf, const std::vector<double*>& U,
                                   const double* ref_sumsq, double* core, double* factors, DecompRep* rep) {
   const auto tr = Clock::now();
   CK(cudaEventRecord(out_ready_, st_));
+  double rel_cf = 0.0;
+  std::vector<ResultCopy> res;
+  res.push_back({core, core_buf, cs.count() * sizeof(double)});
+  {
+    size_t ofs = 0;
+    for (int n = 0; n < sh.N; ++n) {
+      res.push_back({factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double)});
+      ofs += sh.d[n] * ranks[n];
+    }
+  }
+  if (closed_form_residual(core_buf, cs.count(), ref_sumsq, &rel_cf)) {
+    const auto td = Clock::now();
+    copy_results(res, st_);
+    rep->d2h_seconds = since(td);
+    rep->relative_residual = rel_cf;
+    rep->residual_seconds = since(tr);
+    return;
+  }
   const double* out = residual_enqueue(A, sh, ranks, core_buf, U);
   trace("residual enqueued");
   const auto td = Clock::now();
   CK(cudaStreamWaitEvent(cp_st_, out_ready_, 0));
-  CK(cudaMemcpyAsync(core, core_buf, cs.count() * sizeof(double), cudaMemcpyDefault, cp_st_));
-  size_t ofs = 0;
-  for (int n = 0; n < sh.N; ++n) {
-    CK(cudaMemcpyAsync(factors + ofs, U[n], sh.d[n] * ranks[n] * sizeof(double), cudaMemcpyDefault, cp_st_));
-    ofs += sh.d[n] * ranks[n];
-  }
-  CK(cudaStreamSynchronize(cp_st_));
+  copy_results(res, cp_st_);
   trace("results copied");
   rep->d2h_seconds = since(td);
   rep->relative_residual = residual_read(out, ref_sumsq);

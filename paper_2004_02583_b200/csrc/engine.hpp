@@ -7,6 +7,7 @@
 //   st_hosvd      hosvd.cpp:127-191 (order, ALS, QR, R_hat R^T shrink)
 // while every pass over the tensor and every small solve runs on the GPU.
 #pragma once
+#include <functional>
 
 #include <chrono>
 #include <cstdint>
@@ -21,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include "comm.hpp"
+#include "coop.cuh"
 #include "eig.hpp"
 #include "kernels.cuh"
 
@@ -189,13 +191,36 @@ class Engine {
     double norm = 0.0;
     const double* hist_host = nullptr;   // pinned staging, rep.iterations values
     const double* sumsq_host = nullptr;  // pinned staging: ||working tensor||^2
+    // graph mode (device-side sweep loop): the staged control block, settled
+    // by collect() after the final synchronisation
+    const AlsCtrl* ctrl_host = nullptr;
+    double fc_bytes = 0.0;
+    int body_launches = 0;
+    uint32_t r = 0;
   };
   // Host-visible results of the decomposition drivers are staged in pinned
   // memory with asynchronous copies and read after the driver's single final
   // synchronisation (one slot of max_iters + 1 doubles per mode), and the
   // per-mode times are CUDA events on the stream.
   void stage_reserve(int modes, int max_iters);
-  void collect(AlsOut& o, ModeRep& dst) const;
+  void collect(AlsOut& o, ModeRep& dst);
+  void settle(AlsOut& o);
+  // device-side sweep loops (CUDA graph WHILE nodes), cached per operand set
+  bool use_graph_loop() const;
+  cudaGraphExec_t capture_sweep_loop(const std::function<void(GraphCond)>& body, int* body_launches);
+  void clear_graphs();
+  std::map<std::vector<uint64_t>, std::pair<cudaGraphExec_t, int>> graphs_;
+  bool graph_failed_ = false;
+  struct ResultCopy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  void copy_results(const std::vector<ResultCopy>& outs, cudaStream_t s);
+  void* out_stage_ = nullptr;  // pinned (results bound for pageable memory)
+  size_t out_stage_n_ = 0;
+  static constexpr int kMaxStageModes = 64;
+  AlsCtrl* stage_ctrl_ = nullptr;  // pinned
   void mode_begin(int k);
   void mode_end(int k);
   double mode_seconds(int k);
@@ -250,6 +275,8 @@ class Engine {
   void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   // SVD / EIG engines: U (device, I x r) <- leading eigenvectors of A_(n) A_(n)^T
   void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U, bool refine);
+  static constexpr double kClosedFormMinRel = 2e-4;
+  bool closed_form_residual(const double* core_buf, uint64_t ncore, const double* ref_sumsq_host, double* rel);
   // dst <- A x_m U_m^T for every m != skip, ascending (multi_mode_product with
   // the other factors, hooi.cpp:82-88); returns dst's shape
   Shape ttm_others(const double* A, const Shape& sh, const std::vector<uint64_t>& ranks,

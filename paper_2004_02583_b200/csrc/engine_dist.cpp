@@ -178,17 +178,20 @@ void Engine::dist_core_and_residual(const double* A, const Shape& L, uint64_t k0
   rep->passes = passes_;
   rep->bytes = bytes_;
   const auto td = Clock::now();
-  CK(cudaMemcpyAsync(core_host, core_buf, cs.count() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  std::vector<ResultCopy> res;
+  res.push_back({core_host, core_buf, cs.count() * sizeof(double)});
   size_t ofs = 0;
   for (int n = 0; n < N; ++n) {
-    CK(cudaMemcpyAsync(factors_host + ofs, U[n], G.d[n] * ranks[n] * sizeof(double), cudaMemcpyDeviceToHost,
-                       st_));
+    res.push_back({factors_host + ofs, U[n], G.d[n] * ranks[n] * sizeof(double)});
     ofs += G.d[n] * ranks[n];
   }
-  sync();
+  copy_results(res, st_);
   rep->d2h_seconds = since(td);
   const auto tr = Clock::now();
-  rep->relative_residual = relative_residual_dev(A, L, ranks, core_buf, Us, outs[0].sumsq_host);
+  double rel_cf = 0.0;  // the core and ||A||^2 are replicated: every rank decides alike
+  rep->relative_residual = closed_form_residual(core_buf, cs.count(), outs[0].sumsq_host, &rel_cf)
+                               ? rel_cf
+                               : relative_residual_dev(A, L, ranks, core_buf, Us, outs[0].sumsq_host);
   rep->residual_seconds = since(tr);
 }
 

@@ -86,10 +86,13 @@ cudaError_t launch_chol(const double* part, int nparts, uint64_t part_ld, int pa
 // nparts == 0). Writes Q (col-major), R (r x r col-major), and R^T padded
 // i-major into rt (nullable, ld ldrt) for the st-HOSVD shrink. When
 // check_degenerate, sets status->degenerate_col per als.cpp:74-86.
-// work: rows*r + rows*r + r doubles.
+// work: rows*r + rows*r + r doubles. only_if (nullable): the kernel returns at
+// once while *only_if == 0 (the CholQR2 fast path's fallback, see
+// Engine::qr_dev); degen_out (nullable) receives the collapse column too.
 cudaError_t launch_qr(const double* Y, int nparts, uint64_t ldy_or_ldp, uint32_t rows, uint32_t r,
                       double* q, double* rmat, double* rt, uint32_t ldrt, double* work,
-                      int check_degenerate, DevStatus* status, cudaStream_t st);
+                      int check_degenerate, DevStatus* status, cudaStream_t st,
+                      const int32_t* only_if = nullptr, int32_t* degen_out = nullptr);
 
 
 // out[0] = sum of `n` partials in fixed order (into status->sumsq when dst null).

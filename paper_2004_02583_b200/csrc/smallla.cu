@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(1024) qr_kernel(const double* __restrict__ Y, 
                                                   uint64_t ldy, uint32_t m, uint32_t n, double* q,
                                                   double* rmat, double* rt, uint32_t ldrt,
                                                   double* work, int check_degenerate,
-                                                  DevStatus* status) {
+                                                  DevStatus* status, const int32_t* only_if,
+                                                  int32_t* degen_out) {
+  if (only_if && *only_if == 0) return;  // fallback mode: the fast path found nothing to redo
   __shared__ double red[32];
   __shared__ double dots[64];
   __shared__ double betas[64];
@@ -233,7 +235,8 @@ __global__ void __launch_bounds__(1024) qr_kernel(const double* __restrict__ Y, 
         break;
       }
     }
-    status->degenerate_col = bad;
+    if (status) status->degenerate_col = bad;
+    if (degen_out) *degen_out = bad;
   }
 }
 
@@ -642,9 +645,10 @@ cudaError_t launch_chol(const double* part, int nparts, uint64_t part_ld, int ro
 
 cudaError_t launch_qr(const double* Y, int nparts, uint64_t ldy, uint32_t rows, uint32_t r,
                       double* q, double* rmat, double* rt, uint32_t ldrt, double* work,
-                      int check_degenerate, DevStatus* status, cudaStream_t st) {
+                      int check_degenerate, DevStatus* status, cudaStream_t st, const int32_t* only_if,
+                      int32_t* degen_out) {
   qr_kernel<<<1, 1024, 0, st>>>(Y, nparts, ldy, rows, r, q, rmat, rt, ldrt, work,
-                                check_degenerate, status);
+                                check_degenerate, status, only_if, degen_out);
   return cudaGetLastError();
 }
 

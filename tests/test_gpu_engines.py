@@ -114,7 +114,10 @@ def test_engines_agree_and_als_lands_nearby(ctx):
     for u, v, w in zip(ts.factors, te.factors, ta.factors):
         assert column_diff(u, v) <= 1e-12
         assert principal_sine(w, u) <= 1e-6
-    assert abs(rs.relative_residual - re_.relative_residual) <= 1e-14
+    # rel err 1e-3 takes the closed form ||A||^2 - ||G||^2 (Engine::closed_form_residual):
+    # the two engines' cores differ in the last bits, so their residuals agree to
+    # ~1e-13, inside the 1e-10 parity bar
+    assert abs(rs.relative_residual - re_.relative_residual) <= 1e-11
     assert abs(ra.relative_residual - rs.relative_residual) <= 1e-8
 
 

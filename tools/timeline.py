@@ -22,6 +22,7 @@ def main():
     p.add_argument("--config", type=int, default=5)
     p.add_argument("--warm", type=int, default=2)
     p.add_argument("--gaps", type=int, default=15)
+    p.add_argument("--dump", action="store_true", help="print every activity (start, duration, name)")
     a = p.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -69,9 +70,15 @@ def main():
     print(f"config {a.config}: span {span / 1e3:.3f} ms, device busy {busy / 1e3:.3f} ms "
           f"({100 * busy / span:.1f} %), {len(ks)} activities, idle {(span - busy) / 1e3:.3f} ms "
           f"in {len(gaps)} gaps; engine seconds {rep.seconds * 1e3:.3f} ms")
+    def short(n):
+        return n.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0][-60:]
+
+    if a.dump:
+        for s_, e_, n in ks:
+            print(f"  {(s_ - t0) / 1e3:9.4f} ms  {(e_ - s_):8.1f} us  {short(n)}")
     per = {}
     for s_, e_, n in ks:
-        k = n.split("(")[0][-60:]
+        k = short(n)
         per[k] = per.get(k, 0.0) + (e_ - s_)
     for k, v in sorted(per.items(), key=lambda x: -x[1]):
         print(f"  {v / 1e3:9.3f} ms  {k}")
