@@ -1,8 +1,11 @@
 """The device-side sweep loop (TKG_GRAPH=1: one CUDA graph per mode with a
-WHILE node whose condition the finish step sets, Engine::run_als) against the
-default host-batched sweeps: the same kernels in the same order, so the
-results must be bit-identical, including the iteration cap, the reports and
-the error path of a singular Gram matrix."""
+WHILE node whose condition the finish step sets, Engine::run_als; t-HOSVD then
+runs its independent modes concurrently, one stream and buffer set each)
+against the default host-batched sweeps: the same kernels, so factors and core
+must be bit-identical and the iteration counts, statuses and error paths
+equal. Concurrent t-HOSVD modes each fuse ||A||^2 into their own init pass
+(a different summation order from mode 1's), so their residual histories
+agree to rounding, not bitwise."""
 import json
 import os
 import subprocess
@@ -18,7 +21,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = [("t", [40, 30, 24], [5, 4, 3], 1e-9, 50), ("st", [24, 20, 16, 12], [4, 3, 5, 2], 1e-9, 50),
-         ("t", [60, 50, 40], [6, 5, 4], 0.0, 7), ("st", [200, 30, 20], [50, 8, 6], 1e-10, 50)]
+         ("t", [60, 50, 40], [6, 5, 4], 0.0, 7), ("st", [200, 40, 30], [50, 10, 8], 1e-10, 50)]
 
 _SCRIPT = r"""
 import json, sys, numpy as np
@@ -60,7 +63,9 @@ def test_graph_loop_matches_host_batches():
     g, h = run(True), run(False)
     assert len(g) == len(h)
     for a, b in zip(g[:-1], h[:-1]):
-        assert a["modes"] == b["modes"]
+        assert [m[:3] for m in a["modes"]] == [m[:3] for m in b["modes"]]
+        for ma, mb in zip(a["modes"], b["modes"]):
+            assert np.allclose(ma[3], mb[3], rtol=1e-12, atol=0)
         assert a["rel"] == b["rel"]
         assert np.array_equal(np.array(a["core"]), np.array(b["core"]))
         for u, v in zip(a["factors"], b["factors"]):

@@ -18,8 +18,8 @@ for c in 3 1 5; do
 done
 for c in 3 1 5; do
   # reports stay on the box (gpurun_out is capped at 64 MiB); summaries come back
-  timeout 900 ncu --set full --import-source on --clock-control none \
-    -k regex:"fc_tma_kernel|fr_tma_kernel|expand_tma|finish_step" -c 8 -o /tmp/full_c$c \
+  timeout 900 ncu -f --set full --import-source on --clock-control none \
+    -k regex:"fc_tma_kernel|fr_tma_kernel|fr_wide_kernel|expand_tma|finish_step|prep_cluster|cholqr_cluster" -c 10 -o /tmp/full_c$c \
     python tools/one_step.py --config $c --warm 0 --synth > gpurun_out/prof/ncu_full_c$c.log 2>&1
   python tools/ncu_summary.py /tmp/full_c$c.ncu-rep > gpurun_out/prof/ncu_full_c${c}_summary.txt 2>&1
   python tools/ncu_summary.py /tmp/full_c$c.ncu-rep --json > gpurun_out/prof/ncu_full_c${c}.json 2>&1
