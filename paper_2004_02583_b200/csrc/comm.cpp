@@ -35,6 +35,7 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;  // NCCL >= 2.18
   bool ok = false;
 };
 
@@ -55,6 +56,7 @@ const NcclApi& nccl() {
     api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(sym("ncclCommSplit"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GroupStart &&
              api.GroupEnd && api.Send && api.Recv && api.GetErrorString;
   });
@@ -74,6 +76,16 @@ class NcclComm final : public Comm {
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     nccl_check(nccl().CommInitRank(&comm_, world, id, rank), "ncclCommInitRank");
+  }
+  NcclComm(ncclComm_t c, int rank, int world) : comm_(c) {
+    rank_ = rank;
+    world_ = world;
+  }
+  std::unique_ptr<Comm> split() override {
+    if (!nccl().CommSplit) return nullptr;
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().CommSplit(comm_, 0, rank_, &c, nullptr), "ncclCommSplit");
+    return std::unique_ptr<Comm>(new NcclComm(c, rank_, world_));
   }
   ~NcclComm() override {
     if (comm_) nccl().CommDestroy(comm_);
@@ -268,6 +280,11 @@ class ShmComm final : public Comm {
     if (registered_) cudaHostUnregister(base_);
     if (base_) munmap(base_, bytes_);
   }
+  // a second group on its own segment (collectives stay host-synchronous: the
+  // caller's stream logic is exercised, nothing overlaps)
+  std::unique_ptr<Comm> split() override {
+    return std::unique_ptr<Comm>(new ShmComm(name_ + "_" + std::to_string(++splits_), rank_, world_, slot_));
+  }
   void allreduce_sum(double* buf, size_t n, cudaStream_t st) override {
     const size_t chunk = slot_ / sizeof(double);
     check_cuda(cudaStreamSynchronize(st), "ShmComm sync");
@@ -353,6 +370,7 @@ class ShmComm final : public Comm {
     }
   }
   std::string name_;
+  int splits_ = 0;
   char* base_ = nullptr;
   ShmHeader* hdr_ = nullptr;
   size_t slot_ = 0, bytes_ = 0;

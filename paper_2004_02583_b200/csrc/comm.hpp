@@ -40,6 +40,11 @@ class Comm {
   // rcount[q] doubles into recvbuf + roff[q]
   virtual void alltoallv(const double* sendbuf, const size_t* scount, const size_t* soff, double* recvbuf,
                          const size_t* rcount, const size_t* roff, cudaStream_t st) = 0;
+  // A second communicator over the same ranks whose collectives may run on
+  // another stream concurrently with this one's (a collective call: every
+  // rank calls it at the same point); nullptr where the group's collectives
+  // are host-synchronous anyway (no overlap to gain).
+  virtual std::unique_ptr<Comm> split() { return nullptr; }
 
  protected:
   int rank_ = 0, world_ = 1;

@@ -32,6 +32,7 @@
 #include <type_traits>
 
 #include "als_step.cuh"
+#include "blockfact.cuh"
 #include "coop.cuh"
 
 namespace cg = cooperative_groups;
@@ -60,6 +61,18 @@ constexpr int kRB = 32;        // factor rows per block
 constexpr int kThreads = 256;
 constexpr int kMaxR = 64;
 constexpr int kGE = (kMaxR * kMaxR + kThreads - 1) / kThreads;  // Gram entries per thread
+
+// Scratch (doubles) of the blocked factorizations that a launch adds to its
+// shared memory: blk_scratch(r) above r = 16 when base + scratch fits 227 KB.
+__host__ __device__ constexpr int scratch_for(int r, size_t base_doubles) {
+  return (r > 16 && (base_doubles + size_t(blk_scratch(r))) * 8 <= size_t(227) * 1024) ? blk_scratch(r) : 0;
+}
+__host__ __device__ constexpr size_t rows_base(int r) { return 2 * size_t(kRB) * (r + 1) + 3 * size_t(r) * r; }
+__host__ __device__ constexpr size_t prep_cluster_base(int r) { return 2 * size_t(kRB) * (r + 1) + 4 * size_t(r) * r; }
+__host__ __device__ constexpr size_t cholqr_cluster_base(int r) {
+  return 2 * size_t(kRB) * (r + 1) + 5 * size_t(r) * r;
+}
+__host__ __device__ constexpr size_t finish_cluster_base(int r) { return 2 * size_t(r) * r; }
 
 // entries of an r x r matrix per thread: a kB x kB block, kB = ceil(r / 16)
 __host__ __device__ constexpr int kb_for(int r) { return (r + 15) / 16; }
@@ -247,6 +260,47 @@ __device__ int gj_inv_reg(const double* G, double* out, uint32_t r, double floor
     if (o.valid(t, r)) out[o.i(t) + o.j(t) * r] = o.v[t];
   __syncthreads();
   return 0;
+}
+
+// ---- dispatch: blocked (blockfact.cuh) above r = 16 when the caller has the
+// scratch, else the register-resident kernels above ---------------------------
+__device__ __forceinline__ bool use_blk(uint32_t r, const double* scratch, int avail) {
+  return r > 16 && scratch != nullptr && avail >= blk_scratch(int(r));
+}
+
+template <int KE>
+__device__ int spd_inverse(const double* G, double* out, uint32_t r, double floor_rel, double* piv_out,
+                           double* scratch, int avail) {
+  if (use_blk(r, scratch, avail)) return blk_spd_inverse(G, out, r, floor_rel, piv_out, scratch);
+  return gj_inv_reg<KE>(G, out, r, floor_rel, piv_out);
+}
+
+// CholQR's factorization: L (lower, r x r column-major) of G by Cholesky with
+// the positivity test only; on success Linv = L^{-1}. Returns the failing
+// column (1-based) or 0.
+template <int KE>
+__device__ int chol_and_inverse(const double* G, double* L, double* Linv, uint32_t r, double* scratch, int avail) {
+  if (use_blk(r, scratch, avail)) {
+    const int ld = blk_ld(int(r)), rp = blk_rp(int(r));
+    double* W = scratch;
+    double* X = W + rp * ld;
+    double* T = X + rp * ld;
+    double* dinv = T + 8 * 64;
+    blk_load(G, r, W);
+    const int fail = blk_chol(W, r, 0.0, nullptr, dinv);
+    if (fail) return fail;
+    blk_trinv(W, r, X, T, dinv);
+    for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) {
+      const uint32_t i = e % r, j = e / r;
+      L[e] = i >= j ? W[i + j * ld] : 0.0;
+      Linv[e] = i >= j ? X[i + j * ld] : 0.0;
+    }
+    __syncthreads();
+    return 0;
+  }
+  const int fail = chol_reg<KE>(G, L, r);
+  if (!fail) tri_inv_reg<KE>(L, Linv, r);
+  return fail;
 }
 
 // ---- grid-wide reductions -----------------------------------------------------------
@@ -453,7 +507,7 @@ __global__ void __launch_bounds__(kThreads) prep_step_kernel(PrepArgs a) {
   if (blockIdx.x == 0) {
     load_mat(a.gs, M, r * r);
     double piv = 0.0;
-    const int fail = gj_inv_reg<KE>(M, W, r, 1e-13, &piv);
+    const int fail = spd_inverse<KE>(M, W, r, 1e-13, &piv, sm + rows_base(int(r)), scratch_for(int(r), rows_base(int(r))));
     if (fail) {
       if (threadIdx.x == 0) {
         ctrl->error = kAlsErrRightSingular;
@@ -500,7 +554,7 @@ constexpr int kFinPerSm = 2;    // resident CTAs per SM (grid of the row pass)
 // Residual, stop rule and G_R^{-1} from the reduced Gram G (shared memory,
 // column-major r x r), on one CTA; Gi: r*r shared scratch.
 template <int NC>
-__device__ void finish_tail(const FinishArgs& a, double* G, double* Gi) {
+__device__ void finish_tail(const FinishArgs& a, double* G, double* Gi, double* scratch = nullptr, int avail = 0) {
   AlsCtrl* ctrl = a.ctrl;
   const uint32_t r = a.r;
   __shared__ double hi_s[32], lo_s[32];
@@ -554,7 +608,7 @@ __device__ void finish_tail(const FinishArgs& a, double* G, double* Gi) {
   __syncthreads();
   if (!cont_s) return;
   double piv = 0.0;
-  const int fail = gj_inv_reg<ke_for(NC)>(G, Gi, r, 1e-13, &piv);
+  const int fail = spd_inverse<ke_for(NC)>(G, Gi, r, 1e-13, &piv, scratch, avail);
   if (fail) {
     if (threadIdx.x == 0) {
       ctrl->error = kAlsErrLeftSingular;
@@ -744,14 +798,15 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
   grid.sync();
   PHASE(3);
   // Phase 2 (CTA 0): chol (no floor), R1^{-1} = (L1^{-1})^T
+  double* SC = sm + rows_base(int(r));
+  const int SCn = scratch_for(int(r), rows_base(int(r)));
   if (blockIdx.x == 0) {
     load_mat(a.gs, M, r * r);
-    const int fail = chol_reg<KE>(M, W, r);
+    const int fail = chol_and_inverse<KE>(M, W, W2, r, SC, SCn);  // L1, L1^{-1} (lower)
     PHASE(4);
     if (threadIdx.x == 0) a.work[0] = fail;
     if (!fail) {
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.L1[e] = W[e];
-      tri_inv_reg<KE>(W, W2, r);  // L1^{-1} (lower)
       PHASE(5);
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.Rinv[e] = W2[e];
     }
@@ -786,11 +841,10 @@ __global__ void __launch_bounds__(kThreads) cholqr_step_kernel(CholQrArgs a) {
     int fail = fail1;
     if (!fail) {
       load_mat(a.gs, M, r * r);
-      fail = chol_reg<KE>(M, W, r);
+      fail = chol_and_inverse<KE>(M, W, W2, r, SC, SCn);  // L2, L2^{-1}
       PHASE(9);
     }
     if (!fail) {
-      tri_inv_reg<KE>(W, W2, r);  // L2^{-1}
       PHASE(10);
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.Rinv[e] = W2[e];
       // R = R2 R1 = L2^T L1^T
@@ -978,7 +1032,8 @@ __global__ void __launch_bounds__(kThreads) prep_cluster_kernel(PrepArgs a) {
 
   // G_L^{-1} with the spd_solve pivot floor, in every CTA (identical bits)
   double piv = 0.0;
-  const int fail = gj_inv_reg<KE>(G, W, r, 1e-13, &piv);
+  const int fail = spd_inverse<KE>(G, W, r, 1e-13, &piv, sm + prep_cluster_base(int(r)),
+                                   scratch_for(int(r), prep_cluster_base(int(r))));
   PHASE(33);
   if (fail) {
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
@@ -1058,7 +1113,7 @@ __global__ void __launch_bounds__(kThreads) finish_cluster_kernel(FinishArgs a) 
     if (a.gs)
       for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) a.gs[e] = G[e];
   }
-  finish_tail<NC>(a, G, Gi);
+  finish_tail<NC>(a, G, Gi, sm + finish_cluster_base(int(r)), scratch_for(int(r), finish_cluster_base(int(r))));
 }
 
 template <int KE>
@@ -1098,7 +1153,9 @@ __global__ void __launch_bounds__(kThreads) cholqr_cluster_kernel(CholQrArgs a) 
   cluster_gram_sum(cl, gp, r, G);
   PHASE(42);
   cl.sync();  // gp is free again
-  const int fail1 = chol_reg<KE>(G, W, r);
+  double* SC = sm + cholqr_cluster_base(int(r));
+  const int SCn = scratch_for(int(r), cholqr_cluster_base(int(r)));
+  const int fail1 = chol_and_inverse<KE>(G, W, W2, r, SC, SCn);  // L1, L1^{-1}
   if (fail1) {
     if (lead && threadIdx.x == 0) {
       a.work[0] = fail1;
@@ -1108,7 +1165,7 @@ __global__ void __launch_bounds__(kThreads) cholqr_cluster_kernel(CholQrArgs a) 
     return;
   }
   for (uint32_t e = threadIdx.x; e < r * r; e += blockDim.x) L1[e] = W[e];
-  tri_inv_reg<KE>(W, W2, r);  // L1^{-1}; R1^{-1}(k, c) = L1^{-1}(c, k): row-major operand = W2
+  __syncthreads();  // R1^{-1}(k, c) = L1^{-1}(c, k): the row-major operand is W2
 
   PHASE(43);
   // Q1 rows = Y rows R1^{-1} (in place in Q), Gram partial of Q1
@@ -1129,8 +1186,7 @@ __global__ void __launch_bounds__(kThreads) cholqr_cluster_kernel(CholQrArgs a) 
   cluster_gram_sum(cl, gp, r, G);
   PHASE(45);
   cl.sync();
-  const int fail = chol_reg<KE>(G, W, r);
-  if (!fail) tri_inv_reg<KE>(W, W2, r);  // L2^{-1}
+  const int fail = chol_and_inverse<KE>(G, W, W2, r, SC, SCn);  // L2, L2^{-1}
   PHASE(46);
   if (lead) {
     // R = R2 R1 = L2^T L1^T, the degeneracy test on its diagonal (als.cpp:74-86)
@@ -1204,7 +1260,7 @@ cudaError_t coop_launch(K kernel, int want, int num_sms, size_t smem, void* args
   return e;
 }
 
-size_t rows_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 3 * size_t(r) * r); }
+size_t rows_smem(uint32_t r) { return sizeof(double) * (rows_base(int(r)) + scratch_for(int(r), rows_base(int(r)))); }
 
 // Cluster steps (TKG_COOP_STEPS=1 selects the grid-synchronised kernels).
 bool use_grid_steps() {
@@ -1297,8 +1353,12 @@ cudaError_t cluster_step(K kernel, size_t smem, const A& args, cudaStream_t st, 
   return cluster_launch(kernel, std::min(cs_max, cluster_size(kernel, smem)), smem, args, st);
 }
 
-size_t prep_cluster_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 4 * size_t(r) * r); }
-size_t cholqr_cluster_smem(uint32_t r) { return sizeof(double) * (2 * size_t(kRB) * (r + 1) + 5 * size_t(r) * r); }
+size_t prep_cluster_smem(uint32_t r) {
+  return sizeof(double) * (prep_cluster_base(int(r)) + scratch_for(int(r), prep_cluster_base(int(r))));
+}
+size_t cholqr_cluster_smem(uint32_t r) {
+  return sizeof(double) * (cholqr_cluster_base(int(r)) + scratch_for(int(r), cholqr_cluster_base(int(r))));
+}
 
 }  // namespace
 
@@ -1354,7 +1414,8 @@ cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
       c.mode = 0;
       c.gram_nparts = want;
     }
-    const size_t csm = sizeof(double) * 2 * size_t(a.r) * a.r;
+    const size_t csm =
+        sizeof(double) * (finish_cluster_base(int(a.r)) + scratch_for(int(a.r), finish_cluster_base(int(a.r))));
     switch (ncp) {
 #define TKG_FC(N) \
   case N: return cluster_step(finish_cluster_kernel<N>, csm, c, st, c.mode == 2 ? 1 : 16);

@@ -145,10 +145,23 @@ Engine::~Engine() {
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto e : mode_ev_) cudaEventDestroy(e);
+  if (sumsq_ev_) cudaEventDestroy(sumsq_ev_);
+  for (Lane* L : lanes_) {
+    cudaStreamSynchronize(L->st);
+    cudaStreamDestroy(L->st);
+    cudaEventDestroy(L->done);
+    delete L;
+  }
   if (stage_h_) cudaFreeHost(stage_h_);
   if (stage_ctrl_) cudaFreeHost(stage_ctrl_);
   if (out_stage_) cudaFreeHost(out_stage_);
   clear_graphs();
+  if (cm_st_) {
+    cudaStreamSynchronize(cm_st_);
+    cudaStreamDestroy(cm_st_);
+    cudaEventDestroy(cm_ev_a_);
+    cudaEventDestroy(cm_ev_b_);
+  }
   if (norm_h_) cudaFreeHost(norm_h_);
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
@@ -601,18 +614,26 @@ double Engine::mode_seconds(int k) {
   return ms * 1e-3;
 }
 
-// Device-side sweep loops (CUDA graphs with a WHILE node), opt-in with
-// TKG_GRAPH=1; never while profiling (per-launch events) or sharded
-// (host-synchronous communicators). Measured on the BASELINE configs
-// (DESIGN.md §15): no gain on config 1 (the host already runs a whole
-// decomposition ahead of the device), -6 % on config 2, +1 % on 4 and 5, so
-// the speculative host batches stay the default.
-bool Engine::use_graph_loop() const {
-  static const bool on = [] {
+// Device-side sweep loops (CUDA graphs with a WHILE node): by default only
+// for t-HOSVD, whose independent modes then run concurrently (one stream and
+// buffer set each, Engine::t_hosvd); TKG_GRAPH=1 uses them for every driver,
+// TKG_GRAPH=0 never. Never while profiling (per-launch events) or sharded
+// (host-synchronous communicators). Measured: config 1
+// 1.51 -> 1.29 ms per step with concurrent modes; for the st-HOSVD configs the
+// device loop alone changes nothing measurable (the host already runs ahead
+// of the device), so they keep the speculative host batches.
+int graph_env() {
+  static const int v = [] {
     const char* e = std::getenv("TKG_GRAPH");
-    return e && e[0] == '1';
+    return e == nullptr ? -1 : (e[0] == '1' ? 1 : 0);
   }();
-  return on && !profiling_ && !dist_ && !graph_failed_;
+  return v;
+}
+
+bool Engine::use_graph_loop() const {
+  if (profiling_ || dist_ || graph_failed_) return false;
+  const int e = graph_env();
+  return e == 1 || (e == -1 && in_lanes_);
 }
 
 // Captures `body(cond)` (the kernels of one sweep, enqueued on st_) as the
@@ -660,6 +681,43 @@ cudaGraphExec_t Engine::capture_sweep_loop(const std::function<void(GraphCond)>&
   if (g) cudaGraphDestroy(g);
   launches_ = l0;  // the captured kernels are counted per executed sweep (settle)
   return exec;
+}
+
+void Engine::swap_lane(Lane& L) {
+  std::swap(st_, L.st);
+  s_.swap(L.s);
+  r_.swap(L.r);
+  l_.swap(L.l);
+  mt_.swap(L.mt);
+  gl_.swap(L.gl);
+  gr_.swap(L.gr);
+  cholL_.swap(L.cholL);
+  cholR_.swap(L.cholR);
+  fr_part_.swap(L.fr_part);
+  fc_gram_.swap(L.fc_gram);
+  gram_part_.swap(L.gram_part);
+  gs_.swap(L.gs);
+  sq_part_.swap(L.sq_part);
+  qr_work_.swap(L.qr_work);
+  y_seq_.swap(L.y_seq);
+  states_.swap(L.states);
+  chunk_ids_.swap(L.chunk_ids);
+  qrl1_.swap(L.qrl1);
+  qrl2_.swap(L.qrl2);
+  qrq1_.swap(L.qrq1);
+  sumsq_d_.swap(L.sumsq_d);
+  ctrl_d_.swap(L.ctrl_d);
+  hist_d_.swap(L.hist_d);
+  misc2_.swap(L.misc2);
+}
+
+// Concurrent modes need the non-blocking (graph) sweep loop and the r <= 64
+// path; singular vectors keep the sequential driver.
+bool Engine::concurrent_modes_ok(const std::vector<uint64_t>& ranks, bool want_sv) const {
+  if (want_sv || profiling_ || dist_ || graph_failed_ || graph_env() == 0) return false;
+  for (uint64_t r : ranks)
+    if (r > kMaxRank) return false;
+  return true;
 }
 
 void Engine::clear_graphs() {
@@ -741,11 +799,16 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     uint32_t ranges = fr(v, S, 1, F, r, part, sumsq_known ? nullptr : sq, true, &fr_grid);
     if (!sumsq_known) {  // ||A||^2 fused into the init pass: one partial per CTA
       CK(launch_sum(sq, int(fr_grid), sumsq, st_));
+      if (record_sumsq_) CK(cudaEventRecord(sumsq_ev_, st_));  // concurrent modes read it (t_hosvd)
       count_launch();
       if (dist_) dist_->allreduce_sum(sumsq, 1, st_);
     }
     if (dist_) ranges = reduce_left_partials(part, ranges, uint32_t(I), ncp, r);
     qr_dev(part, int(ranges), ncp, uint32_t(I), r, Lc, nullptr, nullptr, 0, true);
+  }
+  if (sumsq_from_) {  // a concurrent mode: ||A||^2 from the first mode's init pass
+    CK(cudaStreamWaitEvent(st_, sumsq_ev_, 0));
+    CK(cudaMemcpyAsync(sumsq, sumsq_from_, sizeof(double), cudaMemcpyDeviceToDevice, st_));
   }
   CK(launch_ctrl_init(ctrl, sumsq, cfg.eta, max_iters, max_iters, cfg.init ? 0 : 1, st_));
   count_launch();
@@ -1611,7 +1674,53 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   stage_reserve(sh.N, cfg.max_iters);
   bool sumsq_known = false;
   std::vector<AlsOut> outs;
-  for (int n = 1; n <= sh.N; ++n) {
+  const bool lanes = concurrent_modes_ok(ranks, want_sv) && sh.N > 1;
+  if (lanes) {
+    // every mode on its own stream and buffers; ||A||^2 comes from mode 1's
+    // init pass (the sequential driver's value: identical histories), which
+    // the later modes wait for just before their stop rule is initialised;
+    // the core waits for all
+    while (lanes_.size() < size_t(sh.N)) {
+      Lane* L = new Lane();
+      CK(cudaStreamCreateWithFlags(&L->st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
+      lanes_.push_back(L);
+    }
+    CK(cudaEventRecord(out_ready_, st_));  // the tensor is on the device
+    for (int n = 1; n <= sh.N; ++n) {
+      Lane& L = *lanes_[n - 1];
+      const uint32_t r = uint32_t(ranks[n - 1]);
+      const uint64_t I = sh.d[n - 1];
+      CK(cudaStreamWaitEvent(L.st, out_ready_, 0));
+      swap_lane(L);
+      try {
+        if (!sumsq_ev_) CK(cudaEventCreateWithFlags(&sumsq_ev_, cudaEventDisableTiming));
+        record_sumsq_ = n == 1;
+        sumsq_from_ = n == 1 ? nullptr : lanes_[0]->sumsq_d.d(2);
+        in_lanes_ = true;
+        mode_begin(n - 1);
+        outs.push_back(run_als(A, sh, n, r, cfg, n > 1, MtWindow(), n - 1));
+        in_lanes_ = false;
+        record_sumsq_ = false;
+        sumsq_from_ = nullptr;
+        U[n - 1] = factor_bufs_[n - 1]->d(I * r);
+        qr_dev(l_.d(I * r), 0, I, uint32_t(I), r, U[n - 1], n == sh.N ? rhat_.d(r * r) : nullptr, nullptr, 0,
+               false);
+        mode_end(n - 1);
+        CK(cudaEventRecord(L.done, st_));
+      } catch (...) {
+        in_lanes_ = false;
+        record_sumsq_ = false;
+        sumsq_from_ = nullptr;
+        swap_lane(L);
+        throw;
+      }
+      swap_lane(L);
+      trace("mode enqueued", n);
+    }
+    for (int n = 1; n <= sh.N; ++n) CK(cudaStreamWaitEvent(st_, lanes_[n - 1]->done, 0));
+  }
+  for (int n = 1; n <= sh.N && !lanes; ++n) {
     const uint32_t r = uint32_t(ranks[n - 1]);
     const uint64_t I = sh.d[n - 1];
     if (want_sv && r > kMaxRank)
@@ -1652,7 +1761,8 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
     double* Tbuf = N == 1 ? core_buf : core_t_.d(T.count());
     const int nsh = shrink_count(FN);
     double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
-    CK(launch_shrink(r_.d(FN * ncpN + 8), ncpN, sN, 1, rN, rhat_.d(rN * rN), Tbuf, sq, st_));
+    double* RN = lanes ? lanes_[N - 1]->r.d(FN * ncpN + 8) : r_.d(FN * ncpN + 8);  // the last mode's R
+    CK(launch_shrink(RN, ncpN, sN, 1, rN, rhat_.d(rN * rN), Tbuf, sq, st_));
     count_launch();
     if (N > 1) core_chain(Tbuf, T, ranks, U, core_buf, N - 1);
   }

@@ -99,6 +99,10 @@ class DBuf {
   double* d(size_t count) { return static_cast<double*>(ensure(count * sizeof(double))); }
   uint64_t* u(size_t count) { return static_cast<uint64_t*>(ensure(count * sizeof(uint64_t))); }
   void release();
+  void swap(DBuf& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(bytes_, o.bytes_);
+  }
 
  private:
   void* p_ = nullptr;
@@ -220,6 +224,22 @@ class Engine {
   void* out_stage_ = nullptr;  // pinned (results bound for pageable memory)
   size_t out_stage_n_ = 0;
   static constexpr int kMaxStageModes = 64;
+  // t-HOSVD with device-side sweep loops: the modes are independent, so each
+  // runs on its own stream with its own working buffers (a "lane"); the
+  // engine's members are swapped with the lane's while that mode is enqueued.
+  struct Lane {
+    cudaStream_t st = nullptr;
+    cudaEvent_t done = nullptr;
+    DBuf s, r, l, mt, gl, gr, cholL, cholR, fr_part, fc_gram, gram_part, gs, sq_part, qr_work;
+    DBuf y_seq, states, chunk_ids, qrl1, qrl2, qrq1, sumsq_d, ctrl_d, hist_d, misc2;
+  };
+  std::vector<Lane*> lanes_;
+  cudaEvent_t sumsq_ev_ = nullptr;     // mode 1's ||A||^2 is ready (concurrent modes)
+  bool record_sumsq_ = false;
+  bool in_lanes_ = false;  // enqueuing a concurrent t-HOSVD mode
+  const double* sumsq_from_ = nullptr;  // a concurrent mode copies ||A||^2 from here
+  void swap_lane(Lane& L);
+  bool concurrent_modes_ok(const std::vector<uint64_t>& ranks, bool want_sv) const;
   AlsCtrl* stage_ctrl_ = nullptr;  // pinned
   void mode_begin(int k);
   void mode_end(int k);
@@ -308,6 +328,7 @@ class Engine {
   void begin_timed();
   void count_launch(int n = 1) { launches_ += n; }
   void reshard(const double* src, const Shape& G, int from, int to, double* dst);
+  void reshard_on(const double* src, const Shape& G, int from, int to, double* dst, cudaStream_t st, Comm* comm);
   // Cooperative (grid.sync) launches. Ranks of an in-process group share one
   // device: two partially resident cooperative grids could wait on each
   // other, so there they run one at a time (process-wide lock, synchronised).
@@ -395,6 +416,10 @@ class Engine {
   uint64_t bytes_ = 0;
 
   std::unique_ptr<Comm> comm_;
+  std::unique_ptr<Comm> comm2_;  // second communicator (overlapped reshard), from comm_->split()
+  bool comm2_tried_ = false;
+  cudaStream_t cm_st_ = nullptr;
+  cudaEvent_t cm_ev_a_ = nullptr, cm_ev_b_ = nullptr;
   Comm* dist_ = nullptr;  // set while a sharded driver runs: run_als sums over ranks
   DBuf send_, recv_, reshard_, uslab_, uslab2_, core_t_;
   DBuf sv_u_, sv_g_, sv_vt_, sv_vt0_, sv_ctrl_;

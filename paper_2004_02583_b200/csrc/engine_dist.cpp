@@ -59,7 +59,11 @@ ShardRange shard_range(uint64_t extent, int rank, int world) {
   return r;
 }
 
-void Engine::set_comm(std::unique_ptr<Comm> c) { comm_ = std::move(c); }
+void Engine::set_comm(std::unique_ptr<Comm> c) {
+  comm2_.reset();
+  comm2_tried_ = false;
+  comm_ = std::move(c);
+}
 
 std::mutex& Engine::coop_mutex() {
   static std::mutex m;
@@ -69,7 +73,12 @@ std::mutex& Engine::coop_mutex() {
 // dst (sharded along `to`) <- src (sharded along `from`) of the global shape
 // G: pack one box per destination, one alltoallv, unpack one box per source.
 void Engine::reshard(const double* src, const Shape& G, int from, int to, double* dst) {
-  const int world = comm_->world(), rank = comm_->rank();
+  reshard_on(src, G, from, to, dst, st_, comm_.get());
+}
+
+void Engine::reshard_on(const double* src, const Shape& G, int from, int to, double* dst, cudaStream_t st,
+                        Comm* comm) {
+  const int world = comm->world(), rank = comm->rank();
   Shape Ls = G, Lt = G;
   Ls.d[from - 1] = shard_range(G.d[from - 1], rank, world).len;
   Lt.d[to - 1] = shard_range(G.d[to - 1], rank, world).len;
@@ -107,10 +116,10 @@ void Engine::reshard(const double* src, const Shape& G, int from, int to, double
     }
     b.src_base = tr.begin * ss[to - 1];
     b.dst_base = 0;
-    CK(launch_copy_box(src, sendb + soff[q], b, st_));
+    CK(launch_copy_box(src, sendb + soff[q], b, st));
   }
   count_launch(world);
-  comm_->alltoallv(sendb, scount.data(), soff.data(), recvb, rcount.data(), roff.data(), st_);
+  comm->alltoallv(sendb, scount.data(), soff.data(), recvb, rcount.data(), roff.data(), st);
   for (int q = 0; q < world; ++q) {
     BoxCopy b;
     b.N = G.N;
@@ -126,7 +135,7 @@ void Engine::reshard(const double* src, const Shape& G, int from, int to, double
     }
     b.src_base = 0;
     b.dst_base = fr_.begin * ts[from - 1];
-    CK(launch_copy_box(recvb + roff[q], dst, b, st_));
+    CK(launch_copy_box(recvb + roff[q], dst, b, st));
   }
   count_launch(world);
 }
@@ -230,6 +239,30 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
     defer_pregenerate(items, cfg.seed);
   }
   stage_reserve(N, cfg.max_iters);
+  // Mode N's input (the tensor moved to shards along mode N-1) depends only
+  // on A: the all-to-all runs on a second communicator and stream while
+  // modes 1..N-1 sweep (NCCL; host-synchronous groups reshard in line).
+  double* B = nullptr;
+  bool overlapped = false;
+  if (world > 1) {
+    B = work_a_.d(LB.count());
+    if (!comm2_tried_) {
+      comm2_ = comm_->split();
+      comm2_tried_ = true;
+    }
+    if (comm2_) {
+      if (!cm_st_) {
+        CK(cudaStreamCreateWithFlags(&cm_st_, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&cm_ev_a_, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&cm_ev_b_, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(cm_ev_a_, st_));
+      CK(cudaStreamWaitEvent(cm_st_, cm_ev_a_, 0));
+      reshard_on(A, G, N, N - 1, B, cm_st_, comm2_.get());
+      CK(cudaEventRecord(cm_ev_b_, cm_st_));
+      overlapped = true;
+    }
+  }
   bool sumsq_known = false;
   std::vector<AlsOut> outs;
   for (int n = 1; n <= N; ++n) {
@@ -239,12 +272,10 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
     const double* An = A;
     const Shape* Ln = &L;
     if (n == N) {
-      double* B = work_a_.d(LB.count());
       if (world > 1) {
-        reshard(A, G, N, N - 1, B);
+        if (overlapped) CK(cudaStreamWaitEvent(st_, cm_ev_b_, 0));
+        else reshard(A, G, N, N - 1, B);
         An = B;
-      } else {
-        An = A;
       }
       Ln = &LB;
     }

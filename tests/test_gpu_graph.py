@@ -2,10 +2,9 @@
 WHILE node whose condition the finish step sets, Engine::run_als; t-HOSVD then
 runs its independent modes concurrently, one stream and buffer set each)
 against the default host-batched sweeps: the same kernels, so factors and core
-must be bit-identical and the iteration counts, statuses and error paths
-equal. Concurrent t-HOSVD modes each fuse ||A||^2 into their own init pass
-(a different summation order from mode 1's), so their residual histories
-agree to rounding, not bitwise."""
+must be bit-identical (concurrent t-HOSVD modes take ||A||^2 from mode 1's
+init pass, as the sequential driver does), and so must the iteration counts,
+statuses, residual histories and error paths."""
 import json
 import os
 import subprocess
@@ -63,13 +62,13 @@ def test_graph_loop_matches_host_batches():
     g, h = run(True), run(False)
     assert len(g) == len(h)
     for a, b in zip(g[:-1], h[:-1]):
-        assert [m[:3] for m in a["modes"]] == [m[:3] for m in b["modes"]]
-        for ma, mb in zip(a["modes"], b["modes"]):
-            assert np.allclose(ma[3], mb[3], rtol=1e-12, atol=0)
+        assert a["modes"] == b["modes"]
         assert a["rel"] == b["rel"]
         assert np.array_equal(np.array(a["core"]), np.array(b["core"]))
         for u, v in zip(a["factors"], b["factors"]):
             assert np.array_equal(np.array(u), np.array(v))
-    # the capped case stopped at max_iters with status 1 (kMaxItersReached)
-    assert all(m[1] == 7 and m[2] == "max_iters_reached" for m in g[2]["modes"])
+    # the capped case (eta = 0) never ran past max_iters = 7; a mode stops
+    # earlier only when two residuals are bitwise equal (|prev - res| = 0)
+    assert all(m[1] <= 7 and (m[1] == 7 or m[2] == "converged") for m in g[2]["modes"])
+    assert any(m[2] == "max_iters_reached" for m in g[2]["modes"])
     assert g[-1] == h[-1]
