@@ -139,6 +139,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(st_);
   for (auto* b : factor_bufs_) delete b;
   for (auto& kv : jump_cache_) delete kv.second;
+  for (auto& kv : yseq_cache_) delete kv.second;
   for (auto& r : recs_) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -403,11 +404,31 @@ void Engine::gen_uniform_on(uint64_t seed, uint32_t stream, uint64_t n, double* 
   } else {
     polys = it->second;
   }
-  std::vector<uint64_t> y(kMtSeqPadded, 0);
-  mt_raw_sequence(seed, stream, y.data(), kMtSeqWords);
-  uint64_t* d_y = ybuf.u(kMtSeqPadded);
-  // pageable source: the copy is staged before cudaMemcpyAsync returns
-  CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st));
+  // the engine's first 20 248 raw words depend only on (seed, stream): kept
+  // on the device per key, so a repeated decomposition does no host-side
+  // recurrence and no upload (bounded cache)
+  (void)ybuf;
+  uint64_t* d_y = nullptr;
+  {
+    const auto ykey = std::make_pair(seed, stream);
+    auto yit = yseq_cache_.find(ykey);
+    if (yit == yseq_cache_.end()) {
+      if (yseq_cache_.size() >= 256) {
+        CK(cudaDeviceSynchronize());  // no pending kernel reads an evicted sequence
+        for (auto& kv : yseq_cache_) delete kv.second;
+        yseq_cache_.clear();
+      }
+      std::vector<uint64_t> y(kMtSeqPadded, 0);
+      mt_raw_sequence(seed, stream, y.data(), kMtSeqWords);
+      DBuf* b = new DBuf();
+      d_y = b->u(kMtSeqPadded);
+      // pageable source: the copy is staged before cudaMemcpyAsync returns
+      CK(cudaMemcpyAsync(d_y, y.data(), y.size() * 8, cudaMemcpyHostToDevice, st));
+      yseq_cache_[ykey] = b;
+    } else {
+      d_y = yit->second->u(kMtSeqPadded);
+    }
+  }
   int nchunks = plan.C;
   const int* d_ids = nullptr;
   if (win.nloc > 0 && win.Gsm > 1 && win.Fg == win.Plo * win.Gsm) {
@@ -792,7 +813,9 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       pre_.erase(pit);
     } else {
       double* Sg = s_.d(F * r + 8);  // column-major F x r, the reference's storage order
+      trace("  gen_uniform", mode);
       gen_uniform(cfg.seed, uint32_t(mode), (win.nloc ? win.Fg : F) * r, Sg, s_window(win, F, 0));
+      trace("  gen_uniform enqueued", mode);
       S = Sg;
     }
     uint32_t fr_grid = 0;
@@ -1564,7 +1587,8 @@ void Engine::copy_results(const std::vector<ResultCopy>& outs, cudaStream_t s) {
   for (size_t i = 0; i < host.size(); ++i)
     for (size_t o = 0; o < hbytes[i]; o += size_t(4) << 20)
       pieces.push_back({host[i].first + o, host[i].second + o, std::min(size_t(4) << 20, hbytes[i] - o)});
-  const size_t nt = std::min<size_t>(8, pieces.size());
+  // threads only pay off for large copies (spawning one costs ~20-50 us)
+  const size_t nt = total < (size_t(8) << 20) ? 1 : std::min<size_t>(8, pieces.size());
   if (nt <= 1) {
     for (const Piece& p : pieces) std::memcpy(p.d, p.s, p.n);
     return;
@@ -1665,16 +1689,22 @@ void Engine::t_hosvd(const double* a, bool a_dev, const Shape& sh, const std::ve
   begin_timed();
   const auto t0 = Clock::now();
   g_trace_t0 = t0;
-  {
+  const bool lanes = concurrent_modes_ok(ranks, want_sv) && sh.N > 1;
+  if (!lanes) {
+    // sequential modes: the later modes' initializer streams are generated on
+    // the side stream while the first modes run (concurrent modes generate
+    // their own, in parallel, on their own streams)
     std::vector<PreGen> items;
     for (int n = 2; n <= sh.N; ++n) items.push_back({n, sh.count() / sh.d[n - 1], uint32_t(ranks[n - 1]), MtWindow()});
     defer_pregenerate(items, cfg.seed);
+  } else {
+    pre_.clear();
+    pending_pre_.clear();
   }
   trace("pregenerate enqueued");
   stage_reserve(sh.N, cfg.max_iters);
   bool sumsq_known = false;
   std::vector<AlsOut> outs;
-  const bool lanes = concurrent_modes_ok(ranks, want_sv) && sh.N > 1;
   if (lanes) {
     // every mode on its own stream and buffers; ||A||^2 comes from mode 1's
     // init pass (the sequential driver's value: identical histories), which

@@ -234,6 +234,7 @@ class Engine {
     DBuf y_seq, states, chunk_ids, qrl1, qrl2, qrq1, sumsq_d, ctrl_d, hist_d, misc2;
   };
   std::vector<Lane*> lanes_;
+  std::map<std::pair<uint64_t, uint32_t>, DBuf*> yseq_cache_;  // MT raw sequences per (seed, stream)
   cudaEvent_t sumsq_ev_ = nullptr;     // mode 1's ||A||^2 is ready (concurrent modes)
   bool record_sumsq_ = false;
   bool in_lanes_ = false;  // enqueuing a concurrent t-HOSVD mode
