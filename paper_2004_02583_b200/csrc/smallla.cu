@@ -297,12 +297,15 @@ __global__ void sumsq_diff_kernel(const double* __restrict__ a, const double* __
 // ---- st-HOSVD shrink ---------------------------------------------------------
 // working <- tensorize(R_hat R^T) (hosvd.cpp:176-178): out(jl, c, p) =
 // sum_k R[j][k] R_hat(c, k) for every fiber j = jl + p*s, i.e. a tall-skinny
-// F x r x r product. A CTA takes 128-fiber tiles of R (row-major [F][ld],
-// one contiguous block), runs DMMA against R_hat^T held in shared memory,
-// stages the r x 128 result in shared memory and writes each output column
-// as one coalesced run of fibers; ||out||^2 per CTA.
+// F x r x r product. A persistent CTA walks 128-fiber tiles of R (row-major
+// [F][ld], one contiguous block): the next tile streams into the second
+// buffer with cp.async while the current one runs DMMA against R_hat^T held
+// in shared memory; the r x 128 result is staged in the current buffer and
+// each output column (or, for s = 1, the tile's contiguous fiber-major
+// block) written as coalesced runs; ||out||^2 per CTA.
 constexpr int kShrinkThreads = 256;
-constexpr int kShrinkTile = 128;
+constexpr int kShrinkTile = 64;              // two CTAs per SM overlap each other's phases
+constexpr int kShrinkMT = kShrinkTile / 64;  // 8-fiber row tiles per warp
 
 template <int NC>
 __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
@@ -310,9 +313,11 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
     const double* __restrict__ rhat, double* __restrict__ out, double* sumsq_part) {
   constexpr int kLd = NC + 4;            // fragment rows 4 (mod 16) apart
   constexpr int kLdO = kShrinkTile + 4;
+  constexpr int kBuf = kShrinkTile * kLd;
+  constexpr int kChunks = NC / 2;        // 16-byte chunks per row
   extern __shared__ __align__(16) double sm[];
-  double* Rs = sm;                       // [128][kLd]; reused as Os [NC][kLdO]
-  double* Bs = sm + kShrinkTile * kLd;   // [NC][kLd]: Bs[k][c] = R_hat(c, k)
+  double* Bs = sm;                       // [NC][kLd]: Bs[k][c] = R_hat(c, k)
+  double* Rb = sm + NC * kLd;            // 2 x [128][kLd]; the current one becomes Os
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r8 = lane >> 2;
   for (int e = threadIdx.x; e < NC * NC; e += blockDim.x) {
@@ -321,55 +326,70 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
   }
   const uint64_t F = s * P;
   const uint64_t ntiles = (F + kShrinkTile - 1) / kShrinkTile;
-  double sq = 0.0;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  auto issue = [&](uint64_t tile, double* buf) {
     const uint64_t j0 = tile * kShrinkTile;
     const int nf = int(F - j0 < uint64_t(kShrinkTile) ? F - j0 : uint64_t(kShrinkTile));
-    __syncthreads();  // previous tile's readers of Rs / Os are done
-    for (int e = threadIdx.x; e < kShrinkTile * (NC / 2); e += blockDim.x) {
-      const int row = e / (NC / 2), c = (e % (NC / 2)) * 2;
-      double2 v = make_double2(0.0, 0.0);
-      if (row < nf) v = *reinterpret_cast<const double2*>(R + (j0 + row) * ld + c);
-      Rs[row * kLd + c] = c < int(r) ? v.x : 0.0;  // R's padding columns are never written
-      Rs[row * kLd + c + 1] = c + 1 < int(r) ? v.y : 0.0;
+    for (int e = threadIdx.x; e < nf * kChunks; e += blockDim.x) {
+      const int row = e / kChunks, c = (e % kChunks) * 2;
+      cp_async16(buf + row * kLd + c, R + (j0 + row) * ld + c);
+    }
+  };
+  double sq = 0.0;
+  uint64_t tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, Rb);
+  cp_async_commit();
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    double* cur = Rb + (it & 1) * kBuf;
+    const uint64_t nxt = tile + gridDim.x;
+    __syncthreads();  // the previous tile's readers of the other buffer (its Os) are done
+    if (nxt < ntiles) issue(nxt, Rb + ((it + 1) & 1) * kBuf);
+    cp_async_commit();
+    cp_async_wait<1>();
+    const uint64_t j0 = tile * kShrinkTile;
+    const int nf = int(F - j0 < uint64_t(kShrinkTile) ? F - j0 : uint64_t(kShrinkTile));
+    __syncthreads();  // the current tile landed for every thread
+    // R's padding columns and the rows past F are zero for the product
+    for (int e = threadIdx.x; e < kShrinkTile * NC; e += blockDim.x) {
+      const int row = e / NC, c = e % NC;
+      if (row >= nf || c >= int(r)) cur[row * kLd + c] = 0.0;
     }
     __syncthreads();
-    double acc[2][NC / 8][2];
+    double acc[kShrinkMT][NC / 8][2];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < kShrinkMT; ++m)
 #pragma unroll
       for (int n = 0; n < NC / 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 #pragma unroll
     for (int t = 0; t < NC / 4; ++t) {
       const int kk = 4 * t + q;
-      double af[2], bf[NC / 8];
+      double af[kShrinkMT], bf[NC / 8];
 #pragma unroll
-      for (int m = 0; m < 2; ++m) af[m] = Rs[(warp * 16 + m * 8 + r8) * kLd + kk];
+      for (int m = 0; m < kShrinkMT; ++m) af[m] = cur[(warp * 8 * kShrinkMT + m * 8 + r8) * kLd + kk];
 #pragma unroll
       for (int n = 0; n < NC / 8; ++n) bf[n] = Bs[kk * kLd + n * 8 + r8];
 #pragma unroll
       for (int n = 0; n < NC / 8; ++n)
 #pragma unroll
-        for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+        for (int m = 0; m < kShrinkMT; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
     }
-    __syncthreads();  // Rs becomes the staging buffer Os
-    double* Os = Rs;
+    __syncthreads();  // the current buffer becomes the staging buffer Os
+    double* Os = cur;
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+    for (int m = 0; m < kShrinkMT; ++m)
 #pragma unroll
       for (int n = 0; n < NC / 8; ++n)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int f = warp * 16 + m * 8 + r8, c = n * 8 + 2 * q + e;
+          const int f = warp * 8 * kShrinkMT + m * 8 + r8, c = n * 8 + 2 * q + e;
           Os[s == 1 ? f * (NC + 1) + c : c * kLdO + f] = acc[m][n][e];
         }
     __syncthreads();
-    if (s == 1) {  // mode-1 output: a fiber's r values are one contiguous run
-      for (int e = threadIdx.x; e < int(r) * kShrinkTile; e += blockDim.x) {
+    if (s == 1) {  // mode-1 output: the tile's fibers are one contiguous block of nf * r values
+      double* o = out + j0 * r;
+      for (int e = threadIdx.x; e < int(r) * nf; e += blockDim.x) {
         const int f = e / int(r), c = e - f * int(r);
-        if (f >= nf) continue;
         const double v = Os[f * (NC + 1) + c];  // fiber-major staging: conflict-free reads
-        out[c + (j0 + f) * r] = v;
+        o[e] = v;
         sq = fma(v, v, sq);
       }
     } else {
@@ -383,6 +403,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
       }
     }
   }
+  cp_async_wait<0>();
   sq = block_sum(sq, red);
   if (threadIdx.x == 0) sumsq_part[blockIdx.x] = sq;
 }
@@ -607,7 +628,7 @@ cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, 
   const uint32_t nc = r <= 8 ? 8 : (r + 7) / 8 * 8;
 #define TKG_S(N)                                                                                    \
   if (nc == N) {                                                                                    \
-    const size_t smem = sizeof(double) * (size_t(kShrinkTile) * (N + 4) + size_t(N) * (N + 4));     \
+    const size_t smem = sizeof(double) * (2 * size_t(kShrinkTile) * (N + 4) + size_t(N) * (N + 4)); \
     cudaError_t e = raise_smem_limit(shrink_kernel<N>, smem);                                       \
     if (e != cudaSuccess) return e;                                                                 \
     shrink_kernel<N><<<grid, kShrinkThreads, smem, st>>>(R, ld, s, P, r, rhat, out, sumsq_part);   \
