@@ -77,6 +77,13 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 // modulo the 16-double bank window, i.e. ld = 4 (mod 16).
 __host__ __device__ constexpr int smem_ld(int nc) { return nc + ((4 - nc) % 16 + 16) % 16; }
 
+// Programmatic dependent launch (the kernels' griddepcontrol.wait) for the
+// contraction grids and the small steps. Off while an engine records per-launch
+// CUDA events (bench.py's per-class pass): a PDL launch starts early and its
+// event interval would include the wait for the previous kernel.
+int& pdl_off_count();
+inline bool pdl_enabled() { return pdl_off_count() == 0; }
+
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (never
 // lowers it): several host threads sharing a device (in-process ranks) may
 // launch one kernel with different sizes, and a per-call set could lower the

@@ -974,7 +974,7 @@ cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t st, Args...
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
@@ -1035,6 +1035,11 @@ cudaError_t expand_tma_launch(const CUtensorMap& X, const CUtensorMap& U, const 
 }
 
 }  // namespace
+
+int& pdl_off_count() {
+  static int n = 0;  // engines currently profiling (host-side setting, read at launch)
+  return n;
+}
 
 int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt) {
   if (!encode_fn() || !aligned16(v.base) || !aligned16(mt) || (ldmt % 2) != 0) return -1;

@@ -135,6 +135,7 @@ Engine::Engine(int device) : device_(device) {
 }
 
 Engine::~Engine() {
+  if (profiling_) pdl_off_count() -= 1;
   cudaSetDevice(device_);
   cudaStreamSynchronize(st_);
   for (auto* b : factor_bufs_) delete b;

@@ -180,7 +180,10 @@ class Engine {
 
   void bench_contractions(const double* dA, const Shape& sh, int mode, uint32_t r, int reps,
                           double* out_ms);
-  void set_profiling(bool on) { profiling_ = on; }
+  void set_profiling(bool on) {
+    if (on != profiling_) pdl_off_count() += on ? 1 : -1;
+    profiling_ = on;
+  }
   void force_v1(bool on) { force_v1_ = on; }
   void timer_start();
   double timer_stop();
