@@ -109,6 +109,10 @@ void fill_report(tkg_ctx* ctx, const tkg::DecompRep& r, int order, tkg_report* o
 
 tkg::Engine& eng(tkg_ctx* ctx) {
   if (!ctx || !ctx->eng) tkg::raise(TKG_E_UNSUPPORTED, "null tkg context");
+  // the calling thread may have another device current (one process driving
+  // several contexts): every entry point runs on the context's device
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != ctx->eng->device()) cudaSetDevice(ctx->eng->device());
   return *ctx->eng;
 }
 

@@ -180,6 +180,7 @@ class Engine {
 
   void bench_contractions(const double* dA, const Shape& sh, int mode, uint32_t r, int reps,
                           double* out_ms);
+  int device() const { return device_; }
   void set_profiling(bool on) {
     if (on != profiling_) pdl_off_count() += on ? 1 : -1;
     profiling_ = on;

@@ -14,6 +14,7 @@
 //
 // Reference call sites: hosvd.cpp:74-125 (t_hosvd), 127-191 (st_hosvd).
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <string>
 
@@ -246,8 +247,9 @@ void Engine::t_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint64
   bool overlapped = false;
   if (world > 1) {
     B = work_a_.d(LB.count());
-    if (!comm2_tried_) {
-      comm2_ = comm_->split();
+    if (!comm2_tried_) {  // TKG_NO_SPLIT=1: reshard in line (no second communicator)
+      const char* e = std::getenv("TKG_NO_SPLIT");
+      if (!(e && e[0] == '1')) comm2_ = comm_->split();
       comm2_tried_ = true;
     }
     if (comm2_) {
