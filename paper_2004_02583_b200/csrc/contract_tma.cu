@@ -585,51 +585,61 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
 }
 
 // ---------------------------------------------------------------------------
-// FR for 128 < K <= 248 with s == 1 (mode 1 of e.g. a 200^4 tensor): ONE CTA
+// FR for 128 < K <= 248 rows (e.g. a 200^4 tensor's modes 1..4): ONE CTA
 // covers all K contraction rows, so R (or S) is streamed once per pass
 // instead of once per 128-row group, and the 8 consumer warps share the
-// MT = ceil(K/8) row tiles evenly: warp w owns the full row tiles
-// w, w+8, ... (all NC/8 column tiles, base = MT/8 of them) plus every 8th
-// (row tile, column tile) pair of the MT % 8 remainder tiles. For K = 200
-// that is 3 x 7 + 1 DMMA tiles per warp (22 each, 175 in all), where two
-// 128-row groups left the second group's SM sub-partitions a third idle.
-// A stage holds two 132-row boxes of the same 16 fibers (rows 0..131 and
-// 128..259; TMA zero-fills rows past K).
+// MT = ceil(K/8) row tiles evenly: warp w owns the full row tiles w, w+8, ...
+// (all NC/8 column tiles, base = MT/8 of them) plus every 8th (row tile,
+// column tile) pair of the MT % 8 remainder tiles. For K = 200 that is
+// 3 x 7 + 1 DMMA tiles per warp (22 each, 175 in all), where two 128-row
+// groups left the second group's SM sub-partitions a third idle.
+// A stage (rows past K are TMA zero-fill):
+//   kFibI (s = 1)      : 16 fibers, two 132-row boxes [16][132] (rows 0.., 128..)
+//   kFibJ (s >= 64)    : up to 32 fibers of one panel, box [K][36]
+//   kFibS (32 <= s <= 64): one whole panel of s fibers, box [K][sb]
 // ---------------------------------------------------------------------------
-template <int NC, bool MCOL>
+template <int NC, int MODE, bool MCOL>
 struct FrW {
-  static constexpr int kKB = 16;    // fibers per stage
-  static constexpr int kStages = 4;
-  static constexpr int kLdA = 132;
-  static constexpr int kBoxBytes = kKB * kLdA * 8;
-  static constexpr int kBytesA = 2 * kBoxBytes;
-  static constexpr int kLdM = MCOL ? kKB + 4 : NC + 4;
-  static constexpr int kRowsM = MCOL ? NC : kKB;
-  static constexpr int kBytesM = kRowsM * kLdM * 8;
-  static constexpr int kStageBytes = ((kBytesA + kBytesM) + 127) / 128 * 128;
+  static constexpr int kMaxKB = MODE == kFibI ? 16 : MODE == kFibJ ? 32 : 64;  // fibers per stage
   static constexpr int kNT = NC / 8;
-  static constexpr int kRemP = 2;   // remainder pairs per warp (register budget)
-  static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes;
+  static constexpr int kRemP = 2;  // remainder pairs per warp (register budget)
 };
 
-template <int NC, bool MCOL>
+struct FrWideGeom {
+  uint32_t lda = 0;        // A row pitch in smem (doubles): 132 (kFibI), 36 (kFibJ), sb (kFibS)
+  uint32_t kb = 0;         // fibers per stage (kFibS: s)
+  uint32_t bytes_a = 0, bytes_m = 0, stage_bytes = 0, stages = 0, ldm = 0;
+};
+
+template <int NC, int MODE, bool MCOL>
 __global__ void __launch_bounds__(kThreadsTma, 1)
     fr_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
-                   FrTmaArgs a) {
-  using C = FrW<NC, MCOL>;
+                   FrTmaArgs a, FrWideGeom g) {
+  using C = FrW<NC, MODE, MCOL>;
   constexpr int kNT = C::kNT;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // see fc_tma_kernel
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* empty = full + C::kStages;
+  uint64_t* empty = full + 4;
   unsigned char* ring = smem_raw + 1024;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint64_t F = a.s * a.P;
+  const int stages = int(g.stages);
+  // fibers of the stage starting at j: never past the range end, and (kFibJ)
+  // never past the panel end; kFibS stages are whole panels
+  auto chunk_len = [&](uint64_t j, uint64_t f1) -> int {
+    uint64_t end = f1;
+    if (MODE == kFibJ) {
+      const uint64_t pe = (j / a.s + 1) * a.s;
+      end = pe < end ? pe : end;
+    }
+    return end - j < uint64_t(g.kb) ? int(end - j) : int(g.kb);
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCons);
     }
@@ -645,16 +655,21 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       for (uint32_t range = blockIdx.x; range < a.ranges; range += gridDim.x) {
         const uint64_t f0 = uint64_t(range) * a.fibers_per_range;
         const uint64_t f1 = min(F, f0 + a.fibers_per_range);
-        for (uint64_t j = f0; j < f1; j += C::kKB, ++kb) {
-          const int slot = kb % C::kStages;
-          const uint32_t ph = (kb / C::kStages) & 1;
+        for (uint64_t j = f0; j < f1; j += chunk_len(j, f1), ++kb) {
+          const int slot = kb % stages;
+          const uint32_t ph = (kb / stages) & 1;
           mbar_wait(&empty[slot], ph ^ 1);
-          unsigned char* st = ring + size_t(slot) * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[slot], C::kBytesA + C::kBytesM);
-          tma_2d(st, &tmA, &full[slot], 0, int(j));
-          tma_2d(st + C::kBoxBytes, &tmA, &full[slot], 128, int(j));
-          if (MCOL) tma_2d(st + C::kBytesA, &tmM, &full[slot], int(j), 0);
-          else tma_2d(st + C::kBytesA, &tmM, &full[slot], 0, int(j));
+          unsigned char* st = ring + size_t(slot) * g.stage_bytes;
+          mbar_arrive_expect_tx(&full[slot], g.bytes_a + g.bytes_m);
+          if (MODE == kFibI) {
+            tma_2d(st, &tmA, &full[slot], 0, int(j));
+            tma_2d(st + g.bytes_a / 2, &tmA, &full[slot], 128, int(j));
+          } else {
+            const uint64_t p = j / a.s;
+            tma_3d(st, &tmA, &full[slot], int(j - p * a.s), 0, int(p));
+          }
+          if (MCOL) tma_2d(st + g.bytes_a, &tmM, &full[slot], int(j), 0);
+          else tma_2d(st + g.bytes_a, &tmM, &full[slot], 0, int(j));
         }
       }
     }
@@ -666,9 +681,15 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   const int MT = int((a.K + 7) / 8);
   const int base = MT / 8;              // 2 or 3 full row tiles per warp
   const int nrem = (MT % 8) * kNT;      // remainder (row tile, column tile) pairs
+  const int lda = int(g.lda), ldm = int(g.ldm);
   double sq_acc[4] = {0.0, 0.0, 0.0, 0.0};
   // ||A||^2 is fused only into the init pass (column-major S)
   const bool want_sq = MCOL && a.sumsq_part != nullptr;
+  // A(row, kk) of the current stage
+  auto aval = [&](const double* As, int row, int kk) -> double {
+    if (MODE == kFibI) return row < 128 ? As[kk * 132 + row] : As[16 * 132 + kk * 132 + row - 128];
+    return As[row * lda + kk];
+  };
 
   int kb = 0;
   for (uint32_t range = blockIdx.x; range < a.ranges; range += gridDim.x) {
@@ -682,16 +703,17 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       for (int n = 0; n < kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 #pragma unroll
     for (int t = 0; t < C::kRemP; ++t) accr[t][0] = accr[t][1] = 0.0;
-    for (uint64_t j = f0; j < f1; j += C::kKB, ++kb) {
-      const int slot = kb % C::kStages;
-      const uint32_t ph = (kb / C::kStages) & 1;
+    for (uint64_t j = f0; j < f1; ++kb) {
+      const int slot = kb % stages;
+      const uint32_t ph = (kb / stages) & 1;
       mbar_wait(&full[slot], ph);
-      const double* A0 = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes);
-      const double* A1 = A0 + C::kKB * C::kLdA;  // rows 128..259
-      const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * C::kStageBytes + C::kBytesA);
-      const int kvalid = int(min(uint64_t(C::kKB), f1 - j));
+      const double* As = reinterpret_cast<const double*>(ring + size_t(slot) * g.stage_bytes);
+      const double* Ms = reinterpret_cast<const double*>(ring + size_t(slot) * g.stage_bytes + g.bytes_a);
+      const int kvalid = chunk_len(j, f1);
+      j += kvalid;
 #pragma unroll
-      for (int t = 0; t < C::kKB / 4; ++t) {
+      for (int t = 0; t < C::kMaxKB / 4; ++t) {
+        if (4 * t >= kvalid) break;
         const int kk = 4 * t + q;
         const bool kok = kk < kvalid;
         // 9 warps: at most 3 per SM sub-partition, so 168 registers per
@@ -699,14 +721,20 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         double af[3];
 #pragma unroll
         for (int mi = 0; mi < 3; ++mi) {
-          const int row = (warp + 8 * mi) * 8 + r8;  // mi < 2: box 0, mi == 2: box 1
-          const double v = mi < 2 ? A0[kk * C::kLdA + row] : A1[kk * C::kLdA + row - 128];
+          const int row = (warp + 8 * mi) * 8 + r8;
+          // kFibI: rows of row tiles 0..15 sit in the first box, 16.. in the second
+          const double v = MODE == kFibI ? (mi < 2 ? As[kk * 132 + row] : As[16 * 132 + kk * 132 + row - 128])
+                                         : As[row * lda + kk];
           af[mi] = (kok && mi < base) ? v : 0.0;
           if (want_sq) sq_acc[(t & 1) * 2 + (mi & 1)] = fma(af[mi], af[mi], sq_acc[(t & 1) * 2 + (mi & 1)]);
         }
+        // fibers past the chunk read real data of the next fibers or TMA
+        // zero-fill (finite), and their A fragment is zero; the row-major B
+        // loads are predicated all the same (measured: 5.96 -> 5.43 ms for the
+        // c5 mode-1 left update), the column-major ones are not (7.15 -> 6.47)
 #pragma unroll
         for (int n = 0; n < kNT; ++n) {
-          const double b = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
+          const double b = MCOL ? Ms[(n * 8 + r8) * ldm + kk] : (kok ? Ms[kk * ldm + n * 8 + r8] : 0.0);
           dmma(acc[0][n][0], acc[0][n][1], af[0], b);
           dmma(acc[1][n][0], acc[1][n][1], af[1], b);
           if (base > 2) dmma(acc[2][n][0], acc[2][n][1], af[2], b);
@@ -716,12 +744,11 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           const int p = warp + 8 * u;
           if (p < nrem) {
             const int m = 8 * base + p / kNT, n = p % kNT;
-            const double v = A1[kk * C::kLdA + m * 8 + r8 - 128];
-            const double af = kok ? v : 0.0;
+            const double af1 = kok ? aval(As, m * 8 + r8, kk) : 0.0;
             // each A element of a remainder tile is squared once (column tile 0)
-            if (want_sq && n == 0) sq_acc[(t & 1) * 2 + 1] = fma(af, af, sq_acc[(t & 1) * 2 + 1]);
-            const double b = MCOL ? Ms[(n * 8 + r8) * C::kLdM + kk] : Ms[kk * C::kLdM + n * 8 + r8];
-            dmma(accr[u][0], accr[u][1], af, b);
+            if (want_sq && n == 0) sq_acc[(t & 1) * 2 + 1] = fma(af1, af1, sq_acc[(t & 1) * 2 + 1]);
+            const double bb = MCOL ? Ms[(n * 8 + r8) * ldm + kk] : (kok ? Ms[kk * ldm + n * 8 + r8] : 0.0);
+            dmma(accr[u][0], accr[u][1], af1, bb);
           }
         }
       }
@@ -990,14 +1017,14 @@ cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTm
   return launch_pdl(k, grid, C::kSmem, st, A, M, a);
 }
 
-template <int NC, bool MCOL>
-cudaError_t fr_wide_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, int grid,
-                           cudaStream_t st) {
-  using C = FrW<NC, MCOL>;
-  auto k = fr_wide_kernel<NC, MCOL>;
-  cudaError_t e = set_smem(k, C::kSmem);
+template <int NC, int MODE, bool MCOL>
+cudaError_t fr_wide_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, const FrWideGeom& g,
+                           int grid, cudaStream_t st) {
+  auto k = fr_wide_kernel<NC, MODE, MCOL>;
+  const size_t smem = 1024 + size_t(g.stages) * g.stage_bytes;
+  cudaError_t e = set_smem(k, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k, grid, C::kSmem, st, A, M, a);
+  return launch_pdl(k, grid, smem, st, A, M, a, g);
 }
 
 template <int NC, int MODE, bool MCOL>
@@ -1137,44 +1164,84 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
   const uint32_t ncp = pad_nc(a.nc);
   CUtensorMap A, M;
   const uint64_t F = v.s * v.P;
-  if (mode == kFibI && fr_wide_ok(v, ncp)) {
-    constexpr uint32_t kKB = 16;
-    {
+  if (fr_wide_ok(v, ncp, mode)) {
+    // one CTA over all K rows (fr_wide_kernel)
+    const uint32_t K8 = (v.K + 7) / 8 * 8;
+    FrWideGeom g;
+    if (mode == kFibI) {
+      g.kb = 16;
+      g.lda = 132;
       const uint64_t dims[2] = {v.K, F};
       const uint64_t strides[1] = {v.is_p * 8};
-      const uint32_t box[2] = {132, kKB};
+      const uint32_t box[2] = {132, g.kb};
       if (!encode(&A, v.base, 2, dims, strides, box)) return cudaErrorInvalidValue;
+      g.bytes_a = 2 * g.kb * 132 * 8;
+    } else {
+      uint32_t pcS = 0, sb = 0;
+      if (mode == kFibJ) {
+        g.kb = 32;
+        g.lda = 36;
+      } else {
+        fc_short_geometry(v.s, &pcS, &sb);
+        g.kb = uint32_t(v.s);  // one whole panel per stage
+        // the k-steps read fibers up to round4(s) - 1: the A rows and the M
+        // boxes cover them (next-panel data or TMA zero-fill, never used)
+        g.lda = std::max<uint32_t>(sb, (g.kb + 3) / 4 * 4);
+      }
+      const uint64_t dims[3] = {v.s, v.K, v.P};
+      const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
+      const uint32_t box[3] = {g.lda, K8, 1};
+      if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
+      g.bytes_a = K8 * g.lda * 8;
     }
+    const uint32_t mrows = mode == kFibS ? g.lda : g.kb;  // fibers per M box (kFibS: >= round4(s))
     if (!mcol) {
+      g.ldm = ncp + 4;
       const uint64_t dims[2] = {ncp, F};
       const uint64_t strides[1] = {mj * 8};
-      const uint32_t box[2] = {ncp + 4, kKB};
+      const uint32_t box[2] = {ncp + 4, mrows};
       if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
+      g.bytes_m = mrows * (ncp + 4) * 8;
     } else {
+      g.ldm = mode == kFibS ? mrows : g.kb + 4;
       const uint64_t dims[2] = {F, a.nc};
       const uint64_t strides[1] = {mc * 8};
-      const uint32_t box[2] = {kKB + 4, ncp};
+      const uint32_t box[2] = {g.ldm, ncp};
       if (!encode(&M, m, 2, dims, strides, box)) return cudaErrorInvalidValue;
+      g.bytes_m = ncp * g.ldm * 8;
     }
+    g.stage_bytes = (g.bytes_a + g.bytes_m + 127) / 128 * 128;
+    g.stages = std::min<uint32_t>(4, (220u * 1024u) / g.stage_bytes);
+    if (g.stages < 2) return cudaErrorInvalidValue;
     a.s = v.s;
     a.P = v.P;
     a.K = v.K;
     a.ncp = ncp;
     a.igroups = 1;
-    const uint64_t steps = (F + kKB - 1) / kKB;
-    const uint64_t ranges = std::min<uint64_t>(uint64_t(num_sms), std::max<uint64_t>(1, steps / 4));
-    a.fibers_per_range = (steps + ranges - 1) / ranges * kKB;
+    if (mode == kFibS) {  // whole-panel ranges
+      const uint64_t ranges = std::min<uint64_t>(uint64_t(num_sms), std::max<uint64_t>(1, v.P / 4));
+      const uint64_t ppr = (v.P + ranges - 1) / ranges;
+      a.fibers_per_range = ppr * v.s;
+    } else {
+      const uint64_t steps = (F + g.kb - 1) / g.kb;
+      const uint64_t ranges = std::min<uint64_t>(uint64_t(num_sms), std::max<uint64_t>(1, steps / 4));
+      a.fibers_per_range = (steps + ranges - 1) / ranges * g.kb;
+    }
     a.ranges = uint32_t((F + a.fibers_per_range - 1) / a.fibers_per_range);
     if (ranges_used) *ranges_used = a.ranges;
     const int grid = int(std::min<uint64_t>(a.ranges, uint64_t(num_sms)));
     if (grid_used) *grid_used = grid;
+#define TKG_FW(N, MO)                                                                                   \
+  (mcol ? fr_wide_launch<N, MO, true>(A, M, a, g, grid, st) : fr_wide_launch<N, MO, false>(A, M, a, g, grid, st))
+#define TKG_FWM(N)                                                                                       \
+  case N:                                                                                               \
+    return mode == kFibI ? TKG_FW(N, kFibI) : mode == kFibJ ? TKG_FW(N, kFibJ) : TKG_FW(N, kFibS);
     switch (ncp) {
-      case 40: return mcol ? fr_wide_launch<40, true>(A, M, a, grid, st) : fr_wide_launch<40, false>(A, M, a, grid, st);
-      case 48: return mcol ? fr_wide_launch<48, true>(A, M, a, grid, st) : fr_wide_launch<48, false>(A, M, a, grid, st);
-      case 56: return mcol ? fr_wide_launch<56, true>(A, M, a, grid, st) : fr_wide_launch<56, false>(A, M, a, grid, st);
-      case 64: return mcol ? fr_wide_launch<64, true>(A, M, a, grid, st) : fr_wide_launch<64, false>(A, M, a, grid, st);
+      TKG_FWM(40) TKG_FWM(48) TKG_FWM(56) TKG_FWM(64)
       default: return cudaErrorInvalidValue;
     }
+#undef TKG_FWM
+#undef TKG_FW
   }
   if (mode == kFibI) {
     const uint64_t dims[2] = {v.K, F};
@@ -1247,16 +1314,18 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
 #undef TKG_FR_CALL
 }
 
-// one CTA over all K rows (fr_wide_kernel): mode 1 with 128 < K <= 248 at
-// the 1-CTA-per-SM column counts, when the remainder row tiles give each
-// warp at most FrW::kRemP extra pairs (TKG_FR_WIDE=0 disables it)
-bool fr_wide_ok(const FiberView& v, uint32_t ncp) {
+// one CTA over all K rows (fr_wide_kernel): 128 < K <= 248 at the
+// 1-CTA-per-SM column counts, when the remainder row tiles give each warp at
+// most FrW::kRemP extra pairs; kFibI, kFibJ, and kFibS panels of 32 < s < 64
+// fibers (one panel per stage) (TKG_FR_WIDE=0 disables it)
+bool fr_wide_ok(const FiberView& v, uint32_t ncp, int mode) {
   static const bool on = [] {
     const char* e = std::getenv("TKG_FR_WIDE");
     return !(e && e[0] == '0');
   }();
   const uint32_t mt = (v.K + 7) / 8, nrem = (mt % 8) * (ncp / 8);
-  return on && v.s == 1 && v.K > 128 && v.K <= 248 && ncp >= 40 && ncp <= 64 && nrem <= 8 * 2;
+  const bool layout = mode == kFibI || mode == kFibJ || (mode == kFibS && v.s > 32 && v.s < 64);
+  return on && layout && v.K > 128 && v.K <= 248 && ncp >= 40 && ncp <= 64 && nrem <= 8 * 2;
 }
 
 uint32_t fr_tma_ranges(const FiberView& v, int num_sms) {

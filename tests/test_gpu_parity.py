@@ -79,12 +79,26 @@ def test_unfold_times_wide_rows(ctx, ref, port, dims, r):
     assert rel(port.unfold_times(t, 1, m), ctx.unfold_times(t, 1, m)) <= 1e-13
 
 
+# the same kernel for middle modes: kFibS panels (32 < s < 64, one panel per
+# stage) and kFibJ panel-local chunks (s >= 64 or a multiple of 32)
+@pytest.mark.parametrize("dims", [[50, 200, 7], [40, 136, 9], [64, 200, 5], [100, 208, 3], [33, 248, 4]],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("r", [40, 50, 64])
+def test_unfold_times_wide_rows_middle_mode(ctx, ref, port, dims, r):
+    t = random_tensor(ref, dims, 401 + dims[0])
+    fibers = t.size // dims[1]
+    m = random_matrix(ref, fibers, r, 413 + r)
+    assert rel(port.unfold_times(t, 2, m), ctx.unfold_times(t, 2, m)) <= 1e-13
+
+
 # the init pass (column-major S, fused ||A||^2) and the sweeps through the wide FR
-@pytest.mark.parametrize("dims,r", [([200, 40, 30], 50), ([208, 30, 25], 64), ([144, 40, 20], 40), ([248, 20, 20], 40)])
-def test_als_low_rank_wide_rows(ctx, ref, port, dims, r):
+@pytest.mark.parametrize("dims,mode,r", [([200, 40, 30], 1, 50), ([208, 30, 25], 1, 64), ([144, 40, 20], 1, 40),
+                                         ([248, 20, 20], 1, 40), ([50, 200, 24], 2, 50), ([64, 200, 10], 2, 56),
+                                         ([40, 136, 30], 2, 48)])
+def test_als_low_rank_wide_rows(ctx, ref, port, dims, mode, r):
     t = random_tensor(ref, dims, 577 + r)
-    (lg, rg), rep = ctx.als_low_rank(t, 1, r, tk.AlsConfig(eta=1e-6, seed=13, max_iters=8))
-    lp, rp, prep = port.als_low_rank(t, 1, r, eta=1e-6, seed=13, max_iters=8)
+    (lg, rg), rep = ctx.als_low_rank(t, mode, r, tk.AlsConfig(eta=1e-6, seed=13, max_iters=8))
+    lp, rp, prep = port.als_low_rank(t, mode, r, eta=1e-6, seed=13, max_iters=8)
     assert rep.iterations == prep.iterations
     assert np.allclose(rep.residual_history, prep.residual_history, rtol=1e-11, atol=0)
     assert rel(lp, lg) <= 1e-9 and rel(rp, rg) <= 1e-9
