@@ -91,6 +91,21 @@ def test_unfold_times_wide_rows_middle_mode(ctx, ref, port, dims, r):
     assert rel(port.unfold_times(t, 2, m), ctx.unfold_times(t, 2, m)) <= 1e-13
 
 
+# FC on short panels (kFibS) with more than 32 columns: tiles of up to ~150
+# fibers whose extra row tiles are dealt to the warps as (row tile, column
+# tile) pairs
+@pytest.mark.parametrize("dims", [[50, 200, 7], [34, 200, 5], [18, 100, 20], [40, 136, 9], [62, 64, 11]],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("r", [33, 40, 48, 50, 56, 64])
+def test_unfold_t_times_short_panels(ctx, ref, port, dims, r):
+    t = random_tensor(ref, dims, 431 + dims[0])
+    l = random_matrix(ref, dims[1], r, 433 + r)
+    assert rel(port.unfold_t_times(t, 2, l), ctx.unfold_t_times(t, 2, l)) <= 1e-13
+    # the same contraction as a TTM with tensor-layout output (the st-HOSVD path)
+    u = random_matrix(ref, r, dims[1], 437 + r)
+    assert rel(port.mode_n_product(t, u, 2), ctx.mode_n_product(t, u, 2)) <= 1e-13
+
+
 # the init pass (column-major S, fused ||A||^2) and the sweeps through the wide FR
 @pytest.mark.parametrize("dims,mode,r", [([200, 40, 30], 1, 50), ([208, 30, 25], 1, 64), ([144, 40, 20], 1, 40),
                                          ([248, 20, 20], 1, 40), ([50, 200, 24], 2, 50), ([64, 200, 10], 2, 56),
