@@ -1271,7 +1271,17 @@ bool use_grid_steps() {
   return v;
 }
 
-constexpr uint32_t kClusterPrepMaxI = 512;
+constexpr uint32_t kClusterPrepMaxI = 1024;  // c3 (concurrent modes) 43.4 -> 43.0 ms; c4 at 2048 rows: slower
+constexpr uint32_t kClusterQrMaxI = 512;
+// prep (after the grid partial-sum kernel): the cluster kernel up to this many
+// rows (TKG_CLUSTER_PREP_MAXI overrides; measured in DESIGN.md §15)
+uint32_t cluster_prep_max_i() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("TKG_CLUSTER_PREP_MAXI");
+    return e ? uint32_t(std::atoi(e)) : kClusterPrepMaxI;
+  }();
+  return v;
+}
 
 template <class K, class... Args>
 cudaError_t pdl_launch(K kernel, int grid, int block, cudaStream_t st, Args... args) {
@@ -1379,7 +1389,7 @@ cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st) {
   // kernel (summing them on 16 SMs is latency-bound), then one cluster runs
   // the rest of the step; taller factors keep the grid-synchronised kernel
   // (tools/small_bench.cu).
-  if (!use_grid_steps() && a.I <= kClusterPrepMaxI) {
+  if (!use_grid_steps() && a.I <= cluster_prep_max_i()) {
     if (a.from_partials && a.nparts > 1) {
       const uint64_t threads = uint64_t(a.I) * a.r * 8;
       cudaError_t e = pdl_launch(slot0_reduce_kernel, int((threads + 255) / 256), 256, st, a.part, a.nparts, a.I,
@@ -1437,7 +1447,7 @@ cudaError_t launch_cholqr_step(CholQrArgs a, int num_sms, cudaStream_t st) {
   // cluster CholQR2 while a CTA's rows fit one 32-row block (I <= 512), after
   // a full-grid sum of the split-K partials; taller factors stream more rows
   // per SM than 16 SMs sustain
-  if (!use_grid_steps() && a.I <= kClusterPrepMaxI) {
+  if (!use_grid_steps() && a.I <= kClusterQrMaxI) {
     if (a.nparts > 1) {  // no stop check: the initializer runs before ctrl_init
       const uint64_t threads = uint64_t(a.I) * a.r * 8;
       cudaError_t e = pdl_launch(slot0_reduce_kernel, int((threads + 255) / 256), 256, st, a.Y, a.nparts, a.I,
