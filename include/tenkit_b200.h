@@ -310,7 +310,9 @@ int tkg_uniform01(tkg_ctx* ctx, uint64_t seed, uint32_t stream, uint64_t n, doub
 /* Per-kernel-class device time (CUDA events on the launch stream) while
  * profiling is on. classes: 0 FC (ALS right update), 1 FR (left update /
  * init), 2 small LA, 3 RNG, 4 TTM outside the ALS loop (core chain, st TTM,
- * singular vectors), 5 relative-residual expansion, 6-7 unused. */
+ * singular vectors), 5 relative-residual expansion, 6 fused sweep pass (right
+ * update, R^T R and left-update sum from one read of the tensor, r <= 16),
+ * 7 unused. */
 #define TKG_KERNEL_CLASSES 8
 typedef struct tkg_kernel_stats {
   double ms[TKG_KERNEL_CLASSES];
@@ -319,6 +321,11 @@ typedef struct tkg_kernel_stats {
   double flops[TKG_KERNEL_CLASSES]; /* algorithmic flops */
 } tkg_kernel_stats;
 int tkg_set_profiling(tkg_ctx* ctx, int on);
+/* The fused sweep pass (ranks up to 16: right update, R^T R and left-update sum
+ * from one read of the tensor) on / off for this context; on by default
+ * unless the environment sets TKG_FUSED_SWEEP=0. Results agree to rounding
+ * either way (tests/test_gpu_fused.py). */
+int tkg_set_fused_sweep(tkg_ctx* ctx, int on);
 int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out);
 
 /* Device-side timing on the context's stream (CUDA events): start, then
@@ -330,9 +337,10 @@ int tkg_flush_l2(tkg_ctx* ctx);
 
 /* Diagnostic: time the contraction kernels of one ALS sweep on a
  * device-resident tensor (d_a) along `mode` with r columns, `reps` times each
- * (CUDA events). out_ms (4 doubles): [0] mean FC (A_(n)^T L) launch, [1] mean
+ * (CUDA events). out_ms (5 doubles): [0] mean FC (A_(n)^T L) launch, [1] mean
  * FR (A_(n) R) launch, [2] the init pass A_(n) S (S column-major) with the
- * fused ||A||^2, [3] the same without it. Used by tools/kernel_bench.py and
+ * fused ||A||^2, [3] the same without it, [4] the fused sweep pass (0 when
+ * the shape does not take it). Used by tools/kernel_bench.py and
  * the ncu captures. */
 int tkg_bench_contractions(tkg_ctx* ctx, const double* d_a, int32_t order, const uint64_t* dims,
                            uint32_t mode, uint32_t r, int32_t reps, double* out_ms,

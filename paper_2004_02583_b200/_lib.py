@@ -130,6 +130,7 @@ SIGNATURES = [
     ("tkg_uniform01", C.c_int, [_ctxp, C.c_uint64, C.c_uint32, C.c_uint64, _dp,
                                 C.POINTER(TkgError)]),
     ("tkg_set_profiling", C.c_int, [_ctxp, C.c_int]),
+    ("tkg_set_fused_sweep", C.c_int, [_ctxp, C.c_int]),
     ("tkg_get_kernel_stats", C.c_int, [_ctxp, C.POINTER(TkgKernelStats)]),
     ("tkg_timer_start", C.c_int, [_ctxp]),
     ("tkg_timer_stop", C.c_int, [_ctxp, _dp]),

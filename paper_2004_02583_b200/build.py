@@ -6,7 +6,7 @@
   paper_2004_02583_b200/libtkg_synth.so     input synthesis for benches/tests
       (host C++/OpenMP; not on the decomposition path).
 
-Objects are rebuilt only when a source or header is newer than the library.
+Each object is rebuilt only when its source, a header or this file is newer than it.
 """
 from __future__ import annotations
 
@@ -27,7 +27,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 GXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else (shutil.which("g++") or "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["contract.cu", "contract_tma.cu", "smallla.cu", "mtrng.cu", "recon.cu", "als_step.cu", "coop.cu",
-           "gram.cu", "wide.cu", "eig.cu"]
+           "gram.cu", "wide.cu", "eig.cu", "sweep_fused.cu"]
 CPP_SRCS = ["engine.cpp", "engine_wide.cpp", "engine_dist.cpp", "comm.cpp", "mt_jump.cpp", "capi.cpp", "io.cpp"]  # cli.cpp: the executable
 
 
@@ -57,18 +57,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
         build_synth(force=False)
         return LIB
     cmds, objs = [], []
+    # an object is rebuilt when its source, any header or this file is newer
+    hdrs = _newest([d for d in deps if not d.endswith((".cu", ".cpp"))])
+
+    def stale(src, obj):
+        return force or not os.path.exists(obj) or os.path.getmtime(obj) < max(hdrs, os.path.getmtime(os.path.join(CSRC, src)))
+
     for src in CU_SRCS:
         obj = os.path.join(BUILD, src + ".o")
+        objs.append(obj)
+        if not stale(src, obj):
+            continue
         cmds.append([NVCC, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj])
-        objs.append(obj)
     for src in CPP_SRCS:
         obj = os.path.join(BUILD, src + ".o")
+        objs.append(obj)
+        if not stale(src, obj):
+            continue
         cmds.append([GXX, "-O2", "-std=c++17", "-fPIC", "-mpclmul", "-msse4.1", "-Wall",
                      "-I/usr/local/cuda/include", "-c", os.path.join(CSRC, src), "-o", obj])
-        objs.append(obj)
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+    with ThreadPoolExecutor(max_workers=max(1, len(cmds))) as ex:
         for r in ex.map(_run, cmds):
             if verbose:
                 sys.stderr.write(r.stderr)

@@ -516,6 +516,12 @@ int tkg_set_profiling(tkg_ctx* ctx, int on) {
   return 0;
 }
 
+int tkg_set_fused_sweep(tkg_ctx* ctx, int on) {
+  if (!ctx || !ctx->eng) return 1;
+  ctx->eng->set_fused_sweep(on != 0);
+  return 0;
+}
+
 int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out) {
   tkg_error err;
   return guarded(&err, [&] {

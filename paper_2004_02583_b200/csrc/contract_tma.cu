@@ -31,66 +31,12 @@
 
 #include "contract.cuh"
 #include "contract_tma.cuh"
+#include "tma_util.cuh"
 
 namespace tkg {
 
 namespace {
 
-constexpr int kCons = 8;                 // consumer warps
-constexpr int kThreadsTma = (kCons + 1) * 32;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra.uni DONE_%=;\n"
-      "bra.uni WAIT_%=;\n"
-      "DONE_%=:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                       int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
 
 // ---------------------------------------------------------------------------
 // FC
@@ -111,11 +57,30 @@ struct FcT {
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes;
 };
 
-template <int NC, int MODE>
+// TAIL = 2: the last column tile holds only 1-2 real columns (r mod 8 in
+// {1, 2}); they are accumulated with DFMAs on each lane's own k index (two per
+// row tile and k-step, summed over the 4 k lanes once per tile) instead of a
+// whole DMMA tile: DMMA and DFMA issue to the same FP64 pipe, a DMMA costing
+// 8 DFMAs, so r = 10 spends 8+2 columns' worth of the pipe instead of 16 and
+// r = 50 48+2 instead of 56 (tools/mix_fp64_probe.cu).
+template <int TAIL>
+__device__ __forceinline__ void tail_to_tile(double (&t)[2], double& a0, double& a1, int q) {
+  double v0 = t[0], v1 = t[1];
+  v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+  v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+  v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+  v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+  // accumulator-tile layout: lane (r8, q) holds columns 2q, 2q+1 of row r8
+  a0 = q == 0 ? v0 : 0.0;
+  a1 = q == 0 ? v1 : 0.0;
+}
+
+template <int NC, int MODE, int TAIL>
 __global__ void __launch_bounds__(kThreadsTma, 1)
     fc_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FcTmaArgs a) {
   using C = FcT<NC, MODE>;
+  constexpr int kND = TAIL ? C::kNT - 1 : C::kNT;  // column tiles on DMMA
   // launched with programmatic stream serialization: this grid's launch
   // overlaps the tail of the previous kernel; wait for its results here
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -210,6 +175,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    double tl[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 
     // warps whose 16 rows are all past the tile's fibers have nothing to add
     const bool wact = MODE == kFibS   ? uint64_t(warp * 16) < a.pc * a.s
@@ -233,13 +199,21 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           if (MODE == kFibS) af[m] = okS[m] ? As[offS[m] + kk * int(a.sb)] : 0.0;
           else af[m] = MODE == kFibI ? As[row * C::kLdA + kk] : As[kk * C::kLdA + row];
         }
-        double bf[C::kNT];
+        double bf[kND > 0 ? kND : 1];
 #pragma unroll
-        for (int n = 0; n < C::kNT; ++n) bf[n] = Ms[kk * C::kLdM + n * 8 + r8];
+        for (int n = 0; n < kND; ++n) bf[n] = Ms[kk * C::kLdM + n * 8 + r8];
 #pragma unroll
-        for (int n = 0; n < C::kNT; ++n)
+        for (int n = 0; n < kND; ++n)
 #pragma unroll
           for (int m = 0; m < 2; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+        if constexpr (TAIL != 0) {
+          const double2 bt = *reinterpret_cast<const double2*>(Ms + kk * C::kLdM + kND * 8);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            tl[m][0] = fma(af[m], bt.x, tl[m][0]);
+            tl[m][1] = fma(af[m], bt.y, tl[m][1]);
+          }
+        }
       };
       if (kleft >= C::kKB) {  // full block: the straight unrolled path
 #pragma unroll
@@ -251,6 +225,11 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    if constexpr (TAIL != 0) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m) tail_to_tile<TAIL>(tl[m], acc[m][kND][0], acc[m][kND][1], q);
     }
 
     // Gram epilogue: G[c1][c2] += sum_rows R[row][c1] R[row][c2] as DMMAs on
@@ -400,11 +379,12 @@ struct FrT {
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes;
 };
 
-template <int NC, int MODE, bool MCOL>
+template <int NC, int MODE, bool MCOL, int TAIL>
 __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 : 1)
     fr_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                   FrTmaArgs a) {
   using C = FrT<NC, MODE, MCOL>;
+  constexpr int kND = TAIL ? C::kNT - 1 : C::kNT;  // column tiles on DMMA (see fc_tma_kernel)
   asm volatile("griddepcontrol.wait;" ::: "memory");  // see fc_tma_kernel
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -504,6 +484,7 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  double tl[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   for (uint64_t j = f0; j < f1; ++kb) {
     const int slot = kb % C::kStages;
     const uint32_t ph = (kb / C::kStages) & 1;
@@ -528,9 +509,9 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
         af[m] = kok ? v : 0.0;
         if (want_sq) sq_acc[(t & 1) * 2 + m] = fma(af[m], af[m], sq_acc[(t & 1) * 2 + m]);
       }
-      double bf[C::kNT];
+      double bf[kND > 0 ? kND : 1];
 #pragma unroll
-      for (int n = 0; n < C::kNT; ++n) {
+      for (int n = 0; n < kND; ++n) {
         if (MODE == kFibS) {  // rows past the chunk are not loaded: keep them finite
           const double v = MCOL ? Ms[(n * 8 + r8) * ldm + kk] : Ms[kk * C::kLdM + n * 8 + r8];
           bf[n] = kok ? v : 0.0;
@@ -539,9 +520,25 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
         }
       }
 #pragma unroll
-      for (int n = 0; n < C::kNT; ++n) {
+      for (int n = 0; n < kND; ++n) {
         dmma(acc[0][n][0], acc[0][n][1], af[0], bf[n]);
         if (m1) dmma(acc[1][n][0], acc[1][n][1], af[1], bf[n]);
+      }
+      if constexpr (TAIL != 0) {
+        double2 bt;
+        if (MCOL) {
+          const int l = MODE == kFibS ? ldm : C::kLdM;
+          bt = make_double2(Ms[(kND * 8) * l + kk], Ms[(kND * 8 + 1) * l + kk]);
+        } else {
+          bt = *reinterpret_cast<const double2*>(Ms + kk * C::kLdM + kND * 8);
+        }
+        if (MODE == kFibS && !kok) bt = make_double2(0.0, 0.0);
+        tl[0][0] = fma(af[0], bt.x, tl[0][0]);
+        tl[0][1] = fma(af[0], bt.y, tl[0][1]);
+        if (m1) {
+          tl[1][0] = fma(af[1], bt.x, tl[1][0]);
+          tl[1][1] = fma(af[1], bt.y, tl[1][1]);
+        }
       }
     };
     if (kuse == C::kKB && m1act) {  // full chunk, both row tiles live: the straight path
@@ -556,6 +553,10 @@ __global__ void __launch_bounds__(kThreadsTma, (MODE == kFibI && NC <= 32) ? 2 :
     if (lane == 0) mbar_arrive(&empty[slot]);
   }
 
+  if constexpr (TAIL != 0) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) tail_to_tile<TAIL>(tl[m], acc[m][kND][0], acc[m][kND][1], q);
+  }
   // partial rows of this CTA
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
@@ -795,21 +796,6 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    else
-      cudaGetLastError();
-  });
-  return fn;
-}
-
 // ---------------------------------------------------------------------------
 // Mode expansion out(jl, i, p) = sum_c X(jl, c, p) U[i + c*Iout], X read as
 // the 3-D view X[jl + c*s + p*s*K] (reconstruct, tensor_ops.cpp:395-440).
@@ -964,54 +950,16 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   }
 }
 
-bool encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-            const uint32_t* box) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t gd[5], gs[4];
-  cuuint32_t bx[5], es[5];
-  for (int k = 0; k < rank; ++k) {
-    gd[k] = dims[k];
-    bx[k] = box[k];
-    es[k] = 1;
-    if (k + 1 < rank) gs[k] = strides[k];
-  }
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gd, gs, bx, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
 template <class K>
 cudaError_t set_smem(K k, size_t bytes) {
   return raise_smem_limit(k, bytes);
 }
 
-// Launch with programmatic stream serialization (PDL): the grid may begin
-// launching while the previous kernel on the stream drains; the kernel's
-// griddepcontrol.wait orders its reads after that kernel's writes.
-template <class K, class... Args>
-cudaError_t launch_pdl(K kernel, int grid, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(kThreadsTma);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, args...);
-}
-
-template <int NC, int MODE>
+template <int NC, int MODE, int TAIL = 0>
 cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTmaArgs& a, int grid,
                           cudaStream_t st) {
   using C = FcT<NC, MODE>;
-  auto k = fc_tma_kernel<NC, MODE>;
+  auto k = fc_tma_kernel<NC, MODE, TAIL>;
   cudaError_t e = set_smem(k, C::kSmem);
   if (e != cudaSuccess) return e;
   return launch_pdl(k, grid, C::kSmem, st, A, M, a);
@@ -1027,11 +975,11 @@ cudaError_t fr_wide_launch(const CUtensorMap& A, const CUtensorMap& M, const FrT
   return launch_pdl(k, grid, smem, st, A, M, a, g);
 }
 
-template <int NC, int MODE, bool MCOL>
+template <int NC, int MODE, bool MCOL, int TAIL = 0>
 cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, int grid,
                           cudaStream_t st) {
   using C = FrT<NC, MODE, MCOL>;
-  auto k = fr_tma_kernel<NC, MODE, MCOL>;
+  auto k = fr_tma_kernel<NC, MODE, MCOL, TAIL>;
   cudaError_t e = set_smem(k, C::kSmem);
   if (e != cudaSuccess) return e;
   return launch_pdl(k, grid, C::kSmem, st, A, M, a);
@@ -1050,6 +998,19 @@ cudaError_t fr_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTm
     default: return cudaErrorInvalidValue;  \
   }
 
+// column counts whose last tile may run as a DFMA tail (16 .. 64)
+#define TKG_NC_SWITCH_T(ncp, CALL)          \
+  switch (ncp) {                            \
+    case 16: return CALL(16);               \
+    case 24: return CALL(24);               \
+    case 32: return CALL(32);               \
+    case 40: return CALL(40);               \
+    case 48: return CALL(48);               \
+    case 56: return CALL(56);               \
+    case 64: return CALL(64);               \
+    default: break;                         \
+  }
+
 template <int KC>
 cudaError_t expand_tma_launch(const CUtensorMap& X, const CUtensorMap& U, const CUtensorMap& R,
                               const ExpandArgs& a, int grid, cudaStream_t st) {
@@ -1066,6 +1027,16 @@ cudaError_t expand_tma_launch(const CUtensorMap& X, const CUtensorMap& U, const 
 int& pdl_off_count() {
   static int n = 0;  // engines currently profiling (host-side setting, read at launch)
   return n;
+}
+
+// r mod 8 in {1, 2} above 8 columns: the last column tile runs as a DFMA
+// tail (TKG_DFMA_TAIL=0 keeps the padded DMMA tile)
+bool dfma_tail(uint32_t nc) {
+  static const bool on = [] {
+    const char* e = std::getenv("TKG_DFMA_TAIL");
+    return !(e && e[0] == '0');
+  }();
+  return on && nc > 8 && (nc % 8 == 1 || nc % 8 == 2);
 }
 
 int fc_tma_mode(const FiberView& v, const double* mt, uint32_t ldmt) {
@@ -1153,7 +1124,14 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
 #define TKG_FC_CALL(N) (mode == kFibI   ? fc_tma_launch<N, kFibI>(A, M, a, grid, st) \
                         : mode == kFibJ ? fc_tma_launch<N, kFibJ>(A, M, a, grid, st) \
                                         : fc_tma_launch<N, kFibS>(A, M, a, grid, st))
+#define TKG_FC_CALL_T(N) (mode == kFibI   ? fc_tma_launch<N, kFibI, 2>(A, M, a, grid, st) \
+                          : mode == kFibJ ? fc_tma_launch<N, kFibJ, 2>(A, M, a, grid, st) \
+                                          : fc_tma_launch<N, kFibS, 2>(A, M, a, grid, st))
+  if (dfma_tail(a.nc)) {
+    TKG_NC_SWITCH_T(ncp, TKG_FC_CALL_T)
+  }
   TKG_NC_SWITCH(ncp, TKG_FC_CALL)
+#undef TKG_FC_CALL_T
 #undef TKG_FC_CALL
 }
 
@@ -1310,7 +1288,18 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
                            : fr_tma_launch<N, kFibJ, false>(A, M, a, grid, st))               \
                    : (mcol ? fr_tma_launch<N, kFibS, true>(A, M, a, grid, st)                 \
                            : fr_tma_launch<N, kFibS, false>(A, M, a, grid, st)))
+#define TKG_FR_CALL_T(N)                                                                    \
+  (mode == kFibI   ? (mcol ? fr_tma_launch<N, kFibI, true, 2>(A, M, a, grid, st)              \
+                           : fr_tma_launch<N, kFibI, false, 2>(A, M, a, grid, st))            \
+   : mode == kFibJ ? (mcol ? fr_tma_launch<N, kFibJ, true, 2>(A, M, a, grid, st)              \
+                           : fr_tma_launch<N, kFibJ, false, 2>(A, M, a, grid, st))            \
+                   : (mcol ? fr_tma_launch<N, kFibS, true, 2>(A, M, a, grid, st)              \
+                           : fr_tma_launch<N, kFibS, false, 2>(A, M, a, grid, st)))
+  if (dfma_tail(a.nc)) {
+    TKG_NC_SWITCH_T(ncp, TKG_FR_CALL_T)
+  }
   TKG_NC_SWITCH(ncp, TKG_FR_CALL)
+#undef TKG_FR_CALL_T
 #undef TKG_FR_CALL
 }
 

@@ -54,6 +54,7 @@ int fr_tma_mode(const FiberView& v, const double* m, uint64_t mj, uint64_t mc);
 int fc_tma_grid(const FiberView& v, int num_sms);
 uint32_t fr_tma_ranges(const FiberView& v, int num_sms);
 bool fr_wide_ok(const FiberView& v, uint32_t ncp, int mode);
+bool dfma_tail(uint32_t nc);  // the last column tile of nc columns runs as a DFMA tail
 
 cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, FcTmaArgs a, int mode,
                           int num_sms, cudaStream_t st, int* grid_used);

@@ -15,6 +15,7 @@
 #include "coop.cuh"
 #include "contract_tma.cuh"
 #include "mt_jump.hpp"
+#include "sweep_fused.cuh"
 
 namespace tkg {
 
@@ -327,6 +328,42 @@ void Engine::fc(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc
   }
 }
 
+bool Engine::sweep_fused_usable(const FiberView& v, const double* mt, uint32_t nc, const double* R) const {
+  return fused_sweep_ && !force_v1_ && !dist_ && sweep_fused_ok(v, mt, nc, R);
+}
+
+int Engine::sweep_fused(const FiberView& v, const double* mt, uint32_t nc, double* R, double* partial,
+                        double* gram_part, bool count_pass, const int32_t* skip) {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (profiling_) {
+    ev = ev_pair();
+    CK(cudaEventRecord(ev.first, st_));
+  }
+  SweepFusedArgs a;
+  a.mt = mt;
+  a.nc = nc;
+  a.R = R;
+  a.partial = partial;
+  a.gram_part = gram_part;
+  a.skip = skip;
+  int grid = 0;
+  CK(launch_sweep_fused(v, a, sms_, st_, &grid));
+  count_launch();
+  const double elems = double(v.s) * double(v.P) * double(v.K);
+  const double F = double(v.s) * double(v.P);
+  // the pass reads A and L' and writes R and the K x r sum: one tensor pass
+  const double bytes = 8.0 * (elems + F * nc + 2.0 * double(v.K) * nc);
+  if (profiling_) {
+    CK(cudaEventRecord(ev.second, st_));
+    record(kClsSweep, ev.first, ev.second, bytes, 4.0 * elems * nc);
+  }
+  if (count_pass) {
+    passes_ += 1;
+    bytes_ += uint64_t(bytes);
+  }
+  return grid;
+}
+
 int Engine::fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc) {
   const int mode = force_v1_ ? -1 : fc_tma_mode(v, mt, ldmt);
   return mode >= 0 ? fc_tma_grid(v, sms_) : fc_grid_for(v, nc, sms_);
@@ -623,8 +660,9 @@ void Engine::settle(AlsOut& o) {
   o.norm = h.norm;
   // FC of sweeps 1..iter, FR of sweeps 1..iter-1 (or iter when the cap ended it)
   const int fr_run = h.stop ? h.iter - 1 : h.iter;
-  passes_ += uint64_t(h.iter + fr_run);
-  bytes_ += uint64_t(double(h.iter + fr_run) * o.fc_bytes);
+  const int npass = o.fused ? h.iter : h.iter + fr_run;  // a fused sweep is one tensor pass
+  passes_ += uint64_t(npass);
+  bytes_ += uint64_t(double(npass) * o.fc_bytes);
   launches_ += uint64_t(std::max(1, h.iter)) * uint64_t(o.body_launches);
 }
 
@@ -787,7 +825,9 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   double* GR = gr_.d(kMaxRank * kMaxRank);
   double* cholL = cholL_.d(kMaxRank * kMaxRank);
   double* cholR = cholR_.d(kMaxRank * kMaxRank);
-  const uint32_t nranges = fr_ranges(v, r);
+  // r <= 16 (HBM-bound): one fused pass per sweep instead of FC + FR
+  const bool fused = sweep_fused_usable(v, Mt, r, R);
+  const uint32_t nranges = std::max(fr_ranges(v, r), fused ? uint32_t(sweep_fused_grid(v, r, sms_)) : 0u);
   double* part = fr_part_.d(size_t(nranges) * I * ncp);
   double* sq = sq_part_.d(size_t(std::max(4096, sumsq_partials_count(sh.count()))));
   double* sumsq = sumsq_d_.d(2);
@@ -857,7 +897,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   double* gs = gs_.d(size_t(r) * r);
   // Gram of R: fused into the FC epilogue up to ncp 32, else a row pass inside finish_step
   const bool fused_gram = ncp <= kFcGramMaxNc;
-  const int nfin = std::max(finish_step_grid(F, sms_), fc_grid(v, Mt, ncp, r));
+  const int nfin = std::max({finish_step_grid(F, sms_), fc_grid(v, Mt, ncp, r), fused ? sweep_fused_grid(v, r, sms_) : 0});
   double* gpr = fc_gram_.d(size_t(nfin) * ncp * ncp);
   uint32_t last_ranges = 0;
   auto prep_args = [&](int from_partials, int nparts) {
@@ -907,13 +947,22 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     const std::vector<uint64_t> key = {uint64_t(v.base), v.s, v.P, v.K, v.is_i, v.is_p, r, ncp,
                                        uint64_t(Mt), uint64_t(R), uint64_t(gpr), uint64_t(part), uint64_t(Lc),
                                        uint64_t(GL), uint64_t(GLinv), uint64_t(GRinv), uint64_t(gs),
-                                       uint64_t(gpl), uint64_t(ctrl), uint64_t(hist), uint64_t(sms_)};
+                                       uint64_t(gpl), uint64_t(ctrl), uint64_t(hist), uint64_t(sms_),
+                                       uint64_t(fused)};
     auto it = graphs_.find(key);
     if (it != graphs_.end()) {
       loop = it->second.first;
       body_launches = it->second.second;
     } else {
       loop = capture_sweep_loop([&](GraphCond cond) {
+        if (fused) {
+          const int used = sweep_fused(v, Mt, r, R, part, gpr, false, stop);
+          const FinishArgs fa = finish_args(used, cond);
+          CK(launch_finish_step(fa, sms_, st_));
+          const PrepArgs pa = prep_args(1, used);
+          CK(launch_prep_step(pa, sms_, st_));
+          return;
+        }
         int fc_used = 0;
         fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, false, stop,
            fused_gram ? gpr : nullptr);
@@ -954,6 +1003,7 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
     out.fc_bytes = 8.0 * (double(sh.count()) + double(F) * r + double(I) * r);
     out.body_launches = body_launches;
     out.r = r;
+    out.fused = fused;
     out.rep.iterations = 0;
     trace("als graph enqueued", mode);
     return out;
@@ -988,8 +1038,10 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
       }
       const size_t rec_fc = recs_.size();
       int fc_used = 0;
-      fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, true, stop,
-         fused_gram ? gpr : nullptr);
+      if (fused) fc_used = sweep_fused(v, Mt, r, R, part, gpr, true, stop);
+      else
+        fc(v, Mt, ncp, r, R, ncp, 1, s * ncp, nullptr, nullptr, &fc_used, true, stop,
+           fused_gram ? gpr : nullptr);
       trace("  fc launched", k);
       if (profiling_) spec_recs_.push_back({k, 0, rec_fc});
       FinishArgs fa;
@@ -1024,6 +1076,11 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
         trace("  finish launched", k);
         if (profiling_) spec_recs_.push_back({k, 0, rec});
       }
+      if (fused) {
+        last_ranges = uint32_t(fc_used);  // the fused pass wrote one left-update partial per CTA
+        count_launch(2);
+        continue;
+      }
       const size_t rec_fr = recs_.size();
       last_ranges = fr(v, R, ncp, 1, r, part, nullptr, true, nullptr, stop);
       if (dist_) last_ranges = reduce_left_partials(part, last_ranges, uint32_t(I), ncp, r);
@@ -1056,9 +1113,11 @@ Engine::AlsOut Engine::run_als(const double* A, const Shape& sh, int mode, uint3
   // (the stop decision of sweep `iter` skips its left update).
   {
     const int fr_run = h.stop ? h.iter - 1 : h.iter;
-    const int skipped = (enqueued - h.iter) + (enqueued - fr_run);
+    // fused sweeps: one pass per enqueued sweep, executed for sweeps 1..iter
+    const int skipped = fused ? enqueued - h.iter : (enqueued - h.iter) + (enqueued - fr_run);
     const double elems = double(sh.count());
-    const double bytes = 8.0 * (elems + double(F) * r + double(I) * r);
+    const double bytes = fused ? 8.0 * (elems + double(F) * r + 2.0 * double(I) * r)
+                               : 8.0 * (elems + double(F) * r + double(I) * r);
     passes_ -= uint64_t(skipped);
     bytes_ -= uint64_t(skipped * bytes);
     for (const SpecRec& sr : spec_recs_) {
@@ -1511,9 +1570,10 @@ double Engine::residual_read(const double* out, const double* ref_sumsq_host) {
 // identity behind hosvd's error analysis), used when it is accurate to well
 // inside the parity tolerance: its rounding error is a few eps ||A||^2 (the
 // two sums, G's own rounding, the factors' orthonormality defect), i.e.
-// |d rel| ~ 1e-15 / (2 rel); at rel >= kClosedFormMinRel that is <= 5e-12
-// against the 1e-10 bar (BASELINE.json). Smaller residuals (exact or nearly
-// exact fits, config 3 at 1e-4) take the explicit expansion pass. false when
+// |d rel| ~ 1e-15 / (2 rel); at rel >= kClosedFormMinRel that is <= 2e-11
+// against the 1e-10 bar (BASELINE.json; config 3 at rel 1e-4 measured
+// 4.1e-12 against the compiled reference). Smaller residuals (exact or nearly
+// exact fits) take the explicit expansion pass. false when
 // the explicit pass is needed (or forced: TKG_EXPLICIT_RESIDUAL=1).
 bool Engine::closed_form_residual(const double* core_buf, uint64_t ncore, const double* ref_sumsq_host,
                                   double* rel) {
@@ -1534,7 +1594,11 @@ bool Engine::closed_form_residual(const double* core_buf, uint64_t ncore, const 
   const double a2 = *ref_sumsq_host;
   if (a2 == 0.0) raise(3, "relative_error: reference tensor has zero norm");
   const double rel2 = (a2 - g2h) / a2;
-  if (!(rel2 >= kClosedFormMinRel * kClosedFormMinRel)) return false;
+  static const double min_rel = [] {
+    const char* e = std::getenv("TKG_CLOSED_FORM_MIN_REL");
+    return e ? std::atof(e) : kClosedFormMinRel;
+  }();
+  if (!(rel2 >= min_rel * min_rel)) return false;
   *rel = std::sqrt(rel2);
   return true;
 }
@@ -2329,6 +2393,19 @@ void Engine::bench_contractions(const double* A, const Shape& sh, int mode, uint
     CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&ms, e0, e1));
     out_ms[with_sq ? 2 : 3] = ms / reps;
+  }
+  // the fused sweep pass (r <= 16): FC + R^T R + FR from one read
+  out_ms[4] = 0.0;
+  if (sweep_fused_usable(v, Mt, r, R)) {
+    double* partf = fr_part_.d(size_t(std::max<uint32_t>(nranges, uint32_t(sweep_fused_grid(v, r, sms_)))) * I * ncp);
+    double* gpr = fc_gram_.d(size_t(sweep_fused_grid(v, r, sms_)) * ncp * ncp);
+    sweep_fused(v, Mt, r, R, partf, gpr, false, nullptr);
+    CK(cudaEventRecord(e0, st_));
+    for (int k = 0; k < reps; ++k) sweep_fused(v, Mt, r, R, partf, gpr, false, nullptr);
+    CK(cudaEventRecord(e1, st_));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    out_ms[4] = ms / reps;
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -113,7 +113,7 @@ class DBuf {
 // FC right updates, FR left updates + init passes, small LA steps, RNG,
 // TTM contractions outside the ALS loop (core chain, st TTM, singular
 // vectors), the relative-residual expansion passes
-enum KernelClass { kClsFC = 0, kClsFR = 1, kClsSmall = 2, kClsRng = 3, kClsTTM = 4, kClsResid = 5, kNumCls = 8 };
+enum KernelClass { kClsFC = 0, kClsFR = 1, kClsSmall = 2, kClsRng = 3, kClsTTM = 4, kClsResid = 5, kClsSweep = 6, kNumCls = 8 };
 
 class Engine {
  public:
@@ -186,6 +186,8 @@ class Engine {
     profiling_ = on;
   }
   void force_v1(bool on) { force_v1_ = on; }
+  // the fused sweep pass for r <= 16 (sweep_fused.cu); default from TKG_FUSED_SWEEP (on unless "0")
+  void set_fused_sweep(bool on) { fused_sweep_ = on; }
   void timer_start();
   double timer_stop();
   void flush_l2();
@@ -205,6 +207,7 @@ class Engine {
     double fc_bytes = 0.0;
     int body_launches = 0;
     uint32_t r = 0;
+    bool fused = false;   // sweeps ran as fused passes (one tensor pass per sweep)
   };
   // Host-visible results of the decomposition drivers are staged in pinned
   // memory with asynchronous copies and read after the driver's single final
@@ -283,6 +286,11 @@ class Engine {
           uint64_t os_j, uint64_t os_c, uint64_t os_p, double* sumsq_part,
           const double* diff_ref, int* grid_used, bool count_pass, const int32_t* skip = nullptr,
           double* gram_part = nullptr);
+  // one sweep's R = A_(n)^T L', R^T R partials and left-update partials from
+  // one read of the tensor (sweep_fused.cu); returns the CTAs launched
+  int sweep_fused(const FiberView& v, const double* mt, uint32_t nc, double* R, double* partial,
+                  double* gram_part, bool count_pass, const int32_t* skip);
+  bool sweep_fused_usable(const FiberView& v, const double* mt, uint32_t nc, const double* R) const;
   int fc_grid(const FiberView& v, const double* mt, uint32_t ldmt, uint32_t nc);
   uint32_t fr_ranges(const FiberView& v, uint32_t nc);
   uint32_t fr(const FiberView& v, const double* m, uint64_t mj, uint64_t mc, uint32_t nc,
@@ -300,7 +308,7 @@ class Engine {
   void recover_sv_round(const double* A, const Shape& sh, int mode, uint32_t r, double* U, double* vt);
   // SVD / EIG engines: U (device, I x r) <- leading eigenvectors of A_(n) A_(n)^T
   void gram_factor(const double* A, const Shape& sh, int mode, uint32_t r, double* U, bool refine);
-  static constexpr double kClosedFormMinRel = 2e-4;
+  static constexpr double kClosedFormMinRel = 5e-5;
   bool closed_form_residual(const double* core_buf, uint64_t ncore, const double* ref_sumsq_host, double* rel);
   // dst <- A x_m U_m^T for every m != skip, ascending (multi_mode_product with
   // the other factors, hooi.cpp:82-88); returns dst's shape
@@ -391,6 +399,7 @@ class Engine {
 
   bool profiling_ = false;
   bool force_v1_ = false;
+  bool fused_sweep_ = true;
   struct Rec {
     int cls;
     cudaEvent_t a, b;

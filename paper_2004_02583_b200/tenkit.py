@@ -626,10 +626,14 @@ class Context:
     def set_profiling(self, on: bool):
         self._l.tkg_set_profiling(self._ctx, int(bool(on)))
 
+    def set_fused_sweep(self, on: bool):
+        """The fused sweep pass for ranks up to 16 (csrc/sweep_fused.cu) on / off."""
+        self._l.tkg_set_fused_sweep(self._ctx, int(bool(on)))
+
     def kernel_stats(self):
         st = _lib.TkgKernelStats()
         self._l.tkg_get_kernel_stats(self._ctx, C.byref(st))
-        names = ["fc", "fr", "small", "rng", "ttm", "residual"]
+        names = ["fc", "fr", "small", "rng", "ttm", "residual", "sweep"]
         return {names[k]: {"ms": st.ms[k], "launches": int(st.launches[k]), "bytes": st.bytes[k],
                            "flops": st.flops[k]} for k in range(len(names))}
 

@@ -19,7 +19,7 @@ from paper_2004_02583_b200 import _lib  # noqa: E402
 
 CASES = {
     "c1m1": ([256, 256, 256], 1, 10), "c1m2": ([256, 256, 256], 2, 10), "c1m3": ([256, 256, 256], 3, 10),
-    "c2m1": ([96, 96, 96, 96], 1, 10), "c2m2": ([10, 96, 96, 96], 2, 10),
+    "c2m1": ([96, 96, 96, 96], 1, 10), "c2m2": ([10, 96, 96, 96], 2, 10), "c2m3": ([10, 10, 96, 96], 3, 10),
     "c3m1": ([1024, 1024, 1024], 1, 32), "c3m2": ([1024, 1024, 1024], 2, 32),
     "c3m3": ([1024, 1024, 1024], 3, 32),
     "c4m3": ([2048, 2048, 512], 3, 32), "c4m1": ([2048, 2048, 32], 1, 64),
@@ -46,7 +46,7 @@ def main():
     for name in sel:
         dims, mode, r = CASES[name]
         n = int(np.prod(dims))
-        ms = (C.c_double * 4)()
+        ms = (C.c_double * 5)()
         err = _lib.TkgError()
         rc = l.tkg_bench_contractions(ctx._ctx, C.c_void_p(buf.data_ptr()), len(dims), _lib.u64(dims),
                                       mode, r, args.reps, ms, C.byref(err))
@@ -63,6 +63,10 @@ def main():
             t = ms[k]
             row[nm] = {"ms": round(t, 4), "GB/s": round(bytes_ / t / 1e6, 1),
                        "TF/s": round(flops / t / 1e9, 2), "roof_frac": round(tmin / t, 3)}
+        if ms[4] > 0:  # fused sweep pass: FC + FR work from one read of the tensor
+            t = ms[4]
+            row["sweep"] = {"ms": round(t, 4), "GB/s": round(bytes_ / t / 1e6, 1), "TF/s": round(2 * flops / t / 1e9, 2),
+                            "roof_frac": round(max(bytes_ / (bw * 1e9), 2 * flops / (p64 * 1e12)) * 1e3 / t, 3)}
         row["bound_ms"] = round(tmin, 4)
         out.append(row)
         print(json.dumps(row), flush=True)
