@@ -322,9 +322,10 @@ typedef struct tkg_kernel_stats {
 } tkg_kernel_stats;
 int tkg_set_profiling(tkg_ctx* ctx, int on);
 /* The fused sweep pass (ranks up to 16: right update, R^T R and left-update sum
- * from one read of the tensor) on / off for this context; on by default
- * unless the environment sets TKG_FUSED_SWEEP=0. Results agree to rounding
- * either way (tests/test_gpu_fused.py). */
+ * from one read of the tensor) on / off for this context; off by default
+ * unless the environment sets TKG_FUSED_SWEEP=1 (DESIGN.md has the
+ * measurements). Results agree to rounding either way
+ * (tests/test_gpu_fused.py). */
 int tkg_set_fused_sweep(tkg_ctx* ctx, int on);
 int tkg_get_kernel_stats(tkg_ctx* ctx, tkg_kernel_stats* out);
 

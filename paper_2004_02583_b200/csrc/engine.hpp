@@ -11,6 +11,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -186,7 +187,8 @@ class Engine {
     profiling_ = on;
   }
   void force_v1(bool on) { force_v1_ = on; }
-  // the fused sweep pass for r <= 16 (sweep_fused.cu); default from TKG_FUSED_SWEEP (on unless "0")
+  // the fused sweep pass for r <= 16 (sweep_fused.cu): off unless switched on
+  // here or by TKG_FUSED_SWEEP=1 (measured slower inside the decompositions)
   void set_fused_sweep(bool on) { fused_sweep_ = on; }
   void timer_start();
   double timer_stop();
@@ -399,7 +401,10 @@ class Engine {
 
   bool profiling_ = false;
   bool force_v1_ = false;
-  bool fused_sweep_ = true;
+  bool fused_sweep_ = [] {
+    const char* e = std::getenv("TKG_FUSED_SWEEP");
+    return e != nullptr && e[0] == '1';
+  }();
   struct Rec {
     int cls;
     cudaEvent_t a, b;

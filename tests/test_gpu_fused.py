@@ -27,7 +27,9 @@ def rel(a, b):
 
 @pytest.fixture(scope="module")
 def ctx():
-    return tk.Context(0)
+    c = tk.Context(0)
+    c.set_fused_sweep(True)  # off by default
+    return c
 
 
 @pytest.fixture(scope="module")
@@ -59,7 +61,7 @@ CASES = [
     ([96, 40, 30], 1, 10),     # one box, DFMA tail
     ([128, 50, 9], 1, 8),      # one box, 8 columns
     ([100, 37, 11], 1, 12),    # K = 4 (mod 16): no padding; 16 columns without a tail
-    ([30, 64, 17], 1, 3),      # short fibers
+    ([40, 64, 17], 1, 3),      # short fibers
     ([256, 30, 12], 1, 10),    # two boxes
     ([250, 33, 7], 1, 16),     # two boxes, K not a multiple of 8
     ([200, 21, 13], 1, 9),     # two boxes, one tail column
