@@ -34,6 +34,7 @@
 #include "als_step.cuh"
 #include "blockfact.cuh"
 #include "coop.cuh"
+#include "contract_tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -696,24 +697,61 @@ __global__ void __launch_bounds__(kThreads, kFinPerSm) finish_step_kernel(Finish
       if (b + kStg - 1 < b1) issue(b + kStg - 1, int((b - b0 + kStg - 1) % kStg));
       cp_async_commit();
       const double* t = tile + size_t(slot) * kRows * kLd;
-      auto steps = [&](auto S) {
+      // TAIL: the last column tile holds 1-2 real columns (r mod 8 in {1, 2});
+      // its kNT tiles (tm, kNT-1) are each lane's own-row products with those
+      // two values (DFMA, summed over the 4 k lanes after the pass) instead of
+      // DMMA tiles that are three quarters padding
+      auto steps = [&](auto S, auto T) {
         constexpr int sset = decltype(S)::value;
+        constexpr bool kTail = decltype(T)::value;
 #pragma unroll
         for (int ks = 0; ks < kKs; ++ks) {
           const double* rp = t + ((group * kKs + ks) * 4 + q) * kLd;
           double fr[kNT];
 #pragma unroll
           for (int c = 0; c < kNT; ++c) fr[c] = rp[c * 8 + r8];
+          double2 tv = make_double2(0.0, 0.0);
+          if (kTail) tv = *reinterpret_cast<const double2*>(rp + (kNT - 1) * 8);
           int idx = 0;
 #pragma unroll
           for (int tm = 0; tm < kNT; ++tm)
 #pragma unroll
             for (int tn = tm; tn < kNT; ++tn, ++idx)
-              if (idx % kSets == sset) dmma(acc[idx / kSets][0], acc[idx / kSets][1], fr[tm], fr[tn]);
+              if (idx % kSets == sset) {
+                if (kTail && tn == kNT - 1) {
+                  acc[idx / kSets][0] = fma(fr[tm], tv.x, acc[idx / kSets][0]);
+                  acc[idx / kSets][1] = fma(fr[tm], tv.y, acc[idx / kSets][1]);
+                } else {
+                  dmma(acc[idx / kSets][0], acc[idx / kSets][1], fr[tm], fr[tn]);
+                }
+              }
         }
       };
-      if (kSets == 2 && set == 1) steps(std::integral_constant<int, 1>{});
-      else steps(std::integral_constant<int, 0>{});
+      using std::integral_constant;
+      if (a.gram_tail && kNT > 1) {
+        if (kSets == 2 && set == 1) steps(integral_constant<int, 1>{}, integral_constant<bool, true>{});
+        else steps(integral_constant<int, 0>{}, integral_constant<bool, true>{});
+      } else {
+        if (kSets == 2 && set == 1) steps(integral_constant<int, 1>{}, integral_constant<bool, false>{});
+        else steps(integral_constant<int, 0>{}, integral_constant<bool, false>{});
+      }
+    }
+    if (a.gram_tail && kNT > 1) {
+      // the tail tiles in accumulator-tile layout: lane (r8, q = 0) holds columns 0, 1
+      int idx = 0;
+#pragma unroll
+      for (int tm = 0; tm < kNT; ++tm)
+#pragma unroll
+        for (int tn = tm; tn < kNT; ++tn, ++idx)
+          if (tn == kNT - 1 && idx % kSets == set) {
+            double v0 = acc[idx / kSets][0], v1 = acc[idx / kSets][1];
+            v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+            v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+            acc[idx / kSets][0] = q == 0 ? v0 : 0.0;
+            acc[idx / kSets][1] = q == 0 ? v1 : 0.0;
+          }
     }
     cp_async_wait<0>();
     __syncthreads();  // the ring is free: the warp partials are summed there, warp 0 first
@@ -1407,6 +1445,7 @@ cudaError_t launch_prep_step(PrepArgs a, int num_sms, cudaStream_t st) {
 }
 
 cudaError_t launch_finish_step(FinishArgs a, int num_sms, cudaStream_t st) {
+  a.gram_tail = dfma_tail(a.r) ? 1 : 0;
   const uint32_t ntri = a.r * (a.r + 1) / 2;
   const int want = a.mode == 2 ? 1
                    : a.gram_nparts ? int(std::min<uint32_t>(uint32_t(num_sms), (ntri + 7) / 8))

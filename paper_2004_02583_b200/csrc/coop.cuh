@@ -46,6 +46,8 @@ struct FinishArgs {
   int mode = 0;                  // 0 full step; 1 only the R^T R partials of the R pass
                                  // (gpart[grid], see finish_step_grid); 2 only the CTA-0
                                  // part from the reduced Gram in gs (sharded runs)
+  int gram_tail = 0;             // set by the launcher: r mod 8 in {1, 2}, the last column
+                                 // tile of the R pass runs as a DFMA tail (see fc_tma_kernel)
 };
 
 struct CholQrArgs {

@@ -197,7 +197,9 @@ def test_als_contraction_ratio_kat(ctx):
 
 
 @pytest.mark.parametrize("dims,mode,r", [([7, 8, 6], 1, 2), ([7, 8, 6], 2, 3), ([7, 8, 6], 3, 2),
-                                         ([30, 20, 10], 2, 5), ([12, 10, 8, 6], 4, 3)])
+                                         ([30, 20, 10], 2, 5), ([12, 10, 8, 6], 4, 3),
+                                         # r > 32: R^T R by the row pass of finish_step; r mod 8 in {1, 2}: DFMA tail
+                                         ([90, 64, 40], 1, 50), ([64, 90, 40], 2, 41), ([80, 70, 30], 1, 48)])
 def test_als_low_rank_matches_oracle(ctx, ref, port, dims, mode, r):
     t = random_tensor(ref, dims, 573 + mode)
     (lg, rg), rep = ctx.als_low_rank(t, mode, r, tk.AlsConfig(eta=1e-6, seed=11))
