@@ -486,7 +486,7 @@ def b200_arm(args, c, world, rank, local):
 
     peaks = load_peaks()
     # dominant kernel class over the timed region
-    cls = max(("fc", "fr"), key=lambda k: stats[k]["ms"])
+    cls = max(("fc", "fr", "sweep"), key=lambda k: stats.get(k, {"ms": 0.0})["ms"])
     st = stats[cls]
     per_launch_ms = st["ms"] / max(1, st["launches"])
     ai = st["flops"] / max(1.0, st["bytes"])
@@ -501,7 +501,8 @@ def b200_arm(args, c, world, rank, local):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["hbm_src"]}
     roof.update({"kernel": {"fc": "FC fiber contraction (ALS right update A_(n)^T L')",
-                            "fr": "FR fiber reduction (left update A_(n) R, init A_(n) S)"}[cls],
+                            "fr": "FR fiber reduction (left update A_(n) R, init A_(n) S)",
+                            "sweep": "fused sweep pass (right update, R^T R and left-update sum from one read)"}[cls],
                  "traffic": (ncu_traffic(args.config, cls) or {}).get("dram_bytes_per_launch"),
                  "traffic_source": ncu_traffic(args.config, cls), "launch_ms": per_launch_ms,
                  "arith_intensity_flop_per_byte": ai, "ridge_flop_per_byte": ridge,
