@@ -380,7 +380,8 @@ VALUE_BASIS = ("effective: algorithmic bytes of the REFERENCE algorithm's tensor
                "iteration counts (init + k right + (k-1) left per mode, t: core TTM chain over A, "
                "st: shrink; 8(|A| + F r + I r) per contraction, SURVEY §8(d)) / step time; the same "
                "byte count for both arms. The B200 t-HOSVD path skips the first core TTM pass over A "
-               "(DESIGN §3) and runs a fused residual pass the count does not credit")
+               "(DESIGN §3); its relative residual is the closed form ||A||^2 - ||G||^2, or below rel 5e-5 a fused "
+               "expansion pass the count does not credit (DESIGN §5)")
 
 
 # ---- B200 arm ------------------------------------------------------------------------
