@@ -49,8 +49,8 @@ struct FcT {
   static constexpr int kLdA = MODE == kFibI ? 36 : 132; // padded inner extent of the A box
   static constexpr int kRowsA = MODE == kFibI ? kTF : kKB;
   static constexpr int kLdM = NC + 4;
-  // kFibS: the A box is {sb, 32, pc} with pc*sb <= 160 (runtime size)
-  static constexpr int kBytesA = MODE == kFibS ? kKB * 160 * 8 : kRowsA * kLdA * 8;
+  // kFibS: the A box is {sb, 32, pc} with pc*sb <= 208 (runtime size)
+  static constexpr int kBytesA = MODE == kFibS ? kKB * 208 * 8 : kRowsA * kLdA * 8;
   static constexpr int kBytesM = kKB * kLdM * 8;
   static constexpr int kStageBytes = ((kBytesA + kBytesM) + 127) / 128 * 128;
   static constexpr int kNT = NC / 8;
@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   // panel p (rows past s are TMA zero-fill and are not stored)
   const uint64_t tpp = MODE == kFibJ ? (a.s + C::kTF - 1) / C::kTF : 1;
   // kFibS tiles are a.pc whole panels (a.pc * s <= 128 fibers)
+  const bool strad = MODE == kFibS && a.straddle != 0;
   const uint64_t ntiles = MODE == kFibJ   ? tpp * a.P
-                          : MODE == kFibS ? (a.P + a.pc - 1) / a.pc
+                          : MODE == kFibS ? (strad ? (F + C::kTF - 1) / C::kTF : (a.P + a.pc - 1) / a.pc)
                                           : (F + C::kTF - 1) / C::kTF;
   const int nkb = int((a.K + C::kKB - 1) / C::kKB);
   const int stage_bytes = MODE == kFibS ? int(a.stage_bytes) : C::kStageBytes;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
           } else if (MODE == kFibJ) {
             tma_3d(st, &tmA, &full[slot], int(jl0), kb * C::kKB, int(tp));
           } else {
-            tma_3d(st, &tmA, &full[slot], 0, kb * C::kKB, int(tile * a.pc));
+            tma_3d(st, &tmA, &full[slot], 0, kb * C::kKB, strad ? int(j0 / a.s) : int(tile * a.pc));
           }
           tma_2d(st + bytes_a, &tmM, &full[slot], 0, kb * C::kKB);
         }
@@ -149,7 +150,8 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   // column kk sits at (panel*kKB + kk)*sb + jl
   int offS[2] = {0, 0};
   bool okS[2] = {true, true};
-  if (MODE == kFibS) {
+  uint32_t pS[2] = {0, 0}, jlS[2] = {0, 0};  // straddling tiles: panel and in-panel index of the rows
+  if (MODE == kFibS && !strad) {
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
       const int row = warp * 16 + m * 8 + r8;
@@ -177,8 +179,21 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       for (int n = 0; n < C::kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
     double tl[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 
+    if (strad) {
+      // row m of the tile is fiber j0 + m: panel j / s (the box starts at the
+      // panel of j0), in-panel index j % s
+      const uint32_t p0 = uint32_t(j0 / a.s);
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const uint64_t j = j0 + uint64_t(warp * 16 + m * 8 + r8);
+        okS[m] = j < F;
+        pS[m] = uint32_t(j) / uint32_t(a.s);
+        jlS[m] = uint32_t(j) - pS[m] * uint32_t(a.s);
+        offS[m] = okS[m] ? int((pS[m] - p0) * C::kKB) * int(a.sb) + int(jlS[m]) : 0;
+      }
+    }
     // warps whose 16 rows are all past the tile's fibers have nothing to add
-    const bool wact = MODE == kFibS   ? uint64_t(warp * 16) < a.pc * a.s
+    const bool wact = MODE == kFibS   ? (strad ? j0 + uint64_t(warp * 16) < F : uint64_t(warp * 16) < a.pc * a.s)
                       : MODE == kFibJ ? jl0 + uint64_t(warp * 16) < a.s
                                       : j0 + uint64_t(warp * 16) < F;
     for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -271,10 +286,15 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         if (jl >= a.s) continue;
       } else if (MODE == kFibS) {
         if (!okS[m]) continue;
-        const int row = warp * 16 + m * 8 + r8;
-        const uint64_t pcm = uint64_t(row) / a.s;
-        p = tile * a.pc + pcm;
-        jl = uint64_t(row) - pcm * a.s;
+        if (strad) {
+          p = pS[m];
+          jl = jlS[m];
+        } else {
+          const int row = warp * 16 + m * 8 + r8;
+          const uint64_t pcm = uint64_t(row) / a.s;
+          p = tile * a.pc + pcm;
+          jl = uint64_t(row) - pcm * a.s;
+        }
         if (p >= a.P) continue;
       } else {
         const uint64_t j = j0 + warp * 16 + m * 8 + r8;
@@ -1069,6 +1089,23 @@ void fc_short_geometry(uint64_t s, uint32_t* pc, uint32_t* sb) {
   *sb = (b <= s + s / 4) ? b : uint32_t(s);
 }
 
+// kFibS FC with every tile row live: tiles of 128 consecutive fibers across
+// panel boundaries; a tile starting anywhere in a panel spans at most
+// floor((s + 126) / s) + 1 panels. Taken when whole-panel tiles would leave
+// rows idle and the wider box still fits the stage (pc * sb <= 208 doubles
+// per contraction index); TKG_FC_STRADDLE=0 keeps whole-panel tiles.
+bool fc_straddle_geometry(uint64_t s, uint64_t P, uint32_t sb, uint32_t* pc) {
+  static const bool on = [] {
+    const char* e = std::getenv("TKG_FC_STRADDLE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || 128 % s == 0) return false;
+  const uint32_t span = uint32_t(std::min<uint64_t>((s + 126) / s + 1, P));
+  if (span > 256 || uint64_t(span) * sb > 208) return false;
+  *pc = span;
+  return true;
+}
+
 // kFibS FR: panels per chunk (kf = pc * s <= 64 fibers) and the panel ranges
 void fr_short_geometry(const FiberView& v, int num_sms, uint32_t* pc, uint64_t* ppr, uint32_t* ranges) {
   *pc = uint32_t(64 / v.s);
@@ -1103,6 +1140,7 @@ cudaError_t launch_fc_tma(const FiberView& v, const double* mt, uint32_t ldmt, F
     if (!encode(&A, v.base, 3, dims, strides, box)) return cudaErrorInvalidValue;
   } else {
     fc_short_geometry(v.s, &a.pc, &a.sb);
+    a.straddle = fc_straddle_geometry(v.s, v.P, a.sb, &a.pc) ? 1 : 0;
     const uint64_t dims[3] = {v.s, v.K, v.P};
     const uint64_t strides[2] = {v.is_i * 8, v.is_p * 8};
     const uint32_t box[3] = {a.sb, 32, a.pc};

@@ -26,6 +26,10 @@ struct FcTmaArgs {
   // kFibS (short panels): a tile is pc whole panels (pc*s <= 128 fibers), the
   // A box {sb, 32, pc} (sb >= s, TMA zero-fills past s); runtime stage sizes
   uint32_t pc = 1, sb = 0, bytes_a = 0, stage_bytes = 0;
+  // kFibS, straddle = 1: a tile is 128 consecutive fibers whatever panels they
+  // fall in (every tile row live); its box starts at the first fiber's panel
+  // and spans pc panels
+  uint32_t straddle = 0;
 };
 
 // NC (padded column count) up to which the FC kernel can fuse the Gram of
