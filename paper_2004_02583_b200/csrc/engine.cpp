@@ -1991,7 +1991,7 @@ void Engine::st_hosvd(const double* a, bool a_dev, const Shape& sh, const std::v
       ev = ev_pair();
       CK(cudaEventRecord(ev.first, st_));
     }
-    CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_));
+    CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_, true));  // R_hat: qr_dev's upper factor
     if (profiling_) {
       // shrink: reads R (F x r), writes the r x F working tensor, 2 r^2 F flops
       CK(cudaEventRecord(ev.second, st_));

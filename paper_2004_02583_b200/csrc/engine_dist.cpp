@@ -422,7 +422,7 @@ void Engine::st_hosvd_sharded(const double* a, bool a_dev, const Shape& G, uint6
     double* dst = bufs[which]->d(nxt.count());
     const int nsh = shrink_count(F);
     double* sq = sq_part_.d(size_t(std::max(4096, nsh)));
-    CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_));
+    CK(launch_shrink(r_.d(F * ncp + 8), ncp, s, P, r, rhat_.d(r * r), dst, sq, st_, true));  // R_hat: qr_dev's upper factor
     CK(launch_sum(sq, nsh, sumsq_d_.d(2), st_));
     count_launch(2);
     comm_->allreduce_sum(sumsq_d_.d(2), 1, st_);

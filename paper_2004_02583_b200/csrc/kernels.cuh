@@ -115,8 +115,11 @@ cudaError_t launch_sumsq_diff(const double* a, const double* b, uint64_t n, doub
 // out[jl + c*s + p*s*r] = sum_c' rhat[c + c'*r] * R[(p*s + jl)*ld + c'], plus
 // per-CTA partial sums of squares of the output (the next mode's ||B||^2).
 int shrink_count(uint64_t F);
+// rhat_upper: rhat is upper triangular (a QR factor): the kernel skips the
+// products with its zero blocks.
 cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
-                          const double* rhat, double* out, double* sumsq_part, cudaStream_t st);
+                          const double* rhat, double* out, double* sumsq_part, cudaStream_t st,
+                          bool rhat_upper = false);
 
 // Mode expansion out(jl, i, p) = sum_c in(jl, c, p) U[i + c*Iout] (recon.cu);
 // with ref set, accumulates sum (ref - out)^2 per CTA instead of storing.

@@ -307,7 +307,10 @@ constexpr int kShrinkThreads = 256;
 constexpr int kShrinkTile = 64;              // two CTAs per SM overlap each other's phases
 constexpr int kShrinkMT = kShrinkTile / 64;  // 8-fiber row tiles per warp
 
-template <int NC>
+// UPPER: R_hat is upper triangular (the QR factor of the st-HOSVD drivers), so
+// k-step t (rows 4t .. 4t+3 of R_hat^T) reaches only the column tiles n with
+// 8n <= 4t + 3: 56 of the 98 DMMAs per row tile at 56 columns.
+template <int NC, bool UPPER>
 __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
     const double* __restrict__ R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
     const double* __restrict__ rhat, double* __restrict__ out, double* sumsq_part) {
@@ -348,10 +351,18 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
     const uint64_t j0 = tile * kShrinkTile;
     const int nf = int(F - j0 < uint64_t(kShrinkTile) ? F - j0 : uint64_t(kShrinkTile));
     __syncthreads();  // the current tile landed for every thread
-    // R's padding columns and the rows past F are zero for the product
-    for (int e = threadIdx.x; e < kShrinkTile * NC; e += blockDim.x) {
-      const int row = e / NC, c = e % NC;
-      if (row >= nf || c >= int(r)) cur[row * kLd + c] = 0.0;
+    // R's padding columns (never written by the contraction kernels) and the
+    // rows past F are zero for the product
+    const int npad = NC - int(r);
+    for (int e = threadIdx.x; e < kShrinkTile * npad; e += blockDim.x) {
+      const int row = e / npad, c = int(r) + e % npad;
+      cur[row * kLd + c] = 0.0;
+    }
+    if (nf < kShrinkTile) {
+      for (int e = threadIdx.x; e < (kShrinkTile - nf) * int(r); e += blockDim.x) {
+        const int row = nf + e / int(r), c = e % int(r);
+        cur[row * kLd + c] = 0.0;
+      }
     }
     __syncthreads();
     double acc[kShrinkMT][NC / 8][2];
@@ -366,11 +377,14 @@ __global__ void __launch_bounds__(kShrinkThreads, 2) shrink_kernel(
 #pragma unroll
       for (int m = 0; m < kShrinkMT; ++m) af[m] = cur[(warp * 8 * kShrinkMT + m * 8 + r8) * kLd + kk];
 #pragma unroll
-      for (int n = 0; n < NC / 8; ++n) bf[n] = Bs[kk * kLd + n * 8 + r8];
+      for (int n = 0; n < NC / 8; ++n)
+        if (!UPPER || 8 * n <= 4 * t + 3) bf[n] = Bs[kk * kLd + n * 8 + r8];
 #pragma unroll
       for (int n = 0; n < NC / 8; ++n)
+        if (!UPPER || 8 * n <= 4 * t + 3) {
 #pragma unroll
-        for (int m = 0; m < kShrinkMT; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+          for (int m = 0; m < kShrinkMT; ++m) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+        }
     }
     __syncthreads();  // the current buffer becomes the staging buffer Os
     double* Os = cur;
@@ -623,15 +637,17 @@ int shrink_count(uint64_t F) {
 }
 
 cudaError_t launch_shrink(const double* R, uint64_t ld, uint64_t s, uint64_t P, uint32_t r,
-                          const double* rhat, double* out, double* sumsq_part, cudaStream_t st) {
+                          const double* rhat, double* out, double* sumsq_part, cudaStream_t st,
+                          bool rhat_upper) {
   const int grid = shrink_count(s * P);
   const uint32_t nc = r <= 8 ? 8 : (r + 7) / 8 * 8;
 #define TKG_S(N)                                                                                    \
   if (nc == N) {                                                                                    \
     const size_t smem = sizeof(double) * (2 * size_t(kShrinkTile) * (N + 4) + size_t(N) * (N + 4)); \
-    cudaError_t e = raise_smem_limit(shrink_kernel<N>, smem);                                       \
+    auto k = rhat_upper ? shrink_kernel<N, true> : shrink_kernel<N, false>;                         \
+    cudaError_t e = raise_smem_limit(k, smem);                                                      \
     if (e != cudaSuccess) return e;                                                                 \
-    shrink_kernel<N><<<grid, kShrinkThreads, smem, st>>>(R, ld, s, P, r, rhat, out, sumsq_part);   \
+    k<<<grid, kShrinkThreads, smem, st>>>(R, ld, s, P, r, rhat, out, sumsq_part);                   \
     return cudaGetLastError();                                                                      \
   }
   TKG_S(8) TKG_S(16) TKG_S(24) TKG_S(32) TKG_S(40) TKG_S(48) TKG_S(56) TKG_S(64)
