@@ -632,12 +632,29 @@ struct FrWideGeom {
   uint32_t bytes_a = 0, bytes_m = 0, stage_bytes = 0, stages = 0, ldm = 0;
 };
 
-template <int NC, int MODE, bool MCOL>
-__global__ void __launch_bounds__(kThreadsTma, 1)
+// REBAL: launched with 12 warps: the 8 consumer warps (warpgroups 0 and 1), the
+// producer warp and three idle warps that fill its warpgroup. The producer's
+// warpgroup hands its registers back (setmaxnreg.dec) and the consumers take
+// them (setmaxnreg.inc: 168 -> 232 per thread), which is what the 3 full row
+// tiles + 2 remainder pairs + DFMA tail of a warp need without spills.
+// REBAL = false keeps the 9-warp launch at 168 registers (no tail): the
+// mode-1 left update (kFibI, row-major R) measured faster that way (c5:
+// 5.45 ms against 6.00 ms rebalanced, 5.79 ms rebalanced with the tail),
+// every other variant faster rebalanced (c5 mode 2: 1.51 -> 1.40 ms, init
+// passes 6.43 -> 5.94 ms and 1.59 -> 1.46 ms).
+constexpr int kThreadsWide = 12 * 32;
+
+template <int NC, int MODE, bool MCOL, int TAIL, bool REBAL>
+__global__ void __launch_bounds__(REBAL ? kThreadsWide : kThreadsTma, 1)
     fr_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
                    FrTmaArgs a, FrWideGeom g) {
   using C = FrW<NC, MODE, MCOL>;
   constexpr int kNT = C::kNT;
+  // column tiles on DMMA; with TAIL the last tile's 1-2 real columns run as
+  // DFMAs (see fc_tma_kernel). The remainder pairs then cover the kND DMMA
+  // tiles of a remainder row tile, and the warp holding its column tile 0
+  // also accumulates that row tile's tail.
+  constexpr int kND = TAIL ? kNT - 1 : kNT;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // see fc_tma_kernel
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -668,8 +685,9 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   }
   __syncthreads();
 
-  if (warp == kCons) {
-    if (lane == 0) {
+  if (warp >= kCons) {
+    if constexpr (REBAL) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
+    if (warp == kCons && lane == 0) {
       prefetch_map(&tmA);
       prefetch_map(&tmM);
       int kb = 0;
@@ -696,12 +714,13 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     }
     return;
   }
+  if constexpr (REBAL) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
 
   const int q = lane & 3;
   const int r8 = lane >> 2;
   const int MT = int((a.K + 7) / 8);
   const int base = MT / 8;              // 2 or 3 full row tiles per warp
-  const int nrem = (MT % 8) * kNT;      // remainder (row tile, column tile) pairs
+  const int nrem = (MT % 8) * kND;      // remainder (row tile, column tile) pairs
   const int lda = int(g.lda), ldm = int(g.ldm);
   double sq_acc[4] = {0.0, 0.0, 0.0, 0.0};
   // ||A||^2 is fused only into the init pass (column-major S)
@@ -724,6 +743,10 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
       for (int n = 0; n < kNT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 #pragma unroll
     for (int t = 0; t < C::kRemP; ++t) accr[t][0] = accr[t][1] = 0.0;
+    double tl[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double tlr[C::kRemP][2];
+#pragma unroll
+    for (int t = 0; t < C::kRemP; ++t) tlr[t][0] = tlr[t][1] = 0.0;
     for (uint64_t j = f0; j < f1; ++kb) {
       const int slot = kb % stages;
       const uint32_t ph = (kb / stages) & 1;
@@ -754,22 +777,38 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
         // loads are predicated all the same (measured: 5.96 -> 5.43 ms for the
         // c5 mode-1 left update), the column-major ones are not (7.15 -> 6.47)
 #pragma unroll
-        for (int n = 0; n < kNT; ++n) {
+        for (int n = 0; n < kND; ++n) {
           const double b = MCOL ? Ms[(n * 8 + r8) * ldm + kk] : (kok ? Ms[kk * ldm + n * 8 + r8] : 0.0);
           dmma(acc[0][n][0], acc[0][n][1], af[0], b);
           dmma(acc[1][n][0], acc[1][n][1], af[1], b);
           if (base > 2) dmma(acc[2][n][0], acc[2][n][1], af[2], b);
         }
+        double2 bt = make_double2(0.0, 0.0);
+        if constexpr (TAIL != 0) {
+          if (MCOL) bt = make_double2(Ms[(kND * 8) * ldm + kk], Ms[(kND * 8 + 1) * ldm + kk]);
+          else if (kok) bt = *reinterpret_cast<const double2*>(Ms + kk * ldm + kND * 8);
+#pragma unroll
+          for (int mi = 0; mi < 3; ++mi) {
+            tl[mi][0] = fma(af[mi], bt.x, tl[mi][0]);
+            tl[mi][1] = fma(af[mi], bt.y, tl[mi][1]);
+          }
+        }
 #pragma unroll
         for (int u = 0; u < C::kRemP; ++u) {
           const int p = warp + 8 * u;
           if (p < nrem) {
-            const int m = 8 * base + p / kNT, n = p % kNT;
+            const int m = 8 * base + p / kND, n = p % kND;
             const double af1 = kok ? aval(As, m * 8 + r8, kk) : 0.0;
             // each A element of a remainder tile is squared once (column tile 0)
             if (want_sq && n == 0) sq_acc[(t & 1) * 2 + 1] = fma(af1, af1, sq_acc[(t & 1) * 2 + 1]);
             const double bb = MCOL ? Ms[(n * 8 + r8) * ldm + kk] : (kok ? Ms[kk * ldm + n * 8 + r8] : 0.0);
             dmma(accr[u][0], accr[u][1], af1, bb);
+            if constexpr (TAIL != 0) {
+              if (n == 0) {
+                tlr[u][0] = fma(af1, bt.x, tlr[u][0]);
+                tlr[u][1] = fma(af1, bt.y, tlr[u][1]);
+              }
+            }
           }
         }
       }
@@ -778,6 +817,12 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     }
     // this range's partial rows
     double* dst0 = a.partial + size_t(range) * a.K * a.ncp;
+    if constexpr (TAIL != 0) {
+#pragma unroll
+      for (int mi = 0; mi < 3; ++mi) tail_to_tile<TAIL>(tl[mi], acc[mi][kND][0], acc[mi][kND][1], q);
+#pragma unroll
+      for (int u = 0; u < C::kRemP; ++u) tail_to_tile<TAIL>(tlr[u], tlr[u][0], tlr[u][1], q);
+    }
 #pragma unroll
     for (int mi = 0; mi < 3; ++mi) {
       if (mi >= base) continue;
@@ -792,10 +837,16 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
     for (int u = 0; u < C::kRemP; ++u) {
       const int p = warp + 8 * u;
       if (p >= nrem) continue;
-      const int i = (8 * base + p / kNT) * 8 + r8, n = p % kNT;
-      if (i < int(a.K))
+      const int i = (8 * base + p / kND) * 8 + r8, n = p % kND;
+      if (i < int(a.K)) {
         *reinterpret_cast<double2*>(dst0 + size_t(i) * a.ncp + n * 8 + 2 * q) =
             make_double2(accr[u][0], accr[u][1]);
+        if constexpr (TAIL != 0) {
+          if (n == 0)
+            *reinterpret_cast<double2*>(dst0 + size_t(i) * a.ncp + kND * 8 + 2 * q) =
+                make_double2(tlr[u][0], tlr[u][1]);
+        }
+      }
     }
   }
   if (want_sq) {
@@ -985,14 +1036,15 @@ cudaError_t fc_tma_launch(const CUtensorMap& A, const CUtensorMap& M, const FcTm
   return launch_pdl(k, grid, C::kSmem, st, A, M, a);
 }
 
-template <int NC, int MODE, bool MCOL>
+template <int NC, int MODE, bool MCOL, int TAIL = 0>
 cudaError_t fr_wide_launch(const CUtensorMap& A, const CUtensorMap& M, const FrTmaArgs& a, const FrWideGeom& g,
                            int grid, cudaStream_t st) {
-  auto k = fr_wide_kernel<NC, MODE, MCOL>;
+  constexpr bool kRebal = !(MODE == kFibI && !MCOL);
+  auto k = fr_wide_kernel<NC, MODE, MCOL, kRebal ? TAIL : 0, kRebal>;
   const size_t smem = 1024 + size_t(g.stages) * g.stage_bytes;
   cudaError_t e = set_smem(k, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k, grid, smem, st, A, M, a, g);
+  return launch_pdl_threads(k, grid, kRebal ? kThreadsWide : kThreadsTma, smem, st, A, M, a, g);
 }
 
 template <int NC, int MODE, bool MCOL, int TAIL = 0>
@@ -1247,13 +1299,20 @@ cudaError_t launch_fr_tma(const FiberView& v, const double* m, uint64_t mj, uint
     if (ranges_used) *ranges_used = a.ranges;
     const int grid = int(std::min<uint64_t>(a.ranges, uint64_t(num_sms)));
     if (grid_used) *grid_used = grid;
-#define TKG_FW(N, MO)                                                                                   \
-  (mcol ? fr_wide_launch<N, MO, true>(A, M, a, g, grid, st) : fr_wide_launch<N, MO, false>(A, M, a, g, grid, st))
-#define TKG_FWM(N)                                                                                       \
-  case N:                                                                                               \
-    return mode == kFibI ? TKG_FW(N, kFibI) : mode == kFibJ ? TKG_FW(N, kFibJ) : TKG_FW(N, kFibS);
+#define TKG_FW(N, MO, T)                                                              \
+  (mcol ? fr_wide_launch<N, MO, true, T>(A, M, a, g, grid, st)                        \
+        : fr_wide_launch<N, MO, false, T>(A, M, a, g, grid, st))
+#define TKG_FWM(N, T)                                                                  \
+  case N:                                                                             \
+    return mode == kFibI ? TKG_FW(N, kFibI, T) : mode == kFibJ ? TKG_FW(N, kFibJ, T) : TKG_FW(N, kFibS, T);
+    if (dfma_tail(a.nc)) {
+      switch (ncp) {
+        TKG_FWM(40, 2) TKG_FWM(48, 2) TKG_FWM(56, 2) TKG_FWM(64, 2)
+        default: return cudaErrorInvalidValue;
+      }
+    }
     switch (ncp) {
-      TKG_FWM(40) TKG_FWM(48) TKG_FWM(56) TKG_FWM(64)
+      TKG_FWM(40, 0) TKG_FWM(48, 0) TKG_FWM(56, 0) TKG_FWM(64, 0)
       default: return cudaErrorInvalidValue;
     }
 #undef TKG_FWM
