@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -300,8 +301,21 @@ MtPlan mt_plan(uint64_t total, bool side) {
   C = std::max<uint64_t>(1, std::min<uint64_t>(C, 296));
   // streams generated on the side stream, behind the sweeps of earlier modes,
   // are not latency-critical: a quarter of the chunks (a quarter of the jump
-  // work competing with the sweeps for the SMs) and 4x longer chunks
-  if (side) C = std::max<uint64_t>(1, C / 4);
+  // work competing with the sweeps for the SMs) and 4x longer chunks — but no
+  // chunk longer than kSideMaxJ draws: a generator CTA that sits on an SM for
+  // a millisecond slows that SM's share of every statically scheduled
+  // contraction grid and keeps cluster launches waiting (config 5: 76.2 ->
+  // 73.7 ms per step with short side chunks; config 4, whose side chunks are
+  // short already, is 1 ms slower with 4x the jump work)
+  static const uint64_t side_max_j = [] {
+    const char* e = std::getenv("TKG_SIDE_MAX_J");
+    return e ? uint64_t(std::max(1, std::atoi(e))) : uint64_t(400000);
+  }();
+  if (side) {
+    const uint64_t quarter = std::max<uint64_t>(1, C / 4);
+    const uint64_t by_len = (total + side_max_j - 1) / side_max_j;
+    C = std::min<uint64_t>(C, std::max(quarter, by_len));
+  }
   p.C = static_cast<int>(C);
   p.J = (total + C - 1) / C;
   if (p.J == 0) p.J = 1;
